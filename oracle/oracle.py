@@ -1,0 +1,245 @@
+"""ctypes wrapper of the fp64 CPU oracle (oracle/pdilqr_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: importable from tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs.  The product package never imports this module, and this
+module never imports the product package.  Argument marshalling only; all arithmetic is in C.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "pdilqr_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_up = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O3, OpenMP).  Plain x86-64 code (no -march=native) so the
+    same binary runs on the GPU box's host."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-std=gnu11", "-O3", "-fopenmp", "-fPIC", "-shared",
+                               "-Wall", "-o", _LIB, _SRC])
+    return _LIB
+
+
+class SrbdParams(C.Structure):
+    _fields_ = [("dt", C.c_double), ("mass", C.c_double), ("inertia", C.c_double * 9),
+                ("gravity", C.c_double * 3), ("w_x", C.c_double * 12), ("w_x_term", C.c_double * 12),
+                ("w_u_stance", C.c_double), ("w_u_swing", C.c_double), ("mu_friction", C.c_double),
+                ("f_min", C.c_double), ("f_max", C.c_double), ("barrier_mu", C.c_double),
+                ("barrier_delta", C.c_double)]
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "SrbdParams":
+        p = cls()
+        for name, _ in cls._fields_:
+            v = d[name]
+            if isinstance(v, (list, tuple, np.ndarray)):
+                arr = getattr(p, name)
+                for i, e in enumerate(v):
+                    arr[i] = float(e)
+            else:
+                setattr(p, name, float(v))
+        return p
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = C.CDLL(build())
+        i, d, PP = C.c_int, C.c_double, C.POINTER(SrbdParams)
+        L.oracle_riccati.argtypes = [i, i, i] + [_dp] * 11 + [_dp] * 4
+        L.oracle_riccati.restype = i
+        L.oracle_rollout_dual.argtypes = [i, i, i] + [_dp] * 8 + [_dp] * 3
+        L.oracle_solve_lq.argtypes = [i, i, i] + [_dp] * 11 + [_dp] * 3 + [_dp] * 4
+        L.oracle_solve_lq.restype = i
+        L.oracle_solve_lq_batch.argtypes = [i, i, i, i] + [_dp] * 11 + [_dp] * 3 + [_ip, i]
+        L.oracle_srbd_f.argtypes = [PP, _dp, _dp, _dp, _up, _dp]
+        L.oracle_srbd_jac.argtypes = [PP, _dp, _dp, _dp, _up, _dp, _dp]
+        L.oracle_srbd_h.argtypes = [PP, _dp, _dp, _dp, _up, _dp]
+        for f in ("oracle_barrier", "oracle_barrier_d1", "oracle_barrier_d2"):
+            getattr(L, f).argtypes = [d, d, d]
+            getattr(L, f).restype = d
+        L.oracle_srbd_linearize.argtypes = [PP, i] + [_dp] * 6 + [_up, _dp] + [_dp] * 11
+        L.oracle_srbd_linearize.restype = i
+        L.oracle_srbd_linearize_batch.argtypes = [PP, i, i] + [_dp] * 6 + [_up, _dp] + [_dp] * 11 + [_ip, i]
+        L.oracle_srbd_cost.argtypes = [PP, i, _dp, _dp, _dp, _dp, _up]
+        L.oracle_srbd_cost.restype = d
+        L.oracle_srbd_theta.argtypes = [PP, i, _dp, _dp, _dp, _up, _dp]
+        L.oracle_srbd_theta.restype = d
+        L.oracle_srbd_cost_slope.argtypes = [PP, i, _dp, _dp, _dp, _dp, _up, _dp, _dp]
+        L.oracle_srbd_cost_slope.restype = d
+        L.oracle_srbd_line_search.argtypes = [PP, i, i, d, d] + [_dp] * 5 + [_up, _dp, _dp, _dp] + [_dp] * 3
+        L.oracle_srbd_line_search.restype = i
+        L.oracle_srbd_step.argtypes = [PP, i, i, d, d] + [_dp] * 6 + [_up, _dp] + [_dp] * 4
+        L.oracle_srbd_step.restype = i
+        L.oracle_srbd_step_batch.argtypes = [PP, i, i, i, d, d] + [_dp] * 6 + [_up, _dp, _dp, i]
+        L.oracle_max_threads.restype = i
+        _lib = L
+    return _lib
+
+
+def _c(a, dtype=np.float64):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def max_threads() -> int:
+    return lib().oracle_max_threads()
+
+
+# ----------------------------------------------------------------------------- LQ
+
+def solve_lq_single(qp: dict, b: int = 0):
+    """One instance b of a batched LQ dict -> dict with K, k, P, p, dx, du, dlam, info."""
+    A = _c(qp["A"][b]); N1, n, _ = A.shape
+    N = N1 - 1
+    m = qp["Bm"].shape[-1]
+    out = {"K": np.zeros((N + 1, m, n)), "k": np.zeros((N + 1, m)), "P": np.zeros((N + 2, n, n)),
+           "p": np.zeros((N + 2, n)), "dx": np.zeros((N + 2, n)), "du": np.zeros((N + 1, m)),
+           "dlam": np.zeros((N + 2, n))}
+    info = lib().oracle_solve_lq(N, n, m, A, _c(qp["Bm"][b]), _c(qp["c"][b]), _c(qp["Q"][b]),
+                                 _c(qp["R"][b]), _c(qp["S"][b]), _c(qp["q"][b]), _c(qp["r"][b]),
+                                 _c(qp["P_term"][b]), _c(qp["p_term"][b]), _c(qp["dx0"][b]),
+                                 out["dx"], out["du"], out["dlam"], out["K"], out["k"], out["P"], out["p"])
+    out["info"] = info
+    return out
+
+
+def solve_lq(qp: dict, nthreads: int | None = None):
+    """Batched LQ solve -> dict dx[B][N+2][n], du[B][N+1][m], dlam[B][N+2][n], info[B]."""
+    A = _c(qp["A"]); Bn, N1, n, _ = A.shape
+    m = qp["Bm"].shape[-1]
+    N = N1 - 1
+    dx = np.zeros((Bn, N + 2, n)); du = np.zeros((Bn, N + 1, m)); dl = np.zeros((Bn, N + 2, n))
+    info = np.zeros(Bn, np.int32)
+    lib().oracle_solve_lq_batch(Bn, N, n, m, A, _c(qp["Bm"]), _c(qp["c"]), _c(qp["Q"]), _c(qp["R"]),
+                                _c(qp["S"]), _c(qp["q"]), _c(qp["r"]), _c(qp["P_term"]),
+                                _c(qp["p_term"]), _c(qp["dx0"]), dx, du, dl, info,
+                                nthreads or max_threads())
+    return {"dx": dx, "du": du, "dlam": dl, "info": info}
+
+
+# ----------------------------------------------------------------------------- SRBD
+
+def srbd_f(params: dict, x, u, feet, contact):
+    out = np.zeros(12)
+    lib().oracle_srbd_f(C.byref(SrbdParams.from_dict(params)), _c(x), _c(u), _c(feet), _c(contact, np.uint8), out)
+    return out
+
+
+def srbd_h(params: dict, x, u, feet, contact):
+    out = np.zeros(12)
+    lib().oracle_srbd_h(C.byref(SrbdParams.from_dict(params)), _c(x), _c(u), _c(feet), _c(contact, np.uint8), out)
+    return out
+
+
+def srbd_jac(params: dict, x, u, feet, contact):
+    Fx = np.zeros((12, 12)); Fu = np.zeros((12, 12))
+    lib().oracle_srbd_jac(C.byref(SrbdParams.from_dict(params)), _c(x), _c(u), _c(feet),
+                          _c(contact, np.uint8), Fx, Fu)
+    return Fx, Fu
+
+
+def barrier(xi, mu, delta):
+    return lib().oracle_barrier(float(xi), float(mu), float(delta))
+
+
+def barrier_d1(xi, mu, delta):
+    return lib().oracle_barrier_d1(float(xi), float(mu), float(delta))
+
+
+def barrier_d2(xi, mu, delta):
+    return lib().oracle_barrier_d2(float(xi), float(mu), float(delta))
+
+
+def _uref(prob, b=None):
+    u = prob.get("u_ref")
+    if u is None:
+        u = np.zeros_like(prob["u"])
+    return _c(u if b is None else u[b])
+
+
+def srbd_linearize(prob: dict, nthreads: int | None = None):
+    """Batched linearisation of an SRBD problem dict (workloads.synth.srbd_problem layout)."""
+    x = _c(prob["x"]); Bn, N2, n = x.shape
+    N = N2 - 2
+    m = 12
+    out = {"A": np.zeros((Bn, N + 1, n, n)), "Bm": np.zeros((Bn, N + 1, n, m)), "c": np.zeros((Bn, N + 1, n)),
+           "Q": np.zeros((Bn, N + 1, n, n)), "R": np.zeros((Bn, N + 1, m, m)), "S": np.zeros((Bn, N + 1, m, n)),
+           "q": np.zeros((Bn, N + 1, n)), "r": np.zeros((Bn, N + 1, m)), "P_term": np.zeros((Bn, n, n)),
+           "p_term": np.zeros((Bn, n)), "dx0": np.zeros((Bn, n))}
+    info = np.zeros(Bn, np.int32)
+    lib().oracle_srbd_linearize_batch(
+        C.byref(SrbdParams.from_dict(prob["params"])), Bn, N, x, _c(prob["u"]), _c(prob["lam"]),
+        _c(prob["x0"]), _c(prob["x_ref"]), _uref(prob), _c(prob["contact"], np.uint8), _c(prob["feet"]),
+        out["A"], out["Bm"], out["c"], out["Q"], out["R"], out["S"], out["q"], out["r"],
+        out["P_term"], out["p_term"], out["dx0"], info, nthreads or max_threads())
+    out["info"] = info
+    return out
+
+
+def srbd_cost(prob, b, x=None, u=None):
+    x = prob["x"][b] if x is None else x
+    u = prob["u"][b] if u is None else u
+    N = x.shape[0] - 2
+    return lib().oracle_srbd_cost(C.byref(SrbdParams.from_dict(prob["params"])), N, _c(x), _c(u),
+                                  _c(prob["x_ref"][b]), _uref(prob, b), _c(prob["contact"][b], np.uint8))
+
+
+def srbd_theta(prob, b, x=None, u=None):
+    x = prob["x"][b] if x is None else x
+    u = prob["u"][b] if u is None else u
+    N = x.shape[0] - 2
+    return lib().oracle_srbd_theta(C.byref(SrbdParams.from_dict(prob["params"])), N, _c(x), _c(u),
+                                   _c(prob["x0"][b]), _c(prob["contact"][b], np.uint8), _c(prob["feet"][b]))
+
+
+def srbd_line_search(prob, b, dx, du, n_alpha=10, c1=1e-4, theta_max=None):
+    """Returns (j, J[n_alpha], theta[n_alpha], (J0, theta0, slope))."""
+    x = prob["x"][b]
+    N = x.shape[0] - 2
+    tm = 1e-2 * (N + 1) if theta_max is None else theta_max
+    Ja = np.zeros(n_alpha); tha = np.zeros(n_alpha); base = np.zeros(3)
+    j = lib().oracle_srbd_line_search(C.byref(SrbdParams.from_dict(prob["params"])), N, n_alpha, c1, tm,
+                                      _c(x), _c(prob["u"][b]), _c(prob["x0"][b]), _c(prob["x_ref"][b]),
+                                      _uref(prob, b), _c(prob["contact"][b], np.uint8), _c(prob["feet"][b]),
+                                      _c(dx), _c(du), Ja, tha, base)
+    return j, Ja, tha, base
+
+
+def srbd_step_single(prob, b, n_alpha=10, c1=1e-4, theta_max=0.0):
+    """One SQP iteration of instance b; returns (x, u, lam, stats[5], dx, du, dlam) (copies)."""
+    x = _c(prob["x"][b]).copy(); u = _c(prob["u"][b]).copy(); lam = _c(prob["lam"][b]).copy()
+    N = x.shape[0] - 2
+    st = np.zeros(5)
+    dx = np.zeros((N + 2, 12)); du = np.zeros((N + 1, 12)); dl = np.zeros((N + 2, 12))
+    lib().oracle_srbd_step(C.byref(SrbdParams.from_dict(prob["params"])), N, n_alpha, c1, theta_max,
+                           x, u, lam, _c(prob["x0"][b]), _c(prob["x_ref"][b]), _uref(prob, b),
+                           _c(prob["contact"][b], np.uint8), _c(prob["feet"][b]), st, dx, du, dl)
+    return x, u, lam, st, dx, du, dl
+
+
+def srbd_step(prob: dict, n_alpha=10, c1=1e-4, theta_max=0.0, nthreads: int | None = None):
+    """Batched SRBD step, in place on prob['x'], prob['u'], prob['lam'] (must be float64
+    C-contiguous).  Returns stats[B][5] = (cost, theta, alpha, accepted, info)."""
+    x = prob["x"]; Bn, N2, _ = x.shape
+    N = N2 - 2
+    for k in ("x", "u", "lam"):
+        assert prob[k].dtype == np.float64 and prob[k].flags.c_contiguous
+    st = np.zeros((Bn, 5))
+    lib().oracle_srbd_step_batch(C.byref(SrbdParams.from_dict(prob["params"])), Bn, N, n_alpha, c1,
+                                 theta_max, prob["x"], prob["u"], prob["lam"], _c(prob["x0"]),
+                                 _c(prob["x_ref"]), _uref(prob), _c(prob["contact"], np.uint8),
+                                 _c(prob["feet"]), st, nthreads or max_threads())
+    return st

@@ -1,0 +1,762 @@
+/*
+ * oracle/pdilqr_oracle.c -- plain fp64 CPU oracle for the Primal-Dual iLQR hot path
+ * (arXiv 2506.07823, /root/reference/PAPER.md; cited as P:<line>).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing in the product path may load this file.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs call it.  It shares no code, header, table or helper with the CUDA path
+ * (paper_2506_07823_b200/csrc); the two are written independently from the paper.
+ *
+ * What it computes, and how:
+ *  - LQ/KKT subproblem (Eq. 4): the unique KKT solution, obtained by the
+ *    sequential Riccati recursion (Eq. 5), the forward pass (Eq. 6)
+ *    and the dual update (Eq. 7).  No scan, no blocking, no reordering.
+ *  - SRBD model with ZYX Euler angles (n=12, reading R13),
+ *    explicit Euler discretisation (reading R14), analytic Jacobians.
+ *  - Gauss-Newton cost + relaxed barriers, Lagrangian gradients q,r.
+ *  - Filter line search on the fixed grid alpha in {2^0..2^-9}, linear
+ *    update (Eq. 16), constraint violation theta (Eq. 17, reading R9).
+ *
+ * Parity pins for every function live in tests/test_oracle_*.py.
+ *
+ * Array conventions (one instance, row-major, fp64):
+ *   A[N+1][n][n] Bm[N+1][n][m] c[N+1][n] Q[N+1][n][n] R[N+1][m][m] S[N+1][m][n]
+ *   q[N+1][n] r[N+1][m] Pt[n][n] pt[n] dx0[n]
+ *   K[N+1][m][n] k[N+1][m] P[N+2][n][n] p[N+2][n]
+ *   dx[N+2][n] du[N+1][m] dlam[N+2][n]
+ */
+#include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define IDX2(i, j, ld) ((size_t)(i) * (size_t)(ld) + (size_t)(j))
+
+/* ------------------------------------------------------------------------- */
+/* small dense helpers (plain loops)                                         */
+/* ------------------------------------------------------------------------- */
+
+/* Cholesky G = L L^T in place (lower triangle).  Returns 0 on success, 1 if G is
+ * not (numerically) positive definite. */
+static int chol(int m, double *G) {
+    for (int j = 0; j < m; ++j) {
+        double d = G[IDX2(j, j, m)];
+        for (int k = 0; k < j; ++k) d -= G[IDX2(j, k, m)] * G[IDX2(j, k, m)];
+        if (!(d > 0.0)) return 1;
+        d = sqrt(d);
+        G[IDX2(j, j, m)] = d;
+        for (int i = j + 1; i < m; ++i) {
+            double s = G[IDX2(i, j, m)];
+            for (int k = 0; k < j; ++k) s -= G[IDX2(i, k, m)] * G[IDX2(j, k, m)];
+            G[IDX2(i, j, m)] = s / d;
+        }
+    }
+    return 0;
+}
+
+/* Solve (L L^T) X = Y for X in place; Y is m x ncol row-major. */
+static void chol_solve(int m, const double *L, int ncol, double *Y) {
+    for (int c = 0; c < ncol; ++c) {
+        for (int i = 0; i < m; ++i) { /* forward: L z = y */
+            double s = Y[IDX2(i, c, ncol)];
+            for (int k = 0; k < i; ++k) s -= L[IDX2(i, k, m)] * Y[IDX2(k, c, ncol)];
+            Y[IDX2(i, c, ncol)] = s / L[IDX2(i, i, m)];
+        }
+        for (int i = m - 1; i >= 0; --i) { /* backward: L^T x = z */
+            double s = Y[IDX2(i, c, ncol)];
+            for (int k = i + 1; k < m; ++k) s -= L[IDX2(k, i, m)] * Y[IDX2(k, c, ncol)];
+            Y[IDX2(i, c, ncol)] = s / L[IDX2(i, i, m)];
+        }
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* LQ subproblem: Riccati (Eq. 5), rollout (Eq. 6), dual update (Eq. 7)     */
+/* ------------------------------------------------------------------------- */
+
+/* Eq. 5, for i = N..0, starting from P_{N+1} = Pt, p_{N+1} = pt:
+ *   G = R + B^T P' B,  H = S + B^T P' A,  h = B^T (p' + P' b) + r,
+ *   K = -G^{-1} H,     k = -G^{-1} h,
+ *   P = Q + A^T P' A + K^T H,   p = q + A^T (p' + P' b) + K^T h.
+ * Returns 0, or 1 + i if G_i is not positive definite (SPEC S:45 names the node). */
+int oracle_riccati(int N, int n, int m,
+                   const double *A, const double *Bm, const double *c,
+                   const double *Q, const double *R, const double *S,
+                   const double *q, const double *r,
+                   const double *Pt, const double *pt,
+                   double *K, double *k, double *P, double *p) {
+    const size_t nn = (size_t)n * n, nm = (size_t)n * m, mm = (size_t)m * m;
+    double *PB = malloc(sizeof(double) * nm);      /* P' B      (n x m) */
+    double *PA = malloc(sizeof(double) * nn);      /* P' A      (n x n) */
+    double *G = malloc(sizeof(double) * mm);
+    double *Y = malloc(sizeof(double) * (size_t)m * (n + 1)); /* [H | h] -> G^-1 [H | h] */
+    double *Hh = malloc(sizeof(double) * (size_t)m * (n + 1)); /* copy of [H | h] */
+    double *w = malloc(sizeof(double) * n);        /* p' + P' b */
+    int status = 0;
+
+    memcpy(P + (size_t)(N + 1) * nn, Pt, sizeof(double) * nn);
+    memcpy(p + (size_t)(N + 1) * n, pt, sizeof(double) * n);
+
+    for (int i = N; i >= 0; --i) {
+        const double *Ai = A + (size_t)i * nn, *Bi = Bm + (size_t)i * nm, *bi = c + (size_t)i * n;
+        const double *Qi = Q + (size_t)i * nn, *Ri = R + (size_t)i * mm, *Si = S + (size_t)i * nm;
+        const double *qi = q + (size_t)i * n, *ri = r + (size_t)i * m;
+        const double *Pn = P + (size_t)(i + 1) * nn, *pn = p + (size_t)(i + 1) * n;
+        double *Pi = P + (size_t)i * nn, *pi = p + (size_t)i * n;
+        double *Ki = K + (size_t)i * nm, *ki = k + (size_t)i * m;
+
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < m; ++b) {
+                double s = 0;
+                for (int t = 0; t < n; ++t) s += Pn[IDX2(a, t, n)] * Bi[IDX2(t, b, m)];
+                PB[IDX2(a, b, m)] = s;
+            }
+        for (int a = 0; a < n; ++a)
+            for (int b = 0; b < n; ++b) {
+                double s = 0;
+                for (int t = 0; t < n; ++t) s += Pn[IDX2(a, t, n)] * Ai[IDX2(t, b, n)];
+                PA[IDX2(a, b, n)] = s;
+            }
+        for (int a = 0; a < n; ++a) {
+            double s = pn[a];
+            for (int t = 0; t < n; ++t) s += Pn[IDX2(a, t, n)] * bi[t];
+            w[a] = s;
+        }
+        /* G = R + B^T P' B */
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) {
+                double s = Ri[IDX2(a, b, m)];
+                for (int t = 0; t < n; ++t) s += Bi[IDX2(t, a, m)] * PB[IDX2(t, b, m)];
+                G[IDX2(a, b, m)] = s;
+            }
+        /* H = S + B^T P' A  -> Y[:, 0:n];  h = B^T w + r -> Y[:, n] */
+        for (int a = 0; a < m; ++a) {
+            for (int b = 0; b < n; ++b) {
+                double s = Si[IDX2(a, b, n)];
+                for (int t = 0; t < n; ++t) s += Bi[IDX2(t, a, m)] * PA[IDX2(t, b, n)];
+                Y[IDX2(a, b, n + 1)] = s;
+            }
+            double s = ri[a];
+            for (int t = 0; t < n; ++t) s += Bi[IDX2(t, a, m)] * w[t];
+            Y[IDX2(a, n, n + 1)] = s;
+        }
+        /* P_i = Q + A^T P' A + K^T H, p_i = q + A^T w + K^T h */
+        memcpy(Hh, Y, sizeof(double) * (size_t)m * (n + 1));
+        if (chol(m, G)) { status = 1 + i; break; }
+        chol_solve(m, G, n + 1, Y); /* Y = G^{-1} [H | h] */
+        for (int a = 0; a < m; ++a) {
+            for (int b = 0; b < n; ++b) Ki[IDX2(a, b, n)] = -Y[IDX2(a, b, n + 1)];
+            ki[a] = -Y[IDX2(a, n, n + 1)];
+        }
+        for (int a = 0; a < n; ++a) {
+            for (int b = 0; b < n; ++b) {
+                double s = Qi[IDX2(a, b, n)];
+                for (int t = 0; t < n; ++t) s += Ai[IDX2(t, a, n)] * PA[IDX2(t, b, n)];
+                for (int t = 0; t < m; ++t) s += Ki[IDX2(t, a, n)] * Hh[IDX2(t, b, n + 1)];
+                Pi[IDX2(a, b, n)] = s;
+            }
+            double s = qi[a];
+            for (int t = 0; t < n; ++t) s += Ai[IDX2(t, a, n)] * w[t];
+            for (int t = 0; t < m; ++t) s += Ki[IDX2(t, a, n)] * Hh[IDX2(t, n, n + 1)];
+            pi[a] = s;
+        }
+    }
+    free(PB); free(PA); free(G); free(Y); free(Hh); free(w);
+    return status;
+}
+
+/* Eq. 6: du_i = K_i dx_i + k_i ; dx_{i+1} = A_i dx_i + B_i du_i + b_i,
+ * dx_0 = xhat_0 - x_0.  Eq. 7: dlam_i = P_i dx_i + p_i, i=0..N+1. */
+void oracle_rollout_dual(int N, int n, int m,
+                         const double *A, const double *Bm, const double *c,
+                         const double *K, const double *k,
+                         const double *P, const double *p, const double *dx0,
+                         double *dx, double *du, double *dlam) {
+    const size_t nn = (size_t)n * n, nm = (size_t)n * m;
+    memcpy(dx, dx0, sizeof(double) * n);
+    for (int i = 0; i <= N; ++i) {
+        const double *xi = dx + (size_t)i * n;
+        double *ui = du + (size_t)i * m;
+        double *xn = dx + (size_t)(i + 1) * n;
+        for (int a = 0; a < m; ++a) {
+            double s = k[(size_t)i * m + a];
+            for (int t = 0; t < n; ++t) s += K[(size_t)i * nm + IDX2(a, t, n)] * xi[t];
+            ui[a] = s;
+        }
+        for (int a = 0; a < n; ++a) {
+            double s = c[(size_t)i * n + a];
+            for (int t = 0; t < n; ++t) s += A[(size_t)i * nn + IDX2(a, t, n)] * xi[t];
+            for (int t = 0; t < m; ++t) s += Bm[(size_t)i * nm + IDX2(a, t, m)] * ui[t];
+            xn[a] = s;
+        }
+    }
+    for (int i = 0; i <= N + 1; ++i)
+        for (int a = 0; a < n; ++a) {
+            double s = p[(size_t)i * n + a];
+            for (int t = 0; t < n; ++t) s += P[(size_t)i * nn + IDX2(a, t, n)] * dx[(size_t)i * n + t];
+            dlam[(size_t)i * n + a] = s;
+        }
+}
+
+/* The whole LQ solve for one instance.  K,k,P,p may be NULL (then scratch is used). */
+int oracle_solve_lq(int N, int n, int m,
+                    const double *A, const double *Bm, const double *c,
+                    const double *Q, const double *R, const double *S,
+                    const double *q, const double *r,
+                    const double *Pt, const double *pt, const double *dx0,
+                    double *dx, double *du, double *dlam,
+                    double *K, double *k, double *P, double *p) {
+    const size_t nn = (size_t)n * n, nm = (size_t)n * m;
+    double *Kw = K ? K : malloc(sizeof(double) * (N + 1) * nm);
+    double *kw = k ? k : malloc(sizeof(double) * (N + 1) * m);
+    double *Pw = P ? P : malloc(sizeof(double) * (N + 2) * nn);
+    double *pw = p ? p : malloc(sizeof(double) * (N + 2) * n);
+    int st = oracle_riccati(N, n, m, A, Bm, c, Q, R, S, q, r, Pt, pt, Kw, kw, Pw, pw);
+    if (st == 0) oracle_rollout_dual(N, n, m, A, Bm, c, Kw, kw, Pw, pw, dx0, dx, du, dlam);
+    if (!K) free(Kw);
+    if (!k) free(kw);
+    if (!P) free(Pw);
+    if (!p) free(pw);
+    return st;
+}
+
+/* Batched LQ solve over B independent instances (batch-outermost arrays). */
+void oracle_solve_lq_batch(int Bn, int N, int n, int m,
+                           const double *A, const double *Bm, const double *c,
+                           const double *Q, const double *R, const double *S,
+                           const double *q, const double *r,
+                           const double *Pt, const double *pt, const double *dx0,
+                           double *dx, double *du, double *dlam, int32_t *info, int nthreads) {
+    const size_t nn = (size_t)n * n, nm = (size_t)n * m, mm = (size_t)m * m;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int b = 0; b < Bn; ++b) {
+        const size_t S1 = (size_t)(N + 1);
+        info[b] = oracle_solve_lq(N, n, m, A + b * S1 * nn, Bm + b * S1 * nm, c + b * S1 * n,
+                                  Q + b * S1 * nn, R + b * S1 * mm, S + b * S1 * nm,
+                                  q + b * S1 * n, r + b * S1 * m, Pt + b * nn, pt + b * n,
+                                  dx0 + b * (size_t)n, dx + b * (S1 + 1) * n, du + b * S1 * m,
+                                  dlam + b * (S1 + 1) * n, NULL, NULL, NULL, NULL);
+    }
+}
+
+/* ------------------------------------------------------------------------- */
+/* SRBD model, ZYX Euler angles (reading R13), explicit Euler    */
+/* ------------------------------------------------------------------------- */
+/* state x = [p(3) world position, Theta(3) = (roll, pitch, yaw), v(3) world velocity,
+ *            w(3) body angular velocity];  input u = [f_0 .. f_3] world-frame GRFs.    */
+
+typedef struct {
+    double dt, mass, inertia[9], gravity[3];
+    double w_x[12], w_x_term[12], w_u_stance, w_u_swing;
+    double mu_friction, f_min, f_max, barrier_mu, barrier_delta;
+} oracle_srbd_params;
+
+#define NX 12
+#define NU 12
+#define NFEET 4
+#define PITCH_GUARD (M_PI / 2.0 - 0.1)
+
+static void mat3_mul(const double *X, const double *Y, double *Z) {
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            double s = 0;
+            for (int t = 0; t < 3; ++t) s += X[3 * i + t] * Y[3 * t + j];
+            Z[3 * i + j] = s;
+        }
+}
+
+/* inverse of a 3x3 matrix by the adjugate formula */
+static void mat3_inv(const double *M, double *Mi) {
+    double a = M[0], b = M[1], c = M[2], d = M[3], e = M[4], f = M[5], g = M[6], h = M[7], i = M[8];
+    double det = a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g);
+    Mi[0] = (e * i - f * h) / det; Mi[1] = (c * h - b * i) / det; Mi[2] = (b * f - c * e) / det;
+    Mi[3] = (f * g - d * i) / det; Mi[4] = (a * i - c * g) / det; Mi[5] = (c * d - a * f) / det;
+    Mi[6] = (d * h - e * g) / det; Mi[7] = (b * g - a * h) / det; Mi[8] = (a * e - b * d) / det;
+}
+
+/* R(Theta) = Rz(yaw) Ry(pitch) Rx(roll) and its three partial derivatives. */
+static void rot_zyx(const double *th, double *R, double *dR /* [3][9] or NULL */) {
+    double cr = cos(th[0]), sr = sin(th[0]), cp = cos(th[1]), sp = sin(th[1]);
+    double cy = cos(th[2]), sy = sin(th[2]);
+    double Rx[9] = {1, 0, 0, 0, cr, -sr, 0, sr, cr};
+    double Ry[9] = {cp, 0, sp, 0, 1, 0, -sp, 0, cp};
+    double Rz[9] = {cy, -sy, 0, sy, cy, 0, 0, 0, 1};
+    double T[9];
+    mat3_mul(Ry, Rx, T);
+    mat3_mul(Rz, T, R);
+    if (dR) {
+        double dRx[9] = {0, 0, 0, 0, -sr, -cr, 0, cr, -sr};
+        double dRy[9] = {-sp, 0, cp, 0, 0, 0, -cp, 0, -sp};
+        double dRz[9] = {-sy, -cy, 0, cy, -sy, 0, 0, 0, 0};
+        mat3_mul(Ry, dRx, T); mat3_mul(Rz, T, dR + 0);
+        mat3_mul(dRy, Rx, T); mat3_mul(Rz, T, dR + 9);
+        mat3_mul(Ry, Rx, T);  mat3_mul(dRz, T, dR + 18);
+    }
+}
+
+static void cross3(const double *a, const double *b, double *c) {
+    c[0] = a[1] * b[2] - a[2] * b[1];
+    c[1] = a[2] * b[0] - a[0] * b[2];
+    c[2] = a[0] * b[1] - a[1] * b[0];
+}
+
+/* skew(a) such that skew(a) b = a x b */
+static void skew3(const double *a, double *S) {
+    S[0] = 0;     S[1] = -a[2]; S[2] = a[1];
+    S[3] = a[2];  S[4] = 0;     S[5] = -a[0];
+    S[6] = -a[1]; S[7] = a[0];  S[8] = 0;
+}
+
+/* Continuous SRBD dynamics f(x,u):
+ *   pdot = v;  Thetadot = E(Theta)^{-1} w  (ZYX);  vdot = (1/m) sum_j c_j f_j + g;
+ *   wdot = I^{-1} ( R^T sum_j c_j (r_j - p) x f_j  -  w x I w ).                      */
+void oracle_srbd_f(const oracle_srbd_params *P, const double *x, const double *u,
+                   const double *feet /*[4][3]*/, const uint8_t *contact /*[4]*/, double *xd) {
+    const double *pos = x, *th = x + 3, *v = x + 6, *w = x + 9;
+    double R[9], Ii[9];
+    rot_zyx(th, R, NULL);
+    mat3_inv(P->inertia, Ii);
+    double sr = sin(th[0]), cr = cos(th[0]), cp = cos(th[1]), tp = tan(th[1]);
+    xd[0] = v[0]; xd[1] = v[1]; xd[2] = v[2];
+    xd[3] = w[0] + sr * tp * w[1] + cr * tp * w[2];
+    xd[4] = cr * w[1] - sr * w[2];
+    xd[5] = (sr * w[1] + cr * w[2]) / cp;
+    double F[3] = {0, 0, 0}, tau_w[3] = {0, 0, 0};
+    for (int j = 0; j < NFEET; ++j) {
+        if (!contact[j]) continue;
+        const double *f = u + 3 * j;
+        double rr[3] = {feet[3 * j] - pos[0], feet[3 * j + 1] - pos[1], feet[3 * j + 2] - pos[2]};
+        double t[3];
+        cross3(rr, f, t);
+        for (int a = 0; a < 3; ++a) { F[a] += f[a]; tau_w[a] += t[a]; }
+    }
+    for (int a = 0; a < 3; ++a) xd[6 + a] = F[a] / P->mass + P->gravity[a];
+    double tau_b[3], Iw[3], wxIw[3], rhs[3];
+    for (int a = 0; a < 3; ++a) {
+        tau_b[a] = R[0 + a] * tau_w[0] + R[3 + a] * tau_w[1] + R[6 + a] * tau_w[2]; /* R^T tau */
+        Iw[a] = P->inertia[3 * a] * w[0] + P->inertia[3 * a + 1] * w[1] + P->inertia[3 * a + 2] * w[2];
+    }
+    cross3(w, Iw, wxIw);
+    for (int a = 0; a < 3; ++a) rhs[a] = tau_b[a] - wxIw[a];
+    for (int a = 0; a < 3; ++a) xd[9 + a] = Ii[3 * a] * rhs[0] + Ii[3 * a + 1] * rhs[1] + Ii[3 * a + 2] * rhs[2];
+}
+
+/* Analytic Jacobians Fx = df/dx (12x12), Fu = df/du (12x12) of the continuous dynamics. */
+void oracle_srbd_jac(const oracle_srbd_params *P, const double *x, const double *u,
+                     const double *feet, const uint8_t *contact, double *Fx, double *Fu) {
+    const double *pos = x, *th = x + 3, *w = x + 9;
+    memset(Fx, 0, sizeof(double) * NX * NX);
+    memset(Fu, 0, sizeof(double) * NX * NU);
+    double R[9], dR[27], Ii[9];
+    rot_zyx(th, R, dR);
+    mat3_inv(P->inertia, Ii);
+    double sr = sin(th[0]), cr = cos(th[0]), sp = sin(th[1]), cp = cos(th[1]), tp = tan(th[1]);
+    /* pdot = v */
+    for (int a = 0; a < 3; ++a) Fx[IDX2(a, 6 + a, NX)] = 1.0;
+    /* Thetadot = E^{-1}(roll,pitch) w */
+    Fx[IDX2(3, 3, NX)] = cr * tp * w[1] - sr * tp * w[2];
+    Fx[IDX2(3, 4, NX)] = (sr * w[1] + cr * w[2]) / (cp * cp);
+    Fx[IDX2(4, 3, NX)] = -sr * w[1] - cr * w[2];
+    Fx[IDX2(5, 3, NX)] = (cr * w[1] - sr * w[2]) / cp;
+    Fx[IDX2(5, 4, NX)] = (sr * w[1] + cr * w[2]) * sp / (cp * cp);
+    Fx[IDX2(3, 9, NX)] = 1.0; Fx[IDX2(3, 10, NX)] = sr * tp; Fx[IDX2(3, 11, NX)] = cr * tp;
+    Fx[IDX2(4, 10, NX)] = cr;  Fx[IDX2(4, 11, NX)] = -sr;
+    Fx[IDX2(5, 10, NX)] = sr / cp; Fx[IDX2(5, 11, NX)] = cr / cp;
+    /* vdot = sum c_j f_j / m + g */
+    for (int j = 0; j < NFEET; ++j)
+        if (contact[j])
+            for (int a = 0; a < 3; ++a) Fu[IDX2(6 + a, 3 * j + a, NU)] = 1.0 / P->mass;
+    /* wdot = I^{-1}(R^T tau_w - w x I w), tau_w = sum c_j (r_j - p) x f_j */
+    double tau_w[3] = {0, 0, 0}, dtau_dp[9] = {0};
+    for (int j = 0; j < NFEET; ++j) {
+        if (!contact[j]) continue;
+        const double *f = u + 3 * j;
+        double rr[3] = {feet[3 * j] - pos[0], feet[3 * j + 1] - pos[1], feet[3 * j + 2] - pos[2]};
+        double t[3], Sf[9], Sr[9];
+        cross3(rr, f, t);
+        for (int a = 0; a < 3; ++a) tau_w[a] += t[a];
+        skew3(f, Sf);                /* d[(r - p) x f]/dp = skew(f) */
+        for (int a = 0; a < 9; ++a) dtau_dp[a] += Sf[a];
+        skew3(rr, Sr);               /* d[(r - p) x f]/df = skew(r - p) */
+        double RtS[9], IiRtS[9], Rt[9];
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) Rt[3 * a + b] = R[3 * b + a];
+        mat3_mul(Rt, Sr, RtS);
+        mat3_mul(Ii, RtS, IiRtS);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) Fu[IDX2(9 + a, 3 * j + b, NU)] = IiRtS[3 * a + b];
+    }
+    double Rt[9], M1[9], M2[9];
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Rt[3 * a + b] = R[3 * b + a];
+    mat3_mul(Rt, dtau_dp, M1);
+    mat3_mul(Ii, M1, M2);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Fx[IDX2(9 + a, b, NX)] = M2[3 * a + b];
+    for (int k = 0; k < 3; ++k) { /* d(R^T tau_w)/dTheta_k = (dR/dTheta_k)^T tau_w */
+        double col[3];
+        for (int a = 0; a < 3; ++a)
+            col[a] = dR[9 * k + 0 + a] * tau_w[0] + dR[9 * k + 3 + a] * tau_w[1] + dR[9 * k + 6 + a] * tau_w[2];
+        for (int a = 0; a < 3; ++a)
+            Fx[IDX2(9 + a, 3 + k, NX)] = Ii[3 * a] * col[0] + Ii[3 * a + 1] * col[1] + Ii[3 * a + 2] * col[2];
+    }
+    /* d(-w x I w)/dw = -(skew(w) I - skew(I w)) */
+    double Iw[3], Sw[9], SIw[9], SwI[9], D[9];
+    for (int a = 0; a < 3; ++a)
+        Iw[a] = P->inertia[3 * a] * w[0] + P->inertia[3 * a + 1] * w[1] + P->inertia[3 * a + 2] * w[2];
+    skew3(w, Sw);
+    skew3(Iw, SIw);
+    mat3_mul(Sw, P->inertia, SwI);
+    for (int a = 0; a < 9; ++a) D[a] = -(SwI[a] - SIw[a]);
+    double IiD[9];
+    mat3_mul(Ii, D, IiD);
+    for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) Fx[IDX2(9 + a, 9 + b, NX)] = IiD[3 * a + b];
+}
+
+/* Explicit Euler step h(x,u) = x + dt f(x,u) (reading R14). */
+void oracle_srbd_h(const oracle_srbd_params *P, const double *x, const double *u,
+                   const double *feet, const uint8_t *contact, double *xn) {
+    double xd[NX];
+    oracle_srbd_f(P, x, u, feet, contact, xd);
+    for (int a = 0; a < NX; ++a) xn[a] = x[a] + P->dt * xd[a];
+}
+
+/* ------------------------------------------------------------------------- */
+/* relaxed barrier (sign reading R11: feasible <=> xi > 0)        */
+/* ------------------------------------------------------------------------- */
+double oracle_barrier(double xi, double mu, double delta) {
+    if (xi >= delta) return -mu * log(xi);
+    double t = (xi - 2.0 * delta) / delta;
+    return 0.5 * mu * (t * t - 1.0) - mu * log(delta);
+}
+double oracle_barrier_d1(double xi, double mu, double delta) {
+    if (xi >= delta) return -mu / xi;
+    return mu * (xi - 2.0 * delta) / (delta * delta);
+}
+double oracle_barrier_d2(double xi, double mu, double delta) {
+    if (xi >= delta) return mu / (xi * xi);
+    return mu / (delta * delta);
+}
+
+/* The six linear constraints xi_c(f) = g_c . f_j + h_c per stance foot j: friction
+ * pyramid (4) and normal-force bounds (2).  Gradient written into g[3], offset h. */
+static void foot_constraint(const oracle_srbd_params *P, int c, double *g, double *h) {
+    double mu = P->mu_friction;
+    g[0] = g[1] = g[2] = 0; *h = 0;
+    switch (c) {
+    case 0: g[0] = -1; g[2] = mu; break;         /* mu fz - fx */
+    case 1: g[0] = 1;  g[2] = mu; break;         /* mu fz + fx */
+    case 2: g[1] = -1; g[2] = mu; break;         /* mu fz - fy */
+    case 3: g[1] = 1;  g[2] = mu; break;         /* mu fz + fy */
+    case 4: g[2] = 1;  *h = -P->f_min; break;    /* fz - fmin  */
+    default: g[2] = -1; *h = P->f_max; break;    /* fmax - fz  */
+    }
+}
+
+static double u_weight(const oracle_srbd_params *P, const uint8_t *contact, int a) {
+    return contact[a / 3] ? P->w_u_stance : P->w_u_swing;
+}
+
+/* Stage cost l_i (P:290-297 NLS form + barriers on stance feet), i = 0..N. */
+static double stage_cost(const oracle_srbd_params *P, const double *x, const double *u,
+                         const double *xr, const double *ur, const uint8_t *contact) {
+    double J = 0;
+    for (int a = 0; a < NX; ++a) J += 0.5 * P->w_x[a] * (x[a] - xr[a]) * (x[a] - xr[a]);
+    for (int a = 0; a < NU; ++a) {
+        double d = u[a] - (ur ? ur[a] : 0.0);
+        J += 0.5 * u_weight(P, contact, a) * d * d;
+    }
+    for (int j = 0; j < NFEET; ++j) {
+        if (!contact[j]) continue;
+        for (int cc = 0; cc < 6; ++cc) {
+            double g[3], h;
+            foot_constraint(P, cc, g, &h);
+            double xi = g[0] * u[3 * j] + g[1] * u[3 * j + 1] + g[2] * u[3 * j + 2] + h;
+            J += oracle_barrier(xi, P->barrier_mu, P->barrier_delta);
+        }
+    }
+    return J;
+}
+
+static double term_cost(const oracle_srbd_params *P, const double *x, const double *xr) {
+    double J = 0;
+    for (int a = 0; a < NX; ++a) J += 0.5 * P->w_x_term[a] * (x[a] - xr[a]) * (x[a] - xr[a]);
+    return J;
+}
+
+static int pitch_ok(const double *x) { return fabs(x[4]) < PITCH_GUARD && isfinite(x[4]); }
+
+/* Linearise + quadraticise at the iterate (x,u,lam):
+ *   A = I + dt Fx, B = dt Fu, b_i = h(x_i,u_i) - x_{i+1};
+ *   Q = W_x, S = 0, R = W_u + sum_c B''(xi_c) grad xi_c grad xi_c^T (GN);
+ *   q_i = W_x (x_i - xref_i) + A_i^T lam_{i+1} - lam_i                 (q = grad_x L)
+ *   r_i = W_u (u_i - uref_i) + sum_c B'(xi_c) grad xi_c + B_i^T lam_{i+1}  (r = grad_u L)
+ *   P_{N+1} = W_N, p_{N+1} = W_N (x_{N+1} - xref_{N+1}) - lam_{N+1},  dx0 = xhat0 - x_0.
+ * Returns 0, or -1 if the iterate is outside the Euler-angle guard or not finite. */
+int oracle_srbd_linearize(const oracle_srbd_params *P, int N,
+                          const double *x, const double *u, const double *lam,
+                          const double *x0, const double *xref, const double *uref,
+                          const uint8_t *contact, const double *feet,
+                          double *A, double *Bm, double *c, double *Q, double *R, double *S,
+                          double *q, double *r, double *Pt, double *pt, double *dx0) {
+    for (int i = 0; i <= N + 1; ++i)
+        for (int a = 0; a < NX; ++a)
+            if (!isfinite(x[i * NX + a]) || !isfinite(lam[i * NX + a])) return -1;
+    for (int i = 0; i <= N; ++i) {
+        if (!pitch_ok(x + i * NX)) return -1;
+        for (int a = 0; a < NU; ++a)
+            if (!isfinite(u[i * NU + a])) return -1;
+    }
+    double Fx[NX * NX], Fu[NX * NU];
+    for (int i = 0; i <= N; ++i) {
+        const double *xi = x + i * NX, *ui = u + i * NU, *fi = feet + i * 12;
+        const uint8_t *ci = contact + i * 4;
+        const double *ln = lam + (i + 1) * NX, *li = lam + i * NX;
+        double *Ai = A + (size_t)i * NX * NX, *Bi = Bm + (size_t)i * NX * NU;
+        double *Qi = Q + (size_t)i * NX * NX, *Ri = R + (size_t)i * NU * NU, *Si = S + (size_t)i * NU * NX;
+        oracle_srbd_jac(P, xi, ui, fi, ci, Fx, Fu);
+        for (int a = 0; a < NX; ++a)
+            for (int b = 0; b < NX; ++b) Ai[IDX2(a, b, NX)] = (a == b ? 1.0 : 0.0) + P->dt * Fx[IDX2(a, b, NX)];
+        for (int a = 0; a < NX; ++a)
+            for (int b = 0; b < NU; ++b) Bi[IDX2(a, b, NU)] = P->dt * Fu[IDX2(a, b, NU)];
+        double xn[NX];
+        oracle_srbd_h(P, xi, ui, fi, ci, xn);
+        for (int a = 0; a < NX; ++a) c[i * NX + a] = xn[a] - x[(i + 1) * NX + a];
+        memset(Qi, 0, sizeof(double) * NX * NX);
+        memset(Ri, 0, sizeof(double) * NU * NU);
+        memset(Si, 0, sizeof(double) * NU * NX);
+        for (int a = 0; a < NX; ++a) Qi[IDX2(a, a, NX)] = P->w_x[a];
+        for (int a = 0; a < NU; ++a) Ri[IDX2(a, a, NU)] = u_weight(P, ci, a);
+        double rg[NU];
+        for (int a = 0; a < NU; ++a) rg[a] = u_weight(P, ci, a) * (ui[a] - (uref ? uref[i * NU + a] : 0.0));
+        for (int j = 0; j < NFEET; ++j) {
+            if (!ci[j]) continue;
+            for (int cc = 0; cc < 6; ++cc) {
+                double g[3], h;
+                foot_constraint(P, cc, g, &h);
+                double xi_c = g[0] * ui[3 * j] + g[1] * ui[3 * j + 1] + g[2] * ui[3 * j + 2] + h;
+                double d1 = oracle_barrier_d1(xi_c, P->barrier_mu, P->barrier_delta);
+                double d2 = oracle_barrier_d2(xi_c, P->barrier_mu, P->barrier_delta);
+                for (int a = 0; a < 3; ++a) {
+                    rg[3 * j + a] += d1 * g[a];
+                    for (int b = 0; b < 3; ++b) Ri[IDX2(3 * j + a, 3 * j + b, NU)] += d2 * g[a] * g[b];
+                }
+            }
+        }
+        for (int a = 0; a < NX; ++a) {
+            double s = P->w_x[a] * (xi[a] - xref[i * NX + a]) - li[a];
+            for (int t = 0; t < NX; ++t) s += Ai[IDX2(t, a, NX)] * ln[t];
+            q[i * NX + a] = s;
+        }
+        for (int a = 0; a < NU; ++a) {
+            double s = rg[a];
+            for (int t = 0; t < NX; ++t) s += Bi[IDX2(t, a, NU)] * ln[t];
+            r[i * NU + a] = s;
+        }
+    }
+    memset(Pt, 0, sizeof(double) * NX * NX);
+    for (int a = 0; a < NX; ++a) {
+        Pt[IDX2(a, a, NX)] = P->w_x_term[a];
+        pt[a] = P->w_x_term[a] * (x[(N + 1) * NX + a] - xref[(N + 1) * NX + a]) - lam[(N + 1) * NX + a];
+        dx0[a] = x0[a] - x[a];
+    }
+    return 0;
+}
+
+/* Total cost J(x,u) = sum_{i=0}^{N} l_i + l_{N+1} (Eq. 1 objective), barriers included. */
+double oracle_srbd_cost(const oracle_srbd_params *P, int N, const double *x, const double *u,
+                        const double *xref, const double *uref, const uint8_t *contact) {
+    double J = 0;
+    for (int i = 0; i <= N; ++i)
+        J += stage_cost(P, x + i * NX, u + i * NU, xref + i * NX, uref ? uref + i * NU : NULL, contact + i * 4);
+    return J + term_cost(P, x + (N + 1) * NX, xref + (N + 1) * NX);
+}
+
+/* theta = sum_{i=0}^{N} ||x_{i+1} - h(x_i,u_i)||_2 + ||xhat0 - x_0||_2 (Eq. 17, reading R9). */
+double oracle_srbd_theta(const oracle_srbd_params *P, int N, const double *x, const double *u,
+                         const double *x0, const uint8_t *contact, const double *feet) {
+    double th = 0, d0 = 0;
+    for (int a = 0; a < NX; ++a) d0 += (x0[a] - x[a]) * (x0[a] - x[a]);
+    th += sqrt(d0);
+    for (int i = 0; i <= N; ++i) {
+        double xn[NX], s = 0;
+        oracle_srbd_h(P, x + i * NX, u + i * NU, feet + i * 12, contact + i * 4, xn);
+        for (int a = 0; a < NX; ++a) {
+            double d = x[(i + 1) * NX + a] - xn[a];
+            s += d * d;
+        }
+        th += sqrt(s);
+    }
+    return th;
+}
+
+/* Directional derivative of the cost, grad J(x,u) . (dx,du) (descent test, reading R10). */
+double oracle_srbd_cost_slope(const oracle_srbd_params *P, int N, const double *x, const double *u,
+                              const double *xref, const double *uref, const uint8_t *contact,
+                              const double *dx, const double *du) {
+    double g = 0;
+    for (int i = 0; i <= N; ++i) {
+        const double *xi = x + i * NX, *ui = u + i * NU;
+        const uint8_t *ci = contact + i * 4;
+        for (int a = 0; a < NX; ++a) g += P->w_x[a] * (xi[a] - xref[i * NX + a]) * dx[i * NX + a];
+        for (int a = 0; a < NU; ++a)
+            g += u_weight(P, ci, a) * (ui[a] - (uref ? uref[i * NU + a] : 0.0)) * du[i * NU + a];
+        for (int j = 0; j < NFEET; ++j) {
+            if (!ci[j]) continue;
+            for (int cc = 0; cc < 6; ++cc) {
+                double gg[3], h;
+                foot_constraint(P, cc, gg, &h);
+                double xi_c = gg[0] * ui[3 * j] + gg[1] * ui[3 * j + 1] + gg[2] * ui[3 * j + 2] + h;
+                double d1 = oracle_barrier_d1(xi_c, P->barrier_mu, P->barrier_delta);
+                g += d1 * (gg[0] * du[i * NU + 3 * j] + gg[1] * du[i * NU + 3 * j + 1] + gg[2] * du[i * NU + 3 * j + 2]);
+            }
+        }
+    }
+    for (int a = 0; a < NX; ++a)
+        g += P->w_x_term[a] * (x[(N + 1) * NX + a] - xref[(N + 1) * NX + a]) * dx[(N + 1) * NX + a];
+    return g;
+}
+
+/* Filter acceptance (constants reading R10).  Returns 1 if accepted.
+ *  theta0 > theta_max : "reject the step if it further increases theta"  -> accept iff tha <= th0
+ *  else, descent (g<0): Armijo  J(a) <= J0 + c1 a g
+ *  else               : "at least the cost or theta is decreased"  -> J(a) < J0 or tha < th0 */
+static int filter_accept(double J0, double th0, double g, double Ja, double tha,
+                         double alpha, double c1, double theta_max) {
+    if (!(isfinite(Ja) && isfinite(tha))) return 0;
+    if (th0 > theta_max) return tha <= th0;
+    if (g < 0) return Ja <= J0 + c1 * alpha * g;
+    return (Ja < J0) || (tha < th0);
+}
+
+/* Parallel-grid filter line search and the linear update (Eq. 16).
+ * Writes per-alpha J and theta into Jal/thal if non-NULL (n_alpha entries) and the
+ * baseline (J0, theta0, slope) into base[3] if non-NULL.  Returns the index j of the
+ * accepted alpha = 2^-j, or -1 if every trial was rejected (alpha = 0, no step). */
+int oracle_srbd_line_search(const oracle_srbd_params *P, int N, int n_alpha, double c1, double theta_max,
+                            const double *x, const double *u, const double *x0,
+                            const double *xref, const double *uref,
+                            const uint8_t *contact, const double *feet,
+                            const double *dx, const double *du,
+                            double *Jal, double *thal, double *base) {
+    double J0 = oracle_srbd_cost(P, N, x, u, xref, uref, contact);
+    double th0 = oracle_srbd_theta(P, N, x, u, x0, contact, feet);
+    double g = oracle_srbd_cost_slope(P, N, x, u, xref, uref, contact, dx, du);
+    if (base) { base[0] = J0; base[1] = th0; base[2] = g; }
+    double *xa = malloc(sizeof(double) * (N + 2) * NX), *ua = malloc(sizeof(double) * (N + 1) * NU);
+    int best = -1;
+    for (int j = 0; j < n_alpha; ++j) {
+        double alpha = ldexp(1.0, -j);
+        int ok = 1;
+        for (int t = 0; t < (N + 2) * NX; ++t) xa[t] = x[t] + alpha * dx[t];
+        for (int t = 0; t < (N + 1) * NU; ++t) ua[t] = u[t] + alpha * du[t];
+        for (int i = 0; i <= N; ++i) ok &= pitch_ok(xa + i * NX);
+        double Ja = ok ? oracle_srbd_cost(P, N, xa, ua, xref, uref, contact) : INFINITY;
+        double tha = ok ? oracle_srbd_theta(P, N, xa, ua, x0, contact, feet) : INFINITY;
+        if (Jal) Jal[j] = Ja;
+        if (thal) thal[j] = tha;
+        if (best < 0 && filter_accept(J0, th0, g, Ja, tha, alpha, c1, theta_max)) best = j;
+    }
+    free(xa); free(ua);
+    return best;
+}
+
+/* One SQP/RTI iteration (one iteration per control tick): linearise -> LQ solve
+ * (Riccati) -> dual update -> filter line search -> update x,u,lam in place (Eq. 16).
+ * stats[5] = {cost, theta, alpha, accepted, info}.  dirs (dx,du,dlam) optional out. */
+int oracle_srbd_step(const oracle_srbd_params *P, int N, int n_alpha, double c1, double theta_max,
+                     double *x, double *u, double *lam, const double *x0,
+                     const double *xref, const double *uref,
+                     const uint8_t *contact, const double *feet,
+                     double *stats, double *dx_out, double *du_out, double *dlam_out) {
+    const int n = NX, m = NU;
+    const size_t S1 = (size_t)(N + 1);
+    double *A = malloc(sizeof(double) * S1 * n * n), *Bm = malloc(sizeof(double) * S1 * n * m);
+    double *c = malloc(sizeof(double) * S1 * n), *Q = malloc(sizeof(double) * S1 * n * n);
+    double *R = malloc(sizeof(double) * S1 * m * m), *S = malloc(sizeof(double) * S1 * m * n);
+    double *q = malloc(sizeof(double) * S1 * n), *r = malloc(sizeof(double) * S1 * m);
+    double Pt[NX * NX], pt[NX], d0[NX];
+    double *dx = malloc(sizeof(double) * (S1 + 1) * n), *du = malloc(sizeof(double) * S1 * m);
+    double *dl = malloc(sizeof(double) * (S1 + 1) * n);
+    double theta_thr = theta_max > 0 ? theta_max : 1e-2 * (N + 1);
+    int info = oracle_srbd_linearize(P, N, x, u, lam, x0, xref, uref, contact, feet,
+                                     A, Bm, c, Q, R, S, q, r, Pt, pt, d0);
+    if (info == 0) info = oracle_solve_lq(N, n, m, A, Bm, c, Q, R, S, q, r, Pt, pt, d0, dx, du, dl,
+                                          NULL, NULL, NULL, NULL);
+    if (info == 0) {
+        for (size_t t = 0; t < (S1 + 1) * n; ++t)
+            if (!isfinite(dx[t]) || !isfinite(dl[t])) info = -1;
+        for (size_t t = 0; t < S1 * m; ++t)
+            if (!isfinite(du[t])) info = -1;
+    }
+    double J0 = oracle_srbd_cost(P, N, x, u, xref, uref, contact);
+    double th0 = oracle_srbd_theta(P, N, x, u, x0, contact, feet);
+    double alpha = 0, Jn = J0, thn = th0;
+    int accepted = 0;
+    if (info == 0) {
+        double Jal[32], thal[32];
+        int na = n_alpha > 32 ? 32 : n_alpha;
+        int j = oracle_srbd_line_search(P, N, na, c1, theta_thr, x, u, x0, xref, uref, contact, feet,
+                                        dx, du, Jal, thal, NULL);
+        if (j >= 0) {
+            alpha = ldexp(1.0, -j);
+            accepted = 1;
+            Jn = Jal[j];
+            thn = thal[j];
+            for (size_t t = 0; t < (S1 + 1) * n; ++t) { x[t] += alpha * dx[t]; lam[t] += alpha * dl[t]; }
+            for (size_t t = 0; t < S1 * m; ++t) u[t] += alpha * du[t];
+        }
+    }
+    if (stats) { stats[0] = Jn; stats[1] = thn; stats[2] = alpha; stats[3] = accepted; stats[4] = info; }
+    if (dx_out) memcpy(dx_out, dx, sizeof(double) * (S1 + 1) * n);
+    if (du_out) memcpy(du_out, du, sizeof(double) * S1 * m);
+    if (dlam_out) memcpy(dlam_out, dl, sizeof(double) * (S1 + 1) * n);
+    free(A); free(Bm); free(c); free(Q); free(R); free(S); free(q); free(r);
+    free(dx); free(du); free(dl);
+    return info;
+}
+
+/* Batched SRBD step over B instances (batch-outermost arrays), OpenMP over instances. */
+void oracle_srbd_step_batch(const oracle_srbd_params *P, int Bn, int N, int n_alpha, double c1,
+                            double theta_max, double *x, double *u, double *lam, const double *x0,
+                            const double *xref, const double *uref, const uint8_t *contact,
+                            const double *feet, double *stats, int nthreads) {
+    const size_t S1 = (size_t)(N + 1);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int b = 0; b < Bn; ++b)
+        oracle_srbd_step(P, N, n_alpha, c1, theta_max, x + b * (S1 + 1) * NX, u + b * S1 * NU,
+                         lam + b * (S1 + 1) * NX, x0 + (size_t)b * NX, xref + b * (S1 + 1) * NX,
+                         uref ? uref + b * S1 * NU : NULL, contact + b * S1 * 4, feet + b * S1 * 12,
+                         stats + (size_t)b * 5, NULL, NULL, NULL);
+}
+
+/* Batched linearisation (used by parity tests of pdilqr_linearize). */
+void oracle_srbd_linearize_batch(const oracle_srbd_params *P, int Bn, int N,
+                                 const double *x, const double *u, const double *lam,
+                                 const double *x0, const double *xref, const double *uref,
+                                 const uint8_t *contact, const double *feet,
+                                 double *A, double *Bm, double *c, double *Q, double *R, double *S,
+                                 double *q, double *r, double *Pt, double *pt, double *dx0,
+                                 int32_t *info, int nthreads) {
+    const size_t S1 = (size_t)(N + 1);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int b = 0; b < Bn; ++b)
+        info[b] = oracle_srbd_linearize(
+            P, N, x + b * (S1 + 1) * NX, u + b * S1 * NU, lam + b * (S1 + 1) * NX, x0 + (size_t)b * NX,
+            xref + b * (S1 + 1) * NX, uref ? uref + b * S1 * NU : NULL, contact + b * S1 * 4,
+            feet + b * S1 * 12, A + b * S1 * NX * NX, Bm + b * S1 * NX * NU, c + b * S1 * NX,
+            Q + b * S1 * NX * NX, R + b * S1 * NU * NU, S + b * S1 * NU * NX, q + b * S1 * NX,
+            r + b * S1 * NU, Pt + (size_t)b * NX * NX, pt + (size_t)b * NX, dx0 + (size_t)b * NX);
+}
+
+int oracle_max_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}

@@ -1,0 +1,174 @@
+/*
+ * include/pdilqr.h -- C ABI of libpdilqr.so, the B200 (sm_100a) implementation of the
+ * data-parallel hot path of Primal-Dual iLQR (arXiv 2506.07823, "PAPER.md"; cited P:<line>).
+ *
+ * One call = one batched operation over B independent MPC instances, enqueued on a CUDA stream.
+ * No C++ or torch types cross this boundary: plain structs, plain pointers, sizes.
+ *
+ * Memory ownership.  The caller owns every buffer and the workspace; the library never
+ * allocates device memory and never frees caller memory.  pdilqr_create() only carves the
+ * caller's workspace and copies constants.  pdilqr_linearize/solve_lq/step do no allocation and
+ * no host synchronisation, so they may be captured in a CUDA graph.  The handle itself is a small
+ * host object (malloc'd by create, freed by destroy).
+ *
+ * Layout.  Every array is dense row-major, batch-outermost, in the handle's dtype (float32 or
+ * float64), 16-byte aligned, on the handle's device:
+ *   A [B][N+1][n][n]   Bm[B][N+1][n][m]   c [B][N+1][n]            (dynamics, Eq. 4 / P:130-141)
+ *   Q [B][N+1][n][n]   R [B][N+1][m][m]   S [B][N+1][m][n]          (Hessian blocks)
+ *   q [B][N+1][n]      r [B][N+1][m]                                (gradients)
+ *   P_term[B][n][n]    p_term[B][n]       dx0[B][n]                 (terminal, dx0 = xhat0 - x0)
+ *   dx[B][N+2][n]  du[B][N+1][m]  dlam[B][N+2][n]  K[B][N+1][m][n]  k[B][N+1][m]
+ * Stages i = 0..N carry controls; node N+1 is terminal (reading R20: N = paper's N).
+ *
+ * Errors.  The returned status reports argument, dimension, alignment, workspace and launch
+ * errors, synchronously.  Per-instance numerical failures are reported on the device in
+ * info[b] (int32): 0 = ok; k > 0 = a factorisation failed at stage k-1 (R or G not positive
+ * definite, or I + C~ P~ singular in a scan combine); -1 = non-finite data, or the SRBD iterate is
+ * outside the Euler-angle guard |pitch| < pi/2 - 0.1.  pdilqr_last_error() returns a message
+ * for the last non-OK status of the calling thread.
+ *
+ * Threads / streams.  One handle per concurrent stream; handles are independent.  The device
+ * is fixed at create; every call sets and restores the current device.
+ */
+#ifndef PDILQR_H
+#define PDILQR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDILQR_ABI_VERSION 1
+
+typedef enum {
+    PDILQR_OK = 0,
+    PDILQR_ERR_INVALID_ARG = 1,
+    PDILQR_ERR_DIM = 2,
+    PDILQR_ERR_WORKSPACE = 3,
+    PDILQR_ERR_CUDA = 4,
+    PDILQR_ERR_UNSUPPORTED = 5
+} pdilqr_status;
+
+typedef enum { PDILQR_F32 = 0, PDILQR_F64 = 1 } pdilqr_dtype;
+typedef enum { PDILQR_MODEL_LQ = 0, PDILQR_MODEL_SRBD = 1 } pdilqr_model;
+
+/* Built-in single-rigid-body quadruped model and its cost (SI units).
+ * State x = [p(3) world, Theta(3) = ZYX (roll, pitch, yaw), v(3) world, w(3) body] (n = 12,
+ * reading R13); input u = four world-frame ground reaction forces (m = 12).  Explicit Euler with
+ * step dt (reading R14).  Stage cost 1/2 |x - x_ref|^2_{W_x} + 1/2 |u - u_ref|^2_{W_u} + relaxed
+ * barriers on the friction pyramid and normal-force bounds of stance feet; terminal
+ * cost 1/2 |x - x_ref|^2_{W_term}.  W_u = w_u_stance on stance feet, w_u_swing on swing feet. */
+typedef struct {
+    double dt, mass, inertia[9], gravity[3];
+    double w_x[12], w_x_term[12], w_u_stance, w_u_swing;
+    double mu_friction, f_min, f_max, barrier_mu, barrier_delta;
+} pdilqr_srbd_params;
+
+typedef struct {
+    int32_t N;              /* horizon: stages 0..N, terminal node N+1 (N >= 0)             */
+    int32_t n, m;           /* state / control dimension (SRBD: 12 / 12)                    */
+    int32_t batch;          /* B, number of independent instances (>= 1)                     */
+    pdilqr_dtype dtype;     /* arithmetic type of every array and of the kernels              */
+    pdilqr_model model;     /* LQ: solve_lq only; SRBD: also linearize and step               */
+    int32_t n_alpha;        /* line-search grid size: alpha in {2^0 .. 2^-(n_alpha-1)}; 0 -> 10 */
+    double armijo_c1;       /* Armijo constant (reading R10); 0 -> 1e-4                       */
+    double theta_max;       /* filter threshold on theta (reading R10); <= 0 -> 1e-2 (N+1)    */
+    int32_t leaf_chunk;     /* scan leaf chunk c >= 1: elements folded sequentially per chunk,
+                               chunk summaries combined by a Blelloch tree (Eq. 8).
+                               1 = pure tree over all N+2 elements; >= N+2 = single chunk
+                               (sequential fold).  0 -> library default.                     */
+    int32_t export_policy;  /* reserved (K,k are written whenever pdilqr_dir.K/k are non-NULL) */
+    pdilqr_srbd_params srbd;/* used iff model == PDILQR_MODEL_SRBD                           */
+} pdilqr_config;
+
+typedef struct pdilqr_ctx *pdilqr_handle;
+
+/* Eq. 4 data (read-only device pointers, layout above). */
+typedef struct {
+    const void *A, *Bm, *c, *Q, *R, *S, *q, *r, *P_term, *p_term, *dx0;
+} pdilqr_lq;
+
+/* Same layout, writable (output of pdilqr_linearize). */
+typedef struct {
+    void *A, *Bm, *c, *Q, *R, *S, *q, *r, *P_term, *p_term, *dx0;
+} pdilqr_lq_buf;
+
+/* Search direction (Eq. 6-7) and optional policy (Eq. 5).  K, k may be NULL. */
+typedef struct {
+    void *dx, *du, *dlam, *K, *k;
+} pdilqr_dir;
+
+/* SQP iterate and per-tick data of the SRBD model (device pointers).
+ *   x[B][N+2][12], u[B][N+1][12], lam[B][N+2][12]  (updated in place by pdilqr_step, Eq. 16)
+ *   x0[B][12] (measured state xhat0), x_ref[B][N+2][12], u_ref[B][N+1][12] or NULL (= 0),
+ *   contact[B][N+1][4] uint8 (1 = stance), feet[B][N+1][4][3] world footholds. */
+typedef struct {
+    void *x, *u, *lam;
+    const void *x0, *x_ref, *u_ref;
+    const uint8_t *contact;
+    const void *feet;
+} pdilqr_iterate;
+
+/* Per-instance statistics of one step (device pointers, each [B]; cost/theta/alpha in dtype):
+ * cost J and constraint violation theta (Eq. 17, reading R9) at the new iterate, accepted step
+ * alpha (0 if every trial was rejected), accepted flag, info code (see Errors). */
+typedef struct {
+    void *cost, *theta, *alpha;
+    int32_t *accepted, *info;
+} pdilqr_stats;
+
+/* Bytes of device workspace a handle with this configuration needs. */
+pdilqr_status pdilqr_workspace_bytes(const pdilqr_config *cfg, size_t *bytes);
+
+/* Validate cfg, bind the caller-owned device workspace (>= pdilqr_workspace_bytes, 256-byte
+ * aligned) and create a handle on CUDA device `device`. */
+pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspace, size_t bytes,
+                            pdilqr_handle *out);
+
+pdilqr_status pdilqr_destroy(pdilqr_handle h);
+
+/* LQ/KKT subproblem of Eq. 4 solved by the parallel associative scans of
+ * element initialisation (Eq. 12-13), reverse scan with the combination rule
+ * (Eq. 11, corrected as DESIGN.md readings R1-R2), per-stage policy (Eq. 5 rows),
+ * forward scan of the closed-loop dynamics (Eq. 14-15, reading R6) and the dual update
+ * (Eq. 7).  Writes dir->dx, du, dlam (and K, k if non-NULL); info[b] (device, may be NULL). */
+pdilqr_status pdilqr_solve_lq(pdilqr_handle h, const pdilqr_lq *qp, pdilqr_dir *dir,
+                              int32_t *info, void *stream /* cudaStream_t */);
+
+/* SRBD linearisation + Gauss-Newton quadraticisation at the iterate (
+ * q, r include the multiplier terms, reading R8).  SRBD handles only.  Exposed for inspection;
+ * pdilqr_step performs it internally.  info may be NULL. */
+pdilqr_status pdilqr_linearize(pdilqr_handle h, const pdilqr_iterate *it, pdilqr_lq_buf *out,
+                               int32_t *info, void *stream);
+
+/* One SQP / RTI iteration: linearise, solve the LQ subproblem by the scans, evaluate
+ * the filter line search on the fixed alpha grid in parallel and apply the
+ * linear update x += a dx, u += a du, lam += a dlam in place (Eq. 16).  SRBD handles only.
+ * dir (may be NULL) receives the search direction. */
+pdilqr_status pdilqr_step(pdilqr_handle h, pdilqr_iterate *it, pdilqr_stats *stats,
+                          pdilqr_dir *dir, void *stream);
+
+/* One closed-loop MPC tick with HOST buffers (the paper's usage): copies x0_host
+ * ([B][12], dtype) into the device iterate's x0 buffer, runs pdilqr_step, and copies the first
+ * control u[:,0,:] ([B][12]) and the stats back into u0_host / stats_host (host arrays of
+ * [B] cost, theta, alpha in dtype followed by [B] accepted, [B] info as int32 are written to
+ * the five pointers).  Host buffers should be pinned for asynchronous copies.  The call returns
+ * after the copies are enqueued; synchronise the stream before reading the host outputs. */
+pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *x0_host,
+                               void *u0_host, void *cost_host, void *theta_host, void *alpha_host,
+                               int32_t *accepted_host, int32_t *info_host, void *stream);
+
+/* Number of kernels the last solve_lq / step / linearize call launched (for accounting). */
+int32_t pdilqr_last_launch_count(pdilqr_handle h);
+
+/* Thread-local message for the last non-OK status (never NULL). */
+const char *pdilqr_last_error(void);
+
+int32_t pdilqr_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PDILQR_H */

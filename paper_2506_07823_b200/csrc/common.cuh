@@ -1,0 +1,181 @@
+// common.cuh -- worker-level primitives for small dense matrix algebra on sm_100a.
+//
+// Execution model: a *worker* is a group of WS lanes of one warp
+// (WS = 4, 8, 16 or 32, the next power of two >= max(n, m)).  Lane r of a worker owns ROW r of
+// every matrix it computes on, held in registers with compile-time indices (fully unrolled
+// loops, no local memory).  The other operand of a product is staged in the worker's private
+// shared-memory slice and read with broadcast (all lanes of a worker read the same address;
+// the two workers of a warp read two addresses in different banks) using 16-byte vector loads.
+// Pivot rows of Gauss-Jordan eliminations travel by warp shuffles inside the worker.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pdilqr {
+
+__host__ __device__ constexpr int worker_width(int d) { return d <= 4 ? 4 : d <= 8 ? 8 : d <= 16 ? 16 : 32; }
+__host__ __device__ constexpr int round_up4(int d) { return (d + 3) & ~3; }
+
+// --------------------------------------------------------------------------------- workers
+// Lane mask of the calling thread's worker.  Workers of one warp may diverge (different loop
+// trip counts), so every shuffle / __syncwarp uses the worker's own mask.
+template <int WS>
+__device__ __forceinline__ unsigned worker_mask() {
+    if constexpr (WS == 32) return 0xffffffffu;
+    else return ((1u << WS) - 1u) << (threadIdx.x & 31 & ~(WS - 1));
+}
+template <int WS>
+__device__ __forceinline__ int worker_lane() { return threadIdx.x & (WS - 1); }
+
+template <int WS, typename T>
+__device__ __forceinline__ T wbcast(unsigned mask, T v, int src) { return __shfl_sync(mask, v, src, WS); }
+template <int WS, typename T>
+__device__ __forceinline__ T wxor(unsigned mask, T v, int m) { return __shfl_xor_sync(mask, v, m, WS); }
+
+// ------------------------------------------------------------------------ vector row access
+// Copy NC contiguous values src[0..NC) into registers.  Vectorised (16 B) when the compile-time
+// shape allows it; `valid` < NC zero-fills the tail (padded instantiations).
+template <typename T, int NC, bool VEC>
+__device__ __forceinline__ void ld_row(T (&d)[NC], const T *__restrict__ s, int valid = NC) {
+    if constexpr (VEC && sizeof(T) == 4 && NC % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < NC; j += 4) {
+            float4 v = *reinterpret_cast<const float4 *>(s + j);
+            d[j] = v.x; d[j + 1] = v.y; d[j + 2] = v.z; d[j + 3] = v.w;
+        }
+    } else if constexpr (VEC && sizeof(T) == 8 && NC % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < NC; j += 2) {
+            double2 v = *reinterpret_cast<const double2 *>(s + j);
+            d[j] = v.x; d[j + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < NC; ++j) d[j] = (j < valid) ? s[j] : T(0);
+    }
+}
+
+template <typename T, int NC, bool VEC>
+__device__ __forceinline__ void st_row(T *__restrict__ d, const T (&s)[NC], int valid = NC) {
+    if constexpr (VEC && sizeof(T) == 4 && NC % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < NC; j += 4) *reinterpret_cast<float4 *>(d + j) = make_float4(s[j], s[j + 1], s[j + 2], s[j + 3]);
+    } else if constexpr (VEC && sizeof(T) == 8 && NC % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < NC; j += 2) *reinterpret_cast<double2 *>(d + j) = make_double2(s[j], s[j + 1]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+            if (j < valid) d[j] = s[j];
+    }
+}
+
+// Strided column load: d[k] = s[k * ld], k < valid (zero beyond).
+template <typename T, int NK>
+__device__ __forceinline__ void ld_col(T (&d)[NK], const T *__restrict__ s, int ld, int valid = NK) {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) d[k] = (k < valid) ? s[k * ld] : T(0);
+}
+
+template <typename T, int NC>
+__device__ __forceinline__ void zero(T (&d)[NC]) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) d[j] = T(0);
+}
+
+// ------------------------------------------------------------------------------ products
+// out[j] (+)= sum_k a[k] * Y[k*LDY + j]   (row of a 1xK times KxNC matrix in shared memory)
+template <typename T, int K, int NC, int LDY>
+__device__ __forceinline__ void row_mat(T (&out)[NC], const T (&a)[K], const T *__restrict__ Y) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        T y[NC];
+        ld_row<T, NC, (LDY % (16 / sizeof(T)) == 0)>(y, Y + k * LDY);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) out[j] = fma(a[k], y[j], out[j]);
+    }
+}
+
+// out[j] (+)= sum_k a[k] * Y[j*LDY + k]   (row times the transpose of an NCxK smem matrix)
+template <typename T, int K, int NC, int LDY>
+__device__ __forceinline__ void row_matT(T (&out)[NC], const T (&a)[K], const T *__restrict__ Y) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+        T y[K];
+        ld_row<T, K, (LDY % (16 / sizeof(T)) == 0)>(y, Y + j * LDY);
+        T s = out[j];
+#pragma unroll
+        for (int k = 0; k < K; ++k) s = fma(a[k], y[k], s);
+        out[j] = s;
+    }
+}
+
+// dot of a register row with a shared-memory vector
+template <typename T, int K>
+__device__ __forceinline__ T row_dot(const T (&a)[K], const T *__restrict__ v, T acc) {
+    T y[K];
+    ld_row<T, K, (K % (16 / sizeof(T)) == 0)>(y, v);
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc = fma(a[k], y[k], acc);
+    return acc;
+}
+
+// ------------------------------------------------------------------- Gauss-Jordan solves
+// Solve  M X = RHS  for an NR x NR system distributed one row per lane (lane r < nrows owns
+// row r of M in a[] and of RHS in rhs[]), in place.  Lanes r >= nrows are idle (never pivot).
+//
+// PIVOT = true : partial pivoting by implicit row selection (max |a[k]| over rows not yet used;
+//                ties -> lowest lane).  Rows are never moved: on return the lane that pivoted
+//                column k holds solution row k, and `piv_row` of every lane = the column it
+//                pivoted (-1 for idle lanes).  Used for M = I + C~ P~ (nonsymmetric).
+// PIVOT = false: no pivoting, pivot k = lane k; for symmetric positive definite M (R, G), where
+//                every pivot is a ratio of leading principal minors and must be > 0.
+// Returns false (uniformly across the worker) if a pivot is zero / non-finite (singular) or, for
+// PIVOT = false, non-positive (not positive definite).
+template <typename T, int WS, int NR, int NRHS, bool PIVOT>
+__device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)[NRHS], int lane, int nrows,
+                                             int &piv_row) {
+    bool used = lane >= nrows;
+    bool ok = true;
+    piv_row = -1;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        if (k >= nrows) break;
+        int p;
+        if constexpr (PIVOT) {
+            T v = used ? T(-1) : fabs(a[k]);
+            int bi = lane;
+#pragma unroll
+            for (int off = WS / 2; off >= 1; off >>= 1) {
+                T ov = wxor<WS>(mask, v, off);
+                int oi = wxor<WS>(mask, bi, off);
+                if (ov > v || (ov == v && oi < bi)) { v = ov; bi = oi; }
+            }
+            p = bi;
+        } else {
+            p = k;
+        }
+        const T pv = wbcast<WS>(mask, a[k], p);
+        if constexpr (PIVOT) ok = ok && (pv != T(0)) && isfinite(pv);
+        else ok = ok && (pv > T(0)) && isfinite(pv);
+        const T inv = T(1) / pv;
+        const bool isp = (lane == p);
+        const T f = isp ? T(0) : a[k] * inv;
+        if (isp) { used = true; piv_row = k; }
+#pragma unroll
+        for (int j = k + 1; j < NR; ++j) {
+            const T pj = wbcast<WS>(mask, a[j], p);
+            a[j] = isp ? pj * inv : fma(-f, pj, a[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < NRHS; ++j) {
+            const T pj = wbcast<WS>(mask, rhs[j], p);
+            rhs[j] = isp ? pj * inv : fma(-f, pj, rhs[j]);
+        }
+    }
+    if constexpr (!PIVOT) piv_row = lane < nrows ? lane : -1;
+    return __all_sync(mask, ok);
+}
+
+}  // namespace pdilqr

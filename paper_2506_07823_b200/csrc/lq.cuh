@@ -1,0 +1,815 @@
+// lq.cuh -- LQ/KKT subproblem (Eq. 4) by parallel associative scans on sm_100a.
+//
+// Kernels (one launch each, all stream-ordered, no host sync):
+//   k_elem_init   Eq. 12 / Eq. 13 element initialisation, one worker per (instance, stage)
+//   k_scan_bwd    reverse inclusive scan of value elements with the combination rule (Eq. 11,
+//                 corrected: DESIGN.md readings R1, R2); chunked Blelloch tree, one CTA per instance
+//   k_policy      per-stage policy K, k from the scanned P_{i+1}, p_{i+1} (Eq. 5 rows) and
+//                 the closed-loop elements (Abar, bbar) of Eq. 14
+//   k_scan_fwd    forward inclusive scan of the conditional optimal trajectory (Eq. 15, combine
+//                 order corrected: reading R6) -> dx
+//   k_tail        du = K dx + k (Eq. 6) and the dual update dlam = P dx + p (Eq. 7)
+// Value element e = (A~, C~, P~, b~, p~) of Eq. 10; a "suffix" is an element whose A~ = C~ = b~ = 0
+// (every product that contains the terminal element, Eq. 13), combined by the cheap rule.
+#pragma once
+
+#include <climits>
+
+#include "common.cuh"
+
+namespace pdilqr {
+
+// ---------------------------------------------------------------------------------- layouts
+template <int NX>
+struct VE {  // value element, units of T; every field starts 16-byte aligned
+    static constexpr int A = 0, C = NX * NX, P = 2 * NX * NX, b = 3 * NX * NX, p = 3 * NX * NX + NX;
+    static constexpr int SIZE = 3 * NX * NX + 2 * NX;
+};
+template <int NX>
+struct TE {  // trajectory element (Abar, bbar) of Eq. 15; also used for (P, p) and (K, k) rows
+    static constexpr int A = 0, b = NX * NX, SIZE = NX * NX + NX;
+};
+template <int NX, int NU>
+struct KE {  // policy (K, k) of one stage
+    static constexpr int K = 0, k = NU * NX, SIZE = NU * NX + NU;
+};
+
+enum SlotKind : int { SLOT_IDENT = 0, SLOT_ANCHOR = 1, SLOT_GENERAL = 2 };  // ANCHOR = suffix / anchored prefix
+
+template <typename T>
+struct LqArgs {  // user Eq. 4 data (runtime n, m strides)
+    const T *A, *Bm, *c, *Q, *R, *S, *q, *r, *Pt, *pt, *dx0;
+};
+
+template <typename T>
+struct LqOut {
+    T *dx, *du, *dlam, *K, *k;  // user buffers (K, k may be null)
+};
+
+// Workspace views used by the LQ kernels (sizes in pdilqr.cu).
+template <typename T>
+struct LqWork {
+    T *elems;    // [B][N+2][VE]
+    T *vslots;   // [B][Pv][VE]      (tree slots of the backward scan)
+    T *Pp;       // [B][N+2][TE]      P_i, p_i
+    T *Kk;       // [B][N+1][KE]      K_i, k_i
+    T *tel;      // [B][N+1][TE]      Abar_i, bbar_i
+    T *tslots;   // [B][Pf][TE]       tree slots of the forward scan
+    T *dxw;      // [B][N+2][NX]      dx (padded)
+    int32_t *fail;    // [B] min(stage+1) of a failed factorisation, INT_MAX if none
+    int32_t *nonfin;  // [B] non-finite output flag
+};
+
+// Cooperative copy of NV values (16-byte granules) by one worker.
+template <typename T, int NV, int WS>
+__device__ __forceinline__ void wcopy(T *__restrict__ dst, const T *__restrict__ src, int lane) {
+    static_assert((NV * sizeof(T)) % 16 == 0, "granule");
+    constexpr int NG = NV * sizeof(T) / 16;
+    const int4 *s = reinterpret_cast<const int4 *>(src);
+    int4 *d = reinterpret_cast<int4 *>(dst);
+#pragma unroll 4
+    for (int i = lane; i < NG; i += WS) d[i] = s[i];
+}
+template <typename T, int NV, int WS>
+__device__ __forceinline__ void wzero(T *__restrict__ dst, int lane) {
+    constexpr int NG = NV * sizeof(T) / 16;
+    int4 *d = reinterpret_cast<int4 *>(dst);
+    for (int i = lane; i < NG; i += WS) d[i] = make_int4(0, 0, 0, 0);
+}
+
+// ------------------------------------------------------------------------- value combines
+template <typename T, int NX>
+struct CombineSmem {
+    T e1[VE<NX>::SIZE];  // left operand  e_{i->k}
+    T e2[VE<NX>::SIZE];  // right operand e_{k->j}
+    T X[NX * NX], Y[NX * NX], V[NX * NX];
+    T z[NX], w[NX], y[NX], v[NX];
+};
+
+// Full combination rule e1 (x) e2 (Eq. 11 as corrected in SURVEY App. A / DESIGN.md R1-R2):
+//   M = I + C1 P2 (pivoted Gauss-Jordan), X = M^-1 A1, Y = M^-1 C1, z = M^-1 (b1 - C1 p2)
+//   A = A2 X, b = A2 z + b2, C = A2 Y A2^T + C2, P = A1^T P2 X + P1,
+//   p = A1^T (w - P2 Y w) + p1,  w = p2 + P2 b1      (M^-T = I - P2 M^-1 C1)
+// Operands in smem (s.e1, s.e2); lane r < NX returns row r of A, C, P and b_r, p_r.
+template <typename T, int NX, int WS>
+__device__ __forceinline__ bool combine_full(CombineSmem<T, NX> &s, unsigned mask, int lane, T (&Ao)[NX],
+                                             T (&Co)[NX], T (&Po)[NX], T &bo, T &po) {
+    using L = VE<NX>;
+    const int r = lane < NX ? lane : 0;
+    T c1[NX];
+    ld_row<T, NX, true>(c1, s.e1 + L::C + r * NX);
+    T M[NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) M[j] = (j == r) ? T(1) : T(0);
+    row_mat<T, NX, NX, NX>(M, c1, s.e2 + L::P);
+    T rhs[2 * NX + 1];
+    {
+        T a1[NX];
+        ld_row<T, NX, true>(a1, s.e1 + L::A + r * NX);
+#pragma unroll
+        for (int j = 0; j < NX; ++j) { rhs[j] = a1[j]; rhs[NX + j] = c1[j]; }
+        rhs[2 * NX] = s.e1[L::b + r] - row_dot<T, NX>(c1, s.e2 + L::p, T(0));
+    }
+    int pr;
+    const bool ok = gauss_jordan<T, WS, NX, 2 * NX + 1, true>(mask, M, rhs, lane, NX, pr);
+    if (pr >= 0) {
+        T xr[NX], yr[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) { xr[j] = rhs[j]; yr[j] = rhs[NX + j]; }
+        st_row<T, NX, true>(s.X + pr * NX, xr);
+        st_row<T, NX, true>(s.Y + pr * NX, yr);
+        s.z[pr] = rhs[2 * NX];
+    }
+    __syncwarp(mask);
+    T a2[NX];
+    ld_row<T, NX, true>(a2, s.e2 + L::A + r * NX);
+    zero(Ao);
+    row_mat<T, NX, NX, NX>(Ao, a2, s.X);
+    bo = row_dot<T, NX>(a2, s.z, s.e2[L::b + r]);
+    {
+        T W[NX];
+        zero(W);
+        row_mat<T, NX, NX, NX>(W, a2, s.Y);
+        ld_row<T, NX, true>(Co, s.e2 + L::C + r * NX);
+        row_matT<T, NX, NX, NX>(Co, W, s.e2 + L::A);
+    }
+    T p2[NX];
+    ld_row<T, NX, true>(p2, s.e2 + L::P + r * NX);
+    T wr;
+    {
+        T V[NX];
+        zero(V);
+        row_mat<T, NX, NX, NX>(V, p2, s.X);
+        wr = row_dot<T, NX>(p2, s.e1 + L::b, s.e2[L::p + r]);
+        if (lane < NX) { st_row<T, NX, true>(s.V + r * NX, V); s.w[r] = wr; }
+    }
+    __syncwarp(mask);
+    T a1c[NX];
+    ld_col<T, NX>(a1c, s.e1 + L::A + r, NX);
+    ld_row<T, NX, true>(Po, s.e1 + L::P + r * NX);
+    row_mat<T, NX, NX, NX>(Po, a1c, s.V);
+    {
+        T yr[NX];
+        ld_row<T, NX, true>(yr, s.Y + r * NX);
+        const T yv = row_dot<T, NX>(yr, s.w, T(0));
+        if (lane < NX) s.y[r] = yv;
+    }
+    __syncwarp(mask);
+    const T vr = wr - row_dot<T, NX>(p2, s.y, T(0));
+    if (lane < NX) s.v[r] = vr;
+    __syncwarp(mask);
+    po = row_dot<T, NX>(a1c, s.v, s.e1[L::p + r]);
+    __syncwarp(mask);
+    return ok;
+}
+
+// Cheap rule for a suffix right operand (A2 = C2 = b2 = 0): only P, p of the result are nonzero.
+//   P = A1^T P2 M^-1 A1 + P1,  p = A1^T (w - P2 M^-1 C1 w) + p1,  w = p2 + P2 b1.
+template <typename T, int NX, int WS>
+__device__ __forceinline__ bool combine_cheap(CombineSmem<T, NX> &s, unsigned mask, int lane, T (&Po)[NX], T &po) {
+    using L = VE<NX>;
+    const int r = lane < NX ? lane : 0;
+    T c1[NX];
+    ld_row<T, NX, true>(c1, s.e1 + L::C + r * NX);
+    T M[NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) M[j] = (j == r) ? T(1) : T(0);
+    row_mat<T, NX, NX, NX>(M, c1, s.e2 + L::P);
+    T p2[NX];
+    ld_row<T, NX, true>(p2, s.e2 + L::P + r * NX);
+    const T wr = row_dot<T, NX>(p2, s.e1 + L::b, s.e2[L::p + r]);
+    if (lane < NX) s.w[r] = wr;
+    __syncwarp(mask);
+    T rhs[NX + 1];
+    ld_row<T, NX, true>(*reinterpret_cast<T(*)[NX]>(rhs), s.e1 + L::A + r * NX);
+    rhs[NX] = row_dot<T, NX>(c1, s.w, T(0));
+    int pr;
+    const bool ok = gauss_jordan<T, WS, NX, NX + 1, true>(mask, M, rhs, lane, NX, pr);
+    if (pr >= 0) {
+        st_row<T, NX, true>(s.X + pr * NX, *reinterpret_cast<T(*)[NX]>(rhs));
+        s.y[pr] = rhs[NX];
+    }
+    __syncwarp(mask);
+    {
+        T V[NX];
+        zero(V);
+        row_mat<T, NX, NX, NX>(V, p2, s.X);
+        const T vr = wr - row_dot<T, NX>(p2, s.y, T(0));
+        if (lane < NX) { st_row<T, NX, true>(s.V + r * NX, V); s.v[r] = vr; }
+    }
+    __syncwarp(mask);
+    T a1c[NX];
+    ld_col<T, NX>(a1c, s.e1 + L::A + r, NX);
+    ld_row<T, NX, true>(Po, s.e1 + L::P + r * NX);
+    row_mat<T, NX, NX, NX>(Po, a1c, s.V);
+    po = row_dot<T, NX>(a1c, s.v, s.e1[L::p + r]);
+    __syncwarp(mask);
+    return ok;
+}
+
+// ------------------------------------------------------------------ element init (Eq. 12-13)
+// Per stage i <= N:  GJ on R (SPD, no pivoting) with right-hand sides [S | r | B^T], then
+//   A~ = A - B R^-1 S,  C~ = B R^-1 B^T,  b~ = b - B R^-1 r,  P~ = Q - S^T R^-1 S,  p~ = q - S^T R^-1 r.
+// Terminal element i = N+1 (Eq. 13, reading R4): A~ = C~ = b~ = 0, P~ = P_{N+1}, p~ = p_{N+1}.
+// Padded instantiations (n < NX or m < NU): state rows/cols >= n are zero, R is padded with
+// the identity; the padded entries of every element are then exactly zero.
+template <typename T, int NX, int NU, bool EX>
+__global__ void __launch_bounds__(128) k_elem_init(LqArgs<T> qp, int B, int N, int n, int m, LqWork<T> ws) {
+    constexpr int WS = worker_width(NX > NU ? NX : NU);
+    constexpr int SMW = 2 * NU * NX + round_up4(NU);  // per-worker smem: ZS, ZB, zr
+    using L = VE<NX>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    const int wloc = threadIdx.x / WS;
+    const long gw = (long)blockIdx.x * (blockDim.x / WS) + wloc;
+    const int L2 = N + 2;
+    if (gw >= (long)B * L2) return;  // whole worker exits together
+    const int b = (int)(gw / L2), i = (int)(gw % L2);
+    T *sm = reinterpret_cast<T *>(smraw) + wloc * SMW;
+    T *ZS = sm, *ZB = sm + NU * NX, *zr = sm + 2 * NU * NX;
+    T *e = ws.elems + ((size_t)b * L2 + i) * L::SIZE;
+    const int r = lane < NX ? lane : 0;
+    if (i == N + 1) {  // terminal element
+        if (lane < NX) {
+            T zrow[NX], prow[NX];
+            zero(zrow);
+            if (EX || r < n) ld_row<T, NX, EX>(prow, qp.Pt + (size_t)b * n * n + r * n, n);
+            else zero(prow);
+            st_row<T, NX, true>(e + L::A + r * NX, zrow);
+            st_row<T, NX, true>(e + L::C + r * NX, zrow);
+            st_row<T, NX, true>(e + L::P + r * NX, prow);
+            e[L::b + r] = T(0);
+            e[L::p + r] = (EX || r < n) ? qp.pt[(size_t)b * n + r] : T(0);
+        }
+        return;
+    }
+    const size_t st = (size_t)b * (N + 1) + i;
+    // --- GJ rows: lane r < NU owns row r of R and of [S | r | B^T]
+    {
+        const int ru = lane < NU ? lane : 0;
+        T a[NU], rhs[2 * NX + 1];
+        const bool valid = EX || ru < m;
+        if (valid) {
+            ld_row<T, NU, EX>(a, qp.R + st * m * m + ru * m, m);
+            T srow[NX], bcol[NX];
+            ld_row<T, NX, EX>(srow, qp.S + st * m * n + ru * n, n);
+            ld_col<T, NX>(bcol, qp.Bm + st * n * m + ru, m, n);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) { rhs[j] = srow[j]; rhs[NX + 1 + j] = bcol[j]; }
+            rhs[NX] = qp.r[st * m + ru];
+        } else {
+#pragma unroll
+            for (int j = 0; j < NU; ++j) a[j] = (j == ru) ? T(1) : T(0);
+#pragma unroll
+            for (int j = 0; j < 2 * NX + 1; ++j) rhs[j] = T(0);
+        }
+        int pr;
+        const bool ok = gauss_jordan<T, WS, NU, 2 * NX + 1, false>(mask, a, rhs, lane, NU, pr);
+        if (!ok && lane == 0) atomicMin(ws.fail + b, i + 1);
+        if (pr >= 0) {
+            T t1[NX], t2[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) { t1[j] = rhs[j]; t2[j] = rhs[NX + 1 + j]; }
+            st_row<T, NX, true>(ZS + pr * NX, t1);
+            st_row<T, NX, true>(ZB + pr * NX, t2);
+            zr[pr] = rhs[NX];
+        }
+    }
+    __syncwarp(mask);
+    // --- element rows: lane r < NX owns state row r
+    T brow[NU], scol[NU], row[NX], out[NX];
+    const bool vr = EX || r < n;
+    if (vr) {
+        ld_row<T, NU, EX>(brow, qp.Bm + st * n * m + r * m, m);
+        ld_col<T, NU>(scol, qp.S + st * m * n + r, n, m);
+    } else {
+        zero(brow);
+        zero(scol);
+    }
+    // A~
+    if (vr) ld_row<T, NX, EX>(row, qp.A + st * n * n + r * n, n);
+    else zero(row);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+        T y[NX];
+        ld_row<T, NX, true>(y, ZS + k * NX);
+#pragma unroll
+        for (int j = 0; j < NX; ++j) row[j] = fma(-brow[k], y[j], row[j]);
+    }
+    if (lane < NX) st_row<T, NX, true>(e + L::A + r * NX, row);
+    // C~ = B (R^-1 B^T)
+    zero(out);
+    row_mat<T, NU, NX, NX>(out, brow, ZB);
+    if (lane < NX) st_row<T, NX, true>(e + L::C + r * NX, out);
+    // P~ = Q - S^T (R^-1 S)
+    if (vr) ld_row<T, NX, EX>(row, qp.Q + st * n * n + r * n, n);
+    else zero(row);
+#pragma unroll
+    for (int k = 0; k < NU; ++k) {
+        T y[NX];
+        ld_row<T, NX, true>(y, ZS + k * NX);
+#pragma unroll
+        for (int j = 0; j < NX; ++j) row[j] = fma(-scol[k], y[j], row[j]);
+    }
+    if (lane < NX) st_row<T, NX, true>(e + L::P + r * NX, row);
+    const T cb = vr ? qp.c[st * n + r] : T(0);
+    const T qq = vr ? qp.q[st * n + r] : T(0);
+    T bt = cb, pt = qq;
+#pragma unroll
+    for (int k = 0; k < NU; ++k) { bt = fma(-brow[k], zr[k], bt); pt = fma(-scol[k], zr[k], pt); }
+    if (lane < NX) { e[L::b + r] = bt; e[L::p + r] = pt; }
+}
+
+// -------------------------------------------------------------------- backward scan (Eq. 8-11)
+// One CTA per instance, W workers.  L = N+2 elements are cut into J = ceil(L / chunk) chunks.
+//  phase 1: every chunk j < J-1 is reduced right-to-left into its summary S_j by the full rule;
+//           the last chunk (it holds the terminal element) is folded right-to-left by the cheap
+//           rule, which yields its final suffixes s_i = e_i (x) ... (x) e_{N+1} directly;
+//  phase 2: exclusive suffix products T_j = S_{j+1} (x) ... (x) S_{J-1} by a work-efficient
+//           Blelloch tree (up-sweep / down-sweep, 2 ceil(log2 J) levels) on the reversed slots;
+//  phase 3: every chunk j < J-1 is folded right-to-left from T_j by the cheap rule.
+// Read-out (reading R5): P_i = P~(s_i), p_i = p~(s_i), i = 0..N+1.
+// chunk = 1 is the pure tree over all elements (the paper's scan); chunk >= L the pure fold.
+template <typename T, int NX>
+struct ScanBwd {
+    static constexpr int WS = worker_width(NX);
+    using L = VE<NX>;
+
+    static __device__ __forceinline__ void store_elem_rows(T *dst, const T (&A)[NX], const T (&C)[NX],
+                                                           const T (&P)[NX], T b, T p, int lane) {
+        if (lane < NX) {
+            st_row<T, NX, true>(dst + L::A + lane * NX, A);
+            st_row<T, NX, true>(dst + L::C + lane * NX, C);
+            st_row<T, NX, true>(dst + L::P + lane * NX, P);
+            dst[L::b + lane] = b;
+            dst[L::p + lane] = p;
+        }
+    }
+    static __device__ __forceinline__ void store_suffix_rows(T *dst, const T (&P)[NX], T p, int lane) {
+        if (lane < NX) {
+            T z[NX];
+            zero(z);
+            st_row<T, NX, true>(dst + L::A + lane * NX, z);
+            st_row<T, NX, true>(dst + L::C + lane * NX, z);
+            st_row<T, NX, true>(dst + L::P + lane * NX, P);
+            dst[L::b + lane] = T(0);
+            dst[L::p + lane] = p;
+        }
+    }
+    // write (P, p) of suffix s_i to the value-function buffer
+    static __device__ __forceinline__ void out_Pp(T *Pp_i, const T (&P)[NX], T p, int lane) {
+        if (lane < NX) {
+            st_row<T, NX, true>(Pp_i + lane * NX, P);
+            Pp_i[NX * NX + lane] = p;
+        }
+    }
+};
+
+// CTA = IPB instances x W workers (all instances of a CTA run the same level schedule).
+template <typename T, int NX>
+__global__ void __launch_bounds__(256) k_scan_bwd(int B, int N, int chunk, int J, int Pv, int W, int IPB, LqWork<T> ws) {
+    using SB = ScanBwd<T, NX>;
+    using L = VE<NX>;
+    constexpr int WS = SB::WS;
+    constexpr int TP = TE<NX>::SIZE;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int WI = W * WS, ib = threadIdx.x / WI, w = (threadIdx.x % WI) / WS, lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    CombineSmem<T, NX> &s = reinterpret_cast<CombineSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    int *kind = reinterpret_cast<int *>(smraw + IPB * W * sizeof(CombineSmem<T, NX>)) + ib * Pv;
+    const int b = blockIdx.x * IPB + ib, L2 = N + 2;
+    const bool active = b < B;
+    const int wv = active ? w : (INT_MAX / 2);  // inactive instances skip all work but reach every barrier
+    const int b_ = active ? b : 0;
+    const T *E = ws.elems + (size_t)b_ * L2 * L::SIZE;
+    T *Y = ws.vslots + (size_t)b_ * Pv * L::SIZE;
+    T *Pp = ws.Pp + (size_t)b_ * L2 * TP;
+    int fail = INT_MAX;
+
+    // ---------------- phase 1
+    for (int j = wv; j < J; j += W) {
+        const int lo = j * chunk, hi = min(lo + chunk, L2);
+        wcopy<T, L::SIZE, WS>(s.e2, E + (size_t)(hi - 1) * L::SIZE, lane);
+        __syncwarp(mask);
+        if (j == J - 1) {  // holds the terminal element: suffixes are final
+            if (lane < NX) {
+                T P[NX];
+                ld_row<T, NX, true>(P, s.e2 + L::P + lane * NX);
+                SB::out_Pp(Pp + (size_t)(hi - 1) * TP, P, s.e2[L::p + lane], lane);
+            }
+            for (int i = hi - 2; i >= lo; --i) {
+                wcopy<T, L::SIZE, WS>(s.e1, E + (size_t)i * L::SIZE, lane);
+                __syncwarp(mask);
+                T Po[NX], po;
+                if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, i + 1);
+                if (lane < NX) {
+                    st_row<T, NX, true>(s.e2 + L::P + lane * NX, Po);
+                    s.e2[L::p + lane] = po;
+                }
+                SB::out_Pp(Pp + (size_t)i * TP, Po, po, lane);
+                __syncwarp(mask);
+            }
+            if (J > 1) {
+                T P[NX];
+                ld_row<T, NX, true>(P, s.e2 + L::P + (lane < NX ? lane : 0) * NX);
+                SB::store_suffix_rows(Y, P, s.e2[L::p + (lane < NX ? lane : 0)], lane);
+                if (lane == 0) kind[0] = SLOT_ANCHOR;
+            }
+        } else {
+            for (int i = hi - 2; i >= lo; --i) {
+                wcopy<T, L::SIZE, WS>(s.e1, E + (size_t)i * L::SIZE, lane);
+                __syncwarp(mask);
+                T Ao[NX], Co[NX], Po[NX], bo, po;
+                if (!combine_full<T, NX, WS>(s, mask, lane, Ao, Co, Po, bo, po)) fail = min(fail, i + 1);
+                SB::store_elem_rows(s.e2, Ao, Co, Po, bo, po, lane);
+                __syncwarp(mask);
+            }
+            wcopy<T, L::SIZE, WS>(Y + (size_t)(J - 1 - j) * L::SIZE, s.e2, lane);
+            if (lane == 0) kind[J - 1 - j] = SLOT_GENERAL;
+        }
+        __syncwarp(mask);
+    }
+    for (int t = J + (threadIdx.x % WI); t < Pv; t += WI) kind[t] = SLOT_IDENT;
+    __syncthreads();
+
+    if (J > 1) {
+        // ---------------- phase 2: Blelloch exclusive scan over reversed slots with
+        // y_a (.) y_b := y_b (x) y_a   (slot t holds S_{J-1-t}; slot 0 holds the terminal chunk)
+        for (int d = 1; d < Pv; d <<= 1) {
+            const int np = Pv / (2 * d);
+            for (int q = wv; q < np; q += W) {
+                const int k = 2 * d * (q + 1) - 1, kr = k - d;
+                const int kl_kind = kind[k], kr_kind = kind[kr];
+                __syncwarp(mask);
+                T *Yk = Y + (size_t)k * L::SIZE, *Yr = Y + (size_t)kr * L::SIZE;
+                if (kr_kind == SLOT_IDENT) {
+                    // unchanged
+                } else if (kl_kind == SLOT_IDENT) {
+                    wcopy<T, L::SIZE, WS>(Yk, Yr, lane);
+                    if (lane == 0) kind[k] = kr_kind;
+                } else {
+                    wcopy<T, L::SIZE, WS>(s.e1, Yk, lane);
+                    wcopy<T, L::SIZE, WS>(s.e2, Yr, lane);
+                    __syncwarp(mask);
+                    if (kr_kind == SLOT_ANCHOR) {
+                        T Po[NX], po;
+                        if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, 1);
+                        SB::store_suffix_rows(Yk, Po, po, lane);
+                        if (lane == 0) kind[k] = SLOT_ANCHOR;
+                    } else {
+                        T Ao[NX], Co[NX], Po[NX], bo, po;
+                        if (!combine_full<T, NX, WS>(s, mask, lane, Ao, Co, Po, bo, po)) fail = min(fail, 1);
+                        SB::store_elem_rows(Yk, Ao, Co, Po, bo, po, lane);
+                    }
+                }
+                __syncwarp(mask);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x % WI == 0) kind[Pv - 1] = SLOT_IDENT;
+        __syncthreads();
+        for (int d = Pv / 2; d >= 1; d >>= 1) {
+            const int np = Pv / (2 * d);
+            for (int q = wv; q < np; q += W) {
+                const int k = 2 * d * (q + 1) - 1, kl = k - d;
+                const int kE = kind[k], kt = kind[kl];
+                __syncwarp(mask);
+                T *Yk = Y + (size_t)k * L::SIZE, *Yl = Y + (size_t)kl * L::SIZE;
+                // t = Y[kl]; Y[kl] = Y[k]; Y[k] = t (x) Y[k]
+                wcopy<T, L::SIZE, WS>(s.e1, Yl, lane);
+                wcopy<T, L::SIZE, WS>(s.e2, Yk, lane);
+                __syncwarp(mask);
+                wcopy<T, L::SIZE, WS>(Yl, s.e2, lane);
+                if (kE == SLOT_IDENT) {
+                    wcopy<T, L::SIZE, WS>(Yk, s.e1, lane);
+                    if (lane == 0) { kind[kl] = kE; kind[k] = kt; }
+                } else if (kt == SLOT_IDENT) {
+                    if (lane == 0) { kind[kl] = kE; kind[k] = kE; }
+                } else {
+                    T Po[NX], po;
+                    if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, 1);
+                    SB::store_suffix_rows(Yk, Po, po, lane);
+                    if (lane == 0) { kind[kl] = kE; kind[k] = SLOT_ANCHOR; }
+                }
+                __syncwarp(mask);
+            }
+            __syncthreads();
+        }
+        // ---------------- phase 3
+        for (int j = wv; j < J - 1; j += W) {
+            const int lo = j * chunk, hi = min(lo + chunk, L2);
+            wcopy<T, L::SIZE, WS>(s.e2, Y + (size_t)(J - 1 - j) * L::SIZE, lane);
+            __syncwarp(mask);
+            for (int i = hi - 1; i >= lo; --i) {
+                wcopy<T, L::SIZE, WS>(s.e1, E + (size_t)i * L::SIZE, lane);
+                __syncwarp(mask);
+                T Po[NX], po;
+                if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, i + 1);
+                if (lane < NX) {
+                    st_row<T, NX, true>(s.e2 + L::P + lane * NX, Po);
+                    s.e2[L::p + lane] = po;
+                }
+                SB::out_Pp(Pp + (size_t)i * TP, Po, po, lane);
+                __syncwarp(mask);
+            }
+        }
+    }
+    if (active && fail != INT_MAX && lane == 0) atomicMin(ws.fail + b, fail);
+}
+
+// ---------------------------------------------------------------------- policy (Eq. 5 rows)
+// Per stage i (one worker):  PB = P_{i+1} B,  g = p_{i+1} + P_{i+1} b,
+//   G = R + B^T PB,  H = S + PB^T A,  h = B^T g + r,  K = -G^-1 H,  k = -G^-1 h  (GJ, SPD),
+//   Abar = A + B K,  bbar = B k + b   (Eq. 14).
+template <typename T, int NX, int NU, bool EX>
+__global__ void __launch_bounds__(128) k_policy(LqArgs<T> qp, int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {
+    constexpr int WS = worker_width(NX > NU ? NX : NU);
+    constexpr int SMW = NX * NU + NX * NX + NX * NU + NU * NX + round_up4(NU) + NX + NX;  // B, A, PB, K, k, c, g
+    using KL = KE<NX, NU>;
+    constexpr int TP = TE<NX>::SIZE;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    const int wloc = threadIdx.x / WS;
+    const long gw = (long)blockIdx.x * (blockDim.x / WS) + wloc;
+    if (gw >= (long)B * (N + 1)) return;
+    const int b = (int)(gw / (N + 1)), i = (int)(gw % (N + 1));
+    T *sm = reinterpret_cast<T *>(smraw) + wloc * SMW;
+    T *sB = sm, *sA = sB + NX * NU, *sPB = sA + NX * NX, *sK = sPB + NX * NU, *sk = sK + NU * NX;
+    T *sc = sk + round_up4(NU), *sg = sc + NX;
+    const size_t st = (size_t)b * (N + 1) + i;
+    const int r = lane < NX ? lane : 0;
+    const bool vr = EX || r < n;
+    T brow[NU], arow[NX];
+    if (vr) {
+        ld_row<T, NU, EX>(brow, qp.Bm + st * n * m + r * m, m);
+        ld_row<T, NX, EX>(arow, qp.A + st * n * n + r * n, n);
+    } else {
+        zero(brow);
+        zero(arow);
+    }
+    const T cr = vr ? qp.c[st * n + r] : T(0);
+    if (lane < NX) {
+        st_row<T, NU, true>(sB + r * NU, brow);
+        st_row<T, NX, true>(sA + r * NX, arow);
+        sc[r] = cr;
+    }
+    __syncwarp(mask);
+    const T *Pn = ws.Pp + ((size_t)b * (N + 2) + i + 1) * TP;
+    {
+        T prow[NX], pb[NU];
+        ld_row<T, NX, true>(prow, Pn + r * NX);
+        zero(pb);
+        row_mat<T, NX, NU, NU>(pb, prow, sB);
+        const T g = row_dot<T, NX>(prow, sc, Pn[NX * NX + r]);
+        if (lane < NX) { st_row<T, NU, true>(sPB + r * NU, pb); sg[r] = g; }
+    }
+    __syncwarp(mask);
+    {
+        const int ru = lane < NU ? lane : 0;
+        const bool vu = EX || ru < m;
+        T G[NU], rhs[NX + 1];
+        if (vu) {
+            ld_row<T, NU, EX>(G, qp.R + st * m * m + ru * m, m);
+            ld_row<T, NX, EX>(*reinterpret_cast<T(*)[NX]>(rhs), qp.S + st * m * n + ru * n, n);
+            rhs[NX] = qp.r[st * m + ru];
+        } else {
+#pragma unroll
+            for (int j = 0; j < NU; ++j) G[j] = (j == ru) ? T(1) : T(0);
+#pragma unroll
+            for (int j = 0; j <= NX; ++j) rhs[j] = T(0);
+        }
+        T bcol[NX], pbcol[NX];
+        ld_col<T, NX>(bcol, sB + ru, NU);
+        ld_col<T, NX>(pbcol, sPB + ru, NU);
+        row_mat<T, NX, NU, NU>(G, bcol, sPB);
+        row_mat<T, NX, NX, NX>(*reinterpret_cast<T(*)[NX]>(rhs), pbcol, sA);
+        rhs[NX] = row_dot<T, NX>(bcol, sg, rhs[NX]);
+        int pr;
+        const bool ok = gauss_jordan<T, WS, NU, NX + 1, false>(mask, G, rhs, lane, NU, pr);
+        if (!ok && lane == 0) atomicMin(ws.fail + b, i + 1);
+        if (pr >= 0) {
+            T kr[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) kr[j] = -rhs[j];
+            st_row<T, NX, true>(sK + pr * NX, kr);
+            sk[pr] = -rhs[NX];
+            T *Kw = ws.Kk + st * KL::SIZE;
+            st_row<T, NX, true>(Kw + KL::K + pr * NX, kr);
+            Kw[KL::k + pr] = -rhs[NX];
+            if (out.K != nullptr && (EX || pr < m)) st_row<T, NX, EX>(out.K + st * m * n + pr * n, kr, n);
+            if (out.k != nullptr && (EX || pr < m)) out.k[st * m + pr] = -rhs[NX];
+        }
+    }
+    __syncwarp(mask);
+    T abar[NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) abar[j] = arow[j];
+    row_mat<T, NU, NX, NX>(abar, brow, sK);
+    const T bb = row_dot<T, NU>(brow, sk, cr);
+    if (lane < NX) {
+        T *te = ws.tel + st * TP;
+        st_row<T, NX, true>(te + r * NX, abar);
+        te[NX * NX + r] = bb;
+    }
+}
+
+// ------------------------------------------------------------ forward scan (Eq. 14-15, R6)
+// Elements a_i = (Abar_i, bbar_i), i = 0..N; a_0 is anchored at dx_0 (Abar_{0,1} = 0,
+// bbar_{0,1} = Abar_0 dx_0 + bbar_0).  Composition (a then b) = (Abar_b Abar_a, Abar_b bbar_a + bbar_b).
+// Prefix a_0 (+) ... (+) a_i = (0, dx_{i+1}).  Same chunked Blelloch structure as k_scan_bwd.
+template <typename T, int NX>
+struct FwdSmem {
+    T t1[TE<NX>::SIZE];
+    T t2[TE<NX>::SIZE];
+};
+
+template <typename T, int NX>
+__global__ void __launch_bounds__(256) k_scan_fwd(const T *dx0, int B, int N, int n, int chunk, int J, int Pf, int W,
+                                                   int IPB, LqWork<T> ws, T *dx_out) {
+    constexpr int WS = worker_width(NX);
+    using TL = TE<NX>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int WI = W * WS, ib = threadIdx.x / WI, w = (threadIdx.x % WI) / WS, lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    FwdSmem<T, NX> &s = reinterpret_cast<FwdSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    int *kind = reinterpret_cast<int *>(smraw + IPB * W * sizeof(FwdSmem<T, NX>)) + ib * Pf;
+    const int b = blockIdx.x * IPB + ib, Lf = N + 1;
+    const bool active = b < B;
+    const int b_ = active ? b : 0;
+    const T *E = ws.tel + (size_t)b_ * Lf * TL::SIZE;
+    T *Y = ws.tslots + (size_t)b_ * Pf * TL::SIZE;
+    T *X = ws.dxw + (size_t)b_ * (N + 2) * NX;
+    T *Xo = dx_out + (size_t)b_ * (N + 2) * n;
+    const int wv = active ? w : (INT_MAX / 2);  // inactive instances skip all work but reach every barrier
+    const int r = lane < NX ? lane : 0;
+    const bool EXn = (n == NX);
+    auto put_dx = [&](int node, T v) {
+        if (lane < NX) {
+            X[node * NX + r] = v;
+            if (EXn || r < n) Xo[(size_t)node * n + r] = v;
+        }
+    };
+    // vector fold x <- Abar_i x + bbar_i over [lo, hi), x in s.t2[TL::b..]
+    auto fold = [&](int lo, int hi) {
+        for (int i = lo; i < hi; ++i) {
+            T arow[NX];
+            ld_row<T, NX, true>(arow, E + (size_t)i * TL::SIZE + r * NX);
+            const T v = row_dot<T, NX>(arow, s.t2 + TL::b, E[(size_t)i * TL::SIZE + TL::b + r]);
+            __syncwarp(mask);
+            if (lane < NX) s.t2[TL::b + r] = v;
+            put_dx(i + 1, v);
+            __syncwarp(mask);
+        }
+    };
+    // ---------------- phase 1
+    for (int j = wv; j < J; j += W) {
+        const int lo = j * chunk, hi = min(lo + chunk, Lf);
+        if (j == 0) {
+            const T x0 = (EXn || r < n) ? dx0[(size_t)b_ * n + r] : T(0);
+            if (lane < NX) s.t2[TL::b + r] = x0;
+            put_dx(0, x0);
+            __syncwarp(mask);
+            fold(lo, hi);
+            if (J > 1 && lane < NX) Y[TL::b + r] = s.t2[TL::b + r];
+            if (lane == 0 && J > 1) kind[0] = SLOT_ANCHOR;
+        } else {
+            wcopy<T, TL::SIZE, WS>(s.t2, E + (size_t)lo * TL::SIZE, lane);
+            __syncwarp(mask);
+            for (int i = lo + 1; i < hi; ++i) {
+                T arow[NX], ao[NX];
+                ld_row<T, NX, true>(arow, E + (size_t)i * TL::SIZE + r * NX);
+                zero(ao);
+                row_mat<T, NX, NX, NX>(ao, arow, s.t2 + TL::A);
+                const T bo = row_dot<T, NX>(arow, s.t2 + TL::b, E[(size_t)i * TL::SIZE + TL::b + r]);
+                __syncwarp(mask);
+                if (lane < NX) { st_row<T, NX, true>(s.t2 + TL::A + r * NX, ao); s.t2[TL::b + r] = bo; }
+                __syncwarp(mask);
+            }
+            wcopy<T, TL::SIZE, WS>(Y + (size_t)j * TL::SIZE, s.t2, lane);
+            if (lane == 0) kind[j] = SLOT_GENERAL;
+        }
+        __syncwarp(mask);
+    }
+    for (int t = J + (threadIdx.x % WI); t < Pf; t += WI) kind[t] = SLOT_IDENT;
+    __syncthreads();
+    if (J > 1) {
+        // up-sweep: Y[k] = Y[k-d] (+) Y[k]  (apply Y[k-d] first)
+        for (int d = 1; d < Pf; d <<= 1) {
+            const int np = Pf / (2 * d);
+            for (int q = wv; q < np; q += W) {
+                const int k = 2 * d * (q + 1) - 1, kl = k - d;
+                const int kk = kind[k], kp = kind[kl];
+                __syncwarp(mask);
+                T *Yk = Y + (size_t)k * TL::SIZE, *Yl = Y + (size_t)kl * TL::SIZE;
+                if (kp == SLOT_IDENT) {
+                } else if (kk == SLOT_IDENT) {
+                    wcopy<T, TL::SIZE, WS>(Yk, Yl, lane);
+                    if (lane == 0) kind[k] = kp;
+                } else {
+                    wcopy<T, TL::SIZE, WS>(s.t1, Yl, lane);
+                    wcopy<T, TL::SIZE, WS>(s.t2, Yk, lane);
+                    __syncwarp(mask);
+                    T arow[NX];
+                    ld_row<T, NX, true>(arow, s.t2 + TL::A + r * NX);
+                    const T bo = row_dot<T, NX>(arow, s.t1 + TL::b, s.t2[TL::b + r]);
+                    if (kp == SLOT_ANCHOR) {
+                        if (lane < NX) Yk[TL::b + r] = bo;
+                        if (lane == 0) kind[k] = SLOT_ANCHOR;
+                    } else {
+                        T ao[NX];
+                        zero(ao);
+                        row_mat<T, NX, NX, NX>(ao, arow, s.t1 + TL::A);
+                        if (lane < NX) { st_row<T, NX, true>(Yk + TL::A + r * NX, ao); Yk[TL::b + r] = bo; }
+                    }
+                }
+                __syncwarp(mask);
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x % WI == 0) kind[Pf - 1] = SLOT_IDENT;
+        __syncthreads();
+        // down-sweep: t = Y[kl]; Y[kl] = Y[k]; Y[k] = Y[k] (+) t  (prefix first, then t)
+        for (int d = Pf / 2; d >= 1; d >>= 1) {
+            const int np = Pf / (2 * d);
+            for (int q = wv; q < np; q += W) {
+                const int k = 2 * d * (q + 1) - 1, kl = k - d;
+                const int kE = kind[k], kt = kind[kl];
+                __syncwarp(mask);
+                T *Yk = Y + (size_t)k * TL::SIZE, *Yl = Y + (size_t)kl * TL::SIZE;
+                wcopy<T, TL::SIZE, WS>(s.t1, Yl, lane);
+                wcopy<T, TL::SIZE, WS>(s.t2, Yk, lane);
+                __syncwarp(mask);
+                wcopy<T, TL::SIZE, WS>(Yl, s.t2, lane);
+                if (kE == SLOT_IDENT) {
+                    wcopy<T, TL::SIZE, WS>(Yk, s.t1, lane);
+                    if (lane == 0) { kind[kl] = kE; kind[k] = kt; }
+                } else if (kt == SLOT_IDENT) {
+                    if (lane == 0) { kind[kl] = kE; kind[k] = kE; }
+                } else {  // prefix (anchored vector) then t
+                    T arow[NX];
+                    ld_row<T, NX, true>(arow, s.t1 + TL::A + r * NX);
+                    const T bo = row_dot<T, NX>(arow, s.t2 + TL::b, s.t1[TL::b + r]);
+                    if (lane < NX) Yk[TL::b + r] = bo;
+                    if (lane == 0) { kind[kl] = kE; kind[k] = SLOT_ANCHOR; }
+                }
+                __syncwarp(mask);
+            }
+            __syncthreads();
+        }
+        // phase 3
+        for (int j = wv > 0 ? wv : W; j < J; j += W) {
+            const int lo = j * chunk, hi = min(lo + chunk, Lf);
+            if (lane < NX) s.t2[TL::b + r] = Y[(size_t)j * TL::SIZE + TL::b + r];
+            __syncwarp(mask);
+            fold(lo, hi);
+        }
+    }
+}
+
+// ------------------------------------------------------------ tail: du (Eq. 6), dlam (Eq. 7)
+template <typename T, int NX, int NU>
+__global__ void k_tail(int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {
+    using KL = KE<NX, NU>;
+    constexpr int TP = TE<NX>::SIZE;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long per = (long)(N + 1) * m + (long)(N + 2) * n;
+    if (t >= (long)B * per) return;
+    const int b = (int)(t / per);
+    int rem = (int)(t % per);
+    const T *x = ws.dxw + (size_t)b * (N + 2) * NX;
+    T v;
+    bool bad;
+    if (rem < (N + 1) * m) {
+        const int i = rem / m, a = rem % m;
+        const T *K = ws.Kk + ((size_t)b * (N + 1) + i) * KL::SIZE;
+        v = K[KL::k + a];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) v = fma(K[KL::K + a * NX + j], x[i * NX + j], v);
+        out.du[(size_t)b * (N + 1) * m + rem] = v;
+        bad = !isfinite(v) || !isfinite(x[i * NX + (a < n ? a : 0)]);
+    } else {
+        rem -= (N + 1) * m;
+        const int i = rem / n, a = rem % n;
+        const T *Pp = ws.Pp + ((size_t)b * (N + 2) + i) * TP;
+        v = Pp[NX * NX + a];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) v = fma(Pp[a * NX + j], x[i * NX + j], v);
+        out.dlam[(size_t)b * (N + 2) * n + rem] = v;
+        bad = !isfinite(v) || !isfinite(x[i * NX + a]);
+    }
+    if (bad) ws.nonfin[b] = 1;
+}
+
+// info[b] = factorisation failure stage (k > 0), else -1 if a non-finite output, else 0.
+__global__ void k_finalize_info(int B, const int32_t *fail, const int32_t *nonfin, const int32_t *pre,
+                                       int32_t *info) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    int v = fail[b] != INT_MAX ? fail[b] : (nonfin[b] ? -1 : 0);
+    if (pre != nullptr && pre[b] != 0) v = pre[b];
+    info[b] = v;
+}
+
+}  // namespace pdilqr

@@ -1,0 +1,504 @@
+// pdilqr.cu -- host side of libpdilqr.so: the C ABI of include/pdilqr.h.
+// Validation, workspace carve-up, kernel dispatch and launch sequencing.  No allocation, no host
+// synchronisation in linearize / solve_lq / step (CUDA-graph capturable).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdarg>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "pdilqr.h"
+#include "lq.cuh"
+#include "srbd.cuh"
+
+using namespace pdilqr;
+
+namespace {
+
+thread_local std::string g_err = "ok";
+
+pdilqr_status fail(pdilqr_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+pdilqr_status fail(pdilqr_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+constexpr size_t kAlign = 256;
+constexpr int kMaxAlpha = 15;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+int pow2ceil(int x) {
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Kernel instantiation chosen for (n, m): exact 12x12 (SRBD) or a zero-padded bound.
+enum Variant { V12 = 0, V4 = 1, V8 = 2, V16 = 3 };
+
+bool pick_variant(int n, int m, Variant &v, int &NX, int &NU) {
+    if (n == 12 && m == 12) { v = V12; NX = NU = 12; return true; }
+    const int d = std::max(n, m);
+    if (d <= 4) { v = V4; NX = NU = 4; return true; }
+    if (d <= 8) { v = V8; NX = NU = 8; return true; }
+    if (d <= 16) { v = V16; NX = NU = 16; return true; }
+    return false;
+}
+
+struct Layout {
+    size_t elems, vslots, Pp, Kk, tel, tslots, dxw, fail, nonfin, pre, info_tmp, stats;
+    size_t qp[11];  // SRBD internal QP buffers (A, Bm, c, Q, R, S, q, r, Pt, pt, dx0)
+    size_t dir[3];  // internal direction (dx, du, dlam)
+    size_t total;
+};
+
+}  // namespace
+
+struct pdilqr_ctx {
+    pdilqr_config cfg;
+    int device;
+    Variant var;
+    int NX, NU, esz;
+    int chunk, Jb, Pv, Jf, Pf;
+    char *ws;
+    size_t ws_bytes;
+    Layout lay;
+    SrbdConst K;
+    int launches;
+};
+
+namespace {
+
+pdilqr_status check_cfg(const pdilqr_config *c, Variant &v, int &NX, int &NU) {
+    if (!c) return fail(PDILQR_ERR_INVALID_ARG, "cfg is NULL");
+    if (c->N < 0 || c->batch < 1 || c->n < 1 || c->m < 1)
+        return fail(PDILQR_ERR_DIM, "invalid dimensions N=%d n=%d m=%d batch=%d", c->N, c->n, c->m, c->batch);
+    if (c->dtype != PDILQR_F32 && c->dtype != PDILQR_F64) return fail(PDILQR_ERR_INVALID_ARG, "unknown dtype %d", (int)c->dtype);
+    if (c->model != PDILQR_MODEL_LQ && c->model != PDILQR_MODEL_SRBD)
+        return fail(PDILQR_ERR_INVALID_ARG, "unknown model %d", (int)c->model);
+    if (c->model == PDILQR_MODEL_SRBD && (c->n != 12 || c->m != 12))
+        return fail(PDILQR_ERR_DIM, "SRBD model needs n = m = 12 (got %d, %d)", c->n, c->m);
+    if (c->n_alpha < 0 || c->n_alpha > kMaxAlpha) return fail(PDILQR_ERR_INVALID_ARG, "n_alpha must be in [0, %d]", kMaxAlpha);
+    if (c->leaf_chunk < 0) return fail(PDILQR_ERR_INVALID_ARG, "leaf_chunk must be >= 0");
+    if (!pick_variant(c->n, c->m, v, NX, NU))
+        return fail(PDILQR_ERR_UNSUPPORTED, "n = %d, m = %d: dimensions above 16 are not supported by this build", c->n, c->m);
+    if (c->model == PDILQR_MODEL_SRBD) {
+        const auto &s = c->srbd;
+        if (!(s.dt >= 0) || !(s.mass > 0) || !(s.barrier_mu > 0) || !(s.barrier_delta > 0))
+            return fail(PDILQR_ERR_INVALID_ARG, "invalid SRBD parameters (dt >= 0, mass > 0, barrier mu, delta > 0)");
+    }
+    return PDILQR_OK;
+}
+
+int default_chunk(const pdilqr_config *c) {
+    if (c->leaf_chunk > 0) return c->leaf_chunk;
+    // Batch-parallelism already fills 148 SMs for large B: fold each instance in one chunk.
+    // For small B use the full tree (span 2 ceil(log2 L)).  See DESIGN.md "Scan schedule".
+    return c->batch >= 148 ? c->N + 2 : 1;
+}
+
+Layout make_layout(const pdilqr_config *c, int NX, int NU, int esz, int chunk, int &Jb, int &Pv, int &Jf, int &Pf) {
+    const size_t B = c->batch, N = c->N;
+    const size_t VEs = 3 * NX * NX + 2 * NX, TEs = NX * NX + NX, KEs = NU * NX + NU;
+    Jb = (int)((N + 2 + chunk - 1) / chunk);
+    Jf = (int)((N + 1 + chunk - 1) / chunk);
+    Pv = Jb > 1 ? pow2ceil(Jb) : 1;
+    Pf = Jf > 1 ? pow2ceil(Jf) : 1;
+    Layout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
+    L.elems = take(B * (N + 2) * VEs * esz);
+    L.vslots = take(B * (Jb > 1 ? Pv : 0) * VEs * esz);
+    L.Pp = take(B * (N + 2) * TEs * esz);
+    L.Kk = take(B * (N + 1) * KEs * esz);
+    L.tel = take(B * (N + 1) * TEs * esz);
+    L.tslots = take(B * (Jf > 1 ? Pf : 0) * TEs * esz);
+    L.dxw = take(B * (N + 2) * NX * esz);
+    L.fail = take(B * 4);
+    L.nonfin = take(B * 4);
+    L.pre = take(B * 4);
+    L.info_tmp = take(B * 4);
+    L.stats = take(B * (3 * (size_t)esz + 8));
+    const size_t n = c->n, m = c->m;
+    if (c->model == PDILQR_MODEL_SRBD) {
+        const size_t sz[11] = {(N + 1) * n * n, (N + 1) * n * m, (N + 1) * n, (N + 1) * n * n, (N + 1) * m * m,
+                               (N + 1) * m * n, (N + 1) * n, (N + 1) * m, n * n, n, n};
+        for (int k = 0; k < 11; ++k) L.qp[k] = take(B * sz[k] * esz);
+        L.dir[0] = take(B * (N + 2) * n * esz);
+        L.dir[1] = take(B * (N + 1) * m * esz);
+        L.dir[2] = take(B * (N + 2) * n * esz);
+    }
+    L.total = off;
+    return L;
+}
+
+template <typename T>
+LqWork<T> work(pdilqr_ctx *h) {
+    LqWork<T> w;
+    w.elems = reinterpret_cast<T *>(h->ws + h->lay.elems);
+    w.vslots = reinterpret_cast<T *>(h->ws + h->lay.vslots);
+    w.Pp = reinterpret_cast<T *>(h->ws + h->lay.Pp);
+    w.Kk = reinterpret_cast<T *>(h->ws + h->lay.Kk);
+    w.tel = reinterpret_cast<T *>(h->ws + h->lay.tel);
+    w.tslots = reinterpret_cast<T *>(h->ws + h->lay.tslots);
+    w.dxw = reinterpret_cast<T *>(h->ws + h->lay.dxw);
+    w.fail = reinterpret_cast<int32_t *>(h->ws + h->lay.fail);
+    w.nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
+    return w;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int d) {
+        cudaGetDevice(&prev);
+        if (prev != d) cudaSetDevice(d);
+    }
+    ~DeviceGuard() {
+        int cur;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+pdilqr_status cuda_check(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(PDILQR_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    return PDILQR_OK;
+}
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// --------------------------------------------------------------------------- LQ pipeline
+template <typename T, int NX, int NU, bool EX>
+pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, const int32_t *pre,
+                     cudaStream_t st) {
+    constexpr int WS = worker_width(NX > NU ? NX : NU);
+    constexpr int WSX = worker_width(NX);
+    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
+    LqWork<T> ws = work<T>(h);
+    cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
+    cudaMemsetAsync(ws.nonfin, 0, (size_t)B * 4, st);
+    int launches = 0;
+    {  // element init
+        const int wpb = 128 / WS;
+        const long nw = (long)B * (N + 2);
+        const size_t smem = (size_t)wpb * (2 * NU * NX + round_up4(NU)) * sizeof(T);
+        set_smem(k_elem_init<T, NX, NU, EX>, smem);
+        k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
+        ++launches;
+    }
+    {  // backward scan
+        const int J = h->Jb, Pv = h->Pv;
+        const size_t cs = sizeof(CombineSmem<T, NX>);
+        int W = 1, IPB = 8;
+        if (J > 1) {
+            W = std::max(J - 1, Pv / 2);
+            W = std::min({W, (int)(200 * 1024 / cs), 256 / WSX});
+            W = std::max(W, 1);
+            IPB = std::max(1, std::min(8, 128 / (W * WSX)));
+        }
+        const size_t smem = (size_t)IPB * W * cs + (size_t)IPB * Pv * sizeof(int);
+        set_smem(k_scan_bwd<T, NX>, smem);
+        k_scan_bwd<T, NX><<<(B + IPB - 1) / IPB, IPB * W * WSX, smem, st>>>(B, N, h->chunk, J, Pv, W, IPB, ws);
+        ++launches;
+    }
+    {  // policy
+        const int wpb = 128 / WS;
+        const long nw = (long)B * (N + 1);
+        const size_t smem = (size_t)wpb * (NX * NU + NX * NX + NX * NU + NU * NX + round_up4(NU) + NX + NX) * sizeof(T);
+        set_smem(k_policy<T, NX, NU, EX>, smem);
+        k_policy<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws, out);
+        ++launches;
+    }
+    {  // forward scan
+        const int J = h->Jf, Pf = h->Pf;
+        const size_t cs = sizeof(FwdSmem<T, NX>);
+        int W = 1, IPB = 8;
+        if (J > 1) {
+            W = std::max(J, Pf / 2);
+            W = std::min({W, (int)(200 * 1024 / cs), 256 / WSX});
+            W = std::max(W, 1);
+            IPB = std::max(1, std::min(8, 128 / (W * WSX)));
+        }
+        const size_t smem = (size_t)IPB * W * cs + (size_t)IPB * Pf * sizeof(int);
+        set_smem(k_scan_fwd<T, NX>, smem);
+        k_scan_fwd<T, NX><<<(B + IPB - 1) / IPB, IPB * W * WSX, smem, st>>>(qp.dx0, B, N, n, h->chunk, J, Pf, W, IPB, ws,
+                                                                            out.dx);
+        ++launches;
+    }
+    {  // du, dlam
+        const long tot = (long)B * ((long)(N + 1) * m + (long)(N + 2) * n);
+        k_tail<T, NX, NU><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(B, N, n, m, ws, out);
+        ++launches;
+    }
+    if (info) {
+        k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, ws.nonfin, pre, info);
+        ++launches;
+    }
+    h->launches += launches;
+    return cuda_check("solve_lq launch");
+}
+
+template <typename T>
+pdilqr_status dispatch_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, const int32_t *pre,
+                          cudaStream_t st) {
+    switch (h->var) {
+        case V12: return run_lq<T, 12, 12, true>(h, qp, out, info, pre, st);
+        case V4: return run_lq<T, 4, 4, false>(h, qp, out, info, pre, st);
+        case V8: return run_lq<T, 8, 8, false>(h, qp, out, info, pre, st);
+        default: return run_lq<T, 16, 16, false>(h, qp, out, info, pre, st);
+    }
+}
+
+template <typename T>
+LqArgs<T> internal_qp(pdilqr_ctx *h) {
+    auto p = [&](int k) { return reinterpret_cast<const T *>(h->ws + h->lay.qp[k]); };
+    return LqArgs<T>{p(0), p(1), p(2), p(3), p(4), p(5), p(6), p(7), p(8), p(9), p(10)};
+}
+
+template <typename T>
+SrbdIter<T> iter_of(const pdilqr_iterate *it) {
+    return SrbdIter<T>{reinterpret_cast<const T *>(it->x),    reinterpret_cast<const T *>(it->u),
+                       reinterpret_cast<const T *>(it->lam),  reinterpret_cast<const T *>(it->x0),
+                       reinterpret_cast<const T *>(it->x_ref), reinterpret_cast<const T *>(it->u_ref),
+                       it->contact,                           reinterpret_cast<const T *>(it->feet)};
+}
+
+template <typename T>
+pdilqr_status run_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArgs<T> &outq, int32_t *pre,
+                            cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N;
+    cudaMemsetAsync(pre, 0, (size_t)B * 4, st);
+    const long nw = (long)B * (N + 2);
+    k_srbd_linearize<T><<<(unsigned)((nw + 7) / 8), 128, 0, st>>>(h->K, iter_of<T>(it), B, N, outq, pre);
+    h->launches += 1;
+    return cuda_check("linearize launch");
+}
+
+template <typename T>
+pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N;
+    LqArgs<T> qp = internal_qp<T>(h);
+    int32_t *pre = reinterpret_cast<int32_t *>(h->ws + h->lay.pre);
+    int32_t *info_tmp = reinterpret_cast<int32_t *>(h->ws + h->lay.info_tmp);
+    pdilqr_status s = run_linearize<T>(h, it, qp, pre, st);
+    if (s != PDILQR_OK) return s;
+    LqOut<T> out;
+    if (dir && dir->dx) {
+        out = LqOut<T>{(T *)dir->dx, (T *)dir->du, (T *)dir->dlam, (T *)dir->K, (T *)dir->k};
+    } else {
+        out = LqOut<T>{reinterpret_cast<T *>(h->ws + h->lay.dir[0]), reinterpret_cast<T *>(h->ws + h->lay.dir[1]),
+                       reinterpret_cast<T *>(h->ws + h->lay.dir[2]), nullptr, nullptr};
+    }
+    s = dispatch_lq<T>(h, qp, out, info_tmp, pre, st);
+    if (s != PDILQR_OK) return s;
+    LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
+    k_srbd_linesearch<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, out.dx, out.du, out.dlam, info_tmp, so);
+    h->launches += 1;
+    return cuda_check("step launch");
+}
+
+void inv3(const double *M, double *Mi) {
+    const double a = M[0], b = M[1], c = M[2], d = M[3], e = M[4], f = M[5], g = M[6], hh = M[7], i = M[8];
+    const double det = a * (e * i - f * hh) - b * (d * i - f * g) + c * (d * hh - e * g);
+    Mi[0] = (e * i - f * hh) / det; Mi[1] = (c * hh - b * i) / det; Mi[2] = (b * f - c * e) / det;
+    Mi[3] = (f * g - d * i) / det;  Mi[4] = (a * i - c * g) / det;  Mi[5] = (c * d - a * f) / det;
+    Mi[6] = (d * hh - e * g) / det; Mi[7] = (b * g - a * hh) / det; Mi[8] = (a * e - b * d) / det;
+}
+
+}  // namespace
+
+// ==================================================================================== C ABI
+extern "C" {
+
+int32_t pdilqr_abi_version(void) { return PDILQR_ABI_VERSION; }
+
+const char *pdilqr_last_error(void) { return g_err.c_str(); }
+
+int32_t pdilqr_last_launch_count(pdilqr_handle h) { return h ? h->launches : 0; }
+
+pdilqr_status pdilqr_workspace_bytes(const pdilqr_config *cfg, size_t *bytes) {
+    Variant v;
+    int NX, NU;
+    pdilqr_status s = check_cfg(cfg, v, NX, NU);
+    if (s != PDILQR_OK) return s;
+    if (!bytes) return fail(PDILQR_ERR_INVALID_ARG, "bytes is NULL");
+    int Jb, Pv, Jf, Pf;
+    const int esz = cfg->dtype == PDILQR_F32 ? 4 : 8;
+    *bytes = make_layout(cfg, NX, NU, esz, default_chunk(cfg), Jb, Pv, Jf, Pf).total;
+    return PDILQR_OK;
+}
+
+pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspace, size_t bytes, pdilqr_handle *out) {
+    Variant v;
+    int NX, NU;
+    pdilqr_status s = check_cfg(cfg, v, NX, NU);
+    if (s != PDILQR_OK) return s;
+    if (!out) return fail(PDILQR_ERR_INVALID_ARG, "out is NULL");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+        return fail(PDILQR_ERR_CUDA, "no CUDA device %d (count %d)", device, ndev);
+    const int esz = cfg->dtype == PDILQR_F32 ? 4 : 8;
+    const int chunk = default_chunk(cfg);
+    int Jb, Pv, Jf, Pf;
+    Layout L = make_layout(cfg, NX, NU, esz, chunk, Jb, Pv, Jf, Pf);
+    if (!workspace || bytes < L.total)
+        return fail(PDILQR_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", bytes, L.total);
+    if (reinterpret_cast<uintptr_t>(workspace) % kAlign)
+        return fail(PDILQR_ERR_WORKSPACE, "workspace must be %zu-byte aligned", kAlign);
+    pdilqr_ctx *h = new (std::nothrow) pdilqr_ctx();
+    if (!h) return fail(PDILQR_ERR_INVALID_ARG, "out of host memory");
+    h->cfg = *cfg;
+    if (h->cfg.n_alpha == 0) h->cfg.n_alpha = 10;
+    if (h->cfg.armijo_c1 == 0) h->cfg.armijo_c1 = 1e-4;
+    if (h->cfg.theta_max <= 0) h->cfg.theta_max = 1e-2 * (cfg->N + 1);
+    h->device = device;
+    h->var = v;
+    h->NX = NX;
+    h->NU = NU;
+    h->esz = esz;
+    h->chunk = chunk;
+    h->Jb = Jb; h->Pv = Pv; h->Jf = Jf; h->Pf = Pf;
+    h->ws = static_cast<char *>(workspace);
+    h->ws_bytes = bytes;
+    h->lay = L;
+    h->launches = 0;
+    SrbdConst &K = h->K;
+    std::memset(&K, 0, sizeof K);
+    const pdilqr_srbd_params &p = cfg->srbd;
+    K.dt = p.dt; K.mass = p.mass;
+    for (int k = 0; k < 9; ++k) K.I[k] = p.inertia[k];
+    inv3(p.inertia, K.Iinv);
+    for (int k = 0; k < 3; ++k) K.g[k] = p.gravity[k];
+    for (int k = 0; k < 12; ++k) { K.wx[k] = p.w_x[k]; K.wxt[k] = p.w_x_term[k]; }
+    K.wu_st = p.w_u_stance; K.wu_sw = p.w_u_swing;
+    K.mu = p.mu_friction; K.fmin = p.f_min; K.fmax = p.f_max; K.bmu = p.barrier_mu; K.bdelta = p.barrier_delta;
+    K.theta_max = h->cfg.theta_max; K.c1 = h->cfg.armijo_c1; K.n_alpha = h->cfg.n_alpha;
+    *out = h;
+    return PDILQR_OK;
+}
+
+pdilqr_status pdilqr_destroy(pdilqr_handle h) {
+    delete h;
+    return PDILQR_OK;
+}
+
+pdilqr_status pdilqr_solve_lq(pdilqr_handle h, const pdilqr_lq *qp, pdilqr_dir *dir, int32_t *info, void *stream) {
+    if (!h || !qp || !dir) return fail(PDILQR_ERR_INVALID_ARG, "NULL handle, qp or dir");
+    const void *ptrs[] = {qp->A, qp->Bm, qp->c, qp->Q, qp->R, qp->S, qp->q, qp->r, qp->P_term, qp->p_term, qp->dx0,
+                          dir->dx, dir->du, dir->dlam};
+    for (const void *p : ptrs) {
+        if (!p) return fail(PDILQR_ERR_INVALID_ARG, "NULL array in qp / dir");
+        if (!aligned16(p)) return fail(PDILQR_ERR_INVALID_ARG, "arrays must be 16-byte aligned");
+    }
+    DeviceGuard g(h->device);
+    h->launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (h->cfg.dtype == PDILQR_F32) {
+        LqArgs<float> a{(const float *)qp->A, (const float *)qp->Bm, (const float *)qp->c, (const float *)qp->Q,
+                        (const float *)qp->R, (const float *)qp->S, (const float *)qp->q, (const float *)qp->r,
+                        (const float *)qp->P_term, (const float *)qp->p_term, (const float *)qp->dx0};
+        LqOut<float> o{(float *)dir->dx, (float *)dir->du, (float *)dir->dlam, (float *)dir->K, (float *)dir->k};
+        return dispatch_lq<float>(h, a, o, info, nullptr, st);
+    }
+    LqArgs<double> a{(const double *)qp->A, (const double *)qp->Bm, (const double *)qp->c, (const double *)qp->Q,
+                     (const double *)qp->R, (const double *)qp->S, (const double *)qp->q, (const double *)qp->r,
+                     (const double *)qp->P_term, (const double *)qp->p_term, (const double *)qp->dx0};
+    LqOut<double> o{(double *)dir->dx, (double *)dir->du, (double *)dir->dlam, (double *)dir->K, (double *)dir->k};
+    return dispatch_lq<double>(h, a, o, info, nullptr, st);
+}
+
+static pdilqr_status check_iter(pdilqr_handle h, const pdilqr_iterate *it) {
+    if (!h || !it) return fail(PDILQR_ERR_INVALID_ARG, "NULL handle or iterate");
+    if (h->cfg.model != PDILQR_MODEL_SRBD) return fail(PDILQR_ERR_UNSUPPORTED, "handle was not created for the SRBD model");
+    const void *ptrs[] = {it->x, it->u, it->lam, it->x0, it->x_ref, it->contact, it->feet};
+    for (const void *p : ptrs)
+        if (!p) return fail(PDILQR_ERR_INVALID_ARG, "NULL array in iterate");
+    const void *al[] = {it->x, it->u, it->lam, it->x0, it->x_ref, it->feet};
+    for (const void *p : al)
+        if (!aligned16(p)) return fail(PDILQR_ERR_INVALID_ARG, "iterate arrays must be 16-byte aligned");
+    if (it->u_ref && !aligned16(it->u_ref)) return fail(PDILQR_ERR_INVALID_ARG, "u_ref must be 16-byte aligned");
+    return PDILQR_OK;
+}
+
+pdilqr_status pdilqr_linearize(pdilqr_handle h, const pdilqr_iterate *it, pdilqr_lq_buf *out, int32_t *info,
+                               void *stream) {
+    pdilqr_status s = check_iter(h, it);
+    if (s != PDILQR_OK) return s;
+    if (!out) return fail(PDILQR_ERR_INVALID_ARG, "NULL out");
+    void *ptrs[] = {out->A, out->Bm, out->c, out->Q, out->R, out->S, out->q, out->r, out->P_term, out->p_term, out->dx0};
+    for (void *p : ptrs)
+        if (!p || !aligned16(p)) return fail(PDILQR_ERR_INVALID_ARG, "output arrays must be non-NULL and 16-byte aligned");
+    DeviceGuard g(h->device);
+    h->launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int32_t *pre = info ? info : reinterpret_cast<int32_t *>(h->ws + h->lay.pre);
+    if (h->cfg.dtype == PDILQR_F32) {
+        LqArgs<float> o{(float *)out->A, (float *)out->Bm, (float *)out->c, (float *)out->Q, (float *)out->R,
+                        (float *)out->S, (float *)out->q, (float *)out->r, (float *)out->P_term, (float *)out->p_term,
+                        (float *)out->dx0};
+        return run_linearize<float>(h, it, o, pre, st);
+    }
+    LqArgs<double> o{(double *)out->A, (double *)out->Bm, (double *)out->c, (double *)out->Q, (double *)out->R,
+                     (double *)out->S, (double *)out->q, (double *)out->r, (double *)out->P_term, (double *)out->p_term,
+                     (double *)out->dx0};
+    return run_linearize<double>(h, it, o, pre, st);
+}
+
+pdilqr_status pdilqr_step(pdilqr_handle h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, void *stream) {
+    pdilqr_status s = check_iter(h, it);
+    if (s != PDILQR_OK) return s;
+    if (!stats || !stats->cost || !stats->theta || !stats->alpha || !stats->accepted || !stats->info)
+        return fail(PDILQR_ERR_INVALID_ARG, "NULL stats array");
+    if (dir && dir->dx && (!dir->du || !dir->dlam)) return fail(PDILQR_ERR_INVALID_ARG, "dir needs dx, du and dlam");
+    DeviceGuard g(h->device);
+    h->launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (h->cfg.dtype == PDILQR_F32) return run_step<float>(h, it, stats, dir, st);
+    return run_step<double>(h, it, stats, dir, st);
+}
+
+pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *x0_host, void *u0_host, void *cost_host,
+                               void *theta_host, void *alpha_host, int32_t *accepted_host, int32_t *info_host,
+                               void *stream) {
+    pdilqr_status s = check_iter(h, it);
+    if (s != PDILQR_OK) return s;
+    if (!x0_host || !u0_host) return fail(PDILQR_ERR_INVALID_ARG, "NULL host buffer");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t B = h->cfg.batch, N = h->cfg.N, es = h->esz;
+    cudaMemcpyAsync(const_cast<void *>(it->x0), x0_host, B * 12 * es, cudaMemcpyHostToDevice, st);
+    char *sp = h->ws + h->lay.stats;  // device stats scratch of this handle
+    pdilqr_stats ds;
+    ds.cost = sp;
+    ds.theta = sp + B * es;
+    ds.alpha = sp + 2 * B * es;
+    ds.accepted = reinterpret_cast<int32_t *>(sp + 3 * B * es);
+    ds.info = reinterpret_cast<int32_t *>(sp + 3 * B * es + B * 4);
+    h->launches = 0;
+    s = (h->cfg.dtype == PDILQR_F32) ? run_step<float>(h, it, &ds, nullptr, st) : run_step<double>(h, it, &ds, nullptr, st);
+    if (s != PDILQR_OK) return s;
+    cudaMemcpy2DAsync(u0_host, 12 * es, it->u, (N + 1) * 12 * es, 12 * es, B, cudaMemcpyDeviceToHost, st);
+    if (cost_host) cudaMemcpyAsync(cost_host, ds.cost, B * es, cudaMemcpyDeviceToHost, st);
+    if (theta_host) cudaMemcpyAsync(theta_host, ds.theta, B * es, cudaMemcpyDeviceToHost, st);
+    if (alpha_host) cudaMemcpyAsync(alpha_host, ds.alpha, B * es, cudaMemcpyDeviceToHost, st);
+    if (accepted_host) cudaMemcpyAsync(accepted_host, ds.accepted, B * 4, cudaMemcpyDeviceToHost, st);
+    if (info_host) cudaMemcpyAsync(info_host, ds.info, B * 4, cudaMemcpyDeviceToHost, st);
+    return cuda_check("tick_host");
+}
+
+}  // extern "C"

@@ -1,0 +1,248 @@
+"""Thin Python binding of libpdilqr.so (include/pdilqr.h).  Argument marshalling only: every step
+of the hot path runs in the library's CUDA kernels.  PyTorch provides device memory (the
+workspace and all arrays are torch tensors), the CUDA stream and process groups.
+
+There is no CPU fallback: if the shared library is missing or fails to load, every entry point
+raises.  Names follow include/pdilqr.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+from . import build as _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpdilqr.so")
+
+PDILQR_F32, PDILQR_F64 = 0, 1
+PDILQR_MODEL_LQ, PDILQR_MODEL_SRBD = 0, 1
+STATUS = {0: "PDILQR_OK", 1: "PDILQR_ERR_INVALID_ARG", 2: "PDILQR_ERR_DIM", 3: "PDILQR_ERR_WORKSPACE",
+          4: "PDILQR_ERR_CUDA", 5: "PDILQR_ERR_UNSUPPORTED"}
+
+EXPORTED = ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
+            "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host", "pdilqr_last_launch_count",
+            "pdilqr_last_error", "pdilqr_abi_version")
+
+
+class SrbdParams(C.Structure):
+    _fields_ = [("dt", C.c_double), ("mass", C.c_double), ("inertia", C.c_double * 9),
+                ("gravity", C.c_double * 3), ("w_x", C.c_double * 12), ("w_x_term", C.c_double * 12),
+                ("w_u_stance", C.c_double), ("w_u_swing", C.c_double), ("mu_friction", C.c_double),
+                ("f_min", C.c_double), ("f_max", C.c_double), ("barrier_mu", C.c_double),
+                ("barrier_delta", C.c_double)]
+
+
+class Config(C.Structure):
+    _fields_ = [("N", C.c_int32), ("n", C.c_int32), ("m", C.c_int32), ("batch", C.c_int32),
+                ("dtype", C.c_int), ("model", C.c_int), ("n_alpha", C.c_int32), ("armijo_c1", C.c_double),
+                ("theta_max", C.c_double), ("leaf_chunk", C.c_int32), ("export_policy", C.c_int32),
+                ("srbd", SrbdParams)]
+
+
+class Lq(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("A", "Bm", "c", "Q", "R", "S", "q", "r", "P_term", "p_term", "dx0")]
+
+
+class Dir(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("dx", "du", "dlam", "K", "k")]
+
+
+class Iterate(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("x", "u", "lam", "x0", "x_ref", "u_ref", "contact", "feet")]
+
+
+class Stats(C.Structure):
+    _fields_ = [(k, C.c_void_p) for k in ("cost", "theta", "alpha", "accepted", "info")]
+
+
+_lib = None
+
+
+def lib():
+    """Load libpdilqr.so (building it first if sources are newer).  Raises if unavailable."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH) or _build.needs_build():
+            _build.build()
+        L = C.CDLL(LIB_PATH)
+        vp, i32, st = C.c_void_p, C.c_int32, C.c_int
+        L.pdilqr_workspace_bytes.argtypes = [C.POINTER(Config), C.POINTER(C.c_size_t)]
+        L.pdilqr_create.argtypes = [C.POINTER(Config), C.c_int, vp, C.c_size_t, C.POINTER(vp)]
+        L.pdilqr_destroy.argtypes = [vp]
+        L.pdilqr_solve_lq.argtypes = [vp, C.POINTER(Lq), C.POINTER(Dir), vp, vp]
+        L.pdilqr_linearize.argtypes = [vp, C.POINTER(Iterate), C.POINTER(Lq), vp, vp]
+        L.pdilqr_step.argtypes = [vp, C.POINTER(Iterate), C.POINTER(Stats), C.POINTER(Dir), vp]
+        L.pdilqr_tick_host.argtypes = [vp, C.POINTER(Iterate), vp, vp, vp, vp, vp, vp, vp, vp]
+        L.pdilqr_last_launch_count.argtypes = [vp]
+        L.pdilqr_last_launch_count.restype = i32
+        L.pdilqr_last_error.restype = C.c_char_p
+        L.pdilqr_abi_version.restype = i32
+        for f in ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
+                  "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host"):
+            getattr(L, f).restype = st
+        _lib = L
+    return _lib
+
+
+class PdilqrError(RuntimeError):
+    pass
+
+
+def _check(status: int):
+    if status != 0:
+        raise PdilqrError(f"{STATUS.get(status, status)}: {lib().pdilqr_last_error().decode()}")
+
+
+def srbd_params_struct(d: dict | None) -> SrbdParams:
+    p = SrbdParams()
+    if d is None:
+        return p
+    for name, _ in SrbdParams._fields_:
+        v = d[name]
+        if isinstance(v, (list, tuple)):
+            arr = getattr(p, name)
+            for i, e in enumerate(v):
+                arr[i] = float(e)
+        else:
+            setattr(p, name, float(v))
+    return p
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class PdIlqr:
+    """One library handle: fixed (N, n, m, batch, dtype, model) on one CUDA device.
+
+    The workspace is a torch uint8 tensor owned by this object.  All array arguments must be
+    contiguous CUDA tensors of the handle's dtype (contact: uint8) on the handle's device.
+    """
+
+    def __init__(self, N: int, n: int, m: int, batch: int, dtype=torch.float32, model: str = "lq",
+                 srbd: dict | None = None, n_alpha: int = 10, armijo_c1: float = 1e-4, theta_max: float = 0.0,
+                 leaf_chunk: int = 0, device: int | torch.device | None = None):
+        L = lib()
+        self.N, self.n, self.m, self.batch = N, n, m, batch
+        self.dtype = dtype
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   (device.index if isinstance(device, torch.device) else device))
+        cfg = Config(N=N, n=n, m=m, batch=batch, dtype=PDILQR_F32 if dtype == torch.float32 else PDILQR_F64,
+                     model=PDILQR_MODEL_SRBD if model == "srbd" else PDILQR_MODEL_LQ, n_alpha=n_alpha,
+                     armijo_c1=armijo_c1, theta_max=theta_max, leaf_chunk=leaf_chunk, export_policy=0,
+                     srbd=srbd_params_struct(srbd))
+        self._cfg = cfg
+        nb = C.c_size_t()
+        _check(L.pdilqr_workspace_bytes(C.byref(cfg), C.byref(nb)))
+        self.workspace = torch.empty(max(nb.value, 256), dtype=torch.uint8, device=self.device)
+        h = C.c_void_p()
+        _check(L.pdilqr_create(C.byref(cfg), self.device.index, C.c_void_p(self.workspace.data_ptr()),
+                               nb.value, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib is not None:
+            _lib.pdilqr_destroy(h)
+            self._h = None
+
+    # ------------------------------------------------------------------ helpers
+    def _check_t(self, t, shape, dtype=None):
+        dtype = dtype or self.dtype
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == dtype and t.is_contiguous()
+                and t.device == self.device and tuple(t.shape) == tuple(shape)):
+            raise PdilqrError(f"expected contiguous {dtype} tensor of shape {tuple(shape)} on {self.device}, "
+                              f"got {getattr(t, 'dtype', type(t))} {tuple(getattr(t, 'shape', ()))} "
+                              f"on {getattr(t, 'device', None)}")
+        return t
+
+    def _stream(self, stream):
+        s = torch.cuda.current_stream(self.device) if stream is None else stream
+        return C.c_void_p(s.cuda_stream)
+
+    def lq_shapes(self):
+        B, N, n, m = self.batch, self.N, self.n, self.m
+        return {"A": (B, N + 1, n, n), "Bm": (B, N + 1, n, m), "c": (B, N + 1, n), "Q": (B, N + 1, n, n),
+                "R": (B, N + 1, m, m), "S": (B, N + 1, m, n), "q": (B, N + 1, n), "r": (B, N + 1, m),
+                "P_term": (B, n, n), "p_term": (B, n), "dx0": (B, n)}
+
+    def new_direction(self, policy: bool = False):
+        B, N, n, m = self.batch, self.N, self.n, self.m
+        kw = dict(dtype=self.dtype, device=self.device)
+        d = {"dx": torch.empty(B, N + 2, n, **kw), "du": torch.empty(B, N + 1, m, **kw),
+             "dlam": torch.empty(B, N + 2, n, **kw)}
+        if policy:
+            d["K"] = torch.empty(B, N + 1, m, n, **kw)
+            d["k"] = torch.empty(B, N + 1, m, **kw)
+        return d
+
+    # ------------------------------------------------------------------ entry points
+    def solve_lq(self, qp: dict, out: dict | None = None, policy: bool = False, info=None, stream=None):
+        """pdilqr_solve_lq: returns dict dx, du, dlam (+ K, k) and info (int32 [B])."""
+        for k, shp in self.lq_shapes().items():
+            self._check_t(qp[k], shp)
+        out = out if out is not None else self.new_direction(policy)
+        info = info if info is not None else torch.empty(self.batch, dtype=torch.int32, device=self.device)
+        lq = Lq(**{k: _ptr(qp[k]) for k in self.lq_shapes()})
+        d = Dir(dx=_ptr(out["dx"]), du=_ptr(out["du"]), dlam=_ptr(out["dlam"]), K=_ptr(out.get("K")),
+                k=_ptr(out.get("k")))
+        _check(lib().pdilqr_solve_lq(self._h, C.byref(lq), C.byref(d), _ptr(info), self._stream(stream)))
+        out["info"] = info
+        return out
+
+    def _iterate(self, it: dict) -> Iterate:
+        B, N = self.batch, self.N
+        self._check_t(it["x"], (B, N + 2, 12)); self._check_t(it["u"], (B, N + 1, 12))
+        self._check_t(it["lam"], (B, N + 2, 12)); self._check_t(it["x0"], (B, 12))
+        self._check_t(it["x_ref"], (B, N + 2, 12))
+        if it.get("u_ref") is not None:
+            self._check_t(it["u_ref"], (B, N + 1, 12))
+        self._check_t(it["contact"], (B, N + 1, 4), torch.uint8)
+        self._check_t(it["feet"], (B, N + 1, 4, 3))
+        return Iterate(**{k: _ptr(it.get(k)) for k in ("x", "u", "lam", "x0", "x_ref", "u_ref", "contact", "feet")})
+
+    def linearize(self, it: dict, out: dict | None = None, info=None, stream=None):
+        """pdilqr_linearize: the Eq. 4 data at the iterate (dict of tensors) and info."""
+        if out is None:
+            out = {k: torch.empty(s, dtype=self.dtype, device=self.device) for k, s in self.lq_shapes().items()}
+        info = info if info is not None else torch.empty(self.batch, dtype=torch.int32, device=self.device)
+        itc = self._iterate(it)
+        lq = Lq(**{k: _ptr(out[k]) for k in self.lq_shapes()})
+        _check(lib().pdilqr_linearize(self._h, C.byref(itc), C.byref(lq), _ptr(info), self._stream(stream)))
+        out["info"] = info
+        return out
+
+    def new_stats(self):
+        kw = dict(device=self.device)
+        return {"cost": torch.empty(self.batch, dtype=self.dtype, **kw),
+                "theta": torch.empty(self.batch, dtype=self.dtype, **kw),
+                "alpha": torch.empty(self.batch, dtype=self.dtype, **kw),
+                "accepted": torch.empty(self.batch, dtype=torch.int32, **kw),
+                "info": torch.empty(self.batch, dtype=torch.int32, **kw)}
+
+    def step(self, it: dict, stats: dict | None = None, direction: dict | None = None, stream=None):
+        """pdilqr_step: one SQP/RTI iteration, updates it['x'], it['u'], it['lam'] in place."""
+        stats = stats if stats is not None else self.new_stats()
+        itc = self._iterate(it)
+        st = Stats(**{k: _ptr(stats[k]) for k in ("cost", "theta", "alpha", "accepted", "info")})
+        d = None
+        if direction is not None:
+            d = Dir(dx=_ptr(direction["dx"]), du=_ptr(direction["du"]), dlam=_ptr(direction["dlam"]),
+                    K=_ptr(direction.get("K")), k=_ptr(direction.get("k")))
+        _check(lib().pdilqr_step(self._h, C.byref(itc), C.byref(st), C.byref(d) if d is not None else None,
+                                 self._stream(stream)))
+        return stats
+
+    def tick_host(self, it: dict, x0_host, u0_host, stats_host: dict, stream=None):
+        """pdilqr_tick_host: host x0 in, host u0 + stats out (pinned CPU tensors)."""
+        itc = self._iterate(it)
+        _check(lib().pdilqr_tick_host(self._h, C.byref(itc), _ptr(x0_host), _ptr(u0_host),
+                                      _ptr(stats_host["cost"]), _ptr(stats_host["theta"]),
+                                      _ptr(stats_host["alpha"]), _ptr(stats_host["accepted"]),
+                                      _ptr(stats_host["info"]), self._stream(stream)))
+
+    def last_launch_count(self) -> int:
+        return int(lib().pdilqr_last_launch_count(self._h))

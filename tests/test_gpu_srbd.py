@@ -1,0 +1,185 @@
+"""GPU parity of the SRBD path: pdilqr_linearize against the oracle's linearisation, and
+pdilqr_step (linearise -> scans -> parallel filter line search -> update) against the oracle's
+step (sequential Riccati + the same line search), on identical seeded, dtype-rounded inputs."""
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_util import rel, rel_per_instance, rounded, to_device, to_np
+from workloads import synth
+
+pytestmark = pytest.mark.gpu
+
+ITER_KEYS = ("x", "u", "lam", "x0", "x_ref", "u_ref", "contact", "feet")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_07823_b200 as P
+    P.lib()
+    return P
+
+
+def problem(B, N, seed, dtype, perturb=0.0):
+    prob = synth.srbd_problem(B, N=N, seed=seed)
+    if perturb:
+        rng = np.random.default_rng(seed)
+        prob["x"] += perturb * rng.standard_normal(prob["x"].shape) * 0.01
+        prob["u"] += perturb * rng.standard_normal(prob["u"].shape)
+        prob["lam"] += perturb * rng.standard_normal(prob["lam"].shape)
+    return rounded(prob, dtype)
+
+
+def handle(P, prob, dtype, B, N, leaf_chunk=0):
+    return P.PdIlqr(N=N, n=12, m=12, batch=B, dtype=dtype, model="srbd", srbd=prob["params"], leaf_chunk=leaf_chunk)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_linearize_parity(P, O, dtype):
+    B, N = 9, 20
+    prob = problem(B, N, 21, dtype, perturb=1.0)
+    h = handle(P, prob, dtype, B, N)
+    out = h.linearize(to_device({k: prob[k] for k in ITER_KEYS}, dtype))
+    torch.cuda.synchronize()
+    ref = O.srbd_linearize(prob)
+    assert (to_np(out["info"]) == 0).all()
+    tol = 2e-5 if dtype == torch.float32 else 1e-11
+    for k in ("A", "Bm", "Q", "R", "S", "q", "r", "P_term", "p_term", "dx0"):
+        g = to_np(out[k])
+        for b in range(B):
+            assert np.abs(g[b] - ref[k][b]).max() <= tol * max(1.0, np.abs(ref[k][b]).max()), (k, b)
+    # defects b_i = h(x_i, u_i) - x_{i+1}: absolute error relative to the state scale
+    g = to_np(out["c"])
+    assert np.abs(g - ref["c"]).max() <= tol * max(1.0, np.abs(prob["x"]).max())
+
+
+def alpha_ambiguous(O, prob, b, alpha_gpu):
+    """the oracle's decision at alpha_gpu is within 1e-6 relative of its boundary."""
+    _, _, _, _, dx, du, _ = O.srbd_step_single(prob, b)
+    j, Ja, tha, (J0, th0, g) = O.srbd_line_search(prob, b, dx, du)
+    tm = 1e-2 * (prob["x"].shape[1] - 1)
+    for jj in range(10):
+        al = 2.0 ** -jj
+        if al < min(alpha_gpu, 2.0 ** -max(j, 0)) - 1e-12:
+            break
+        if th0 > tm:
+            m = abs(tha[jj] - th0) / max(th0, 1.0)
+        elif g < 0:
+            m = abs(Ja[jj] - (J0 + 1e-4 * al * g)) / max(abs(J0), 1.0)
+        else:
+            m = min(abs(Ja[jj] - J0) / max(abs(J0), 1.0), abs(tha[jj] - th0) / max(th0, 1.0))
+        if m < 1e-6:
+            return True
+    return False
+
+
+def step_parity(P, O, B, N, dtype, seed, perturb=0.0, leaf_chunk=0, steps=1, sample=None):
+    prob = problem(B, N, seed, dtype, perturb)
+    h = handle(P, prob, dtype, B, N, leaf_chunk)
+    dev = to_device({k: prob[k] for k in ITER_KEYS}, dtype)
+    tol = 1e-4 if dtype == torch.float32 else 1e-9
+    for s in range(steps):
+        st = h.step(dev)
+        torch.cuda.synchronize()
+        ref = {k: prob[k].copy() for k in ("x", "u", "lam")}
+        rp = dict(prob); rp.update(ref)
+        idx = range(B) if sample is None else sample
+        stats_ref = np.zeros((B, 5))
+        for b in idx:
+            x, u, lam, st_r, *_ = O.srbd_step_single(rp, b)
+            ref["x"][b], ref["u"][b], ref["lam"][b] = x, u, lam
+            stats_ref[b] = st_r
+        a_gpu = to_np(st["alpha"])
+        assert (to_np(st["info"])[list(idx)] == 0).all()
+        ok = [b for b in idx if a_gpu[b] == stats_ref[b, 2]]
+        bad = [b for b in idx if a_gpu[b] != stats_ref[b, 2]]
+        for b in bad:
+            assert alpha_ambiguous(O, rp, b, a_gpu[b]), (s, b, a_gpu[b], stats_ref[b, 2])
+        for k in ("x", "u", "lam"):
+            g = to_np(dev[k])
+            for b in ok:
+                # the change of the iterate (alpha * direction) is what the solver computes
+                d_gpu = g[b] - prob[k][b]
+                d_ref = ref[k][b] - prob[k][b]
+                if np.abs(d_ref).max() > 0:
+                    assert rel(d_gpu, d_ref) <= tol, (s, k, b, rel(d_gpu, d_ref))
+        for b in ok:
+            assert to_np(st["accepted"])[b] == stats_ref[b, 3]
+            if stats_ref[b, 3]:
+                assert abs(to_np(st["cost"])[b] - stats_ref[b, 0]) <= 1e-4 * max(1.0, abs(stats_ref[b, 0]))
+        # continue from the GPU iterate (both sides consume the same, rounded, values)
+        for k in ("x", "u", "lam"):
+            prob[k] = to_np(dev[k])
+    return prob
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("chunk", [0, 1, 5])
+def test_step_parity_config2(P, O, dtype, chunk):
+    step_parity(P, O, 3, 50, dtype, seed=31, leaf_chunk=chunk, steps=3)
+
+
+def test_step_parity_perturbed_batch(P, O):
+    step_parity(P, O, 64, 50, torch.float32, seed=32, perturb=1.0, steps=2)
+
+
+@pytest.mark.parametrize("N", [0, 1, 7, 100])
+def test_step_parity_horizons(P, O, N):
+    step_parity(P, O, 5, N, torch.float32, seed=33 + N, steps=2)
+
+
+def test_step_full_batch_4096_sampled(P, O):
+    """Config 3 (B=4096, N=50) in the bench launch configuration; sampled instances vs oracle."""
+    idx = [0, 1, 2047, 4095] + list(np.random.default_rng(1).choice(4096, 12, replace=False))
+    step_parity(P, O, 4096, 50, torch.float32, seed=34, steps=1, sample=idx)
+
+
+def test_tick_host_matches_step(P):
+    B, N = 16, 50
+    prob = problem(B, N, 35, torch.float32)
+    h1 = handle(P, prob, torch.float32, B, N)
+    h2 = handle(P, prob, torch.float32, B, N)
+    d1 = to_device({k: prob[k] for k in ITER_KEYS}, torch.float32)
+    d2 = to_device({k: prob[k] for k in ITER_KEYS}, torch.float32)
+    st = h1.step(d1)
+    x0h = torch.from_numpy(prob["x0"].astype(np.float32)).pin_memory()
+    u0h = torch.empty(B, 12).pin_memory()
+    sh = {"cost": torch.empty(B).pin_memory(), "theta": torch.empty(B).pin_memory(),
+          "alpha": torch.empty(B).pin_memory(), "accepted": torch.empty(B, dtype=torch.int32).pin_memory(),
+          "info": torch.empty(B, dtype=torch.int32).pin_memory()}
+    h2.tick_host(d2, x0h, u0h, sh)
+    torch.cuda.synchronize()
+    assert torch.equal(d1["u"][:, 0, :].cpu(), u0h)
+    assert torch.equal(st["alpha"].cpu(), sh["alpha"])
+    assert torch.equal(d1["x"], d2["x"])
+
+
+def test_step_deterministic(P):
+    B, N = 32, 50
+    prob = problem(B, N, 36, torch.float32, perturb=1.0)
+    outs = []
+    for _ in range(2):
+        h = handle(P, prob, torch.float32, B, N)
+        d = to_device({k: prob[k] for k in ITER_KEYS}, torch.float32)
+        st = h.step(d)
+        torch.cuda.synchronize()
+        outs.append((d["x"].clone(), d["u"].clone(), d["lam"].clone(), st["cost"].clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_pitch_guard_info(P):
+    B, N = 3, 10
+    prob = problem(B, N, 37, torch.float32)
+    prob["x"][1, 4, 4] = 1.5
+    h = handle(P, prob, torch.float32, B, N)
+    d = to_device({k: prob[k] for k in ITER_KEYS}, torch.float32)
+    x_before = d["x"].clone()
+    st = h.step(d)
+    torch.cuda.synchronize()
+    info = to_np(st["info"])
+    assert info[1] == -1 and info[0] == 0 and info[2] == 0
+    assert to_np(st["accepted"])[1] == 0 and to_np(st["alpha"])[1] == 0
+    assert torch.equal(d["x"][1], x_before[1])

@@ -1,0 +1,360 @@
+#!/usr/bin/env python
+"""bench.py -- SRBD MPC solves/s at batch 4096, N=50 (BASELINE.json metric) on B200.
+
+One "step" = one batched pdilqr_step (one SQP/RTI iteration): SRBD linearisation ->
+element init -> reverse associative scan -> policy -> forward scan -> dual update -> parallel
+filter line search -> in-place update, for B independent instances per GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--batch B] [--N N]
+  torchrun --nproc-per-node N bench.py --gpus N ...      (weak scaling: B instances per rank)
+
+Prints ONE JSON line (rank 0).  `value` = instances x steps over all ranks / max-over-ranks device
+time of the K timed steps (CUDA events around the stream, barrier + synchronize on both sides).
+`e2e` = the same metric through pdilqr_tick_host with pinned HOST buffers (x0 in, u0 + stats out,
+copies inside the timed region, one synchronisation per tick).  `roofline` = the dominant kernel's
+algorithmic FP32 flops per launch / its average event-timed duration in the timed region, against
+the FP32 CUDA-core peak.  `cpu_baseline` = the fp64 C oracle (OpenMP over
+instances, all host cores) on a bounded sample of the same workload.  --impl reference times that
+oracle as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workloads import synth  # noqa: E402
+
+METRIC = "SRBD MPC solves/s at batch 4096, N=50"
+ITER_KEYS = ("x", "u", "lam", "x0", "x_ref", "u_ref", "contact", "feet")
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128
+
+
+# ---------------------------------------------------------------------------- flop model
+def flops_per_instance(N: int, n: int = 12, m: int = 12, chunk: int | None = None) -> dict:
+    """Algorithmic FP32 flops of one step per instance, per kernel (SURVEY
+    App. B).  Full combine 16.67 n^3 + 8 n^2, cheap combine (suffix right operand) 8.67 n^3 + 4 n^2,
+    element init m^3/3 + 2 m^2 (2n+1) + 6 n^2 m + 4 n m, policy 4 n^2 m + 2 n m^2 + m^3/3 +
+    2 m^2 (n+1) + 2 n^2 + 2 n m + (Abar, bbar) 2 n^2 m + 2 n m, forward combine 2 n^3 + 2 n^2,
+    forward fold 2 n^2, tail (du, dlam) 2 m n + 2 n^2."""
+    L = N + 2
+    Lf = N + 1
+    c = L if (chunk is None or chunk <= 0) else chunk
+    J = -(-L // c)
+    Jf = -(-Lf // c)
+    full = 16.67 * n ** 3 + 8 * n ** 2
+    cheap = 8.67 * n ** 3 + 4 * n ** 2
+    # backward: reductions of chunks 1..J-2 (c-1 full each), last chunk folds, tree over J
+    # summaries (~J full up-sweep + ~J cheap down-sweep), phase-3 folds of chunks 0..J-2
+    if J == 1:
+        bwd = (L - 1) * cheap
+    else:
+        P2 = 1 << (J - 1).bit_length()
+        last = L - (J - 1) * c
+        bwd = (J - 2) * (c - 1) * full + (last - 1) * cheap + (P2 - 1) * full + (P2 - 1) * cheap + (J - 1) * c * cheap
+    if Jf == 1:
+        fwd = Lf * 2 * n ** 2
+    else:
+        P2 = 1 << (Jf - 1).bit_length()
+        fwd = (Jf - 1) * (c - 1) * (2 * n ** 3 + 2 * n ** 2) + (P2 - 1) * (2 * n ** 3 + 2 * n ** 2) \
+            + Lf * 2 * n ** 2 + (P2 - 1) * 2 * n ** 2
+    init = (N + 1) * (m ** 3 / 3 + 2 * m ** 2 * (2 * n + 1) + 6 * n ** 2 * m + 4 * n * m)
+    policy = (N + 1) * (4 * n ** 2 * m + 2 * n * m ** 2 + m ** 3 / 3 + 2 * m ** 2 * (n + 1) + 2 * n ** 2 + 2 * n * m
+                        + 2 * n ** 2 * m + 2 * n * m)
+    tail = (N + 1) * 2 * m * n + (N + 2) * 2 * n ** 2
+    return {"k_elem_init": init, "k_scan_bwd": bwd, "k_policy": policy, "k_scan_fwd": fwd, "k_tail": tail}
+
+
+def fp32_peak_tflops(sm_mhz: float) -> float:
+    return SM_COUNT * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"bench_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "20"], stdout=f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 7:
+                rows.append(p)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------- oracle baseline
+def cpu_baseline(B: int, N: int, seed: int, budget_s: float = 10.0, sample: int = 1024):
+    """The fp64 oracle as it stands (oracle/pdilqr_oracle.c, OpenMP over instances, all host
+    cores) on a bounded sample of the same workload: repeated steps of `sample` instances until
+    `budget_s` of wall time.  Returns solves/s and what was run."""
+    from oracle import oracle as O
+    O.build()
+    ns = min(sample, B)
+    prob = synth.srbd_problem(ns, N=N, seed=seed)
+    threads = O.max_threads()
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        O.srbd_step(prob, nthreads=threads)
+        reps += 1
+        if time.perf_counter() - t0 >= budget_s:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": ns * reps / dt, "unit": "solves/s", "cores": threads, "kind": "oracle",
+            "sample": f"{reps} batched oracle steps of the first {ns} of {B} config-3 instances (N={N}), "
+                      f"{dt:.1f} s wall, fp64, {threads} OpenMP threads"}
+
+
+def run_reference(args, rank: int):
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    O.build()
+    ns = min(args.ref_sample, args.batch)
+    prob = synth.srbd_problem(ns, N=args.N, seed=synth.BASE_SEED)
+    threads = O.max_threads()
+    for _ in range(args.warmup):
+        O.srbd_step(prob, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.srbd_step(prob, nthreads=threads)
+    dt = time.perf_counter() - t0
+    v = ns * args.steps / dt
+    sample = f"each step = one batched oracle step of {ns} of the {args.batch} config-3 instances (N={args.N})"
+    return {"metric": METRIC, "value": v, "unit": "solves/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (workloads/synth.py, seeded)",
+            "config": {"workload": "srbd_mpc_config3", "batch_per_gpu": args.batch, "N": args.N, "n": 12, "m": 12},
+            "cpu_baseline": {"value": v, "unit": "solves/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+# ---------------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=4096, help="instances per GPU (weak scaling)")
+    ap.add_argument("--N", type=int, default=50)
+    ap.add_argument("--leaf-chunk", type=int, default=0)
+    ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--ref-sample", type=int, default=256)
+    ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON extras)")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        out = run_reference(args, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2506_07823_b200 as P
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    tdt = torch.float32 if args.dtype == "f32" else torch.float64
+    B, N = args.batch, args.N
+
+    prob = synth.srbd_problem(B, N=N, seed=synth.BASE_SEED, first=rank * B)
+    h = P.PdIlqr(N=N, n=12, m=12, batch=B, dtype=tdt, model="srbd", srbd=prob["params"],
+                 leaf_chunk=args.leaf_chunk, device=local)
+    npd = np.float32 if tdt == torch.float32 else np.float64
+
+    def upload():
+        return {k: (torch.from_numpy(np.ascontiguousarray(prob[k] if prob[k].dtype == np.uint8 else prob[k].astype(npd)))
+                    .to(dev)) for k in ITER_KEYS}
+
+    it = upload()
+    stats = h.new_stats()
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(args.warmup):
+        h.step(it, stats)
+    torch.cuda.synchronize()
+    launches_per_step = h.last_launch_count()
+    if args.profile_only:
+        for _ in range(args.steps):
+            h.step(it, stats)
+        torch.cuda.synchronize()
+        if rank == 0:
+            print(json.dumps({"profile_only": True, "steps": args.steps}), flush=True)
+        return
+
+    # --------------------------------------------------------------- timed region (device)
+    clk = ClockSampler(local)
+    h.profile(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    time.sleep(0.05)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        h.step(it, stats)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    prof = h.profile_read()
+    h.profile(False)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * B * args.steps / (ms_max / 1e3)
+
+    # final collective (outside the hot path): all-gather of u0 and stats over NCCL
+    gather_ms = None
+    if world > 1:
+        u0 = it["u"][:, 0, :].contiguous()
+        st = torch.stack([stats["cost"].to(u0.dtype), stats["theta"].to(u0.dtype), stats["alpha"].to(u0.dtype),
+                          stats["accepted"].to(u0.dtype), stats["info"].to(u0.dtype)], 1)
+        g_u0 = torch.empty(world * B, 12, dtype=u0.dtype, device=dev)
+        g_st = torch.empty(world * B, 5, dtype=u0.dtype, device=dev)
+        dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        dist.all_gather_into_tensor(g_u0, u0)
+        dist.all_gather_into_tensor(g_st, st)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        gather_ms = a0.elapsed_time(a1)
+
+    # --------------------------------------------------------------- e2e via host buffers
+    e2e = None
+    if not args.no_e2e:
+        it = upload()
+        x0_host = torch.from_numpy(prob["x0"].astype(npd)).pin_memory()
+        u0_host = torch.empty(B, 12, dtype=tdt).pin_memory()
+        sh = {"cost": torch.empty(B, dtype=tdt).pin_memory(), "theta": torch.empty(B, dtype=tdt).pin_memory(),
+              "alpha": torch.empty(B, dtype=tdt).pin_memory(),
+              "accepted": torch.empty(B, dtype=torch.int32).pin_memory(),
+              "info": torch.empty(B, dtype=torch.int32).pin_memory()}
+        for _ in range(args.warmup):
+            h.tick_host(it, x0_host, u0_host, sh)
+            stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            h.tick_host(it, x0_host, u0_host, sh)
+            stream.synchronize()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        es = np.dtype(npd).itemsize
+        e2e = {"value": world * B * args.steps / (float(t.item()) / 1e3), "unit": "solves/s",
+               "h2d_bytes_per_step": B * 12 * es,
+               "d2h_bytes_per_step": B * 12 * es + 3 * B * es + 2 * B * 4,
+               "api": "pdilqr_tick_host (pinned host x0 -> step -> host u0 + stats, sync per tick)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # --------------------------------------------------------------- roofline of the dominant kernel
+    fl = flops_per_instance(N, chunk=h_chunk(args, B, N))
+    kern = {k: v for k, v in prof.items() if k in fl}
+    dom = max(kern, key=lambda k: kern[k][1]) if kern else None
+    sm_mhz = clocks.get("sm_max_mhz") or 1965.0
+    peak = fp32_peak_tflops(sm_mhz)
+    roof = None
+    if dom:
+        launches, tot = kern[dom]
+        avg_s = tot / launches / 1e3
+        ach = fl[dom] * B / avg_s / 1e12
+        step_ms = ms / args.steps
+        roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                "traffic": None, "flops_per_launch": fl[dom] * B, "avg_launch_ms": avg_s * 1e3,
+                "share_of_step": (tot / launches) / step_ms,
+                "peak_basis": f"FP32 FMA pipe: 148 SMs x 128 lanes x 2 flop x {sm_mhz:.0f} MHz (max SM clock)",
+                "per_kernel_ms": {k: v[1] / v[0] for k, v in prof.items()}}
+
+    cpu = None if args.no_cpu_baseline else cpu_baseline(B, N, synth.BASE_SEED, args.cpu_budget)
+    out = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (workloads/synth.py, seeded; config 3)",
+           "config": {"workload": "srbd_mpc_config3", "batch_per_gpu": B, "N": N, "n": 12, "m": 12,
+                      "leaf_chunk": h_chunk(args, B, N), "n_alpha": 10,
+                      "l2": "working set (QP + scan workspace) ~%.2f GB per GPU > 126 MB L2; no flush needed"
+                            % (h.workspace.numel() / 1e9),
+                      "parallelism": f"batch-sharded dp{world}, no collective on the hot path"},
+           "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "e2e": e2e,
+           "roofline": roof, "cpu_baseline": cpu}
+    if gather_ms is not None:
+        out["final_allgather_ms"] = gather_ms
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def h_chunk(args, B, N):
+    return args.leaf_chunk if args.leaf_chunk > 0 else (N + 2 if B >= 148 else 1)
+
+
+if __name__ == "__main__":
+    main()

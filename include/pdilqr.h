@@ -160,6 +160,17 @@ pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *
                                void *u0_host, void *cost_host, void *theta_host, void *alpha_host,
                                int32_t *accepted_host, int32_t *info_host, void *stream);
 
+/* Per-kernel timing: when enabled, every kernel launch of this handle is bracketed by CUDA
+ * events recorded on the launch stream (host-side bookkeeping; events are created lazily and
+ * owned by the handle).  Enabling/disabling clears the records. */
+pdilqr_status pdilqr_profile(pdilqr_handle h, int32_t enable);
+
+/* Synchronises on the recorded events and aggregates them per kernel: writes up to `max`
+ * entries of kernel name (static strings), launch count and total milliseconds; clears the
+ * records.  Returns the number of distinct kernels (or -1 for a NULL handle). */
+int32_t pdilqr_profile_read(pdilqr_handle h, int32_t max, const char **names, int32_t *launches,
+                            double *total_ms);
+
 /* Number of kernels the last solve_lq / step / linearize call launched (for accounting). */
 int32_t pdilqr_last_launch_count(pdilqr_handle h);
 

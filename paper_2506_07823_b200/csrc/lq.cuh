@@ -34,6 +34,8 @@ struct KE {  // policy (K, k) of one stage
     static constexpr int K = 0, k = NU * NX, SIZE = NU * NX + NU;
 };
 
+constexpr int kFailNone = 0x7f7f7f7f;  // LqWork::fail after cudaMemsetAsync(0x7f): no failure
+
 enum SlotKind : int { SLOT_IDENT = 0, SLOT_ANCHOR = 1, SLOT_GENERAL = 2 };  // ANCHOR = suffix / anchored prefix
 
 template <typename T>
@@ -56,7 +58,7 @@ struct LqWork {
     T *tel;      // [B][N+1][TE]      Abar_i, bbar_i
     T *tslots;   // [B][Pf][TE]       tree slots of the forward scan
     T *dxw;      // [B][N+2][NX]      dx (padded)
-    int32_t *fail;    // [B] min(stage+1) of a failed factorisation, INT_MAX if none
+    int32_t *fail;    // [B] min(stage+1) of a failed factorisation, kFailNone if none
     int32_t *nonfin;  // [B] non-finite output flag
 };
 
@@ -83,13 +85,13 @@ struct CombineSmem {
     T e1[VE<NX>::SIZE];  // left operand  e_{i->k}
     T e2[VE<NX>::SIZE];  // right operand e_{k->j}
     T X[NX * NX], Y[NX * NX], V[NX * NX];
-    T z[NX], w[NX], y[NX], v[NX];
+    T z[NX], w[NX];
 };
 
 // Full combination rule e1 (x) e2 (Eq. 11 as corrected in SURVEY App. A / DESIGN.md R1-R2):
 //   M = I + C1 P2 (pivoted Gauss-Jordan), X = M^-1 A1, Y = M^-1 C1, z = M^-1 (b1 - C1 p2)
 //   A = A2 X, b = A2 z + b2, C = A2 Y A2^T + C2, P = A1^T P2 X + P1,
-//   p = A1^T (w - P2 Y w) + p1,  w = p2 + P2 b1      (M^-T = I - P2 M^-1 C1)
+//   p = A1^T M^-T w + p1 = X^T w + p1,  w = p2 + P2 b1
 // Operands in smem (s.e1, s.e2); lane r < NX returns row r of A, C, P and b_r, p_r.
 template <typename T, int NX, int WS>
 __device__ __forceinline__ bool combine_full(CombineSmem<T, NX> &s, unsigned mask, int lane, T (&Ao)[NX],
@@ -148,61 +150,54 @@ __device__ __forceinline__ bool combine_full(CombineSmem<T, NX> &s, unsigned mas
     ld_col<T, NX>(a1c, s.e1 + L::A + r, NX);
     ld_row<T, NX, true>(Po, s.e1 + L::P + r * NX);
     row_mat<T, NX, NX, NX>(Po, a1c, s.V);
+    // p = A1^T M^-T w + p1 = X^T w + p1  (A1^T M^-T = (M^-1 A1)^T: no I - P2 M^-1 C1 cancellation)
     {
-        T yr[NX];
-        ld_row<T, NX, true>(yr, s.Y + r * NX);
-        const T yv = row_dot<T, NX>(yr, s.w, T(0));
-        if (lane < NX) s.y[r] = yv;
+        T xc[NX];
+        ld_col<T, NX>(xc, s.X + r, NX);
+        po = row_dot<T, NX>(xc, s.w, s.e1[L::p + r]);
     }
-    __syncwarp(mask);
-    const T vr = wr - row_dot<T, NX>(p2, s.y, T(0));
-    if (lane < NX) s.v[r] = vr;
-    __syncwarp(mask);
-    po = row_dot<T, NX>(a1c, s.v, s.e1[L::p + r]);
     __syncwarp(mask);
     return ok;
 }
 
 // Cheap rule for a suffix right operand (A2 = C2 = b2 = 0): only P, p of the result are nonzero.
-//   P = A1^T P2 M^-1 A1 + P1,  p = A1^T (w - P2 M^-1 C1 w) + p1,  w = p2 + P2 b1.
+//   X = M^-1 A1 (M = I + C1 P2),  P = A1^T P2 X + P1,  p = X^T (p2 + P2 b1) + p1.
 template <typename T, int NX, int WS>
 __device__ __forceinline__ bool combine_cheap(CombineSmem<T, NX> &s, unsigned mask, int lane, T (&Po)[NX], T &po) {
     using L = VE<NX>;
     const int r = lane < NX ? lane : 0;
-    T c1[NX];
-    ld_row<T, NX, true>(c1, s.e1 + L::C + r * NX);
     T M[NX];
+    {
+        T c1[NX];
+        ld_row<T, NX, true>(c1, s.e1 + L::C + r * NX);
 #pragma unroll
-    for (int j = 0; j < NX; ++j) M[j] = (j == r) ? T(1) : T(0);
-    row_mat<T, NX, NX, NX>(M, c1, s.e2 + L::P);
+        for (int j = 0; j < NX; ++j) M[j] = (j == r) ? T(1) : T(0);
+        row_mat<T, NX, NX, NX>(M, c1, s.e2 + L::P);
+    }
     T p2[NX];
     ld_row<T, NX, true>(p2, s.e2 + L::P + r * NX);
     const T wr = row_dot<T, NX>(p2, s.e1 + L::b, s.e2[L::p + r]);
     if (lane < NX) s.w[r] = wr;
-    __syncwarp(mask);
-    T rhs[NX + 1];
-    ld_row<T, NX, true>(*reinterpret_cast<T(*)[NX]>(rhs), s.e1 + L::A + r * NX);
-    rhs[NX] = row_dot<T, NX>(c1, s.w, T(0));
+    T rhs[NX];
+    ld_row<T, NX, true>(rhs, s.e1 + L::A + r * NX);
     int pr;
-    const bool ok = gauss_jordan<T, WS, NX, NX + 1, true>(mask, M, rhs, lane, NX, pr);
-    if (pr >= 0) {
-        st_row<T, NX, true>(s.X + pr * NX, *reinterpret_cast<T(*)[NX]>(rhs));
-        s.y[pr] = rhs[NX];
-    }
+    const bool ok = gauss_jordan<T, WS, NX, NX, true>(mask, M, rhs, lane, NX, pr);
+    if (pr >= 0) st_row<T, NX, true>(s.X + pr * NX, rhs);
     __syncwarp(mask);
     {
         T V[NX];
         zero(V);
         row_mat<T, NX, NX, NX>(V, p2, s.X);
-        const T vr = wr - row_dot<T, NX>(p2, s.y, T(0));
-        if (lane < NX) { st_row<T, NX, true>(s.V + r * NX, V); s.v[r] = vr; }
+        if (lane < NX) st_row<T, NX, true>(s.V + r * NX, V);
     }
+    T xc[NX];
+    ld_col<T, NX>(xc, s.X + r, NX);
+    po = row_dot<T, NX>(xc, s.w, s.e1[L::p + r]);
     __syncwarp(mask);
     T a1c[NX];
     ld_col<T, NX>(a1c, s.e1 + L::A + r, NX);
     ld_row<T, NX, true>(Po, s.e1 + L::P + r * NX);
     row_mat<T, NX, NX, NX>(Po, a1c, s.V);
-    po = row_dot<T, NX>(a1c, s.v, s.e1[L::p + r]);
     __syncwarp(mask);
     return ok;
 }
@@ -515,7 +510,7 @@ __global__ void __launch_bounds__(256) k_scan_bwd(int B, int N, int chunk, int J
             }
         }
     }
-    if (active && fail != INT_MAX && lane == 0) atomicMin(ws.fail + b, fail);
+    if (active && fail != INT_MAX && lane == 0) atomicMin(ws.fail + b, (1 << 24) | fail);
 }
 
 // ---------------------------------------------------------------------- policy (Eq. 5 rows)
@@ -588,7 +583,7 @@ __global__ void __launch_bounds__(128) k_policy(LqArgs<T> qp, int B, int N, int 
         rhs[NX] = row_dot<T, NX>(bcol, sg, rhs[NX]);
         int pr;
         const bool ok = gauss_jordan<T, WS, NU, NX + 1, false>(mask, G, rhs, lane, NU, pr);
-        if (!ok && lane == 0) atomicMin(ws.fail + b, i + 1);
+        if (!ok && lane == 0) atomicMin(ws.fail + b, (2 << 24) | (i + 1));
         if (pr >= 0) {
             T kr[NX];
 #pragma unroll
@@ -803,11 +798,13 @@ __global__ void k_tail(int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {
 }
 
 // info[b] = factorisation failure stage (k > 0), else -1 if a non-finite output, else 0.
+// Failures are ranked by origin (R in element init < scan combine < G in the policy), then by
+// stage: fail[b] = (origin << 24) | (stage + 1), min over all failures.
 __global__ void k_finalize_info(int B, const int32_t *fail, const int32_t *nonfin, const int32_t *pre,
                                        int32_t *info) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;
-    int v = fail[b] != INT_MAX ? fail[b] : (nonfin[b] ? -1 : 0);
+    int v = fail[b] != kFailNone ? (fail[b] & 0xFFFFFF) : (nonfin[b] ? -1 : 0);
     if (pre != nullptr && pre[b] != 0) v = pre[b];
     info[b] = v;
 }

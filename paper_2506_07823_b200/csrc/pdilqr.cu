@@ -10,6 +10,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "pdilqr.h"
 #include "lq.cuh"
@@ -63,6 +64,11 @@ struct Layout {
 
 }  // namespace
 
+struct ProfRec {
+    const char *name;
+    cudaEvent_t start, stop;
+};
+
 struct pdilqr_ctx {
     pdilqr_config cfg;
     int device;
@@ -74,7 +80,43 @@ struct pdilqr_ctx {
     Layout lay;
     SrbdConst K;
     int launches;
+    // per-kernel CUDA-event timing (host bookkeeping only; off unless pdilqr_profile(h, 1))
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<ProfRec> recs;
+    cudaEvent_t ev_get() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
 };
+
+namespace {
+// Scoped timing of one kernel launch on `st` when profiling is enabled.
+struct Prof {
+    pdilqr_ctx *h;
+    cudaStream_t st;
+    cudaEvent_t e1 = nullptr;
+    const char *name;
+    Prof(pdilqr_ctx *h_, const char *nm, cudaStream_t s) : h(h_), st(s), name(nm) {
+        if (h->prof) {
+            e1 = h->ev_get();
+            cudaEventRecord(e1, st);
+        }
+    }
+    ~Prof() {
+        if (h->prof) {
+            cudaEvent_t e2 = h->ev_get();
+            cudaEventRecord(e2, st);
+            h->recs.push_back(ProfRec{name, e1, e2});
+        }
+    }
+};
+}  // namespace
 
 namespace {
 
@@ -198,6 +240,7 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         const long nw = (long)B * (N + 2);
         const size_t smem = (size_t)wpb * (2 * NU * NX + round_up4(NU)) * sizeof(T);
         set_smem(k_elem_init<T, NX, NU, EX>, smem);
+        Prof pf(h, "k_elem_init", st);
         k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
         ++launches;
     }
@@ -213,6 +256,7 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         }
         const size_t smem = (size_t)IPB * W * cs + (size_t)IPB * Pv * sizeof(int);
         set_smem(k_scan_bwd<T, NX>, smem);
+        Prof pf(h, "k_scan_bwd", st);
         k_scan_bwd<T, NX><<<(B + IPB - 1) / IPB, IPB * W * WSX, smem, st>>>(B, N, h->chunk, J, Pv, W, IPB, ws);
         ++launches;
     }
@@ -221,6 +265,7 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         const long nw = (long)B * (N + 1);
         const size_t smem = (size_t)wpb * (NX * NU + NX * NX + NX * NU + NU * NX + round_up4(NU) + NX + NX) * sizeof(T);
         set_smem(k_policy<T, NX, NU, EX>, smem);
+        Prof pf(h, "k_policy", st);
         k_policy<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws, out);
         ++launches;
     }
@@ -236,16 +281,19 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         }
         const size_t smem = (size_t)IPB * W * cs + (size_t)IPB * Pf * sizeof(int);
         set_smem(k_scan_fwd<T, NX>, smem);
+        Prof pf(h, "k_scan_fwd", st);
         k_scan_fwd<T, NX><<<(B + IPB - 1) / IPB, IPB * W * WSX, smem, st>>>(qp.dx0, B, N, n, h->chunk, J, Pf, W, IPB, ws,
                                                                             out.dx);
         ++launches;
     }
     {  // du, dlam
         const long tot = (long)B * ((long)(N + 1) * m + (long)(N + 2) * n);
+        Prof pf(h, "k_tail", st);
         k_tail<T, NX, NU><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(B, N, n, m, ws, out);
         ++launches;
     }
     if (info) {
+        Prof pf(h, "k_finalize_info", st);
         k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, ws.nonfin, pre, info);
         ++launches;
     }
@@ -284,7 +332,10 @@ pdilqr_status run_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArg
     const int B = h->cfg.batch, N = h->cfg.N;
     cudaMemsetAsync(pre, 0, (size_t)B * 4, st);
     const long nw = (long)B * (N + 2);
+    {
+    Prof pf(h, "k_srbd_linearize", st);
     k_srbd_linearize<T><<<(unsigned)((nw + 7) / 8), 128, 0, st>>>(h->K, iter_of<T>(it), B, N, outq, pre);
+    }
     h->launches += 1;
     return cuda_check("linearize launch");
 }
@@ -307,7 +358,10 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
     s = dispatch_lq<T>(h, qp, out, info_tmp, pre, st);
     if (s != PDILQR_OK) return s;
     LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
+    {
+    Prof pf(h, "k_srbd_linesearch", st);
     k_srbd_linesearch<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, out.dx, out.du, out.dlam, info_tmp, so);
+    }
     h->launches += 1;
     return cuda_check("step launch");
 }
@@ -393,8 +447,46 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
 }
 
 pdilqr_status pdilqr_destroy(pdilqr_handle h) {
+    if (h) {
+        for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+    }
     delete h;
     return PDILQR_OK;
+}
+
+pdilqr_status pdilqr_profile(pdilqr_handle h, int32_t enable) {
+    if (!h) return fail(PDILQR_ERR_INVALID_ARG, "NULL handle");
+    h->prof = enable != 0;
+    h->recs.clear();
+    h->ev_used = 0;
+    return PDILQR_OK;
+}
+
+int32_t pdilqr_profile_read(pdilqr_handle h, int32_t max, const char **names, int32_t *launches, double *total_ms) {
+    if (!h) return -1;
+    DeviceGuard g(h->device);
+    std::vector<const char *> nm;
+    std::vector<int32_t> cnt;
+    std::vector<double> tot;
+    for (const ProfRec &r : h->recs) {
+        cudaEventSynchronize(r.stop);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.start, r.stop);
+        size_t k = 0;
+        while (k < nm.size() && std::strcmp(nm[k], r.name) != 0) ++k;
+        if (k == nm.size()) { nm.push_back(r.name); cnt.push_back(0); tot.push_back(0); }
+        cnt[k] += 1;
+        tot[k] += ms;
+    }
+    const int32_t n = (int32_t)nm.size();
+    for (int32_t k = 0; k < n && k < max; ++k) {
+        if (names) names[k] = nm[k];
+        if (launches) launches[k] = cnt[k];
+        if (total_ms) total_ms[k] = tot[k];
+    }
+    h->recs.clear();
+    h->ev_used = 0;
+    return n;
 }
 
 pdilqr_status pdilqr_solve_lq(pdilqr_handle h, const pdilqr_lq *qp, pdilqr_dir *dir, int32_t *info, void *stream) {

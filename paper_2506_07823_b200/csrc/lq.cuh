@@ -80,6 +80,21 @@ __device__ __forceinline__ void wzero(T *__restrict__ dst, int lane) {
 }
 
 // ------------------------------------------------------------------------- value combines
+// Symmetrise a row-distributed matrix through shared scratch: out[r][j] = (M[r][j] + M[j][r]) / 2.
+// P~ and C~ are symmetric in exact arithmetic (SPEC S:76 re-symmetrisation); without this, rounding
+// asymmetry accumulates along the scan.
+template <typename T, int NX>
+__device__ __forceinline__ void symmetrize_rows(T (&row)[NX], T *scratch, unsigned mask, int lane) {
+    const int r = lane < NX ? lane : 0;
+    if (lane < NX) st_row<T, NX, true>(scratch + r * NX, row);
+    __syncwarp(mask);
+    T col[NX];
+    ld_col<T, NX>(col, scratch + r, NX);
+#pragma unroll
+    for (int j = 0; j < NX; ++j) row[j] = T(0.5) * (row[j] + col[j]);
+    __syncwarp(mask);
+}
+
 template <typename T, int NX>
 struct CombineSmem {
     T e1[VE<NX>::SIZE];  // left operand  e_{i->k}
@@ -157,6 +172,8 @@ __device__ __forceinline__ bool combine_full(CombineSmem<T, NX> &s, unsigned mas
         po = row_dot<T, NX>(xc, s.w, s.e1[L::p + r]);
     }
     __syncwarp(mask);
+    symmetrize_rows<T, NX>(Po, s.V, mask, lane);
+    symmetrize_rows<T, NX>(Co, s.Y, mask, lane);
     return ok;
 }
 
@@ -199,6 +216,7 @@ __device__ __forceinline__ bool combine_cheap(CombineSmem<T, NX> &s, unsigned ma
     ld_row<T, NX, true>(Po, s.e1 + L::P + r * NX);
     row_mat<T, NX, NX, NX>(Po, a1c, s.V);
     __syncwarp(mask);
+    symmetrize_rows<T, NX>(Po, s.Y, mask, lane);
     return ok;
 }
 

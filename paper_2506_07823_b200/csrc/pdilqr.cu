@@ -15,6 +15,7 @@
 #include "pdilqr.h"
 #include "lq.cuh"
 #include "srbd.cuh"
+#include "srbd_fused.cuh"
 
 using namespace pdilqr;
 
@@ -340,8 +341,47 @@ pdilqr_status run_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArg
     return cuda_check("linearize launch");
 }
 
+// Single-chunk schedule: the fused fold path (srbd_fused.cuh), 2 kernels per step.
+template <typename T>
+pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N;
+    LqWork<T> ws = work<T>(h);
+    int32_t *info_tmp = reinterpret_cast<int32_t *>(h->ws + h->lay.info_tmp);
+    T *dx, *du, *dl;
+    if (dir && dir->dx) {
+        dx = (T *)dir->dx; du = (T *)dir->du; dl = (T *)dir->dlam;
+    } else {
+        dx = reinterpret_cast<T *>(h->ws + h->lay.dir[0]);
+        du = reinterpret_cast<T *>(h->ws + h->lay.dir[1]);
+        dl = reinterpret_cast<T *>(h->ws + h->lay.dir[2]);
+    }
+    {
+        const size_t smem = 8 * sizeof(FoldSmem<T>);
+        set_smem(k_srbd_bwd_fold<T>, smem);
+        Prof pf(h, "k_srbd_bwd_fold", st);
+        k_srbd_bwd_fold<T><<<(B + 7) / 8, 128, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, info_tmp);
+    }
+    {
+        LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
+        Prof pf(h, "k_srbd_fwd_ls", st);
+        k_srbd_fwd_ls<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, ws, dx, du, dl, info_tmp, so);
+    }
+    if (dir && dir->dx && (dir->K || dir->k)) {  // optional policy export (row-major [B][N+1][m][n] / [m])
+        const size_t KS = KE<12, 12>::SIZE;
+        if (dir->K)
+            cudaMemcpy2DAsync(dir->K, 144 * sizeof(T), ws.Kk, KS * sizeof(T), 144 * sizeof(T), (size_t)B * (N + 1),
+                              cudaMemcpyDeviceToDevice, st);
+        if (dir->k)
+            cudaMemcpy2DAsync(dir->k, 12 * sizeof(T), ws.Kk + 144, KS * sizeof(T), 12 * sizeof(T), (size_t)B * (N + 1),
+                              cudaMemcpyDeviceToDevice, st);
+    }
+    h->launches += 2;
+    return cuda_check("step (fused) launch");
+}
+
 template <typename T>
 pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st) {
+    if (h->Jb == 1 && h->cfg.n == 12 && h->cfg.m == 12) return run_step_fused<T>(h, it, stats, dir, st);
     const int B = h->cfg.batch, N = h->cfg.N;
     LqArgs<T> qp = internal_qp<T>(h);
     int32_t *pre = reinterpret_cast<int32_t *>(h->ws + h->lay.pre);

@@ -93,60 +93,30 @@ struct SrbdEval {
     }
 };
 
-// ------------------------------------------------------------------------- linearisation
-// Lane r < 12 of the worker of stage i writes row r of A_i = I + dt Fx, B_i = dt Fu, Q_i, R_i,
-// S_i (= 0), and b_i[r], q_i[r] (= W_x (x - xref) + A^T lam_{i+1} - lam_i), r_i[r]
-// (= W_u (u - uref) + sum B'(xi) grad xi + B^T lam_{i+1}); the stage-(N+1) worker writes
-// P_{N+1} = W_N, p_{N+1} = W_N (x_{N+1} - xref) - lam_{N+1} and dx0 = xhat0 - x_0.
+// Row r of the stage-i linearisation computed by one lane:
+//   Arow = dt Fx[r, :] (A = I + dt Fx; the identity is added by the caller), Brow = dt Fu[r, :],
+//   fr = f_r(x, u), Rrow = row r of R = W_u + sum_c B''(xi_c) grad xi_c grad xi_c^T (control row r),
+//   rg = W_u (u - uref)_r + sum_c B'(xi_c) grad xi_c[r]  (r_i without the multiplier term),
+//   bad = outside the pitch guard or non-finite.
 template <typename T>
-struct SrbdIter {
-    const T *x, *u, *lam, *x0, *xref, *uref;
-    const uint8_t *con;
-    const T *feet;
+struct SrbdRow {
+    T Arow[12], Brow[12], Rrow[12];
+    T fr, rg;
+    bool bad;
 };
 
 template <typename T>
-__global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T> it, int B, int N, LqArgs<T> outc,
-                                                        int32_t *pre_info) {
-    constexpr int WS = 16, NX = 12;
-    LqArgs<T> &o = outc;  // writable views (const-cast below)
-    const int lane = worker_lane<WS>();
-    const unsigned mask = worker_mask<WS>();
-    const int wloc = threadIdx.x / WS;
-    const long gw = (long)blockIdx.x * (blockDim.x / WS) + wloc;
-    __shared__ __align__(16) T smA[8][NX * NX];
-    __shared__ __align__(16) T smB[8][NX * NX];
-    if (gw >= (long)B * (N + 2)) return;
-    const int b = (int)(gw / (N + 2)), i = (int)(gw % (N + 2));
-    const int r = lane < NX ? lane : 0;
-    const T *x = it.x + ((size_t)b * (N + 2) + i) * NX;
-    const T *lam = it.lam + ((size_t)b * (N + 2) + i) * NX;
-    const T *xr = it.xref + ((size_t)b * (N + 2) + i) * NX;
-    if (i == N + 1) {
-        if (lane < NX) {
-            T *Pt = const_cast<T *>(o.Pt) + (size_t)b * NX * NX + r * NX;
-#pragma unroll
-            for (int j = 0; j < NX; ++j) Pt[j] = (j == r) ? T(K.wxt[r]) : T(0);
-            const_cast<T *>(o.pt)[(size_t)b * NX + r] = T(K.wxt[r]) * (x[r] - xr[r]) - lam[r];
-            const T *x0 = it.x + (size_t)b * (N + 2) * NX;
-            const_cast<T *>(o.dx0)[(size_t)b * NX + r] = it.x0[(size_t)b * NX + r] - x0[r];
-            if (!isfinite(x[r]) || !isfinite(lam[r]) || !isfinite(it.x0[(size_t)b * NX + r])) pre_info[b] = -1;
-        }
-        return;
-    }
-    const size_t st = (size_t)b * (N + 1) + i;
-    const T *u = it.u + st * NX;
-    const T *feet = it.feet + st * 12;
-    const uint8_t *con = it.con + st * 4;
-    const T *ln = lam + NX;
-    const T *ur = it.uref ? it.uref + st * NX : nullptr;
+__device__ __forceinline__ void srbd_stage_row(const SrbdConst &K, const T *x, const T *u, const T *feet,
+                                               const uint8_t *con, const T *ur, int r, SrbdRow<T> &o) {
+    constexpr int NX = 12;
     T xv[NX], uv[NX];
     ld_row<T, NX, true>(xv, x);
     ld_row<T, NX, true>(uv, u);
     SrbdEval<T> ev;
     ev.init(K, xv, uv, feet, con);
     const T dt = T(K.dt);
-    T Arow[NX], Brow[NX];
+    T (&Arow)[NX] = o.Arow;
+    T (&Brow)[NX] = o.Brow;
     zero(Arow); zero(Brow);
     const T w0 = xv[9], w1 = xv[10], w2 = xv[11];
     if (r < 3) {
@@ -235,26 +205,18 @@ __global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T>
     // and the defect free of fp cancellation
 #pragma unroll
     for (int j = 0; j < NX; ++j) { Arow[j] = dt * Arow[j]; Brow[j] = dt * Brow[j]; }
-    const T xr_r = x[r], ur_r = u[r];
-    bool bad = !(fabs((double)xv[4]) < kPitchGuard) || !isfinite(fr) || !isfinite(xr_r) || !isfinite(ur_r) ||
-               !isfinite(lam[r]);
-    if (lane < NX) {
-        st_row<T, NX, true>(smA[wloc] + r * NX, Arow);
-        st_row<T, NX, true>(smB[wloc] + r * NX, Brow);
-    }
-    __syncwarp(mask);
-    // column r of dt Fx and of B against lam_{i+1}
-    T ATl = T(0), BTl = T(0);
-#pragma unroll
-    for (int t = 0; t < NX; ++t) { ATl = fma(smA[wloc][t * NX + r], ln[t], ATl); BTl = fma(smB[wloc][t * NX + r], ln[t], BTl); }
+    const T ur_r = u[r];
+    o.bad = !(fabs((double)xv[4]) < kPitchGuard) || !isfinite(fr) || !isfinite(x[r]) || !isfinite(ur_r);
+    o.fr = fr;
     // control row r: foot j = r / 3, axis a = r % 3
     const int j = r / 3, a = r % 3;
     const bool stance = con[j] != 0;
     const T wu = stance ? T(K.wu_st) : T(K.wu_sw);
-    T Rrow[NX];
+    T (&Rrow)[NX] = o.Rrow;
 #pragma unroll
     for (int c = 0; c < NX; ++c) Rrow[c] = (c == r) ? wu : T(0);
     T rg = wu * (ur_r - (ur ? ur[r] : T(0)));
+    T &rgo = o.rg;
     if (stance) {
         const T fx = u[3 * j], fy = u[3 * j + 1], fz = u[3 * j + 2];
         for (int c = 0; c < 6; ++c) {
@@ -275,6 +237,74 @@ __global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T>
             }
         }
     }
+    rgo = rg;
+}
+
+// ------------------------------------------------------------------------- linearisation
+// Lane r < 12 of the worker of stage i writes row r of A_i = I + dt Fx, B_i = dt Fu, Q_i, R_i,
+// S_i (= 0), and b_i[r], q_i[r] (= W_x (x - xref) + A^T lam_{i+1} - lam_i), r_i[r]
+// (= W_u (u - uref) + sum B'(xi) grad xi + B^T lam_{i+1}); the stage-(N+1) worker writes
+// P_{N+1} = W_N, p_{N+1} = W_N (x_{N+1} - xref) - lam_{N+1} and dx0 = xhat0 - x_0.
+template <typename T>
+struct SrbdIter {
+    const T *x, *u, *lam, *x0, *xref, *uref;
+    const uint8_t *con;
+    const T *feet;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T> it, int B, int N, LqArgs<T> outc,
+                                                        int32_t *pre_info) {
+    constexpr int WS = 16, NX = 12;
+    LqArgs<T> &o = outc;  // writable views (const-cast below)
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    const int wloc = threadIdx.x / WS;
+    const long gw = (long)blockIdx.x * (blockDim.x / WS) + wloc;
+    __shared__ __align__(16) T smA[8][NX * NX];
+    __shared__ __align__(16) T smB[8][NX * NX];
+    if (gw >= (long)B * (N + 2)) return;
+    const int b = (int)(gw / (N + 2)), i = (int)(gw % (N + 2));
+    const int r = lane < NX ? lane : 0;
+    const T *x = it.x + ((size_t)b * (N + 2) + i) * NX;
+    const T *lam = it.lam + ((size_t)b * (N + 2) + i) * NX;
+    const T *xr = it.xref + ((size_t)b * (N + 2) + i) * NX;
+    if (i == N + 1) {
+        if (lane < NX) {
+            T *Pt = const_cast<T *>(o.Pt) + (size_t)b * NX * NX + r * NX;
+#pragma unroll
+            for (int j = 0; j < NX; ++j) Pt[j] = (j == r) ? T(K.wxt[r]) : T(0);
+            const_cast<T *>(o.pt)[(size_t)b * NX + r] = T(K.wxt[r]) * (x[r] - xr[r]) - lam[r];
+            const T *x0 = it.x + (size_t)b * (N + 2) * NX;
+            const_cast<T *>(o.dx0)[(size_t)b * NX + r] = it.x0[(size_t)b * NX + r] - x0[r];
+            if (!isfinite(x[r]) || !isfinite(lam[r]) || !isfinite(it.x0[(size_t)b * NX + r])) pre_info[b] = -1;
+        }
+        return;
+    }
+    const size_t st = (size_t)b * (N + 1) + i;
+    const T *u = it.u + st * NX;
+    const T *feet = it.feet + st * 12;
+    const uint8_t *con = it.con + st * 4;
+    const T *ln = lam + NX;
+    const T *ur = it.uref ? it.uref + st * NX : nullptr;
+    SrbdRow<T> row;
+    srbd_stage_row<T>(K, x, u, feet, con, ur, r, row);
+    const T dt = T(K.dt);
+    const T xr_r = x[r];
+    const bool bad = row.bad || !isfinite(lam[r]);
+    if (lane < NX) {
+        st_row<T, NX, true>(smA[wloc] + r * NX, row.Arow);
+        st_row<T, NX, true>(smB[wloc] + r * NX, row.Brow);
+    }
+    __syncwarp(mask);
+    // column r of dt Fx and of B against lam_{i+1}
+    T ATl = T(0), BTl = T(0);
+#pragma unroll
+    for (int t = 0; t < NX; ++t) { ATl = fma(smA[wloc][t * NX + r], ln[t], ATl); BTl = fma(smB[wloc][t * NX + r], ln[t], BTl); }
+    const T fr = row.fr, rg = row.rg;
+    T (&Arow)[NX] = row.Arow;
+    T (&Brow)[NX] = row.Brow;
+    T (&Rrow)[NX] = row.Rrow;
     if (lane < NX) {
         T *Ao = const_cast<T *>(o.A) + st * NX * NX + r * NX;
         T *Bo = const_cast<T *>(o.Bm) + st * NX * NX + r * NX;

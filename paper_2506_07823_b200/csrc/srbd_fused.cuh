@@ -1,0 +1,426 @@
+// srbd_fused.cuh -- fused SRBD step for the single-chunk schedule (leaf_chunk >= N+2): the
+// reverse associative scan degenerates to a right-to-left fold of cheap combines, so the whole
+// backward pass of one instance runs in one worker with every per-stage quantity on chip.
+//
+//   k_srbd_bwd_fold  for i = N .. 0 (one 16-lane worker per instance, lane r owns row r):
+//       linearise stage i  ->  element e_i (Eq. 12, S = 0)  ->
+//       policy K_i, k_i from P_{i+1}, p_{i+1} (Eq. 5 rows) and (Abar_i, bbar_i) (Eq. 14)  ->
+//       s_i = e_i (x) s_{i+1} by the cheap combination rule (Eq. 11, readings R1-R2).
+//     Writes (K_i, k_i), (Abar_i, bbar_i), (P_i, p_i) per stage; nothing else leaves the SM.
+//   k_srbd_fwd_ls    one warp per instance: closed-loop rollout dx_{i+1} = Abar_i dx_i + bbar_i
+//       (the forward scan of Eq. 15 with one chunk), du_i = K_i dx_i + k_i (Eq. 6),
+//       dlam_i = P_i dx_i + p_i (Eq. 7), then the parallel filter line search over the alpha
+//       grid (lanes over stages) and the in-place update (Eq. 16).
+#pragma once
+
+#include "srbd.cuh"
+
+namespace pdilqr {
+
+template <typename T>
+struct FoldSmem {
+    T P[144], A[144], B[144], ZB[144], X[144], V[144], K[144];
+    T p[12], c[12], g[12], bt[12], w[12], zr[12], k[12], pad[4];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+                                                       int32_t *info_out) {
+    constexpr int WS = 16, NX = 12;
+    constexpr int TP = TE<NX>::SIZE;
+    using KL = KE<NX, NX>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    FoldSmem<T> &s = reinterpret_cast<FoldSmem<T> *>(smraw)[threadIdx.x / WS];
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    const int b = blockIdx.x * (blockDim.x / WS) + threadIdx.x / WS;
+    if (b >= B) return;  // whole worker leaves together (no block-level barriers below)
+    const int r = lane < NX ? lane : 0;
+    const bool act = lane < NX;
+    const T *xb = it.x + (size_t)b * (N + 2) * NX;
+    const T *lb = it.lam + (size_t)b * (N + 2) * NX;
+    const T *xrb = it.xref + (size_t)b * (N + 2) * NX;
+    T *Pp = ws.Pp + (size_t)b * (N + 2) * TP;
+    T *Kk = ws.Kk + (size_t)b * (N + 1) * KL::SIZE;
+    T *Te = ws.tel + (size_t)b * (N + 1) * TP;
+    const T dt = T(K.dt);
+    bool bad = false;
+    int fail = INT_MAX;
+    // terminal element e_{N+1} = suffix s_{N+1}: P = W_N, p = W_N (x_{N+1} - xref) - lam_{N+1}  (Eq. 13)
+    {
+        const T xr = xb[(N + 1) * NX + r], lr = lb[(N + 1) * NX + r];
+        T Prow[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) Prow[j] = (j == r) ? T(K.wxt[r]) : T(0);
+        const T pr = T(K.wxt[r]) * (xr - xrb[(N + 1) * NX + r]) - lr;
+        bad = bad || !isfinite(xr) || !isfinite(lr);
+        if (act) {
+            st_row<T, NX, true>(s.P + r * NX, Prow);
+            s.p[r] = pr;
+            st_row<T, NX, true>(Pp + (size_t)(N + 1) * TP + r * NX, Prow);
+            Pp[(size_t)(N + 1) * TP + NX * NX + r] = pr;
+        }
+    }
+    __syncwarp(mask);
+    for (int i = N; i >= 0; --i) {
+        const size_t st = (size_t)b * (N + 1) + i;
+        const T *x = xb + (size_t)i * NX, *lam = lb + (size_t)i * NX, *ln = lam + NX;
+        const T *u = it.u + st * NX, *feet = it.feet + st * 12;
+        const uint8_t *con = it.con + st * 4;
+        const T *ur = it.uref ? it.uref + st * NX : nullptr;
+        // ---------------- linearise stage i
+        SrbdRow<T> row;
+        srbd_stage_row<T>(K, x, u, feet, con, ur, r, row);
+        bad = bad || row.bad || !isfinite(lam[r]);
+        T arow[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) arow[j] = (j == r ? T(1) : T(0)) + row.Arow[j];
+        if (act) {
+            st_row<T, NX, true>(s.A + r * NX, arow);
+            st_row<T, NX, true>(s.B + r * NX, row.Brow);
+            st_row<T, NX, true>(s.X + r * NX, row.Arow);  // dt Fx (scratch)
+            s.c[r] = (x[r] - x[NX + r]) + dt * row.fr;     // b_i = h(x_i, u_i) - x_{i+1}
+        }
+        __syncwarp(mask);
+        T qr, rr;
+        {
+            T ATl = T(0), BTl = T(0);
+#pragma unroll
+            for (int t = 0; t < NX; ++t) { ATl = fma(s.X[t * NX + r], ln[t], ATl); BTl = fma(s.B[t * NX + r], ln[t], BTl); }
+            qr = T(K.wx[r]) * (x[r] - xrb[(size_t)i * NX + r]) + ((ln[r] - lam[r]) + ATl);
+            rr = row.rg + BTl;
+        }
+        // ---------------- element e_i (Eq. 12 with S = 0): A~ = A, P~ = Q, p~ = q,
+        //                  C~ = B R^-1 B^T, b~ = b - B R^-1 r   (R SPD: Gauss-Jordan, no pivoting)
+        {
+            T Ra[NX], rhs[NX + 1];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) Ra[j] = row.Rrow[j];
+            rhs[0] = rr;
+#pragma unroll
+            for (int t = 0; t < NX; ++t) rhs[1 + t] = s.B[t * NX + r];
+            int pr;
+            if (!gauss_jordan<T, WS, NX, NX + 1, false>(mask, Ra, rhs, lane, NX, pr)) fail = min(fail, i + 1);
+            if (pr >= 0) {
+                s.zr[pr] = rhs[0];
+                st_row<T, NX, true>(s.ZB + pr * NX, *reinterpret_cast<T(*)[NX]>(rhs + 1));
+            }
+        }
+        __syncwarp(mask);
+        T ct[NX];
+        zero(ct);
+        row_mat<T, NX, NX, NX>(ct, row.Brow, s.ZB);
+        const T btr = row_dot<T, NX>(row.Brow, s.zr, T(0));
+        if (act) s.bt[r] = s.c[r] - btr;
+        // ---------------- policy for stage i from s_{i+1} = (P_{i+1}, p_{i+1})
+        T prow[NX];
+        ld_row<T, NX, true>(prow, s.P + r * NX);
+        {
+            T pb[NX];
+            zero(pb);
+            row_mat<T, NX, NX, NX>(pb, prow, s.B);
+            const T g = row_dot<T, NX>(prow, s.c, s.p[r]);
+            if (act) { st_row<T, NX, true>(s.V + r * NX, pb); s.g[r] = g; }
+        }
+        __syncwarp(mask);
+        {
+            T bcol[NX], pbcol[NX], G[NX], rhs[NX + 1];
+            ld_col<T, NX>(bcol, s.B + r, NX);
+            ld_col<T, NX>(pbcol, s.V + r, NX);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) G[j] = row.Rrow[j];
+            row_mat<T, NX, NX, NX>(G, bcol, s.V);             // G = R + B^T P B
+            zero(*reinterpret_cast<T(*)[NX]>(rhs));
+            row_mat<T, NX, NX, NX>(*reinterpret_cast<T(*)[NX]>(rhs), pbcol, s.A);  // H = B^T P A
+            rhs[NX] = row_dot<T, NX>(bcol, s.g, rr);           // h = B^T (p + P b) + r
+            int pr;
+            if (!gauss_jordan<T, WS, NX, NX + 1, false>(mask, G, rhs, lane, NX, pr)) fail = min(fail, i + 1);
+            if (pr >= 0) {
+                T kr[NX];
+#pragma unroll
+                for (int j = 0; j < NX; ++j) kr[j] = -rhs[j];
+                st_row<T, NX, true>(s.K + pr * NX, kr);
+                s.k[pr] = -rhs[NX];
+                st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + pr * NX, kr);
+                Kk[(size_t)i * KL::SIZE + KL::k + pr] = -rhs[NX];
+            }
+        }
+        __syncwarp(mask);
+        {
+            T abar[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) abar[j] = arow[j];
+            row_mat<T, NX, NX, NX>(abar, row.Brow, s.K);
+            const T bb = row_dot<T, NX>(row.Brow, s.k, s.c[r]);
+            if (act) {
+                st_row<T, NX, true>(Te + (size_t)i * TP + r * NX, abar);
+                Te[(size_t)i * TP + NX * NX + r] = bb;
+            }
+        }
+        // ---------------- s_i = e_i (x) s_{i+1}, cheap rule: M = I + C~ P', X = M^-1 A,
+        //                  P_i = A^T P' X + Q,  p_i = X^T (p' + P' b~) + q
+        {
+            T M[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) M[j] = (j == r) ? T(1) : T(0);
+            row_mat<T, NX, NX, NX>(M, ct, s.P);
+            const T wr = row_dot<T, NX>(prow, s.bt, s.p[r]);
+            if (act) s.w[r] = wr;
+            T rhs[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) rhs[j] = arow[j];
+            int pr;
+            if (!gauss_jordan<T, WS, NX, NX, true>(mask, M, rhs, lane, NX, pr)) fail = min(fail, i + 1);
+            __syncwarp(mask);                          // everyone is done reading s.X (dt Fx)
+            if (pr >= 0) st_row<T, NX, true>(s.X + pr * NX, rhs);
+        }
+        __syncwarp(mask);
+        {
+            T V[NX];
+            zero(V);
+            row_mat<T, NX, NX, NX>(V, prow, s.X);
+            if (act) st_row<T, NX, true>(s.V + r * NX, V);
+        }
+        T pn;
+        {
+            T xc[NX];
+            ld_col<T, NX>(xc, s.X + r, NX);
+            pn = row_dot<T, NX>(xc, s.w, qr);
+        }
+        __syncwarp(mask);
+        T Pn[NX];
+        {
+            T acol[NX];
+            ld_col<T, NX>(acol, s.A + r, NX);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) Pn[j] = (j == r) ? T(K.wx[r]) : T(0);
+            row_mat<T, NX, NX, NX>(Pn, acol, s.V);
+        }
+        __syncwarp(mask);
+        symmetrize_rows<T, NX>(Pn, s.ZB, mask, lane);
+        if (act) {
+            st_row<T, NX, true>(s.P + r * NX, Pn);
+            s.p[r] = pn;
+            st_row<T, NX, true>(Pp + (size_t)i * TP + r * NX, Pn);
+            Pp[(size_t)i * TP + NX * NX + r] = pn;
+        }
+        __syncwarp(mask);
+    }
+    {
+        const T x0 = it.x0[(size_t)b * NX + r];
+        bad = bad || !isfinite(x0);
+    }
+    const bool any_bad = __any_sync(mask, bad);
+    if (lane == 0) info_out[b] = any_bad ? -1 : (fail != INT_MAX ? fail : 0);
+}
+
+// ------------------------------------------------------------------ forward + line search
+template <typename T>
+__global__ void __launch_bounds__(128) k_srbd_fwd_ls(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+                                                     T *dx, T *du, T *dlam, const int32_t *info_in, LsOut<T> so) {
+    constexpr int NX = 12, NA = 16;
+    constexpr int TP = TE<NX>::SIZE;
+    using KL = KE<NX, NX>;
+    __shared__ __align__(16) T sx[4][16];
+    __shared__ double sJ[4][NA][32], sT[4][NA][32];
+    const int lane = threadIdx.x & 31, wl = threadIdx.x / 32;
+    const int b = blockIdx.x * (blockDim.x / 32) + wl;
+    if (b >= B) return;
+    const int na = K.n_alpha;
+    const T *x = it.x + (size_t)b * (N + 2) * NX, *u = it.u + (size_t)b * (N + 1) * NX;
+    const T *xr = it.xref + (size_t)b * (N + 2) * NX;
+    const T *urf = it.uref ? it.uref + (size_t)b * (N + 1) * NX : nullptr;
+    const T *x0 = it.x0 + (size_t)b * NX;
+    const T *Pp = ws.Pp + (size_t)b * (N + 2) * TP;
+    const T *Kk = ws.Kk + (size_t)b * (N + 1) * KL::SIZE;
+    const T *Te = ws.tel + (size_t)b * (N + 1) * TP;
+    T *Dx = dx + (size_t)b * (N + 2) * NX, *Du = du + (size_t)b * (N + 1) * NX, *Dl = dlam + (size_t)b * (N + 2) * NX;
+    const int info = info_in[b];
+    // ---------------- closed-loop rollout (one chunk of Eq. 15) and du (Eq. 6)
+    const int r = lane & 15;
+    const bool rowl = r < NX;
+    {
+        const T d0 = x0[r < NX ? r : 0] - x[r < NX ? r : 0];
+        if (lane < NX) { sx[wl][r] = d0; Dx[r] = d0; }
+    }
+    __syncwarp();
+    for (int i = 0; i <= N; ++i) {
+        T xv[NX];
+        ld_row<T, NX, true>(xv, sx[wl]);
+        T v;
+        if (lane < 16) {  // dx_{i+1} = Abar_i dx_i + bbar_i
+            T arow[NX];
+            ld_row<T, NX, true>(arow, Te + (size_t)i * TP + (rowl ? r : 0) * NX);
+            v = row_dot<T, NX>(arow, xv, Te[(size_t)i * TP + NX * NX + (rowl ? r : 0)]);
+        } else {          // du_i = K_i dx_i + k_i
+            T krow[NX];
+            ld_row<T, NX, true>(krow, Kk + (size_t)i * KL::SIZE + KL::K + (rowl ? r : 0) * NX);
+            v = row_dot<T, NX>(krow, xv, Kk[(size_t)i * KL::SIZE + KL::k + (rowl ? r : 0)]);
+        }
+        __syncwarp();
+        if (rowl) {
+            if (lane < 16) { sx[wl][r] = v; Dx[(size_t)(i + 1) * NX + r] = v; }
+            else Du[(size_t)i * NX + r] = v;
+        }
+        __syncwarp();
+    }
+    // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel
+    for (int t = lane; t < (N + 2) * NX; t += 32) {
+        const int i = t / NX, a = t % NX;
+        T prow[NX], xv[NX];
+        ld_row<T, NX, true>(prow, Pp + (size_t)i * TP + a * NX);
+        ld_row<T, NX, true>(xv, Dx + (size_t)i * NX);
+        Dl[t] = row_dot<T, NX>(prow, xv, Pp[(size_t)i * TP + NX * NX + a]);
+    }
+    __syncwarp();
+    // ---------------- line search: lane = stage; per alpha slot a (0 = current iterate,
+    // a >= 1: alpha = 2^-(a-1)); per-lane partial sums in shared memory (no unrolled alpha loop)
+    double(*aJ)[32] = sJ[wl];
+    double(*aT)[32] = sT[wl];
+    for (int a = 0; a <= na; ++a) { aJ[a][lane] = 0.0; aT[a][lane] = 0.0; }
+    unsigned guard = 0u;  // bit a: some trial state of slot a leaves the pitch guard
+    double g = 0.0;
+    for (int i = lane; i <= N + 1; i += 32) {
+        const T *xi = x + (size_t)i * NX, *dxi = Dx + (size_t)i * NX;
+        const T *xri = xr + (size_t)i * NX;
+        if (i == N + 1) {  // terminal cost: quadratic in alpha
+            double c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                const double e = (double)xi[k] - (double)xri[k], d = (double)dxi[k];
+                c0 += 0.5 * K.wxt[k] * e * e; c1 += K.wxt[k] * e * d; c2 += 0.5 * K.wxt[k] * d * d;
+            }
+            for (int a = 0; a <= na; ++a) {
+                const double al = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
+                aJ[a][lane] += c0 + al * (c1 + al * c2);
+            }
+            g += c1;
+            continue;
+        }
+        const T *ui = u + (size_t)i * NX, *dui = Du + (size_t)i * NX;
+        const T *feet = it.feet + ((size_t)b * (N + 1) + i) * 12;
+        const uint8_t *con = it.con + ((size_t)b * (N + 1) + i) * 4;
+        const T *uri = urf ? urf + (size_t)i * NX : nullptr;
+        // quadratic tracking costs: c0 + c1 a + c2 a^2
+        double c0 = 0, c1 = 0, c2 = 0;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            const double e = (double)xi[k] - (double)xri[k], d = (double)dxi[k];
+            c0 += 0.5 * K.wx[k] * e * e; c1 += K.wx[k] * e * d; c2 += 0.5 * K.wx[k] * d * d;
+            const double wu = con[k / 3] ? K.wu_st : K.wu_sw;
+            const double eu = (double)ui[k] - (uri ? (double)uri[k] : 0.0), du_ = (double)dui[k];
+            c0 += 0.5 * wu * eu * eu; c1 += wu * eu * du_; c2 += 0.5 * wu * du_ * du_;
+        }
+        g += c1;
+        for (int j = 0; j < 4; ++j) {  // barrier slopes at alpha = 0
+            if (!con[j]) continue;
+            for (int cc = 0; cc < 6; ++cc) {
+                T gx, gy, gz, h;
+                foot_con<T>(cc, T(K.mu), T(K.fmin), T(K.fmax), gx, gy, gz, h);
+                const T xi0 = gx * ui[3 * j] + gy * ui[3 * j + 1] + gz * ui[3 * j + 2] + h;
+                const double dxi_ = (double)gx * dui[3 * j] + (double)gy * dui[3 * j + 1] + (double)gz * dui[3 * j + 2];
+                g += (double)barrier_d1<T>(xi0, T(K.bmu), T(K.bdelta)) * dxi_;
+            }
+        }
+        const T *xn = xi + NX, *dxn = dxi + NX;
+        for (int a = 0; a <= na; ++a) {
+            const double al = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
+            double J = c0 + al * (c1 + al * c2);
+            T xs[NX], us[NX];
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                xs[k] = (T)((double)xi[k] + al * (double)dxi[k]);
+                us[k] = (T)((double)ui[k] + al * (double)dui[k]);
+            }
+            if (!(fabs((double)xi[4] + al * (double)dxi[4]) < kPitchGuard)) guard |= 1u << a;
+            for (int j = 0; j < 4; ++j) {
+                if (!con[j]) continue;
+                for (int cc = 0; cc < 6; ++cc) {
+                    T gx, gy, gz, h;
+                    foot_con<T>(cc, T(K.mu), T(K.fmin), T(K.fmax), gx, gy, gz, h);
+                    const T xi_ = gx * us[3 * j] + gy * us[3 * j + 1] + gz * us[3 * j + 2] + h;
+                    J += (double)barrier_val<T>(xi_, T(K.bmu), T(K.bdelta));
+                }
+            }
+            SrbdEval<T> ev;
+            ev.init(K, xs, us, feet, con);
+            double d2 = 0;
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                const double d = ((double)xn[k] - (double)xi[k]) + al * ((double)dxn[k] - (double)dxi[k]) -
+                                 K.dt * (double)ev.f(K, xs, k);
+                d2 += d * d;
+            }
+            aJ[a][lane] += J;
+            aT[a][lane] += sqrt(d2);
+        }
+    }
+    // fixed-order xor butterflies: every lane ends with bitwise identical sums
+    for (int a = 0; a <= na; ++a) {
+        double vJ = aJ[a][lane], vT = aT[a][lane];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            vJ += __shfl_xor_sync(0xffffffffu, vJ, off);
+            vT += __shfl_xor_sync(0xffffffffu, vT, off);
+        }
+        __syncwarp();
+        aJ[a][lane] = vJ;
+        aT[a][lane] = vT;
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        g += __shfl_xor_sync(0xffffffffu, g, off);
+        guard |= __shfl_xor_sync(0xffffffffu, guard, off);
+    }
+    __syncwarp();
+    // initial-condition term of theta, ||xhat0 - (x0 + a dx0)||  (reading R9)
+    double d0[NX];
+#pragma unroll
+    for (int k = 0; k < NX; ++k) d0[k] = (double)x0[k] - (double)x[k];
+    const double J0 = aJ[0][lane];
+    double th0;
+    {
+        double q = 0;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) q += d0[k] * d0[k];
+        th0 = aT[0][lane] + sqrt(q);
+    }
+    int jb = -1;
+    double Jb = J0, thb = th0;
+    if (info == 0) {
+        for (int a = 1; a <= na; ++a) {
+            const double al = ldexp(1.0, -(a - 1));
+            double q = 0;
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                const double e = d0[k] - al * (double)Dx[k];
+                q += e * e;
+            }
+            const double Ja = aJ[a][lane], tha = aT[a][lane] + sqrt(q);
+            bool ok = !((guard >> a) & 1u) && isfinite(Ja) && isfinite(tha);
+            if (ok) {
+                if (th0 > K.theta_max) ok = tha <= th0;         // "reject if it further increases theta"
+                else if (g < 0) ok = Ja <= J0 + K.c1 * al * g;   // Armijo on descent directions
+                else ok = (Ja < J0) || (tha < th0);              // cost or theta must decrease
+            }
+            if (ok) { jb = a; Jb = Ja; thb = tha; break; }
+        }
+    }
+    const T alpha = jb >= 0 ? (T)ldexp(1.0, -(jb - 1)) : T(0);
+    if (jb >= 0) {  // x, u, lam += alpha (dx, du, dlam)  (Eq. 16), coalesced
+        T *xw = const_cast<T *>(it.x) + (size_t)b * (N + 2) * NX;
+        T *uw = const_cast<T *>(it.u) + (size_t)b * (N + 1) * NX;
+        T *lw = const_cast<T *>(it.lam) + (size_t)b * (N + 2) * NX;
+        for (int t = lane; t < (N + 2) * NX; t += 32) { xw[t] = xw[t] + alpha * Dx[t]; lw[t] = lw[t] + alpha * Dl[t]; }
+        for (int t = lane; t < (N + 1) * NX; t += 32) uw[t] = uw[t] + alpha * Du[t];
+    }
+    if (lane == 0) {
+        so.cost[b] = (T)Jb;
+        so.theta[b] = (T)thb;
+        so.alpha[b] = alpha;
+        so.accepted[b] = jb >= 0 ? 1 : 0;
+        so.info[b] = info;
+    }
+}
+
+}  // namespace pdilqr

@@ -171,6 +171,17 @@ def _rotz(yaw):
     return np.array([[c, -s], [s, c]])
 
 
+def _ref_pos(p0, yaw0, wz, vb, t):
+    """Reference CoM xy at time t for a constant body-frame velocity vb and yaw rate wz:
+    p0 + int_0^t Rz(yaw0 + wz s) vb ds (closed form)."""
+    if abs(wz) < 1e-9:
+        return p0 + t * (_rotz(yaw0) @ vb)
+    s0, c0 = math.sin(yaw0), math.cos(yaw0)
+    s1, c1 = math.sin(yaw0 + wz * t), math.cos(yaw0 + wz * t)
+    ic, is_ = (s1 - s0) / wz, (c0 - c1) / wz            # int cos, int sin
+    return p0 + np.array([ic * vb[0] - is_ * vb[1], is_ * vb[0] + ic * vb[1]])
+
+
 def srbd_problem(B: int, N: int = 50, seed: int = BASE_SEED, first: int = 0, params: dict | None = None,
                  randomize: bool = True):
     """SRBD trot MPC instances (configs 2/3).
@@ -223,8 +234,7 @@ def srbd_problem(B: int, N: int = 50, seed: int = BASE_SEED, first: int = 0, par
                     start += 1.0
                 t_mid = (start + 0.25 - phase) * GAIT_PERIOD
                 yaw_m = yaw0 + wz * t_mid
-                vel_m = _rotz(yaw_m) @ vcmd
-                p_m = p0 + vel_m * t_mid             # first-order reference position
+                p_m = _ref_pos(p0, yaw0, wz, vcmd, t_mid)  # reference CoM position at mid-stance
                 feet[b, i, j, 0:2] = p_m + _rotz(yaw_m) @ HIP_OFFSETS[j]
                 feet[b, i, j, 2] = 0.0
             nst = int(contact[b, i].sum())

@@ -133,12 +133,20 @@ __device__ __forceinline__ T row_dot(const T (&a)[K], const T *__restrict__ v, T
 //                every pivot is a ratio of leading principal minors and must be > 0.
 // Returns false (uniformly across the worker) if a pivot is zero / non-finite (singular) or, for
 // PIVOT = false, non-positive (not positive definite).
-template <typename T, int WS, int NR, int NRHS, bool PIVOT>
+// FULLWARP = true: the caller guarantees the whole warp is converged and passes mask = all lanes
+// (several workers per warp); the pivot search is then an xor butterfly inside each worker's
+// WS-lane segment (plain SHFL.BFLY, no per-worker mask bookkeeping).
+template <typename T, int WS, int NR, int NRHS, bool PIVOT, bool FULLWARP = false>
 __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)[NRHS], int lane, int nrows,
                                              int &piv_row) {
+    // Unnormalised Gauss-Jordan: pivot rows are never scaled during the sweep (multiplier 0 on
+    // the pivot lane, so every update is one shuffle + one FMA, no select); each pivot row is
+    // divided by its pivot once at the end.  Same result as the normalised sweep in exact
+    // arithmetic.
     bool used = lane >= nrows;
     bool ok = true;
     piv_row = -1;
+    T mypiv = T(1);
 #pragma unroll
     for (int k = 0; k < NR; ++k) {
         if (k >= nrows) break;
@@ -149,7 +157,14 @@ __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)
             // |a| among unused rows, ties -> lowest lane; NaN wins (then the pivot check fails).
             const float fa = fabsf((float)a[k]);
             const unsigned key = used ? 0u : ((__float_as_uint(fa) & 0xFFFFFFE0u) | (31u - (unsigned)lane));
-            const unsigned best = __reduce_max_sync(mask, key);
+            unsigned best;
+            if constexpr (FULLWARP) {
+                best = key;
+#pragma unroll
+                for (int off = WS / 2; off >= 1; off >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, off, WS));
+            } else {
+                best = __reduce_max_sync(mask, key);
+            }
             p = 31 - (int)(best & 31u);
         } else {
             p = k;
@@ -157,23 +172,29 @@ __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)
         const T pv = wbcast<WS>(mask, a[k], p);
         if constexpr (PIVOT) ok = ok && (pv != T(0)) && isfinite(pv);
         else ok = ok && (pv > T(0)) && isfinite(pv);
-        const T inv = T(1) / pv;
         const bool isp = (lane == p);
-        const T f = isp ? T(0) : a[k] * inv;
-        if (isp) { used = true; piv_row = k; }
+        const T f = isp ? T(0) : a[k] / pv;
+        if (isp) { used = true; piv_row = k; mypiv = pv; }
 #pragma unroll
-        for (int j = k + 1; j < NR; ++j) {
-            const T pj = wbcast<WS>(mask, a[j], p);
-            a[j] = isp ? pj * inv : fma(-f, pj, a[j]);
-        }
+        for (int j = k + 1; j < NR; ++j) a[j] = fma(-f, wbcast<WS>(mask, a[j], p), a[j]);
 #pragma unroll
-        for (int j = 0; j < NRHS; ++j) {
-            const T pj = wbcast<WS>(mask, rhs[j], p);
-            rhs[j] = isp ? pj * inv : fma(-f, pj, rhs[j]);
-        }
+        for (int j = 0; j < NRHS; ++j) rhs[j] = fma(-f, wbcast<WS>(mask, rhs[j], p), rhs[j]);
+    }
+    {
+        const T inv = T(1) / mypiv;
+#pragma unroll
+        for (int j = 0; j < NRHS; ++j) rhs[j] *= inv;
     }
     if constexpr (!PIVOT) piv_row = lane < nrows ? lane : -1;
-    return __all_sync(mask, ok);
+    if constexpr (FULLWARP) {
+        // uniform within the worker: AND over its WS lanes
+        unsigned v = ok ? 1u : 0u;
+#pragma unroll
+        for (int off = WS / 2; off >= 1; off >>= 1) v &= __shfl_xor_sync(0xffffffffu, v, off, WS);
+        return v != 0u;
+    } else {
+        return __all_sync(mask, ok);
+    }
 }
 
 }  // namespace pdilqr

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -81,6 +82,7 @@ struct pdilqr_ctx {
     Layout lay;
     SrbdConst K;
     int launches;
+    int occ_fold = 4, occ_ls = 4;  // minimum resident CTAs per SM requested from ptxas (register cap: 128)
     // per-kernel CUDA-event timing (host bookkeeping only; off unless pdilqr_profile(h, 1))
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -357,14 +359,28 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
     }
     {
         const size_t smem = 8 * sizeof(FoldSmem<T>);
-        set_smem(k_srbd_bwd_fold<T>, smem);
         Prof pf(h, "k_srbd_bwd_fold", st);
-        k_srbd_bwd_fold<T><<<(B + 7) / 8, 128, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, info_tmp);
+        auto go = [&](auto kern) {
+            set_smem(kern, smem);
+            kern<<<(B + 7) / 8, 128, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, info_tmp);
+        };
+        switch (h->occ_fold) {
+            case 3: go(k_srbd_bwd_fold<T, 3>); break;
+            case 4: go(k_srbd_bwd_fold<T, 4>); break;
+            default: go(k_srbd_bwd_fold<T, 2>); break;
+        }
     }
     {
         LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
         Prof pf(h, "k_srbd_fwd_ls", st);
-        k_srbd_fwd_ls<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, ws, dx, du, dl, info_tmp, so);
+        auto go = [&](auto kern) {
+            kern<<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, ws, dx, du, dl, info_tmp, so);
+        };
+        switch (h->occ_ls) {
+            case 3: go(k_srbd_fwd_ls<T, 3>); break;
+            case 4: go(k_srbd_fwd_ls<T, 4>); break;
+            default: go(k_srbd_fwd_ls<T, 2>); break;
+        }
     }
     if (dir && dir->dx && (dir->K || dir->k)) {  // optional policy export (row-major [B][N+1][m][n] / [m])
         const size_t KS = KE<12, 12>::SIZE;
@@ -482,6 +498,8 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     K.wu_st = p.w_u_stance; K.wu_sw = p.w_u_swing;
     K.mu = p.mu_friction; K.fmin = p.f_min; K.fmax = p.f_max; K.bmu = p.barrier_mu; K.bdelta = p.barrier_delta;
     K.theta_max = h->cfg.theta_max; K.c1 = h->cfg.armijo_c1; K.n_alpha = h->cfg.n_alpha;
+    if (const char *e = std::getenv("PDILQR_OCC_FOLD")) h->occ_fold = std::atoi(e);  // tuning knobs
+    if (const char *e = std::getenv("PDILQR_OCC_LS")) h->occ_ls = std::atoi(e);
     *out = h;
     return PDILQR_OK;
 }

@@ -54,7 +54,9 @@ struct SrbdEval {
     T F[3];      // sum_j c_j f_j
 
     __device__ __forceinline__ void init(const SrbdConst &K, const T *x, const T *u, const T *feet, const uint8_t *con) {
-        sr = sin(x[3]); cr = cos(x[3]); sp = sin(x[4]); cp = cos(x[4]); sy = sin(x[5]); cy = cos(x[5]);
+        sincos(x[3], &sr, &cr);
+        sincos(x[4], &sp, &cp);
+        sincos(x[5], &sy, &cy);
         tp = sp / cp;
         R[0] = cy * cp; R[1] = cy * sp * sr - sy * cr; R[2] = cy * sp * cr + sy * sr;
         R[3] = sy * cp; R[4] = sy * sp * sr + cy * cr; R[5] = sy * sp * cr - cy * sr;

@@ -23,20 +23,25 @@ struct FoldSmem {
     T p[12], c[12], g[12], bt[12], w[12], zr[12], k[12], pad[4];
 };
 
-template <typename T>
-__global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
-                                                       int32_t *info_out) {
+template <typename T, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+                                                             int32_t *info_out) {
     constexpr int WS = 16, NX = 12;
     constexpr int TP = TE<NX>::SIZE;
     using KL = KE<NX, NX>;
     extern __shared__ __align__(16) unsigned char smraw[];
     FoldSmem<T> &s = reinterpret_cast<FoldSmem<T> *>(smraw)[threadIdx.x / WS];
     const int lane = worker_lane<WS>();
-    const unsigned mask = worker_mask<WS>();
-    const int b = blockIdx.x * (blockDim.x / WS) + threadIdx.x / WS;
-    if (b >= B) return;  // whole worker leaves together (no block-level barriers below)
+    // The warp stays converged: both workers run the same schedule; a worker past the end of the
+    // batch recomputes instance B-1 and stores nothing.  All warp collectives use the full mask.
+    const unsigned mask = 0xffffffffu;
+    const int b_raw = blockIdx.x * (blockDim.x / WS) + threadIdx.x / WS;
+    if (__all_sync(0xffffffffu, b_raw >= B)) return;
+    const bool live = b_raw < B;
+    const int b = live ? b_raw : B - 1;
     const int r = lane < NX ? lane : 0;
     const bool act = lane < NX;
+    const bool wr_g = act && live;  // global stores
     const T *xb = it.x + (size_t)b * (N + 2) * NX;
     const T *lb = it.lam + (size_t)b * (N + 2) * NX;
     const T *xrb = it.xref + (size_t)b * (N + 2) * NX;
@@ -57,6 +62,8 @@ __global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> 
         if (act) {
             st_row<T, NX, true>(s.P + r * NX, Prow);
             s.p[r] = pr;
+        }
+        if (wr_g) {
             st_row<T, NX, true>(Pp + (size_t)(N + 1) * TP + r * NX, Prow);
             Pp[(size_t)(N + 1) * TP + NX * NX + r] = pr;
         }
@@ -91,19 +98,39 @@ __global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> 
             rr = row.rg + BTl;
         }
         // ---------------- element e_i (Eq. 12 with S = 0): A~ = A, P~ = Q, p~ = q,
-        //                  C~ = B R^-1 B^T, b~ = b - B R^-1 r   (R SPD: Gauss-Jordan, no pivoting)
+        //                  C~ = B R^-1 B^T, b~ = b - B R^-1 r.  The SRBD Gauss-Newton R is block
+        //                  diagonal (one 3x3 SPD block per foot: diagonal weights + barrier
+        //                  curvature of that foot's constraints), so R^-1 is formed blockwise in
+        //                  closed form (adjugate) by the three lanes of each foot.
+        if (act) {
+            st_row<T, NX, true>(s.ZB + r * NX, row.Rrow);
+            s.zr[r] = rr;
+        }
+        __syncwarp(mask);
         {
-            T Ra[NX], rhs[NX + 1];
+            const int jf = r / 3, ar = r - 3 * (r / 3), o = 3 * jf;
+            const T *Rb = s.ZB + o * NX + o;
+            const T a00 = Rb[0], a01 = Rb[1], a02 = Rb[2];
+            const T a10 = Rb[NX], a11 = Rb[NX + 1], a12 = Rb[NX + 2];
+            const T a20 = Rb[2 * NX], a21 = Rb[2 * NX + 1], a22 = Rb[2 * NX + 2];
+            const T c00 = a11 * a22 - a12 * a21, c01 = a02 * a21 - a01 * a22, c02 = a01 * a12 - a02 * a11;
+            const T c10 = a12 * a20 - a10 * a22, c11 = a00 * a22 - a02 * a20, c12 = a02 * a10 - a00 * a12;
+            const T c20 = a10 * a21 - a11 * a20, c21 = a01 * a20 - a00 * a21, c22 = a00 * a11 - a01 * a10;
+            const T det = a00 * c00 + a01 * c10 + a02 * c20;
+            // SPD check of the block: leading principal minors a00, a00 a11 - a01 a10, det > 0
+            if (!(a00 > T(0)) || !(c22 > T(0)) || !(det > T(0)) || !isfinite(det)) fail = min(fail, i + 1);
+            const T id = T(1) / det;
+            const T q0 = (ar == 0 ? c00 : ar == 1 ? c10 : c20) * id;
+            const T q1 = (ar == 0 ? c01 : ar == 1 ? c11 : c21) * id;
+            const T q2 = (ar == 0 ? c02 : ar == 1 ? c12 : c22) * id;
+            const T zr_r = q0 * s.zr[o] + q1 * s.zr[o + 1] + q2 * s.zr[o + 2];
+            T zb[NX];
 #pragma unroll
-            for (int j = 0; j < NX; ++j) Ra[j] = row.Rrow[j];
-            rhs[0] = rr;
-#pragma unroll
-            for (int t = 0; t < NX; ++t) rhs[1 + t] = s.B[t * NX + r];
-            int pr;
-            if (!gauss_jordan<T, WS, NX, NX + 1, false>(mask, Ra, rhs, lane, NX, pr)) fail = min(fail, i + 1);
-            if (pr >= 0) {
-                s.zr[pr] = rhs[0];
-                st_row<T, NX, true>(s.ZB + pr * NX, *reinterpret_cast<T(*)[NX]>(rhs + 1));
+            for (int t = 0; t < NX; ++t) zb[t] = q0 * s.B[t * NX + o] + q1 * s.B[t * NX + o + 1] + q2 * s.B[t * NX + o + 2];
+            __syncwarp(mask);
+            if (act) {
+                st_row<T, NX, true>(s.ZB + r * NX, zb);
+                s.zr[r] = zr_r;
             }
         }
         __syncwarp(mask);
@@ -134,15 +161,17 @@ __global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> 
             row_mat<T, NX, NX, NX>(*reinterpret_cast<T(*)[NX]>(rhs), pbcol, s.A);  // H = B^T P A
             rhs[NX] = row_dot<T, NX>(bcol, s.g, rr);           // h = B^T (p + P b) + r
             int pr;
-            if (!gauss_jordan<T, WS, NX, NX + 1, false>(mask, G, rhs, lane, NX, pr)) fail = min(fail, i + 1);
+            if (!gauss_jordan<T, WS, NX, NX + 1, false, true>(mask, G, rhs, lane, NX, pr)) fail = min(fail, i + 1);
             if (pr >= 0) {
                 T kr[NX];
 #pragma unroll
                 for (int j = 0; j < NX; ++j) kr[j] = -rhs[j];
                 st_row<T, NX, true>(s.K + pr * NX, kr);
                 s.k[pr] = -rhs[NX];
-                st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + pr * NX, kr);
-                Kk[(size_t)i * KL::SIZE + KL::k + pr] = -rhs[NX];
+                if (live) {
+                    st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + pr * NX, kr);
+                    Kk[(size_t)i * KL::SIZE + KL::k + pr] = -rhs[NX];
+                }
             }
         }
         __syncwarp(mask);
@@ -152,7 +181,7 @@ __global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> 
             for (int j = 0; j < NX; ++j) abar[j] = arow[j];
             row_mat<T, NX, NX, NX>(abar, row.Brow, s.K);
             const T bb = row_dot<T, NX>(row.Brow, s.k, s.c[r]);
-            if (act) {
+            if (wr_g) {
                 st_row<T, NX, true>(Te + (size_t)i * TP + r * NX, abar);
                 Te[(size_t)i * TP + NX * NX + r] = bb;
             }
@@ -170,7 +199,7 @@ __global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> 
 #pragma unroll
             for (int j = 0; j < NX; ++j) rhs[j] = arow[j];
             int pr;
-            if (!gauss_jordan<T, WS, NX, NX, true>(mask, M, rhs, lane, NX, pr)) fail = min(fail, i + 1);
+            if (!gauss_jordan<T, WS, NX, NX, true, true>(mask, M, rhs, lane, NX, pr)) fail = min(fail, i + 1);
             __syncwarp(mask);                          // everyone is done reading s.X (dt Fx)
             if (pr >= 0) st_row<T, NX, true>(s.X + pr * NX, rhs);
         }
@@ -201,6 +230,8 @@ __global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> 
         if (act) {
             st_row<T, NX, true>(s.P + r * NX, Pn);
             s.p[r] = pn;
+        }
+        if (wr_g) {
             st_row<T, NX, true>(Pp + (size_t)i * TP + r * NX, Pn);
             Pp[(size_t)i * TP + NX * NX + r] = pn;
         }
@@ -210,14 +241,17 @@ __global__ void __launch_bounds__(128) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> 
         const T x0 = it.x0[(size_t)b * NX + r];
         bad = bad || !isfinite(x0);
     }
-    const bool any_bad = __any_sync(mask, bad);
-    if (lane == 0) info_out[b] = any_bad ? -1 : (fail != INT_MAX ? fail : 0);
+    unsigned vb = bad ? 1u : 0u;
+#pragma unroll
+    for (int off = WS / 2; off >= 1; off >>= 1) vb |= __shfl_xor_sync(0xffffffffu, vb, off, WS);
+    const bool any_bad = vb != 0u;
+    if (lane == 0 && live) info_out[b] = any_bad ? -1 : (fail != INT_MAX ? fail : 0);
 }
 
 // ------------------------------------------------------------------ forward + line search
-template <typename T>
-__global__ void __launch_bounds__(128) k_srbd_fwd_ls(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
-                                                     T *dx, T *du, T *dlam, const int32_t *info_in, LsOut<T> so) {
+template <typename T, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+                                                           T *dx, T *du, T *dlam, const int32_t *info_in, LsOut<T> so) {
     constexpr int NX = 12, NA = 16;
     constexpr int TP = TE<NX>::SIZE;
     using KL = KE<NX, NX>;

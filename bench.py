@@ -191,6 +191,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--ref-sample", type=int, default=256)
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON extras)")
+    ap.add_argument("--latency", default="25,50,100,200,400,1000",
+                    help="horizons of the B=1 latency sweep (config 2), '' to skip")
+    ap.add_argument("--latency-reps", type=int, default=300)
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -339,6 +342,9 @@ def main():
                 "peak_basis": f"FP32 FMA pipe: 148 SMs x 128 lanes x 2 flop x {sm_mhz:.0f} MHz (max SM clock)",
                 "per_kernel_ms": {k: v[1] / v[0] for k, v in prof.items()}}
 
+    lat = None
+    if args.latency:
+        lat = latency_sweep(P, torch, dev, [int(v) for v in args.latency.split(",")], args.latency_reps)
     cpu = None if args.no_cpu_baseline else cpu_baseline(B, N, synth.BASE_SEED, args.cpu_budget)
     out = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -350,12 +356,70 @@ def main():
                       "parallelism": f"batch-sharded dp{world}, no collective on the hot path"},
            "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "e2e": e2e,
            "roofline": roof, "cpu_baseline": cpu,
-           "kernels_ms": {k: v[1] / v[0] for k, v in prof.items()}}
+           "kernels_ms": {k: v[1] / v[0] for k, v in prof.items()},
+           "latency": lat}
     if gather_ms is not None:
         out["final_allgather_ms"] = gather_ms
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def latency_sweep(P, torch, dev, horizons, reps, warm=30):
+    """Config 2: p50 / p90 single-instance (B=1) pdilqr_step latency vs horizon N, from CUDA-graph
+    replays timed one by one with CUDA events (device time), plus the end-to-end tick through
+    pdilqr_tick_host (pinned x0 in, u0 + stats out, host synchronisation).  fp32 and fp64."""
+    out = {}
+    stream = torch.cuda.Stream(dev)
+    for dt_name, tdt, npd in (("f32", torch.float32, np.float32), ("f64", torch.float64, np.float64)):
+        res = {}
+        for N in horizons:
+            prob = synth.srbd_problem(1, N=N, seed=synth.BASE_SEED + 2, randomize=False)
+            h = P.PdIlqr(N=N, n=12, m=12, batch=1, dtype=tdt, model="srbd", srbd=prob["params"], device=dev.index)
+            it = {k: torch.from_numpy(np.ascontiguousarray(prob[k] if prob[k].dtype == np.uint8 else prob[k].astype(npd)))
+                  .to(dev) for k in ITER_KEYS}
+            st = h.new_stats()
+            pristine = {k: it[k].clone() for k in ("x", "u", "lam")}
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    h.step(it, st, stream=stream)
+                stream.synchronize()
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    h.step(it, st, stream=stream)
+                for _ in range(warm):
+                    g.replay()
+                stream.synchronize()
+                ts = []
+                for _ in range(reps):
+                    for k in ("x", "u", "lam"):      # same input every replay (cold-start iterate)
+                        it[k].copy_(pristine[k])
+                    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(stream); g.replay(); e1.record(stream)
+                    e1.synchronize()
+                    ts.append(e0.elapsed_time(e1) * 1e3)
+                # end to end: host x0 -> tick -> host u0 (+ stats), synchronised
+                x0h = torch.from_numpy(prob["x0"].astype(npd)).pin_memory()
+                u0h = torch.empty(1, 12, dtype=tdt).pin_memory()
+                sh = {"cost": torch.empty(1, dtype=tdt).pin_memory(), "theta": torch.empty(1, dtype=tdt).pin_memory(),
+                      "alpha": torch.empty(1, dtype=tdt).pin_memory(),
+                      "accepted": torch.empty(1, dtype=torch.int32).pin_memory(),
+                      "info": torch.empty(1, dtype=torch.int32).pin_memory()}
+                te = []
+                for r in range(min(reps, 100) + 10):
+                    t0 = time.perf_counter()
+                    h.tick_host(it, x0h, u0h, sh, stream=stream)
+                    stream.synchronize()
+                    if r >= 10:
+                        te.append((time.perf_counter() - t0) * 1e6)
+            res[str(N)] = {"p50_us": float(np.percentile(ts, 50)), "p90_us": float(np.percentile(ts, 90)),
+                           "e2e_p50_us": float(np.percentile(te, 50)), "leaf_chunk": 1,
+                           "launches": h.last_launch_count()}
+            del h, g
+        out[dt_name] = res
+    return {"metric": "p50 single-solve latency vs horizon N (B=1, config 2, full SQP step)", "unit": "us",
+            "timing": "CUDA-graph replay of pdilqr_step, CUDA events per replay (device); e2e = wall time of "
+                      "pdilqr_tick_host + stream sync (host)", "per_dtype": out}
 
 
 def h_chunk(args, B, N):

@@ -84,6 +84,19 @@ __device__ __forceinline__ void zero(T (&d)[NC]) {
     for (int j = 0; j < NC; ++j) d[j] = T(0);
 }
 
+// -------------------------------------------------------------------- packed FP32 FMA (sm_100)
+// c0 += a0*b0, c1 += a1*b1 as one FFMA2 (fma.rn.f32x2): halves the FMA instruction count of every
+// row product; ptxas folds a broadcast scalar operand (a0 == a1) into the .F32 operand form.
+__device__ __forceinline__ void ffma2(float a0, float a1, float b0, float b1, float &c0, float &c1) {
+    asm("{\n .reg .b64 ra, rb, rc;\n mov.b64 ra, {%2, %3};\n mov.b64 rb, {%4, %5};\n mov.b64 rc, {%0, %1};\n"
+        " fma.rn.f32x2 rc, ra, rb, rc;\n mov.b64 {%0, %1}, rc;\n}"
+        : "+f"(c0), "+f"(c1) : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+__device__ __forceinline__ void ffma2(double a0, double a1, double b0, double b1, double &c0, double &c1) {
+    c0 = fma(a0, b0, c0);
+    c1 = fma(a1, b1, c1);
+}
+
 // ------------------------------------------------------------------------------ products
 // out[j] (+)= sum_k a[k] * Y[k*LDY + j]   (row of a 1xK times KxNC matrix in shared memory)
 template <typename T, int K, int NC, int LDY>
@@ -92,8 +105,13 @@ __device__ __forceinline__ void row_mat(T (&out)[NC], const T (&a)[K], const T *
     for (int k = 0; k < K; ++k) {
         T y[NC];
         ld_row<T, NC, (LDY % (16 / sizeof(T)) == 0)>(y, Y + k * LDY);
+        if constexpr (NC % 2 == 0) {
 #pragma unroll
-        for (int j = 0; j < NC; ++j) out[j] = fma(a[k], y[j], out[j]);
+            for (int j = 0; j < NC; j += 2) ffma2(a[k], a[k], y[j], y[j + 1], out[j], out[j + 1]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < NC; ++j) out[j] = fma(a[k], y[j], out[j]);
+        }
     }
 }
 
@@ -104,10 +122,17 @@ __device__ __forceinline__ void row_matT(T (&out)[NC], const T (&a)[K], const T 
     for (int j = 0; j < NC; ++j) {
         T y[K];
         ld_row<T, K, (LDY % (16 / sizeof(T)) == 0)>(y, Y + j * LDY);
-        T s = out[j];
+        if constexpr (K % 2 == 0) {
+            T s0 = out[j], s1 = T(0);
 #pragma unroll
-        for (int k = 0; k < K; ++k) s = fma(a[k], y[k], s);
-        out[j] = s;
+            for (int k = 0; k < K; k += 2) ffma2(a[k], a[k + 1], y[k], y[k + 1], s0, s1);
+            out[j] = s0 + s1;
+        } else {
+            T s = out[j];
+#pragma unroll
+            for (int k = 0; k < K; ++k) s = fma(a[k], y[k], s);
+            out[j] = s;
+        }
     }
 }
 
@@ -116,9 +141,16 @@ template <typename T, int K>
 __device__ __forceinline__ T row_dot(const T (&a)[K], const T *__restrict__ v, T acc) {
     T y[K];
     ld_row<T, K, (K % (16 / sizeof(T)) == 0)>(y, v);
+    if constexpr (K % 2 == 0) {
+        T s1 = T(0);
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc = fma(a[k], y[k], acc);
-    return acc;
+        for (int k = 0; k < K; k += 2) ffma2(a[k], a[k + 1], y[k], y[k + 1], acc, s1);
+        return acc + s1;
+    } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) acc = fma(a[k], y[k], acc);
+        return acc;
+    }
 }
 
 // ------------------------------------------------------------------- Gauss-Jordan solves
@@ -177,8 +209,16 @@ __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)
         if (isp) { used = true; piv_row = k; mypiv = pv; }
 #pragma unroll
         for (int j = k + 1; j < NR; ++j) a[j] = fma(-f, wbcast<WS>(mask, a[j], p), a[j]);
+        if constexpr (NRHS % 2 == 0) {
 #pragma unroll
-        for (int j = 0; j < NRHS; ++j) rhs[j] = fma(-f, wbcast<WS>(mask, rhs[j], p), rhs[j]);
+            for (int j = 0; j < NRHS; j += 2) {
+                const T p0 = wbcast<WS>(mask, rhs[j], p), p1 = wbcast<WS>(mask, rhs[j + 1], p);
+                ffma2(-f, -f, p0, p1, rhs[j], rhs[j + 1]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NRHS; ++j) rhs[j] = fma(-f, wbcast<WS>(mask, rhs[j], p), rhs[j]);
+        }
     }
     {
         const T inv = T(1) / mypiv;

@@ -153,6 +153,21 @@ __device__ __forceinline__ T row_dot(const T (&a)[K], const T *__restrict__ v, T
     }
 }
 
+// Branchless reciprocal for elimination multipliers: MUFU.RCP approximation refined by Newton
+// steps (fp32: one step, <= 1 ulp; fp64: two steps).  No subnormal / slow-path handling: pivots
+// are normal numbers (a zero or non-finite pivot is reported through the `ok` flag).
+__device__ __forceinline__ float rcp_rn(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+__device__ __forceinline__ double rcp_rn(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(r, fma(-x, r, 1.0), r);
+    return fma(r, fma(-x, r, 1.0), r);
+}
+
 // ------------------------------------------------------------------- Gauss-Jordan solves
 // Solve  M X = RHS  for an NR x NR system distributed one row per lane (lane r < nrows owns
 // row r of M in a[] and of RHS in rhs[]), in place.  Lanes r >= nrows are idle (never pivot).
@@ -190,7 +205,15 @@ __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)
             const float fa = fabsf((float)a[k]);
             const unsigned key = used ? 0u : ((__float_as_uint(fa) & 0xFFFFFFE0u) | (31u - (unsigned)lane));
             unsigned best;
-            if constexpr (FULLWARP) {
+            if constexpr (FULLWARP && WS == 32) {
+                best = __reduce_max_sync(0xffffffffu, key);
+            } else if constexpr (FULLWARP && WS == 16) {
+                // two full-warp REDUX (one per half-warp worker), no per-worker mask bookkeeping
+                const bool lo = (threadIdx.x & 16) == 0;
+                const unsigned b0 = __reduce_max_sync(0xffffffffu, lo ? key : 0u);
+                const unsigned b1 = __reduce_max_sync(0xffffffffu, lo ? 0u : key);
+                best = lo ? b0 : b1;
+            } else if constexpr (FULLWARP) {
                 best = key;
 #pragma unroll
                 for (int off = WS / 2; off >= 1; off >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, off, WS));
@@ -201,11 +224,14 @@ __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)
         } else {
             p = k;
         }
+        // reciprocal computed speculatively by every lane, the pivot lane's value is broadcast
+        const T rk = rcp_rn(a[k]);
         const T pv = wbcast<WS>(mask, a[k], p);
+        const T rpv = wbcast<WS>(mask, rk, p);
         if constexpr (PIVOT) ok = ok && (pv != T(0)) && isfinite(pv);
         else ok = ok && (pv > T(0)) && isfinite(pv);
         const bool isp = (lane == p);
-        const T f = isp ? T(0) : a[k] / pv;
+        const T f = isp ? T(0) : a[k] * rpv;
         if (isp) { used = true; piv_row = k; mypiv = pv; }
 #pragma unroll
         for (int j = k + 1; j < NR; ++j) a[j] = fma(-f, wbcast<WS>(mask, a[j], p), a[j]);
@@ -221,7 +247,7 @@ __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)
         }
     }
     {
-        const T inv = T(1) / mypiv;
+        const T inv = rcp_rn(mypiv);
 #pragma unroll
         for (int j = 0; j < NRHS; ++j) rhs[j] *= inv;
     }
@@ -236,5 +262,77 @@ __device__ __forceinline__ bool gauss_jordan(unsigned mask, T (&a)[NR], T (&rhs)
         return __all_sync(mask, ok);
     }
 }
+
+// Compact Gauss-Jordan for fully converged warps (mask = all lanes, several WS-lane workers per
+// warp): same arithmetic as gauss_jordan<..., FULLWARP = true> but the pivot loop is not unrolled
+// (column k of the lane's row is extracted with selects and every column is updated, the pivot
+// row's already-eliminated columns being zero), so the code is ~NR times smaller and the loop body
+// stays resident in the instruction cache.
+template <typename T, int WS, int NR, int NRHS, bool PIVOT>
+__device__ __forceinline__ bool gauss_jordan_compact(T (&a)[NR], T (&rhs)[NRHS], int lane, int &piv_row) {
+    bool used = lane >= NR;
+    bool ok = true;
+    piv_row = -1;
+    T mypiv = T(1);
+#pragma unroll 1
+    for (int k = 0; k < NR; ++k) {
+        T ak = a[0];
+#pragma unroll
+        for (int j = 1; j < NR; ++j) ak = (j == k) ? a[j] : ak;
+        int p;
+        if constexpr (PIVOT) {
+            const unsigned key = used ? 0u : ((__float_as_uint(fabsf((float)ak)) & 0xFFFFFFE0u) | (31u - (unsigned)lane));
+            unsigned best = key;
+#pragma unroll
+            for (int off = WS / 2; off >= 1; off >>= 1) best = max(best, __shfl_xor_sync(0xffffffffu, best, off, WS));
+            p = 31 - (int)(best & 31u);
+        } else {
+            p = k;
+        }
+        const T pv = __shfl_sync(0xffffffffu, ak, p, WS);
+        if constexpr (PIVOT) ok = ok && (pv != T(0)) && isfinite(pv);
+        else ok = ok && (pv > T(0)) && isfinite(pv);
+        const bool isp = (lane == p);
+        const T f = isp ? T(0) : ak * rcp_rn(pv);
+        if (isp) { used = true; piv_row = k; mypiv = pv; }
+        if constexpr (NR % 2 == 0) {
+#pragma unroll
+            for (int j = 0; j < NR; j += 2) {
+                const T p0 = __shfl_sync(0xffffffffu, a[j], p, WS), p1 = __shfl_sync(0xffffffffu, a[j + 1], p, WS);
+                ffma2(-f, -f, p0, p1, a[j], a[j + 1]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NR; ++j) a[j] = fma(-f, __shfl_sync(0xffffffffu, a[j], p, WS), a[j]);
+        }
+        if constexpr (NRHS % 2 == 0) {
+#pragma unroll
+            for (int j = 0; j < NRHS; j += 2) {
+                const T p0 = __shfl_sync(0xffffffffu, rhs[j], p, WS), p1 = __shfl_sync(0xffffffffu, rhs[j + 1], p, WS);
+                ffma2(-f, -f, p0, p1, rhs[j], rhs[j + 1]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < NRHS; ++j) rhs[j] = fma(-f, __shfl_sync(0xffffffffu, rhs[j], p, WS), rhs[j]);
+        }
+    }
+    const T inv = rcp_rn(mypiv);
+#pragma unroll
+    for (int j = 0; j < NRHS; ++j) rhs[j] *= inv;
+    if constexpr (!PIVOT) piv_row = lane < NR ? lane : -1;
+    unsigned v = ok ? 1u : 0u;
+#pragma unroll
+    for (int off = WS / 2; off >= 1; off >>= 1) v &= __shfl_xor_sync(0xffffffffu, v, off, WS);
+    return v != 0u;
+}
+
+// cp.async (LDGSTS) helpers: 16-byte global -> shared copies that complete asynchronously.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NPENDING>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPENDING)); }
 
 }  // namespace pdilqr

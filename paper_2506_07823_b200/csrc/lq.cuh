@@ -585,7 +585,8 @@ __global__ void __launch_bounds__(128) k_policy(LqArgs<T> qp, int B, int N, int 
         T G[NU], rhs[NX + 1];
         if (vu) {
             ld_row<T, NU, EX>(G, qp.R + st * m * m + ru * m, m);
-            ld_row<T, NX, EX>(*reinterpret_cast<T(*)[NX]>(rhs), qp.S + st * m * n + ru * n, n);
+            if (qp.S != nullptr) ld_row<T, NX, EX>(*reinterpret_cast<T(*)[NX]>(rhs), qp.S + st * m * n + ru * n, n);
+            else zero(*reinterpret_cast<T(*)[NX]>(rhs));   // S = 0 (SRBD Gauss-Newton cost)
             rhs[NX] = qp.r[st * m + ru];
         } else {
 #pragma unroll
@@ -825,6 +826,117 @@ __global__ void k_finalize_info(int B, const int32_t *fail, const int32_t *nonfi
     int v = fail[b] != kFailNone ? (fail[b] & 0xFFFFFF) : (nonfin[b] ? -1 : 0);
     if (pre != nullptr && pre[b] != 0) v = pre[b];
     info[b] = v;
+}
+
+// ------------------------------------------------------------ single-chunk reverse scan (J = 1)
+// s_{N+1} = e_{N+1}, s_i = e_i (x) s_{i+1} by the cheap rule for i = N..0: the leaf_chunk >= N+2
+// schedule of k_scan_bwd as a tight per-instance loop.  Two instances per warp, warp kept
+// converged (a worker past the batch recomputes instance B-1 without storing); the next element is
+// prefetched into shared memory with cp.async while the current combine runs; compact Gauss-Jordan
+// keeps the loop body small.
+template <typename T, int NX>
+struct FoldChainSmem {
+    T buf[2][VE<NX>::SIZE];
+    T P[NX * NX], X[NX * NX], V[NX * NX];
+    T p[NX], w[NX];
+};
+
+template <typename T, int NX, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_fold(int B, int N, LqWork<T> ws) {
+    constexpr int WS = worker_width(NX);
+    using L = VE<NX>;
+    constexpr int TP = TE<NX>::SIZE;
+    constexpr int NG = L::SIZE * sizeof(T) / 16;  // 16-byte granules per element
+    extern __shared__ __align__(16) unsigned char smraw[];
+    FoldChainSmem<T, NX> &s = reinterpret_cast<FoldChainSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    const int lane = worker_lane<WS>();
+    const int b_raw = blockIdx.x * (blockDim.x / WS) + threadIdx.x / WS;
+    if (__all_sync(0xffffffffu, b_raw >= B)) return;
+    const bool live = b_raw < B;
+    const int b = live ? b_raw : B - 1;
+    const int r = lane < NX ? lane : 0;
+    const bool act = lane < NX;
+    const T *E = ws.elems + (size_t)b * (N + 2) * L::SIZE;
+    T *Pp = ws.Pp + (size_t)b * (N + 2) * TP;
+    auto prefetch = [&](int i, int slot) {
+        const char *src = reinterpret_cast<const char *>(E + (size_t)i * L::SIZE);
+        char *dst = reinterpret_cast<char *>(s.buf[slot]);
+        for (int g = lane; g < NG; g += WS) cp_async16(dst + 16 * g, src + 16 * g);
+    };
+    prefetch(N, 0);
+    cp_async_commit();
+    {  // s_{N+1} = e_{N+1}: only P~, p~ are nonzero (Eq. 13)
+        T prow[NX];
+        ld_row<T, NX, true>(prow, E + (size_t)(N + 1) * L::SIZE + L::P + r * NX);
+        const T pr = E[(size_t)(N + 1) * L::SIZE + L::p + r];
+        if (act) {
+            st_row<T, NX, true>(s.P + r * NX, prow);
+            s.p[r] = pr;
+            if (live) {
+                st_row<T, NX, true>(Pp + (size_t)(N + 1) * TP + r * NX, prow);
+                Pp[(size_t)(N + 1) * TP + NX * NX + r] = pr;
+            }
+        }
+    }
+    int fail = INT_MAX;
+    for (int i = N; i >= 0; --i) {
+        const int cur = (N - i) & 1;
+        if (i > 0) prefetch(i - 1, cur ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const T *e1 = s.buf[cur];
+        T prow[NX];
+        ld_row<T, NX, true>(prow, s.P + r * NX);
+        T M[NX];
+        {
+            T c1[NX];
+            ld_row<T, NX, true>(c1, e1 + L::C + r * NX);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) M[j] = (j == r) ? T(1) : T(0);
+            row_mat<T, NX, NX, NX>(M, c1, s.P);                      // M = I + C~_i P_{i+1}
+        }
+        const T wr = row_dot<T, NX>(prow, e1 + L::b, s.p[r]);        // w = p' + P' b~_i
+        if (act) s.w[r] = wr;
+        T rhs[NX];
+        ld_row<T, NX, true>(rhs, e1 + L::A + r * NX);
+        int pr;
+        if (!gauss_jordan<T, WS, NX, NX, true, true>(0xffffffffu, M, rhs, lane, NX, pr)) fail = min(fail, i + 1);
+        if (pr >= 0) st_row<T, NX, true>(s.X + pr * NX, rhs);       // X = M^-1 A~_i
+        __syncwarp();
+        {
+            T V[NX];
+            zero(V);
+            row_mat<T, NX, NX, NX>(V, prow, s.X);                    // V = P' X
+            if (act) st_row<T, NX, true>(s.V + r * NX, V);
+        }
+        T pn;
+        {
+            T xc[NX];
+            ld_col<T, NX>(xc, s.X + r, NX);
+            pn = row_dot<T, NX>(xc, s.w, e1[L::p + r]);              // p_i = X^T w + p~_i
+        }
+        __syncwarp();
+        T Pn[NX];
+        {
+            T ac[NX];
+            ld_col<T, NX>(ac, e1 + L::A + r, NX);
+            ld_row<T, NX, true>(Pn, e1 + L::P + r * NX);
+            row_mat<T, NX, NX, NX>(Pn, ac, s.V);                     // P_i = A~^T P' X + P~_i
+        }
+        __syncwarp();
+        symmetrize_rows<T, NX>(Pn, s.X, 0xffffffffu, lane);
+        if (act) {
+            st_row<T, NX, true>(s.P + r * NX, Pn);
+            s.p[r] = pn;
+            if (live) {
+                st_row<T, NX, true>(Pp + (size_t)i * TP + r * NX, Pn);
+                Pp[(size_t)i * TP + NX * NX + r] = pn;
+            }
+        }
+        __syncwarp();
+    }
+    if (live && fail != INT_MAX && lane == 0) atomicMin(ws.fail + b, (1 << 24) | fail);
 }
 
 }  // namespace pdilqr

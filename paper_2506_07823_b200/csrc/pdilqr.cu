@@ -83,6 +83,7 @@ struct pdilqr_ctx {
     SrbdConst K;
     int launches;
     int occ_fold = 4, occ_ls = 4;  // minimum resident CTAs per SM requested from ptxas (register cap: 128)
+    int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
     // per-kernel CUDA-event timing (host bookkeeping only; off unless pdilqr_profile(h, 1))
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -247,7 +248,14 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
         ++launches;
     }
-    {  // backward scan
+    if (h->Jb == 1) {  // single chunk: tight per-instance fold with prefetch
+        const size_t smem = (size_t)(128 / WSX) * sizeof(FoldChainSmem<T, NX>);
+        set_smem(k_fold<T, NX, 4>, smem);
+        Prof pf(h, "k_fold", st);
+        const int ipb = 128 / WSX;
+        k_fold<T, NX, 4><<<(B + ipb - 1) / ipb, 128, smem, st>>>(B, N, ws);
+        ++launches;
+    } else {  // backward scan
         const int J = h->Jb, Pv = h->Pv;
         const size_t cs = sizeof(CombineSmem<T, NX>);
         int W = 1, IPB = 8;
@@ -343,6 +351,58 @@ pdilqr_status run_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArg
     return cuda_check("linearize launch");
 }
 
+// Single-chunk schedule, split path (4 kernels): stage-parallel linearisation + element init,
+// per-instance fold, stage-parallel policy, per-instance rollout + line search + update.
+template <typename T>
+pdilqr_status run_step_split(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir,
+                             cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N;
+    LqWork<T> ws = work<T>(h);
+    int32_t *pre = reinterpret_cast<int32_t *>(h->ws + h->lay.pre);
+    LqArgs<T> qp = internal_qp<T>(h);
+    qp.S = nullptr;
+    T *dx, *du, *dl;
+    if (dir && dir->dx) {
+        dx = (T *)dir->dx; du = (T *)dir->du; dl = (T *)dir->dlam;
+    } else {
+        dx = reinterpret_cast<T *>(h->ws + h->lay.dir[0]);
+        du = reinterpret_cast<T *>(h->ws + h->lay.dir[1]);
+        dl = reinterpret_cast<T *>(h->ws + h->lay.dir[2]);
+    }
+    cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
+    cudaMemsetAsync(pre, 0, (size_t)B * 4, st);
+    {
+        const long nw = (long)B * (N + 2);
+        const size_t smem = 8 * sizeof(LinElemSmem<T>);
+        set_smem(k_srbd_lin_elem<T>, smem);
+        Prof pf(h, "k_srbd_lin_elem", st);
+        k_srbd_lin_elem<T><<<(unsigned)((nw + 7) / 8), 128, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, qp, pre);
+    }
+    {
+        const size_t smem = 8 * sizeof(FoldChainSmem<T, 12>);
+        set_smem(k_fold<T, 12, 4>, smem);
+        Prof pf(h, "k_fold", st);
+        k_fold<T, 12, 4><<<(B + 7) / 8, 128, smem, st>>>(B, N, ws);
+    }
+    {
+        LqOut<T> out{dx, du, dl, dir ? (T *)dir->K : nullptr, dir ? (T *)dir->k : nullptr};
+        const size_t smem = (size_t)8 * (12 * 12 * 4 + 12 + 12 + 12) * sizeof(T);
+        set_smem(k_policy<T, 12, 12, true>, smem);
+        Prof pf(h, "k_policy", st);
+        const long nw = (long)B * (N + 1);
+        k_policy<T, 12, 12, true><<<(unsigned)((nw + 7) / 8), 128, smem, st>>>(qp, B, N, 12, 12, ws, out);
+    }
+    {
+        LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
+        Prof pf(h, "k_srbd_fwd_ls", st);
+        constexpr int WPB = LsWarps<T>::value;
+        k_srbd_fwd_ls<T, 4><<<(B + WPB - 1) / WPB, 32 * WPB, 0, st>>>(h->K, iter_of<T>(it), B, N, ws, dx, du, dl, nullptr, so,
+                                                                       pre);
+    }
+    h->launches += 4;
+    return cuda_check("step (split) launch");
+}
+
 // Single-chunk schedule: the fused fold path (srbd_fused.cuh), 2 kernels per step.
 template <typename T>
 pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st) {
@@ -374,7 +434,8 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
         Prof pf(h, "k_srbd_fwd_ls", st);
         auto go = [&](auto kern) {
-            kern<<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, ws, dx, du, dl, info_tmp, so);
+            constexpr int WPB = LsWarps<T>::value;
+            kern<<<(B + WPB - 1) / WPB, 32 * WPB, 0, st>>>(h->K, iter_of<T>(it), B, N, ws, dx, du, dl, info_tmp, so, nullptr);
         };
         switch (h->occ_ls) {
             case 3: go(k_srbd_fwd_ls<T, 3>); break;
@@ -397,7 +458,8 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
 
 template <typename T>
 pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st) {
-    if (h->Jb == 1 && h->cfg.n == 12 && h->cfg.m == 12) return run_step_fused<T>(h, it, stats, dir, st);
+    if (h->Jb == 1 && h->cfg.n == 12 && h->cfg.m == 12)
+        return h->fused ? run_step_fused<T>(h, it, stats, dir, st) : run_step_split<T>(h, it, stats, dir, st);
     const int B = h->cfg.batch, N = h->cfg.N;
     LqArgs<T> qp = internal_qp<T>(h);
     int32_t *pre = reinterpret_cast<int32_t *>(h->ws + h->lay.pre);
@@ -500,6 +562,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     K.theta_max = h->cfg.theta_max; K.c1 = h->cfg.armijo_c1; K.n_alpha = h->cfg.n_alpha;
     if (const char *e = std::getenv("PDILQR_OCC_FOLD")) h->occ_fold = std::atoi(e);  // tuning knobs
     if (const char *e = std::getenv("PDILQR_OCC_LS")) h->occ_ls = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_FUSED")) h->fused = std::atoi(e);
     *out = h;
     return PDILQR_OK;
 }

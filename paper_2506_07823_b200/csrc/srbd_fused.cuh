@@ -17,6 +17,18 @@
 
 namespace pdilqr {
 
+// SFU fast math in fp32 (line search only: evaluations whose rounding cannot change the LQ solve);
+// accurate libm in fp64.
+__device__ __forceinline__ void fast_sincos(float x, float *s, float *c) { __sincosf(x, s, c); }
+__device__ __forceinline__ void fast_sincos(double x, double *s, double *c) { sincos(x, s, c); }
+__device__ __forceinline__ float fast_log(float x) { return __logf(x); }
+__device__ __forceinline__ double fast_log(double x) { return log(x); }
+
+template <typename T>
+struct LsWarps {  // k_srbd_fwd_ls block = LsWarps * 32 threads (static shared memory <= 48 KB)
+    static constexpr int value = sizeof(T) == 8 ? 2 : 4;
+};
+
 template <typename T>
 struct FoldSmem {
     T P[144], A[144], B[144], ZB[144], X[144], V[144], K[144];
@@ -251,12 +263,16 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
 // ------------------------------------------------------------------ forward + line search
 template <typename T, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
-                                                           T *dx, T *du, T *dlam, const int32_t *info_in, LsOut<T> so) {
+                                                           T *dx, T *du, T *dlam, const int32_t *info_in, LsOut<T> so,
+                                                           const int32_t *pre_info = nullptr) {
     constexpr int NX = 12, NA = 16;
     constexpr int TP = TE<NX>::SIZE;
     using KL = KE<NX, NX>;
-    __shared__ __align__(16) T sx[4][16];
-    __shared__ double sJ[4][NA][32], sT[4][NA][32];
+    constexpr int WPB = LsWarps<T>::value;  // warps (instances) per block
+    __shared__ __align__(16) T sx[WPB][16];
+    __shared__ double sJ[WPB][NA][32], sT[WPB][NA][32];
+    using F = T;                        // line-search evaluation type (fast SFU math for fp32)
+    __shared__ F sDel[WPB][24][32];     // per lane: x_{i+1} - x_i and dx_{i+1} - dx_i of its stage
     const int lane = threadIdx.x & 31, wl = threadIdx.x / 32;
     const int b = blockIdx.x * (blockDim.x / 32) + wl;
     if (b >= B) return;
@@ -269,7 +285,13 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     const T *Kk = ws.Kk + (size_t)b * (N + 1) * KL::SIZE;
     const T *Te = ws.tel + (size_t)b * (N + 1) * TP;
     T *Dx = dx + (size_t)b * (N + 2) * NX, *Du = du + (size_t)b * (N + 1) * NX, *Dl = dlam + (size_t)b * (N + 2) * NX;
-    const int info = info_in[b];
+    int info;
+    if (info_in != nullptr) {
+        info = info_in[b];
+    } else {  // finalise from the pipeline's failure records (see k_finalize_info)
+        const int f = ws.fail[b], pr = pre_info[b];
+        info = pr != 0 ? pr : (f != kFailNone ? (f & 0xFFFFFF) : 0);
+    }
     // ---------------- closed-loop rollout (one chunk of Eq. 15) and du (Eq. 6)
     const int r = lane & 15;
     const bool rowl = r < NX;
@@ -278,25 +300,34 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         if (lane < NX) { sx[wl][r] = d0; Dx[r] = d0; }
     }
     __syncwarp();
+    // lanes 0..11: dx_{i+1} = Abar_i dx_i + bbar_i ; lanes 16..27: du_i = K_i dx_i + k_i.
+    // The next stage's row is loaded while the current one is applied (register double buffer).
+    const T *rowbase = lane < 16 ? Te + (size_t)(rowl ? r : 0) * NX : Kk + KL::K + (size_t)(rowl ? r : 0) * NX;
+    const T *offbase = lane < 16 ? Te + NX * NX + (rowl ? r : 0) : Kk + KL::k + (rowl ? r : 0);
+    const size_t rstride = lane < 16 ? (size_t)TP : (size_t)KL::SIZE;
+    T rcur[NX], ocur;
+    ld_row<T, NX, true>(rcur, rowbase);
+    ocur = offbase[0];
     for (int i = 0; i <= N; ++i) {
+        T rnext[NX], onext = T(0);
+        if (i < N) {
+            ld_row<T, NX, true>(rnext, rowbase + (size_t)(i + 1) * rstride);
+            onext = offbase[(size_t)(i + 1) * rstride];
+        }
         T xv[NX];
         ld_row<T, NX, true>(xv, sx[wl]);
-        T v;
-        if (lane < 16) {  // dx_{i+1} = Abar_i dx_i + bbar_i
-            T arow[NX];
-            ld_row<T, NX, true>(arow, Te + (size_t)i * TP + (rowl ? r : 0) * NX);
-            v = row_dot<T, NX>(arow, xv, Te[(size_t)i * TP + NX * NX + (rowl ? r : 0)]);
-        } else {          // du_i = K_i dx_i + k_i
-            T krow[NX];
-            ld_row<T, NX, true>(krow, Kk + (size_t)i * KL::SIZE + KL::K + (rowl ? r : 0) * NX);
-            v = row_dot<T, NX>(krow, xv, Kk[(size_t)i * KL::SIZE + KL::k + (rowl ? r : 0)]);
-        }
+        const T v = row_dot<T, NX>(rcur, xv, ocur);
         __syncwarp();
         if (rowl) {
             if (lane < 16) { sx[wl][r] = v; Dx[(size_t)(i + 1) * NX + r] = v; }
             else Du[(size_t)i * NX + r] = v;
         }
         __syncwarp();
+        if (i < N) {
+#pragma unroll
+            for (int j = 0; j < NX; ++j) rcur[j] = rnext[j];
+            ocur = onext;
+        }
     }
     // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel
     for (int t = lane; t < (N + 2) * NX; t += 32) {
@@ -308,7 +339,11 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     }
     __syncwarp();
     // ---------------- line search: lane = stage; per alpha slot a (0 = current iterate,
-    // a >= 1: alpha = 2^-(a-1)); per-lane partial sums in shared memory (no unrolled alpha loop)
+    // a >= 1: alpha = 2^-(a-1)); per-lane partial sums in shared memory (no unrolled alpha loop).
+    // Per stage the alpha-invariant parts are computed once: the tracking costs are exact
+    // quadratics c0 + c1 a + c2 a^2 (fp64), the barrier arguments are xi0 + a dxi, the defect is
+    // (x_{i+1} - x_i) + a (dx_{i+1} - dx_i) - dt f(x_i + a dx_i, u_i + a du_i).  Trial states and
+    // the model are evaluated in fp32 (fast sincos / log: SFU), sums in fp64.
     double(*aJ)[32] = sJ[wl];
     double(*aT)[32] = sT[wl];
     for (int a = 0; a <= na; ++a) { aJ[a][lane] = 0.0; aT[a][lane] = 0.0; }
@@ -335,58 +370,105 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         const T *feet = it.feet + ((size_t)b * (N + 1) + i) * 12;
         const uint8_t *con = it.con + ((size_t)b * (N + 1) + i) * 4;
         const T *uri = urf ? urf + (size_t)i * NX : nullptr;
+        F xs0[NX], dxs[NX], us0[NX], dus[NX], fe[12];
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            xs0[k] = (F)xi[k]; dxs[k] = (F)dxi[k]; us0[k] = (F)ui[k]; dus[k] = (F)dui[k];
+            fe[k] = (F)feet[k];
+            sDel[wl][k][lane] = (F)(xi[NX + k] - xi[k]);
+            sDel[wl][NX + k][lane] = (F)(dxi[NX + k] - dxi[k]);
+        }
+        const uint8_t cmask = (uint8_t)((con[0] ? 1 : 0) | (con[1] ? 2 : 0) | (con[2] ? 4 : 0) | (con[3] ? 8 : 0));
         // quadratic tracking costs: c0 + c1 a + c2 a^2
         double c0 = 0, c1 = 0, c2 = 0;
 #pragma unroll
         for (int k = 0; k < NX; ++k) {
             const double e = (double)xi[k] - (double)xri[k], d = (double)dxi[k];
             c0 += 0.5 * K.wx[k] * e * e; c1 += K.wx[k] * e * d; c2 += 0.5 * K.wx[k] * d * d;
-            const double wu = con[k / 3] ? K.wu_st : K.wu_sw;
+            const double wu = ((cmask >> (k / 3)) & 1) ? K.wu_st : K.wu_sw;
             const double eu = (double)ui[k] - (uri ? (double)uri[k] : 0.0), du_ = (double)dui[k];
             c0 += 0.5 * wu * eu * eu; c1 += wu * eu * du_; c2 += 0.5 * wu * du_ * du_;
         }
         g += c1;
-        for (int j = 0; j < 4; ++j) {  // barrier slopes at alpha = 0
-            if (!con[j]) continue;
+        // barrier arguments xi0 + a dxi of the stance-foot constraints and their slopes at a = 0
+        F bx0[24], bdx[24];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
             for (int cc = 0; cc < 6; ++cc) {
-                T gx, gy, gz, h;
-                foot_con<T>(cc, T(K.mu), T(K.fmin), T(K.fmax), gx, gy, gz, h);
-                const T xi0 = gx * ui[3 * j] + gy * ui[3 * j + 1] + gz * ui[3 * j + 2] + h;
-                const double dxi_ = (double)gx * dui[3 * j] + (double)gy * dui[3 * j + 1] + (double)gz * dui[3 * j + 2];
-                g += (double)barrier_d1<T>(xi0, T(K.bmu), T(K.bdelta)) * dxi_;
+                F gx, gy, gz, h;
+                foot_con<F>(cc, (F)K.mu, (F)K.fmin, (F)K.fmax, gx, gy, gz, h);
+                bx0[6 * j + cc] = gx * us0[3 * j] + gy * us0[3 * j + 1] + gz * us0[3 * j + 2] + h;
+                bdx[6 * j + cc] = gx * dus[3 * j] + gy * dus[3 * j + 1] + gz * dus[3 * j + 2];
+                if ((cmask >> j) & 1)
+                    g += (double)barrier_d1<F>(bx0[6 * j + cc], (F)K.bmu, (F)K.bdelta) * (double)bdx[6 * j + cc];
             }
         }
-        const T *xn = xi + NX, *dxn = dxi + NX;
+        const F bmu = (F)K.bmu, bdl = (F)K.bdelta, lbd = fast_log((F)K.bdelta);
         for (int a = 0; a <= na; ++a) {
-            const double al = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
-            double J = c0 + al * (c1 + al * c2);
-            T xs[NX], us[NX];
+            const double ald = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
+            const F al = (F)ald;
+            double J = c0 + ald * (c1 + ald * c2);
+            F Jb = F(0.);
 #pragma unroll
-            for (int k = 0; k < NX; ++k) {
-                xs[k] = (T)((double)xi[k] + al * (double)dxi[k]);
-                us[k] = (T)((double)ui[k] + al * (double)dui[k]);
-            }
-            if (!(fabs((double)xi[4] + al * (double)dxi[4]) < kPitchGuard)) guard |= 1u << a;
             for (int j = 0; j < 4; ++j) {
-                if (!con[j]) continue;
+                if (!((cmask >> j) & 1)) continue;
+#pragma unroll
                 for (int cc = 0; cc < 6; ++cc) {
-                    T gx, gy, gz, h;
-                    foot_con<T>(cc, T(K.mu), T(K.fmin), T(K.fmax), gx, gy, gz, h);
-                    const T xi_ = gx * us[3 * j] + gy * us[3 * j + 1] + gz * us[3 * j + 2] + h;
-                    J += (double)barrier_val<T>(xi_, T(K.bmu), T(K.bdelta));
+                    const F xv = fma(al, bdx[6 * j + cc], bx0[6 * j + cc]);
+                    const F t = (xv - F(2.) * bdl) / bdl;
+                    Jb += xv >= bdl ? -bmu * fast_log(xv) : F(0.5) * bmu * (t * t - F(1.)) - bmu * lbd;
                 }
             }
-            SrbdEval<T> ev;
-            ev.init(K, xs, us, feet, con);
-            double d2 = 0;
+            J += (double)Jb;
+            F xs[NX], us[NX];
+#pragma unroll
+            for (int k = 0; k < NX; ++k) { xs[k] = fma(al, dxs[k], xs0[k]); us[k] = fma(al, dus[k], us0[k]); }
+            if (!(fabs(xs[4]) < (F)kPitchGuard)) guard |= 1u << a;
+            // SRBD f(xs, us) (fast SFU trig): same equations as SrbdEval
+            F sr, cr, sp, cp, sy, cy;
+            fast_sincos(xs[3], &sr, &cr);
+            fast_sincos(xs[4], &sp, &cp);
+            fast_sincos(xs[5], &sy, &cy);
+            const F icp = F(1.) / cp, tp = sp * icp;
+            const F R0 = cy * cp, R1 = cy * sp * sr - sy * cr, R2 = cy * sp * cr + sy * sr;
+            const F R3 = sy * cp, R4 = sy * sp * sr + cy * cr, R5 = sy * sp * cr - cy * sr;
+            const F R6 = -sp, R7 = cp * sr, R8 = cp * cr;
+            F t0 = F(0.), t1 = F(0.), t2 = F(0.), F0 = F(0.), F1 = F(0.), F2 = F(0.);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (!((cmask >> j) & 1)) continue;
+                const F fx = us[3 * j], fy = us[3 * j + 1], fz = us[3 * j + 2];
+                const F rx = fe[3 * j] - xs[0], ry = fe[3 * j + 1] - xs[1], rz = fe[3 * j + 2] - xs[2];
+                t0 += ry * fz - rz * fy; t1 += rz * fx - rx * fz; t2 += rx * fy - ry * fx;
+                F0 += fx; F1 += fy; F2 += fz;
+            }
+            const F w0 = xs[9], w1 = xs[10], w2 = xs[11];
+            F Iw[3], rh[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) Iw[c] = (F)K.I[3 * c] * w0 + (F)K.I[3 * c + 1] * w1 + (F)K.I[3 * c + 2] * w2;
+            rh[0] = R0 * t0 + R3 * t1 + R6 * t2 - (w1 * Iw[2] - w2 * Iw[1]);
+            rh[1] = R1 * t0 + R4 * t1 + R7 * t2 - (w2 * Iw[0] - w0 * Iw[2]);
+            rh[2] = R2 * t0 + R5 * t1 + R8 * t2 - (w0 * Iw[1] - w1 * Iw[0]);
+            F fv[NX];
+            fv[0] = xs[6]; fv[1] = xs[7]; fv[2] = xs[8];
+            fv[3] = w0 + sr * tp * w1 + cr * tp * w2;
+            fv[4] = cr * w1 - sr * w2;
+            fv[5] = (sr * w1 + cr * w2) * icp;
+            const F im = F(1.) / (F)K.mass;
+            fv[6] = F0 * im + (F)K.g[0]; fv[7] = F1 * im + (F)K.g[1]; fv[8] = F2 * im + (F)K.g[2];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                fv[9 + c] = (F)K.Iinv[3 * c] * rh[0] + (F)K.Iinv[3 * c + 1] * rh[1] + (F)K.Iinv[3 * c + 2] * rh[2];
+            const F dtf = (F)K.dt;
+            F d2 = F(0.);
 #pragma unroll
             for (int k = 0; k < NX; ++k) {
-                const double d = ((double)xn[k] - (double)xi[k]) + al * ((double)dxn[k] - (double)dxi[k]) -
-                                 K.dt * (double)ev.f(K, xs, k);
-                d2 += d * d;
+                const F d = fma(al, sDel[wl][NX + k][lane], sDel[wl][k][lane]) - dtf * fv[k];
+                d2 = fma(d, d, d2);
             }
             aJ[a][lane] += J;
-            aT[a][lane] += sqrt(d2);
+            aT[a][lane] += (double)sqrt(d2);
         }
     }
     // fixed-order xor butterflies: every lane ends with bitwise identical sums
@@ -454,6 +536,123 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         so.alpha[b] = alpha;
         so.accepted[b] = jb >= 0 ? 1 : 0;
         so.info[b] = info;
+    }
+}
+
+// ------------------------------------------- stage-parallel linearisation + element init
+// One worker per (instance, stage i = 0..N+1): linearise stage i (a1) and build its value element
+// (a2, Eq. 12 with S = 0, block-diagonal R^-1 in closed form; Eq. 13 for i = N+1) into
+// ws.elems, plus the Eq. 4 blocks the policy needs (A, B, b, R, r) into `qp` (user layout).
+template <typename T>
+struct LinElemSmem {
+    T B[144], F[144], Rr[144], ZB[144];
+    T zr[12], c[12], pad[8];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(128) k_srbd_lin_elem(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+                                                       LqArgs<T> qp, int32_t *pre_info) {
+    constexpr int WS = 16, NX = 12;
+    using L = VE<NX>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    LinElemSmem<T> &s = reinterpret_cast<LinElemSmem<T> *>(smraw)[threadIdx.x / WS];
+    const int lane = worker_lane<WS>();
+    const long gw_raw = (long)blockIdx.x * (blockDim.x / WS) + threadIdx.x / WS;
+    const long total = (long)B * (N + 2);
+    if (__all_sync(0xffffffffu, gw_raw >= total)) return;
+    const bool live = gw_raw < total;
+    const long gw = live ? gw_raw : total - 1;
+    const int b = (int)(gw / (N + 2)), i = (int)(gw % (N + 2));
+    const int r = lane < NX ? lane : 0;
+    const bool act = lane < NX, wr_g = act && live;
+    const T *x = it.x + ((size_t)b * (N + 2) + i) * NX;
+    const T *lam = it.lam + ((size_t)b * (N + 2) + i) * NX;
+    const T *xr = it.xref + ((size_t)b * (N + 2) + i) * NX;
+    T *e = ws.elems + ((size_t)b * (N + 2) + i) * L::SIZE;
+    if (i == N + 1) {  // e_{N+1}: A~ = C~ = b~ = 0, P~ = W_N, p~ = W_N (x - xref) - lam  (Eq. 13)
+        T z[NX], Prow[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) { z[j] = T(0); Prow[j] = (j == r) ? T(K.wxt[r]) : T(0); }
+        const T pr = T(K.wxt[r]) * (x[r] - xr[r]) - lam[r];
+        if (wr_g) {
+            st_row<T, NX, true>(e + L::A + r * NX, z);
+            st_row<T, NX, true>(e + L::C + r * NX, z);
+            st_row<T, NX, true>(e + L::P + r * NX, Prow);
+            e[L::b + r] = T(0);
+            e[L::p + r] = pr;
+            if (!isfinite(x[r]) || !isfinite(lam[r]) || !isfinite(it.x0[(size_t)b * NX + r])) pre_info[b] = -1;
+        }
+        return;  // the partner worker of this warp only uses its own lane mask below
+    }
+    const size_t st = (size_t)b * (N + 1) + i;
+    const T *u = it.u + st * NX, *feet = it.feet + st * 12;
+    const uint8_t *con = it.con + st * 4;
+    const T *ur = it.uref ? it.uref + st * NX : nullptr;
+    const T *ln = lam + NX;
+    const T dt = T(K.dt);
+    SrbdRow<T> row;
+    srbd_stage_row<T>(K, x, u, feet, con, ur, r, row);
+    const bool bad = row.bad || !isfinite(lam[r]);
+    const T cr = (x[r] - x[NX + r]) + dt * row.fr;  // b_i = h(x_i, u_i) - x_{i+1}
+    const unsigned mask = worker_mask<WS>();
+    if (act) {
+        st_row<T, NX, true>(s.B + r * NX, row.Brow);
+        st_row<T, NX, true>(s.F + r * NX, row.Arow);  // dt Fx
+        st_row<T, NX, true>(s.Rr + r * NX, row.Rrow);
+        s.c[r] = cr;
+    }
+    __syncwarp(mask);
+    T ATl = T(0), BTl = T(0);
+#pragma unroll
+    for (int t = 0; t < NX; ++t) { ATl = fma(s.F[t * NX + r], ln[t], ATl); BTl = fma(s.B[t * NX + r], ln[t], BTl); }
+    const T qr = T(K.wx[r]) * (x[r] - xr[r]) + ((ln[r] - lam[r]) + ATl);
+    const T rr = row.rg + BTl;
+    if (act) s.zr[r] = rr;
+    __syncwarp(mask);
+    bool fail = false;
+    {   // R^-1 per foot block (closed form), z = R^-1 r, ZB = R^-1 B^T
+        const int jf = r / 3, ar = r - 3 * (r / 3), o = 3 * jf;
+        const T *Rb = s.Rr + o * NX + o;
+        const T a00 = Rb[0], a01 = Rb[1], a02 = Rb[2];
+        const T a10 = Rb[NX], a11 = Rb[NX + 1], a12 = Rb[NX + 2];
+        const T a20 = Rb[2 * NX], a21 = Rb[2 * NX + 1], a22 = Rb[2 * NX + 2];
+        const T c00 = a11 * a22 - a12 * a21, c01 = a02 * a21 - a01 * a22, c02 = a01 * a12 - a02 * a11;
+        const T c10 = a12 * a20 - a10 * a22, c11 = a00 * a22 - a02 * a20, c12 = a02 * a10 - a00 * a12;
+        const T c20 = a10 * a21 - a11 * a20, c21 = a01 * a20 - a00 * a21, c22 = a00 * a11 - a01 * a10;
+        const T det = a00 * c00 + a01 * c10 + a02 * c20;
+        fail = !(a00 > T(0)) || !(c22 > T(0)) || !(det > T(0)) || !isfinite(det);
+        const T id = T(1) / det;
+        const T q0 = (ar == 0 ? c00 : ar == 1 ? c10 : c20) * id;
+        const T q1 = (ar == 0 ? c01 : ar == 1 ? c11 : c21) * id;
+        const T q2 = (ar == 0 ? c02 : ar == 1 ? c12 : c22) * id;
+        const T z = q0 * s.zr[o] + q1 * s.zr[o + 1] + q2 * s.zr[o + 2];
+        T zb[NX];
+#pragma unroll
+        for (int t = 0; t < NX; ++t) zb[t] = q0 * s.B[t * NX + o] + q1 * s.B[t * NX + o + 1] + q2 * s.B[t * NX + o + 2];
+        __syncwarp(mask);
+        if (act) { st_row<T, NX, true>(s.ZB + r * NX, zb); s.zr[r] = z; }
+    }
+    __syncwarp(mask);
+    T ct[NX];
+    zero(ct);
+    row_mat<T, NX, NX, NX>(ct, row.Brow, s.ZB);                    // C~ = B R^-1 B^T
+    const T bt = cr - row_dot<T, NX>(row.Brow, s.zr, T(0));          // b~ = b - B R^-1 r
+    if (wr_g) {
+        T arow[NX], Prow[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) { arow[j] = (j == r ? T(1) : T(0)) + row.Arow[j]; Prow[j] = (j == r) ? T(K.wx[r]) : T(0); }
+        st_row<T, NX, true>(e + L::A + r * NX, arow);
+        st_row<T, NX, true>(e + L::C + r * NX, ct);
+        st_row<T, NX, true>(e + L::P + r * NX, Prow);
+        e[L::b + r] = bt;
+        e[L::p + r] = qr;
+        st_row<T, NX, true>(const_cast<T *>(qp.A) + st * NX * NX + r * NX, arow);
+        st_row<T, NX, true>(const_cast<T *>(qp.Bm) + st * NX * NX + r * NX, row.Brow);
+        st_row<T, NX, true>(const_cast<T *>(qp.R) + st * NX * NX + r * NX, row.Rrow);
+        const_cast<T *>(qp.c)[st * NX + r] = cr;
+        const_cast<T *>(qp.r)[st * NX + r] = rr;
+        if (bad) pre_info[b] = -1;
+        if (fail) atomicMin(ws.fail + b, i + 1);
     }
 }
 

@@ -15,9 +15,13 @@
 
 #include <climits>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace pdilqr {
+
+namespace cg = cooperative_groups;
 
 // ---------------------------------------------------------------------------------- layouts
 template <int NX>
@@ -379,33 +383,24 @@ struct ScanBwd {
     }
 };
 
-// CTA = IPB instances x W workers (all instances of a CTA run the same level schedule).
+// Work units of the backward scan (one worker each).  Operands are staged from global memory
+// (L2) into the worker's shared slice; results go back to global memory.  `kind` holds the slot
+// kinds of one instance (identity / suffix / general).
 template <typename T, int NX>
-__global__ void __launch_bounds__(256) k_scan_bwd(int B, int N, int chunk, int J, int Pv, int W, int IPB, LqWork<T> ws) {
+struct BwdUnits {
     using SB = ScanBwd<T, NX>;
     using L = VE<NX>;
-    constexpr int WS = SB::WS;
-    constexpr int TP = TE<NX>::SIZE;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    const int WI = W * WS, ib = threadIdx.x / WI, w = (threadIdx.x % WI) / WS, lane = worker_lane<WS>();
-    const unsigned mask = worker_mask<WS>();
-    CombineSmem<T, NX> &s = reinterpret_cast<CombineSmem<T, NX> *>(smraw)[threadIdx.x / WS];
-    int *kind = reinterpret_cast<int *>(smraw + IPB * W * sizeof(CombineSmem<T, NX>)) + ib * Pv;
-    const int b = blockIdx.x * IPB + ib, L2 = N + 2;
-    const bool active = b < B;
-    const int wv = active ? w : (INT_MAX / 2);  // inactive instances skip all work but reach every barrier
-    const int b_ = active ? b : 0;
-    const T *E = ws.elems + (size_t)b_ * L2 * L::SIZE;
-    T *Y = ws.vslots + (size_t)b_ * Pv * L::SIZE;
-    T *Pp = ws.Pp + (size_t)b_ * L2 * TP;
-    int fail = INT_MAX;
+    static constexpr int WS = SB::WS;
+    static constexpr int TP = TE<NX>::SIZE;
 
-    // ---------------- phase 1
-    for (int j = wv; j < J; j += W) {
+    // phase 1: chunk j = [j c, min((j+1) c, L)) reduced right-to-left (the last chunk holds the
+    // terminal element and is folded with the cheap rule, writing its final suffixes).
+    static __device__ void phase1(CombineSmem<T, NX> &s, unsigned mask, int lane, const T *E, T *Y, int *kind, T *Pp,
+                                  int j, int chunk, int J, int L2, int &fail) {
         const int lo = j * chunk, hi = min(lo + chunk, L2);
         wcopy<T, L::SIZE, WS>(s.e2, E + (size_t)(hi - 1) * L::SIZE, lane);
         __syncwarp(mask);
-        if (j == J - 1) {  // holds the terminal element: suffixes are final
+        if (j == J - 1) {
             if (lane < NX) {
                 T P[NX];
                 ld_row<T, NX, true>(P, s.e2 + L::P + lane * NX);
@@ -443,92 +438,189 @@ __global__ void __launch_bounds__(256) k_scan_bwd(int B, int N, int chunk, int J
         }
         __syncwarp(mask);
     }
+    // phase 2 up-sweep node k (level d) on the reversed slots: Y[k] = Y[k] (x) Y[k-d]
+    static __device__ void up(CombineSmem<T, NX> &s, unsigned mask, int lane, T *Y, int *kind, int k, int d, int &fail) {
+        const int kr = k - d;
+        const int kl_kind = kind[k], kr_kind = kind[kr];
+        __syncwarp(mask);
+        T *Yk = Y + (size_t)k * L::SIZE, *Yr = Y + (size_t)kr * L::SIZE;
+        if (kr_kind == SLOT_IDENT) {
+        } else if (kl_kind == SLOT_IDENT) {
+            wcopy<T, L::SIZE, WS>(Yk, Yr, lane);
+            if (lane == 0) kind[k] = kr_kind;
+        } else {
+            wcopy<T, L::SIZE, WS>(s.e1, Yk, lane);
+            wcopy<T, L::SIZE, WS>(s.e2, Yr, lane);
+            __syncwarp(mask);
+            if (kr_kind == SLOT_ANCHOR) {
+                T Po[NX], po;
+                if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, 1);
+                SB::store_suffix_rows(Yk, Po, po, lane);
+                if (lane == 0) kind[k] = SLOT_ANCHOR;
+            } else {
+                T Ao[NX], Co[NX], Po[NX], bo, po;
+                if (!combine_full<T, NX, WS>(s, mask, lane, Ao, Co, Po, bo, po)) fail = min(fail, 1);
+                SB::store_elem_rows(Yk, Ao, Co, Po, bo, po, lane);
+            }
+        }
+        __syncwarp(mask);
+    }
+    // phase 2 down-sweep node k (level d): t = Y[k-d]; Y[k-d] = Y[k]; Y[k] = t (x) Y[k]
+    static __device__ void down(CombineSmem<T, NX> &s, unsigned mask, int lane, T *Y, int *kind, int k, int d, int &fail) {
+        const int kl = k - d;
+        const int kE = kind[k], kt = kind[kl];
+        __syncwarp(mask);
+        T *Yk = Y + (size_t)k * L::SIZE, *Yl = Y + (size_t)kl * L::SIZE;
+        wcopy<T, L::SIZE, WS>(s.e1, Yl, lane);
+        wcopy<T, L::SIZE, WS>(s.e2, Yk, lane);
+        __syncwarp(mask);
+        wcopy<T, L::SIZE, WS>(Yl, s.e2, lane);
+        if (kE == SLOT_IDENT) {
+            wcopy<T, L::SIZE, WS>(Yk, s.e1, lane);
+            if (lane == 0) { kind[kl] = kE; kind[k] = kt; }
+        } else if (kt == SLOT_IDENT) {
+            if (lane == 0) { kind[kl] = kE; kind[k] = kE; }
+        } else {
+            T Po[NX], po;
+            if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, 1);
+            SB::store_suffix_rows(Yk, Po, po, lane);
+            if (lane == 0) { kind[kl] = kE; kind[k] = SLOT_ANCHOR; }
+        }
+        __syncwarp(mask);
+    }
+    // phase 3: chunk j < J-1 folded right-to-left from its exclusive suffix T_j = Y[J-1-j]
+    static __device__ void phase3(CombineSmem<T, NX> &s, unsigned mask, int lane, const T *E, const T *Y, T *Pp, int j,
+                                  int chunk, int J, int L2, int &fail) {
+        const int lo = j * chunk, hi = min(lo + chunk, L2);
+        wcopy<T, L::SIZE, WS>(s.e2, Y + (size_t)(J - 1 - j) * L::SIZE, lane);
+        __syncwarp(mask);
+        for (int i = hi - 1; i >= lo; --i) {
+            wcopy<T, L::SIZE, WS>(s.e1, E + (size_t)i * L::SIZE, lane);
+            __syncwarp(mask);
+            T Po[NX], po;
+            if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, i + 1);
+            if (lane < NX) {
+                st_row<T, NX, true>(s.e2 + L::P + lane * NX, Po);
+                s.e2[L::p + lane] = po;
+            }
+            SB::out_Pp(Pp + (size_t)i * TP, Po, po, lane);
+            __syncwarp(mask);
+        }
+    }
+};
+
+// CTA = IPB instances x W workers (all instances of a CTA run the same level schedule).
+template <typename T, int NX>
+__global__ void __launch_bounds__(256) k_scan_bwd(int B, int N, int chunk, int J, int Pv, int W, int IPB, LqWork<T> ws) {
+    using U = BwdUnits<T, NX>;
+    using L = VE<NX>;
+    constexpr int WS = U::WS;
+    constexpr int TP = TE<NX>::SIZE;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int WI = W * WS, ib = threadIdx.x / WI, w = (threadIdx.x % WI) / WS, lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    CombineSmem<T, NX> &s = reinterpret_cast<CombineSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    int *kind = reinterpret_cast<int *>(smraw + IPB * W * sizeof(CombineSmem<T, NX>)) + ib * Pv;
+    const int b = blockIdx.x * IPB + ib, L2 = N + 2;
+    const bool active = b < B;
+    const int wv = active ? w : (INT_MAX / 2);  // inactive instances skip all work but reach every barrier
+    const int b_ = active ? b : 0;
+    const T *E = ws.elems + (size_t)b_ * L2 * L::SIZE;
+    T *Y = ws.vslots + (size_t)b_ * Pv * L::SIZE;
+    T *Pp = ws.Pp + (size_t)b_ * L2 * TP;
+    int fail = INT_MAX;
+    for (int j = wv; j < J; j += W) U::phase1(s, mask, lane, E, Y, kind, Pp, j, chunk, J, L2, fail);
     for (int t = J + (threadIdx.x % WI); t < Pv; t += WI) kind[t] = SLOT_IDENT;
     __syncthreads();
-
     if (J > 1) {
-        // ---------------- phase 2: Blelloch exclusive scan over reversed slots with
-        // y_a (.) y_b := y_b (x) y_a   (slot t holds S_{J-1-t}; slot 0 holds the terminal chunk)
         for (int d = 1; d < Pv; d <<= 1) {
             const int np = Pv / (2 * d);
-            for (int q = wv; q < np; q += W) {
-                const int k = 2 * d * (q + 1) - 1, kr = k - d;
-                const int kl_kind = kind[k], kr_kind = kind[kr];
-                __syncwarp(mask);
-                T *Yk = Y + (size_t)k * L::SIZE, *Yr = Y + (size_t)kr * L::SIZE;
-                if (kr_kind == SLOT_IDENT) {
-                    // unchanged
-                } else if (kl_kind == SLOT_IDENT) {
-                    wcopy<T, L::SIZE, WS>(Yk, Yr, lane);
-                    if (lane == 0) kind[k] = kr_kind;
-                } else {
-                    wcopy<T, L::SIZE, WS>(s.e1, Yk, lane);
-                    wcopy<T, L::SIZE, WS>(s.e2, Yr, lane);
-                    __syncwarp(mask);
-                    if (kr_kind == SLOT_ANCHOR) {
-                        T Po[NX], po;
-                        if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, 1);
-                        SB::store_suffix_rows(Yk, Po, po, lane);
-                        if (lane == 0) kind[k] = SLOT_ANCHOR;
-                    } else {
-                        T Ao[NX], Co[NX], Po[NX], bo, po;
-                        if (!combine_full<T, NX, WS>(s, mask, lane, Ao, Co, Po, bo, po)) fail = min(fail, 1);
-                        SB::store_elem_rows(Yk, Ao, Co, Po, bo, po, lane);
-                    }
-                }
-                __syncwarp(mask);
-            }
+            for (int q = wv; q < np; q += W) U::up(s, mask, lane, Y, kind, 2 * d * (q + 1) - 1, d, fail);
             __syncthreads();
         }
         if (threadIdx.x % WI == 0) kind[Pv - 1] = SLOT_IDENT;
         __syncthreads();
         for (int d = Pv / 2; d >= 1; d >>= 1) {
             const int np = Pv / (2 * d);
-            for (int q = wv; q < np; q += W) {
-                const int k = 2 * d * (q + 1) - 1, kl = k - d;
-                const int kE = kind[k], kt = kind[kl];
-                __syncwarp(mask);
-                T *Yk = Y + (size_t)k * L::SIZE, *Yl = Y + (size_t)kl * L::SIZE;
-                // t = Y[kl]; Y[kl] = Y[k]; Y[k] = t (x) Y[k]
-                wcopy<T, L::SIZE, WS>(s.e1, Yl, lane);
-                wcopy<T, L::SIZE, WS>(s.e2, Yk, lane);
-                __syncwarp(mask);
-                wcopy<T, L::SIZE, WS>(Yl, s.e2, lane);
-                if (kE == SLOT_IDENT) {
-                    wcopy<T, L::SIZE, WS>(Yk, s.e1, lane);
-                    if (lane == 0) { kind[kl] = kE; kind[k] = kt; }
-                } else if (kt == SLOT_IDENT) {
-                    if (lane == 0) { kind[kl] = kE; kind[k] = kE; }
-                } else {
-                    T Po[NX], po;
-                    if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, 1);
-                    SB::store_suffix_rows(Yk, Po, po, lane);
-                    if (lane == 0) { kind[kl] = kE; kind[k] = SLOT_ANCHOR; }
-                }
-                __syncwarp(mask);
-            }
+            for (int q = wv; q < np; q += W) U::down(s, mask, lane, Y, kind, 2 * d * (q + 1) - 1, d, fail);
             __syncthreads();
         }
-        // ---------------- phase 3
-        for (int j = wv; j < J - 1; j += W) {
-            const int lo = j * chunk, hi = min(lo + chunk, L2);
-            wcopy<T, L::SIZE, WS>(s.e2, Y + (size_t)(J - 1 - j) * L::SIZE, lane);
-            __syncwarp(mask);
-            for (int i = hi - 1; i >= lo; --i) {
-                wcopy<T, L::SIZE, WS>(s.e1, E + (size_t)i * L::SIZE, lane);
-                __syncwarp(mask);
-                T Po[NX], po;
-                if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = min(fail, i + 1);
-                if (lane < NX) {
-                    st_row<T, NX, true>(s.e2 + L::P + lane * NX, Po);
-                    s.e2[L::p + lane] = po;
-                }
-                SB::out_Pp(Pp + (size_t)i * TP, Po, po, lane);
-                __syncwarp(mask);
-            }
-        }
+        for (int j = wv; j < J - 1; j += W) U::phase3(s, mask, lane, E, Y, Pp, j, chunk, J, L2, fail);
     }
     if (active && fail != INT_MAX && lane == 0) atomicMin(ws.fail + b, (1 << 24) | fail);
+}
+
+// Grid-wide variant for the latency regime (few instances): the units of every level are spread
+// over all CTAs of a cooperative launch and the levels are separated by grid-wide barriers, so the
+// span is 2 ceil(log2 J) combine latencies regardless of N (Eq. 8).  Slot kinds live in
+// global memory (`kinds`: [B][Pv]).
+template <typename T, int NX>
+__global__ void __launch_bounds__(128) k_scan_bwd_grid(int B, int N, int chunk, int J, int Pv, LqWork<T> ws, int *kinds) {
+    using U = BwdUnits<T, NX>;
+    using L = VE<NX>;
+    constexpr int WS = U::WS;
+    constexpr int TP = TE<NX>::SIZE;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    cg::grid_group grid = cg::this_grid();
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    CombineSmem<T, NX> &s = reinterpret_cast<CombineSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    const int wpb = blockDim.x / WS;
+    const long gw = (long)blockIdx.x * wpb + threadIdx.x / WS, GW = (long)gridDim.x * wpb;
+    const int L2 = N + 2;
+    auto inst = [&](int b, const T *&E, T *&Y, T *&Pp, int *&kind) {
+        E = ws.elems + (size_t)b * L2 * L::SIZE;
+        Y = ws.vslots + (size_t)b * Pv * L::SIZE;
+        Pp = ws.Pp + (size_t)b * L2 * TP;
+        kind = kinds + (size_t)b * Pv;
+    };
+    auto report = [&](int b, int fail) {
+        if (fail != INT_MAX && lane == 0) atomicMin(ws.fail + b, (1 << 24) | fail);
+    };
+    const T *E; T *Y; T *Pp; int *kind;
+    for (long u = gw; u < (long)B * J; u += GW) {
+        const int b = (int)(u / J), j = (int)(u % J);
+        inst(b, E, Y, Pp, kind);
+        int fail = INT_MAX;
+        U::phase1(s, mask, lane, E, Y, kind, Pp, j, chunk, J, L2, fail);
+        report(b, fail);
+    }
+    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < (long)B * Pv; t += (long)gridDim.x * blockDim.x)
+        if ((int)(t % Pv) >= J) kinds[t] = SLOT_IDENT;
+    if (J == 1) return;
+    grid.sync();
+    for (int d = 1; d < Pv; d <<= 1) {
+        const int np = Pv / (2 * d);
+        for (long u = gw; u < (long)B * np; u += GW) {
+            const int b = (int)(u / np), q = (int)(u % np);
+            inst(b, E, Y, Pp, kind);
+            int fail = INT_MAX;
+            U::up(s, mask, lane, Y, kind, 2 * d * (q + 1) - 1, d, fail);
+            report(b, fail);
+        }
+        grid.sync();
+    }
+    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < B; t += (long)gridDim.x * blockDim.x)
+        kinds[t * Pv + Pv - 1] = SLOT_IDENT;
+    grid.sync();
+    for (int d = Pv / 2; d >= 1; d >>= 1) {
+        const int np = Pv / (2 * d);
+        for (long u = gw; u < (long)B * np; u += GW) {
+            const int b = (int)(u / np), q = (int)(u % np);
+            inst(b, E, Y, Pp, kind);
+            int fail = INT_MAX;
+            U::down(s, mask, lane, Y, kind, 2 * d * (q + 1) - 1, d, fail);
+            report(b, fail);
+        }
+        grid.sync();
+    }
+    for (long u = gw; u < (long)B * (J - 1); u += GW) {
+        const int b = (int)(u / (J - 1)), j = (int)(u % (J - 1));
+        inst(b, E, Y, Pp, kind);
+        int fail = INT_MAX;
+        U::phase3(s, mask, lane, E, Y, Pp, j, chunk, J, L2, fail);
+        report(b, fail);
+    }
 }
 
 // ---------------------------------------------------------------------- policy (Eq. 5 rows)
@@ -640,52 +732,39 @@ struct FwdSmem {
 };
 
 template <typename T, int NX>
-__global__ void __launch_bounds__(256) k_scan_fwd(const T *dx0, int B, int N, int n, int chunk, int J, int Pf, int W,
-                                                   int IPB, LqWork<T> ws, T *dx_out) {
-    constexpr int WS = worker_width(NX);
+struct FwdUnits {
     using TL = TE<NX>;
-    extern __shared__ __align__(16) unsigned char smraw[];
-    const int WI = W * WS, ib = threadIdx.x / WI, w = (threadIdx.x % WI) / WS, lane = worker_lane<WS>();
-    const unsigned mask = worker_mask<WS>();
-    FwdSmem<T, NX> &s = reinterpret_cast<FwdSmem<T, NX> *>(smraw)[threadIdx.x / WS];
-    int *kind = reinterpret_cast<int *>(smraw + IPB * W * sizeof(FwdSmem<T, NX>)) + ib * Pf;
-    const int b = blockIdx.x * IPB + ib, Lf = N + 1;
-    const bool active = b < B;
-    const int b_ = active ? b : 0;
-    const T *E = ws.tel + (size_t)b_ * Lf * TL::SIZE;
-    T *Y = ws.tslots + (size_t)b_ * Pf * TL::SIZE;
-    T *X = ws.dxw + (size_t)b_ * (N + 2) * NX;
-    T *Xo = dx_out + (size_t)b_ * (N + 2) * n;
-    const int wv = active ? w : (INT_MAX / 2);  // inactive instances skip all work but reach every barrier
-    const int r = lane < NX ? lane : 0;
-    const bool EXn = (n == NX);
-    auto put_dx = [&](int node, T v) {
-        if (lane < NX) {
-            X[node * NX + r] = v;
-            if (EXn || r < n) Xo[(size_t)node * n + r] = v;
-        }
-    };
-    // vector fold x <- Abar_i x + bbar_i over [lo, hi), x in s.t2[TL::b..]
-    auto fold = [&](int lo, int hi) {
+    static constexpr int WS = worker_width(NX);
+    // dx_{i+1} = Abar_i dx_i + bbar_i for i in [lo, hi), x in s.t2[TL::b..]; writes dx (padded
+    // workspace X and the user's Xo with n columns)
+    static __device__ void fold(FwdSmem<T, NX> &s, unsigned mask, int lane, const T *E, T *X, T *Xo, int n, int lo, int hi) {
+        const int r = lane < NX ? lane : 0;
         for (int i = lo; i < hi; ++i) {
             T arow[NX];
             ld_row<T, NX, true>(arow, E + (size_t)i * TL::SIZE + r * NX);
             const T v = row_dot<T, NX>(arow, s.t2 + TL::b, E[(size_t)i * TL::SIZE + TL::b + r]);
             __syncwarp(mask);
-            if (lane < NX) s.t2[TL::b + r] = v;
-            put_dx(i + 1, v);
+            if (lane < NX) {
+                s.t2[TL::b + r] = v;
+                X[(i + 1) * NX + r] = v;
+                if (n == NX || r < n) Xo[(size_t)(i + 1) * n + r] = v;
+            }
             __syncwarp(mask);
         }
-    };
-    // ---------------- phase 1
-    for (int j = wv; j < J; j += W) {
+    }
+    static __device__ void phase1(FwdSmem<T, NX> &s, unsigned mask, int lane, const T *E, T *Y, int *kind, T *X, T *Xo,
+                                  const T *dx0b, int n, int j, int chunk, int J, int Lf) {
+        const int r = lane < NX ? lane : 0;
         const int lo = j * chunk, hi = min(lo + chunk, Lf);
         if (j == 0) {
-            const T x0 = (EXn || r < n) ? dx0[(size_t)b_ * n + r] : T(0);
-            if (lane < NX) s.t2[TL::b + r] = x0;
-            put_dx(0, x0);
+            const T x0 = (n == NX || r < n) ? dx0b[r] : T(0);
+            if (lane < NX) {
+                s.t2[TL::b + r] = x0;
+                X[r] = x0;
+                if (n == NX || r < n) Xo[r] = x0;
+            }
             __syncwarp(mask);
-            fold(lo, hi);
+            fold(s, mask, lane, E, X, Xo, n, lo, hi);
             if (J > 1 && lane < NX) Y[TL::b + r] = s.t2[TL::b + r];
             if (lane == 0 && J > 1) kind[0] = SLOT_ANCHOR;
         } else {
@@ -706,79 +785,161 @@ __global__ void __launch_bounds__(256) k_scan_fwd(const T *dx0, int B, int N, in
         }
         __syncwarp(mask);
     }
+    // up-sweep node k: Y[k] = Y[k-d] (+) Y[k]  (apply Y[k-d] first)
+    static __device__ void up(FwdSmem<T, NX> &s, unsigned mask, int lane, T *Y, int *kind, int k, int d) {
+        const int r = lane < NX ? lane : 0;
+        const int kl = k - d;
+        const int kk = kind[k], kp = kind[kl];
+        __syncwarp(mask);
+        T *Yk = Y + (size_t)k * TL::SIZE, *Yl = Y + (size_t)kl * TL::SIZE;
+        if (kp == SLOT_IDENT) {
+        } else if (kk == SLOT_IDENT) {
+            wcopy<T, TL::SIZE, WS>(Yk, Yl, lane);
+            if (lane == 0) kind[k] = kp;
+        } else {
+            wcopy<T, TL::SIZE, WS>(s.t1, Yl, lane);
+            wcopy<T, TL::SIZE, WS>(s.t2, Yk, lane);
+            __syncwarp(mask);
+            T arow[NX];
+            ld_row<T, NX, true>(arow, s.t2 + TL::A + r * NX);
+            const T bo = row_dot<T, NX>(arow, s.t1 + TL::b, s.t2[TL::b + r]);
+            if (kp == SLOT_ANCHOR) {
+                if (lane < NX) Yk[TL::b + r] = bo;
+                if (lane == 0) kind[k] = SLOT_ANCHOR;
+            } else {
+                T ao[NX];
+                zero(ao);
+                row_mat<T, NX, NX, NX>(ao, arow, s.t1 + TL::A);
+                if (lane < NX) { st_row<T, NX, true>(Yk + TL::A + r * NX, ao); Yk[TL::b + r] = bo; }
+            }
+        }
+        __syncwarp(mask);
+    }
+    // down-sweep node k: t = Y[k-d]; Y[k-d] = Y[k]; Y[k] = Y[k] (+) t  (prefix first, then t)
+    static __device__ void down(FwdSmem<T, NX> &s, unsigned mask, int lane, T *Y, int *kind, int k, int d) {
+        const int r = lane < NX ? lane : 0;
+        const int kl = k - d;
+        const int kE = kind[k], kt = kind[kl];
+        __syncwarp(mask);
+        T *Yk = Y + (size_t)k * TL::SIZE, *Yl = Y + (size_t)kl * TL::SIZE;
+        wcopy<T, TL::SIZE, WS>(s.t1, Yl, lane);
+        wcopy<T, TL::SIZE, WS>(s.t2, Yk, lane);
+        __syncwarp(mask);
+        wcopy<T, TL::SIZE, WS>(Yl, s.t2, lane);
+        if (kE == SLOT_IDENT) {
+            wcopy<T, TL::SIZE, WS>(Yk, s.t1, lane);
+            if (lane == 0) { kind[kl] = kE; kind[k] = kt; }
+        } else if (kt == SLOT_IDENT) {
+            if (lane == 0) { kind[kl] = kE; kind[k] = kE; }
+        } else {
+            T arow[NX];
+            ld_row<T, NX, true>(arow, s.t1 + TL::A + r * NX);
+            const T bo = row_dot<T, NX>(arow, s.t2 + TL::b, s.t1[TL::b + r]);
+            if (lane < NX) Yk[TL::b + r] = bo;
+            if (lane == 0) { kind[kl] = kE; kind[k] = SLOT_ANCHOR; }
+        }
+        __syncwarp(mask);
+    }
+};
+
+template <typename T, int NX>
+__global__ void __launch_bounds__(256) k_scan_fwd(const T *dx0, int B, int N, int n, int chunk, int J, int Pf, int W,
+                                                  int IPB, LqWork<T> ws, T *dx_out) {
+    using U = FwdUnits<T, NX>;
+    using TL = TE<NX>;
+    constexpr int WS = U::WS;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int WI = W * WS, ib = threadIdx.x / WI, w = (threadIdx.x % WI) / WS, lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    FwdSmem<T, NX> &s = reinterpret_cast<FwdSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    int *kind = reinterpret_cast<int *>(smraw + IPB * W * sizeof(FwdSmem<T, NX>)) + ib * Pf;
+    const int b = blockIdx.x * IPB + ib, Lf = N + 1;
+    const bool active = b < B;
+    const int b_ = active ? b : 0;
+    const T *E = ws.tel + (size_t)b_ * Lf * TL::SIZE;
+    T *Y = ws.tslots + (size_t)b_ * Pf * TL::SIZE;
+    T *X = ws.dxw + (size_t)b_ * (N + 2) * NX;
+    T *Xo = dx_out + (size_t)b_ * (N + 2) * n;
+    const int wv = active ? w : (INT_MAX / 2);  // inactive instances skip all work but reach every barrier
+    for (int j = wv; j < J; j += W) U::phase1(s, mask, lane, E, Y, kind, X, Xo, dx0 + (size_t)b_ * n, n, j, chunk, J, Lf);
     for (int t = J + (threadIdx.x % WI); t < Pf; t += WI) kind[t] = SLOT_IDENT;
     __syncthreads();
     if (J > 1) {
-        // up-sweep: Y[k] = Y[k-d] (+) Y[k]  (apply Y[k-d] first)
         for (int d = 1; d < Pf; d <<= 1) {
             const int np = Pf / (2 * d);
-            for (int q = wv; q < np; q += W) {
-                const int k = 2 * d * (q + 1) - 1, kl = k - d;
-                const int kk = kind[k], kp = kind[kl];
-                __syncwarp(mask);
-                T *Yk = Y + (size_t)k * TL::SIZE, *Yl = Y + (size_t)kl * TL::SIZE;
-                if (kp == SLOT_IDENT) {
-                } else if (kk == SLOT_IDENT) {
-                    wcopy<T, TL::SIZE, WS>(Yk, Yl, lane);
-                    if (lane == 0) kind[k] = kp;
-                } else {
-                    wcopy<T, TL::SIZE, WS>(s.t1, Yl, lane);
-                    wcopy<T, TL::SIZE, WS>(s.t2, Yk, lane);
-                    __syncwarp(mask);
-                    T arow[NX];
-                    ld_row<T, NX, true>(arow, s.t2 + TL::A + r * NX);
-                    const T bo = row_dot<T, NX>(arow, s.t1 + TL::b, s.t2[TL::b + r]);
-                    if (kp == SLOT_ANCHOR) {
-                        if (lane < NX) Yk[TL::b + r] = bo;
-                        if (lane == 0) kind[k] = SLOT_ANCHOR;
-                    } else {
-                        T ao[NX];
-                        zero(ao);
-                        row_mat<T, NX, NX, NX>(ao, arow, s.t1 + TL::A);
-                        if (lane < NX) { st_row<T, NX, true>(Yk + TL::A + r * NX, ao); Yk[TL::b + r] = bo; }
-                    }
-                }
-                __syncwarp(mask);
-            }
+            for (int q = wv; q < np; q += W) U::up(s, mask, lane, Y, kind, 2 * d * (q + 1) - 1, d);
             __syncthreads();
         }
         if (threadIdx.x % WI == 0) kind[Pf - 1] = SLOT_IDENT;
         __syncthreads();
-        // down-sweep: t = Y[kl]; Y[kl] = Y[k]; Y[k] = Y[k] (+) t  (prefix first, then t)
         for (int d = Pf / 2; d >= 1; d >>= 1) {
             const int np = Pf / (2 * d);
-            for (int q = wv; q < np; q += W) {
-                const int k = 2 * d * (q + 1) - 1, kl = k - d;
-                const int kE = kind[k], kt = kind[kl];
-                __syncwarp(mask);
-                T *Yk = Y + (size_t)k * TL::SIZE, *Yl = Y + (size_t)kl * TL::SIZE;
-                wcopy<T, TL::SIZE, WS>(s.t1, Yl, lane);
-                wcopy<T, TL::SIZE, WS>(s.t2, Yk, lane);
-                __syncwarp(mask);
-                wcopy<T, TL::SIZE, WS>(Yl, s.t2, lane);
-                if (kE == SLOT_IDENT) {
-                    wcopy<T, TL::SIZE, WS>(Yk, s.t1, lane);
-                    if (lane == 0) { kind[kl] = kE; kind[k] = kt; }
-                } else if (kt == SLOT_IDENT) {
-                    if (lane == 0) { kind[kl] = kE; kind[k] = kE; }
-                } else {  // prefix (anchored vector) then t
-                    T arow[NX];
-                    ld_row<T, NX, true>(arow, s.t1 + TL::A + r * NX);
-                    const T bo = row_dot<T, NX>(arow, s.t2 + TL::b, s.t1[TL::b + r]);
-                    if (lane < NX) Yk[TL::b + r] = bo;
-                    if (lane == 0) { kind[kl] = kE; kind[k] = SLOT_ANCHOR; }
-                }
-                __syncwarp(mask);
-            }
+            for (int q = wv; q < np; q += W) U::down(s, mask, lane, Y, kind, 2 * d * (q + 1) - 1, d);
             __syncthreads();
         }
-        // phase 3
-        for (int j = wv > 0 ? wv : W; j < J; j += W) {
+        for (int j = wv > 0 ? wv : W; j < J; j += W) {   // phase 3: chunks j >= 1 from their prefix
             const int lo = j * chunk, hi = min(lo + chunk, Lf);
+            const int r = lane < NX ? lane : 0;
             if (lane < NX) s.t2[TL::b + r] = Y[(size_t)j * TL::SIZE + TL::b + r];
             __syncwarp(mask);
-            fold(lo, hi);
+            U::fold(s, mask, lane, E, X, Xo, n, lo, hi);
         }
+    }
+}
+
+// Grid-wide forward scan (cooperative launch), companion of k_scan_bwd_grid.
+template <typename T, int NX>
+__global__ void __launch_bounds__(128) k_scan_fwd_grid(const T *dx0, int B, int N, int n, int chunk, int J, int Pf,
+                                                       LqWork<T> ws, T *dx_out, int *kinds) {
+    using U = FwdUnits<T, NX>;
+    using TL = TE<NX>;
+    constexpr int WS = U::WS;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    cg::grid_group grid = cg::this_grid();
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    FwdSmem<T, NX> &s = reinterpret_cast<FwdSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    const int wpb = blockDim.x / WS;
+    const long gw = (long)blockIdx.x * wpb + threadIdx.x / WS, GW = (long)gridDim.x * wpb;
+    const int Lf = N + 1;
+    auto E_ = [&](int b) { return ws.tel + (size_t)b * Lf * TL::SIZE; };
+    auto Y_ = [&](int b) { return ws.tslots + (size_t)b * Pf * TL::SIZE; };
+    auto X_ = [&](int b) { return ws.dxw + (size_t)b * (N + 2) * NX; };
+    auto Xo_ = [&](int b) { return dx_out + (size_t)b * (N + 2) * n; };
+    for (long u = gw; u < (long)B * J; u += GW) {
+        const int b = (int)(u / J), j = (int)(u % J);
+        U::phase1(s, mask, lane, E_(b), Y_(b), kinds + (size_t)b * Pf, X_(b), Xo_(b), dx0 + (size_t)b * n, n, j, chunk, J, Lf);
+    }
+    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < (long)B * Pf; t += (long)gridDim.x * blockDim.x)
+        if ((int)(t % Pf) >= J) kinds[t] = SLOT_IDENT;
+    if (J == 1) return;
+    grid.sync();
+    for (int d = 1; d < Pf; d <<= 1) {
+        const int np = Pf / (2 * d);
+        for (long u = gw; u < (long)B * np; u += GW) {
+            const int b = (int)(u / np), q = (int)(u % np);
+            U::up(s, mask, lane, Y_(b), kinds + (size_t)b * Pf, 2 * d * (q + 1) - 1, d);
+        }
+        grid.sync();
+    }
+    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < B; t += (long)gridDim.x * blockDim.x)
+        kinds[t * Pf + Pf - 1] = SLOT_IDENT;
+    grid.sync();
+    for (int d = Pf / 2; d >= 1; d >>= 1) {
+        const int np = Pf / (2 * d);
+        for (long u = gw; u < (long)B * np; u += GW) {
+            const int b = (int)(u / np), q = (int)(u % np);
+            U::down(s, mask, lane, Y_(b), kinds + (size_t)b * Pf, 2 * d * (q + 1) - 1, d);
+        }
+        grid.sync();
+    }
+    for (long u = gw; u < (long)B * (J - 1); u += GW) {
+        const int b = (int)(u / (J - 1)), j = 1 + (int)(u % (J - 1));
+        const int lo = j * chunk, hi = min(lo + chunk, Lf);
+        const int r = lane < NX ? lane : 0;
+        if (lane < NX) s.t2[TL::b + r] = Y_(b)[(size_t)j * TL::SIZE + TL::b + r];
+        __syncwarp(mask);
+        U::fold(s, mask, lane, E_(b), X_(b), Xo_(b), n, lo, hi);
     }
 }
 

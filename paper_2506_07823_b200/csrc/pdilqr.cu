@@ -59,6 +59,7 @@ bool pick_variant(int n, int m, Variant &v, int &NX, int &NU) {
 
 struct Layout {
     size_t elems, vslots, Pp, Kk, tel, tslots, dxw, fail, nonfin, pre, info_tmp, stats;
+    size_t kinds_b, kinds_f, ls_part, ls_cnt;  // grid-scan slot kinds, multi-block line-search scratch
     size_t qp[11];  // SRBD internal QP buffers (A, Bm, c, Q, R, S, q, r, Pt, pt, dx0)
     size_t dir[3];  // internal direction (dx, du, dlam)
     size_t total;
@@ -84,6 +85,8 @@ struct pdilqr_ctx {
     int launches;
     int occ_fold = 4, occ_ls = 4;  // minimum resident CTAs per SM requested from ptxas (register cap: 128)
     int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
+    bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
+    int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
     // per-kernel CUDA-event timing (host bookkeeping only; off unless pdilqr_profile(h, 1))
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -174,6 +177,10 @@ Layout make_layout(const pdilqr_config *c, int NX, int NU, int esz, int chunk, i
     L.pre = take(B * 4);
     L.info_tmp = take(B * 4);
     L.stats = take(B * (3 * (size_t)esz + 8));
+    L.kinds_b = take(B * (size_t)Pv * 4);
+    L.kinds_f = take(B * (size_t)Pf * 4);
+    L.ls_part = take(B * (size_t)((N + 2 + 31) / 32) * 34 * 8);
+    L.ls_cnt = take(B * 4);
     const size_t n = c->n, m = c->m;
     if (c->model == PDILQR_MODEL_SRBD) {
         const size_t sz[11] = {(N + 1) * n * n, (N + 1) * n * m, (N + 1) * n, (N + 1) * n * n, (N + 1) * m * m,
@@ -231,15 +238,15 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 // --------------------------------------------------------------------------- LQ pipeline
 template <typename T, int NX, int NU, bool EX>
 pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, const int32_t *pre,
-                     cudaStream_t st) {
+                     cudaStream_t st, bool skip_init) {
     constexpr int WS = worker_width(NX > NU ? NX : NU);
     constexpr int WSX = worker_width(NX);
     const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
     LqWork<T> ws = work<T>(h);
-    cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
+    if (!skip_init) cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
     cudaMemsetAsync(ws.nonfin, 0, (size_t)B * 4, st);
     int launches = 0;
-    {  // element init
+    if (!skip_init) {  // element init
         const int wpb = 128 / WS;
         const long nw = (long)B * (N + 2);
         const size_t smem = (size_t)wpb * (2 * NU * NX + round_up4(NU)) * sizeof(T);
@@ -254,6 +261,18 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         Prof pf(h, "k_fold", st);
         const int ipb = 128 / WSX;
         k_fold<T, NX, 4><<<(B + ipb - 1) / ipb, 128, smem, st>>>(B, N, ws);
+        ++launches;
+    } else if (h->grid_scan) {  // cooperative grid-wide tree (latency regime)
+        int J = h->Jb, Pv = h->Pv, chunk = h->chunk, Bv = B, Nv = N;
+        int *kinds = reinterpret_cast<int *>(h->ws + h->lay.kinds_b);
+        const int wpb = 128 / WSX;
+        const size_t smem = wpb * sizeof(CombineSmem<T, NX>);
+        set_smem(k_scan_bwd_grid<T, NX>, smem);
+        const long units = (long)B * std::max(J, Pv / 2);
+        const int grid = (int)std::max(1L, std::min((long)h->coop_bwd, (units + wpb - 1) / wpb));
+        void *args[] = {&Bv, &Nv, &chunk, &J, &Pv, &ws, &kinds};
+        Prof pf(h, "k_scan_bwd_grid", st);
+        cudaLaunchCooperativeKernel((const void *)k_scan_bwd_grid<T, NX>, grid, 128, args, smem, st);
         ++launches;
     } else {  // backward scan
         const int J = h->Jb, Pv = h->Pv;
@@ -280,7 +299,21 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         k_policy<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws, out);
         ++launches;
     }
-    {  // forward scan
+    if (h->grid_scan && h->Jf > 1) {  // cooperative grid-wide forward tree
+        int J = h->Jf, Pf = h->Pf, chunk = h->chunk, Bv = B, Nv = N, nv = n;
+        int *kinds = reinterpret_cast<int *>(h->ws + h->lay.kinds_f);
+        const int wpb = 128 / WSX;
+        const size_t smem = wpb * sizeof(FwdSmem<T, NX>);
+        set_smem(k_scan_fwd_grid<T, NX>, smem);
+        const long units = (long)B * std::max(J, Pf / 2);
+        const int grid = (int)std::max(1L, std::min((long)h->coop_fwd, (units + wpb - 1) / wpb));
+        const T *dx0 = qp.dx0;
+        T *dxo = out.dx;
+        void *args[] = {&dx0, &Bv, &Nv, &nv, &chunk, &J, &Pf, &ws, &dxo, &kinds};
+        Prof pf(h, "k_scan_fwd_grid", st);
+        cudaLaunchCooperativeKernel((const void *)k_scan_fwd_grid<T, NX>, grid, 128, args, smem, st);
+        ++launches;
+    } else {  // forward scan
         const int J = h->Jf, Pf = h->Pf;
         const size_t cs = sizeof(FwdSmem<T, NX>);
         int W = 1, IPB = 8;
@@ -314,12 +347,12 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
 
 template <typename T>
 pdilqr_status dispatch_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, const int32_t *pre,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool skip_init = false) {
     switch (h->var) {
-        case V12: return run_lq<T, 12, 12, true>(h, qp, out, info, pre, st);
-        case V4: return run_lq<T, 4, 4, false>(h, qp, out, info, pre, st);
-        case V8: return run_lq<T, 8, 8, false>(h, qp, out, info, pre, st);
-        default: return run_lq<T, 16, 16, false>(h, qp, out, info, pre, st);
+        case V12: return run_lq<T, 12, 12, true>(h, qp, out, info, pre, st, skip_init);
+        case V4: return run_lq<T, 4, 4, false>(h, qp, out, info, pre, st, skip_init);
+        case V8: return run_lq<T, 8, 8, false>(h, qp, out, info, pre, st, skip_init);
+        default: return run_lq<T, 16, 16, false>(h, qp, out, info, pre, st, skip_init);
     }
 }
 
@@ -464,8 +497,26 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
     LqArgs<T> qp = internal_qp<T>(h);
     int32_t *pre = reinterpret_cast<int32_t *>(h->ws + h->lay.pre);
     int32_t *info_tmp = reinterpret_cast<int32_t *>(h->ws + h->lay.info_tmp);
-    pdilqr_status s = run_linearize<T>(h, it, qp, pre, st);
-    if (s != PDILQR_OK) return s;
+    pdilqr_status s = PDILQR_OK;
+    if (h->cfg.n == 12 && h->cfg.m == 12) {
+        // SRBD: linearisation fused with element init (stage-parallel); the LQ pipeline below
+        // then starts at the scan (S = 0 is passed as NULL)
+        LqWork<T> ws = work<T>(h);
+        cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
+        cudaMemsetAsync(pre, 0, (size_t)B * 4, st);
+        const long nw = (long)B * (N + 2);
+        const size_t smem = 8 * sizeof(LinElemSmem<T>);
+        set_smem(k_srbd_lin_elem<T>, smem);
+        {
+            Prof pf(h, "k_srbd_lin_elem", st);
+            k_srbd_lin_elem<T><<<(unsigned)((nw + 7) / 8), 128, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, qp, pre);
+        }
+        h->launches += 1;
+        qp.S = nullptr;
+    } else {
+        s = run_linearize<T>(h, it, qp, pre, st);
+        if (s != PDILQR_OK) return s;
+    }
     LqOut<T> out;
     if (dir && dir->dx) {
         out = LqOut<T>{(T *)dir->dx, (T *)dir->du, (T *)dir->dlam, (T *)dir->K, (T *)dir->k};
@@ -473,12 +524,21 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
         out = LqOut<T>{reinterpret_cast<T *>(h->ws + h->lay.dir[0]), reinterpret_cast<T *>(h->ws + h->lay.dir[1]),
                        reinterpret_cast<T *>(h->ws + h->lay.dir[2]), nullptr, nullptr};
     }
-    s = dispatch_lq<T>(h, qp, out, info_tmp, pre, st);
+    s = (h->cfg.n == 12 && h->cfg.m == 12) ? dispatch_lq<T>(h, qp, out, info_tmp, pre, st, /*skip_init=*/true)
+                                           : dispatch_lq<T>(h, qp, out, info_tmp, pre, st);
     if (s != PDILQR_OK) return s;
     LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
-    {
-    Prof pf(h, "k_srbd_linesearch", st);
-    k_srbd_linesearch<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, out.dx, out.du, out.dlam, info_tmp, so);
+    if (h->grid_scan) {
+        const int S = (N + 2 + 31) / 32;
+        double *part = reinterpret_cast<double *>(h->ws + h->lay.ls_part);
+        int *cnt = reinterpret_cast<int *>(h->ws + h->lay.ls_cnt);
+        cudaMemsetAsync(cnt, 0, (size_t)B * 4, st);
+        Prof pf(h, "k_srbd_ls_multi", st);
+        k_srbd_ls_multi<T><<<dim3(S, B), 32, 0, st>>>(h->K, iter_of<T>(it), B, N, out.dx, out.du, out.dlam, info_tmp, so,
+                                                      part, cnt);
+    } else {
+        Prof pf(h, "k_srbd_linesearch", st);
+        k_srbd_linesearch<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, out.dx, out.du, out.dlam, info_tmp, so);
     }
     h->launches += 1;
     return cuda_check("step launch");
@@ -563,6 +623,33 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_OCC_FOLD")) h->occ_fold = std::atoi(e);  // tuning knobs
     if (const char *e = std::getenv("PDILQR_OCC_LS")) h->occ_ls = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FUSED")) h->fused = std::atoi(e);
+    // latency regime: few instances -> spread every tree level over all SMs (cooperative launch)
+    h->grid_scan = cfg->batch < 148 && (Jb > 1 || Jf > 1);
+    if (const char *e = std::getenv("PDILQR_GRID_SCAN")) h->grid_scan = std::atoi(e) != 0 && (Jb > 1 || Jf > 1);
+    if (h->grid_scan) {
+        DeviceGuard g(device);
+        int sms = 148, nb = 0, nf = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        auto occ = [&](auto kern, size_t smem, int &out) {
+            if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            int per = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
+            out = std::max(1, per) * sms;
+        };
+        if (esz == 4) {
+            if (v == V12) { occ(k_scan_bwd_grid<float, 12>, 8 * sizeof(CombineSmem<float, 12>), nb); occ(k_scan_fwd_grid<float, 12>, 8 * sizeof(FwdSmem<float, 12>), nf); }
+            else if (v == V4) { occ(k_scan_bwd_grid<float, 4>, 32 * sizeof(CombineSmem<float, 4>), nb); occ(k_scan_fwd_grid<float, 4>, 32 * sizeof(FwdSmem<float, 4>), nf); }
+            else if (v == V8) { occ(k_scan_bwd_grid<float, 8>, 16 * sizeof(CombineSmem<float, 8>), nb); occ(k_scan_fwd_grid<float, 8>, 16 * sizeof(FwdSmem<float, 8>), nf); }
+            else { occ(k_scan_bwd_grid<float, 16>, 8 * sizeof(CombineSmem<float, 16>), nb); occ(k_scan_fwd_grid<float, 16>, 8 * sizeof(FwdSmem<float, 16>), nf); }
+        } else {
+            if (v == V12) { occ(k_scan_bwd_grid<double, 12>, 8 * sizeof(CombineSmem<double, 12>), nb); occ(k_scan_fwd_grid<double, 12>, 8 * sizeof(FwdSmem<double, 12>), nf); }
+            else if (v == V4) { occ(k_scan_bwd_grid<double, 4>, 32 * sizeof(CombineSmem<double, 4>), nb); occ(k_scan_fwd_grid<double, 4>, 32 * sizeof(FwdSmem<double, 4>), nf); }
+            else if (v == V8) { occ(k_scan_bwd_grid<double, 8>, 16 * sizeof(CombineSmem<double, 8>), nb); occ(k_scan_fwd_grid<double, 8>, 16 * sizeof(FwdSmem<double, 8>), nf); }
+            else { occ(k_scan_bwd_grid<double, 16>, 8 * sizeof(CombineSmem<double, 16>), nb); occ(k_scan_fwd_grid<double, 16>, 8 * sizeof(FwdSmem<double, 16>), nf); }
+        }
+        h->coop_bwd = nb;
+        h->coop_fwd = nf;
+    }
     *out = h;
     return PDILQR_OK;
 }

@@ -261,95 +261,19 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
 }
 
 // ------------------------------------------------------------------ forward + line search
-template <typename T, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
-                                                           T *dx, T *du, T *dlam, const int32_t *info_in, LsOut<T> so,
-                                                           const int32_t *pre_info = nullptr) {
-    constexpr int NX = 12, NA = 16;
-    constexpr int TP = TE<NX>::SIZE;
-    using KL = KE<NX, NX>;
-    constexpr int WPB = LsWarps<T>::value;  // warps (instances) per block
-    __shared__ __align__(16) T sx[WPB][16];
-    __shared__ double sJ[WPB][NA][32], sT[WPB][NA][32];
-    using F = T;                        // line-search evaluation type (fast SFU math for fp32)
-    __shared__ F sDel[WPB][24][32];     // per lane: x_{i+1} - x_i and dx_{i+1} - dx_i of its stage
-    const int lane = threadIdx.x & 31, wl = threadIdx.x / 32;
-    const int b = blockIdx.x * (blockDim.x / 32) + wl;
-    if (b >= B) return;
-    const int na = K.n_alpha;
-    const T *x = it.x + (size_t)b * (N + 2) * NX, *u = it.u + (size_t)b * (N + 1) * NX;
-    const T *xr = it.xref + (size_t)b * (N + 2) * NX;
-    const T *urf = it.uref ? it.uref + (size_t)b * (N + 1) * NX : nullptr;
-    const T *x0 = it.x0 + (size_t)b * NX;
-    const T *Pp = ws.Pp + (size_t)b * (N + 2) * TP;
-    const T *Kk = ws.Kk + (size_t)b * (N + 1) * KL::SIZE;
-    const T *Te = ws.tel + (size_t)b * (N + 1) * TP;
-    T *Dx = dx + (size_t)b * (N + 2) * NX, *Du = du + (size_t)b * (N + 1) * NX, *Dl = dlam + (size_t)b * (N + 2) * NX;
-    int info;
-    if (info_in != nullptr) {
-        info = info_in[b];
-    } else {  // finalise from the pipeline's failure records (see k_finalize_info)
-        const int f = ws.fail[b], pr = pre_info[b];
-        info = pr != 0 ? pr : (f != kFailNone ? (f & 0xFFFFFF) : 0);
-    }
-    // ---------------- closed-loop rollout (one chunk of Eq. 15) and du (Eq. 6)
-    const int r = lane & 15;
-    const bool rowl = r < NX;
-    {
-        const T d0 = x0[r < NX ? r : 0] - x[r < NX ? r : 0];
-        if (lane < NX) { sx[wl][r] = d0; Dx[r] = d0; }
-    }
-    __syncwarp();
-    // lanes 0..11: dx_{i+1} = Abar_i dx_i + bbar_i ; lanes 16..27: du_i = K_i dx_i + k_i.
-    // The next stage's row is loaded while the current one is applied (register double buffer).
-    const T *rowbase = lane < 16 ? Te + (size_t)(rowl ? r : 0) * NX : Kk + KL::K + (size_t)(rowl ? r : 0) * NX;
-    const T *offbase = lane < 16 ? Te + NX * NX + (rowl ? r : 0) : Kk + KL::k + (rowl ? r : 0);
-    const size_t rstride = lane < 16 ? (size_t)TP : (size_t)KL::SIZE;
-    T rcur[NX], ocur;
-    ld_row<T, NX, true>(rcur, rowbase);
-    ocur = offbase[0];
-    for (int i = 0; i <= N; ++i) {
-        T rnext[NX], onext = T(0);
-        if (i < N) {
-            ld_row<T, NX, true>(rnext, rowbase + (size_t)(i + 1) * rstride);
-            onext = offbase[(size_t)(i + 1) * rstride];
-        }
-        T xv[NX];
-        ld_row<T, NX, true>(xv, sx[wl]);
-        const T v = row_dot<T, NX>(rcur, xv, ocur);
-        __syncwarp();
-        if (rowl) {
-            if (lane < 16) { sx[wl][r] = v; Dx[(size_t)(i + 1) * NX + r] = v; }
-            else Du[(size_t)i * NX + r] = v;
-        }
-        __syncwarp();
-        if (i < N) {
-#pragma unroll
-            for (int j = 0; j < NX; ++j) rcur[j] = rnext[j];
-            ocur = onext;
-        }
-    }
-    // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel
-    for (int t = lane; t < (N + 2) * NX; t += 32) {
-        const int i = t / NX, a = t % NX;
-        T prow[NX], xv[NX];
-        ld_row<T, NX, true>(prow, Pp + (size_t)i * TP + a * NX);
-        ld_row<T, NX, true>(xv, Dx + (size_t)i * NX);
-        Dl[t] = row_dot<T, NX>(prow, xv, Pp[(size_t)i * TP + NX * NX + a]);
-    }
-    __syncwarp();
-    // ---------------- line search: lane = stage; per alpha slot a (0 = current iterate,
-    // a >= 1: alpha = 2^-(a-1)); per-lane partial sums in shared memory (no unrolled alpha loop).
-    // Per stage the alpha-invariant parts are computed once: the tracking costs are exact
-    // quadratics c0 + c1 a + c2 a^2 (fp64), the barrier arguments are xi0 + a dxi, the defect is
-    // (x_{i+1} - x_i) + a (dx_{i+1} - dx_i) - dt f(x_i + a dx_i, u_i + a du_i).  Trial states and
-    // the model are evaluated in fp32 (fast sincos / log: SFU), sums in fp64.
-    double(*aJ)[32] = sJ[wl];
-    double(*aT)[32] = sT[wl];
-    for (int a = 0; a <= na; ++a) { aJ[a][lane] = 0.0; aT[a][lane] = 0.0; }
-    unsigned guard = 0u;  // bit a: some trial state of slot a leaves the pitch guard
-    double g = 0.0;
-    for (int i = lane; i <= N + 1; i += 32) {
+// Line-search contribution of stage i (0..N+1) for every alpha slot a = 0..na (a = 0: current
+// iterate, a >= 1: alpha = 2^-(a-1)): adds J_i(a) to aJ[a][lane] and ||defect_i(a)||_2 to
+// aT[a][lane], the cost slope at a = 0 to g, and sets bit a of guard if the trial pitch leaves the
+// Euler guard.  Tracking costs are exact quadratics in alpha (fp64); barrier arguments are
+// xi0 + a dxi; the defect is (x_{i+1} - x_i) + a (dx_{i+1} - dx_i) - dt f(x_i + a dx_i, u_i + a du_i).
+// Trial states and the model in F (fp32: SFU sincos / log), sums in fp64.
+template <typename T>
+__device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &it, int b, int N, int i, int na,
+                                         const T *x, const T *Dx, const T *u, const T *Du, const T *xr, const T *urf,
+                                         double (*aJ)[32], double (*aT)[32], T (*sDel)[32], int lane, double &g,
+                                         unsigned &guard) {
+    constexpr int NX = 12;
+    using F = T;
         const T *xi = x + (size_t)i * NX, *dxi = Dx + (size_t)i * NX;
         const T *xri = xr + (size_t)i * NX;
         if (i == N + 1) {  // terminal cost: quadratic in alpha
@@ -364,7 +288,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
                 aJ[a][lane] += c0 + al * (c1 + al * c2);
             }
             g += c1;
-            continue;
+            return;
         }
         const T *ui = u + (size_t)i * NX, *dui = Du + (size_t)i * NX;
         const T *feet = it.feet + ((size_t)b * (N + 1) + i) * 12;
@@ -375,8 +299,8 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         for (int k = 0; k < NX; ++k) {
             xs0[k] = (F)xi[k]; dxs[k] = (F)dxi[k]; us0[k] = (F)ui[k]; dus[k] = (F)dui[k];
             fe[k] = (F)feet[k];
-            sDel[wl][k][lane] = (F)(xi[NX + k] - xi[k]);
-            sDel[wl][NX + k][lane] = (F)(dxi[NX + k] - dxi[k]);
+            sDel[k][lane] = (F)(xi[NX + k] - xi[k]);
+            sDel[NX + k][lane] = (F)(dxi[NX + k] - dxi[k]);
         }
         const uint8_t cmask = (uint8_t)((con[0] ? 1 : 0) | (con[1] ? 2 : 0) | (con[2] ? 4 : 0) | (con[3] ? 8 : 0));
         // quadratic tracking costs: c0 + c1 a + c2 a^2
@@ -464,13 +388,103 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
             F d2 = F(0.);
 #pragma unroll
             for (int k = 0; k < NX; ++k) {
-                const F d = fma(al, sDel[wl][NX + k][lane], sDel[wl][k][lane]) - dtf * fv[k];
+                const F d = fma(al, sDel[NX + k][lane], sDel[k][lane]) - dtf * fv[k];
                 d2 = fma(d, d, d2);
             }
             aJ[a][lane] += J;
             aT[a][lane] += (double)sqrt(d2);
         }
     }
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+                                                           T *dx, T *du, T *dlam, const int32_t *info_in, LsOut<T> so,
+                                                           const int32_t *pre_info = nullptr) {
+    constexpr int NX = 12, NA = 16;
+    constexpr int TP = TE<NX>::SIZE;
+    using KL = KE<NX, NX>;
+    constexpr int WPB = LsWarps<T>::value;  // warps (instances) per block
+    __shared__ __align__(16) T sx[WPB][16];
+    __shared__ double sJ[WPB][NA][32], sT[WPB][NA][32];
+    __shared__ T sDel[WPB][24][32];     // per lane: x_{i+1} - x_i and dx_{i+1} - dx_i of its stage
+    const int lane = threadIdx.x & 31, wl = threadIdx.x / 32;
+    const int b = blockIdx.x * (blockDim.x / 32) + wl;
+    if (b >= B) return;
+    const int na = K.n_alpha;
+    const T *x = it.x + (size_t)b * (N + 2) * NX, *u = it.u + (size_t)b * (N + 1) * NX;
+    const T *xr = it.xref + (size_t)b * (N + 2) * NX;
+    const T *urf = it.uref ? it.uref + (size_t)b * (N + 1) * NX : nullptr;
+    const T *x0 = it.x0 + (size_t)b * NX;
+    const T *Pp = ws.Pp + (size_t)b * (N + 2) * TP;
+    const T *Kk = ws.Kk + (size_t)b * (N + 1) * KL::SIZE;
+    const T *Te = ws.tel + (size_t)b * (N + 1) * TP;
+    T *Dx = dx + (size_t)b * (N + 2) * NX, *Du = du + (size_t)b * (N + 1) * NX, *Dl = dlam + (size_t)b * (N + 2) * NX;
+    int info;
+    if (info_in != nullptr) {
+        info = info_in[b];
+    } else {  // finalise from the pipeline's failure records (see k_finalize_info)
+        const int f = ws.fail[b], pr = pre_info[b];
+        info = pr != 0 ? pr : (f != kFailNone ? (f & 0xFFFFFF) : 0);
+    }
+    // ---------------- closed-loop rollout (one chunk of Eq. 15) and du (Eq. 6)
+    const int r = lane & 15;
+    const bool rowl = r < NX;
+    {
+        const T d0 = x0[r < NX ? r : 0] - x[r < NX ? r : 0];
+        if (lane < NX) { sx[wl][r] = d0; Dx[r] = d0; }
+    }
+    __syncwarp();
+    // lanes 0..11: dx_{i+1} = Abar_i dx_i + bbar_i ; lanes 16..27: du_i = K_i dx_i + k_i.
+    // The next stage's row is loaded while the current one is applied (register double buffer).
+    const T *rowbase = lane < 16 ? Te + (size_t)(rowl ? r : 0) * NX : Kk + KL::K + (size_t)(rowl ? r : 0) * NX;
+    const T *offbase = lane < 16 ? Te + NX * NX + (rowl ? r : 0) : Kk + KL::k + (rowl ? r : 0);
+    const size_t rstride = lane < 16 ? (size_t)TP : (size_t)KL::SIZE;
+    T rcur[NX], ocur;
+    ld_row<T, NX, true>(rcur, rowbase);
+    ocur = offbase[0];
+    for (int i = 0; i <= N; ++i) {
+        T rnext[NX], onext = T(0);
+        if (i < N) {
+            ld_row<T, NX, true>(rnext, rowbase + (size_t)(i + 1) * rstride);
+            onext = offbase[(size_t)(i + 1) * rstride];
+        }
+        T xv[NX];
+        ld_row<T, NX, true>(xv, sx[wl]);
+        const T v = row_dot<T, NX>(rcur, xv, ocur);
+        __syncwarp();
+        if (rowl) {
+            if (lane < 16) { sx[wl][r] = v; Dx[(size_t)(i + 1) * NX + r] = v; }
+            else Du[(size_t)i * NX + r] = v;
+        }
+        __syncwarp();
+        if (i < N) {
+#pragma unroll
+            for (int j = 0; j < NX; ++j) rcur[j] = rnext[j];
+            ocur = onext;
+        }
+    }
+    // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel
+    for (int t = lane; t < (N + 2) * NX; t += 32) {
+        const int i = t / NX, a = t % NX;
+        T prow[NX], xv[NX];
+        ld_row<T, NX, true>(prow, Pp + (size_t)i * TP + a * NX);
+        ld_row<T, NX, true>(xv, Dx + (size_t)i * NX);
+        Dl[t] = row_dot<T, NX>(prow, xv, Pp[(size_t)i * TP + NX * NX + a]);
+    }
+    __syncwarp();
+    // ---------------- line search: lane = stage; per alpha slot a (0 = current iterate,
+    // a >= 1: alpha = 2^-(a-1)); per-lane partial sums in shared memory (no unrolled alpha loop).
+    // Per stage the alpha-invariant parts are computed once: the tracking costs are exact
+    // quadratics c0 + c1 a + c2 a^2 (fp64), the barrier arguments are xi0 + a dxi, the defect is
+    // (x_{i+1} - x_i) + a (dx_{i+1} - dx_i) - dt f(x_i + a dx_i, u_i + a du_i).  Trial states and
+    // the model are evaluated in fp32 (fast sincos / log: SFU), sums in fp64.
+    double(*aJ)[32] = sJ[wl];
+    double(*aT)[32] = sT[wl];
+    for (int a = 0; a <= na; ++a) { aJ[a][lane] = 0.0; aT[a][lane] = 0.0; }
+    unsigned guard = 0u;  // bit a: some trial state of slot a leaves the pitch guard
+    double g = 0.0;
+    for (int i = lane; i <= N + 1; i += 32)
+        ls_stage<T>(K, it, b, N, i, na, x, Dx, u, Du, xr, urf, aJ, aT, sDel[wl], lane, g, guard);
     // fixed-order xor butterflies: every lane ends with bitwise identical sums
     for (int a = 0; a <= na; ++a) {
         double vJ = aJ[a][lane], vT = aT[a][lane];
@@ -580,6 +594,8 @@ __global__ void __launch_bounds__(128) k_srbd_lin_elem(SrbdConst K, SrbdIter<T> 
             st_row<T, NX, true>(e + L::P + r * NX, Prow);
             e[L::b + r] = T(0);
             e[L::p + r] = pr;
+            const T *xfirst = it.x + (size_t)b * (N + 2) * NX;
+            const_cast<T *>(qp.dx0)[(size_t)b * NX + r] = it.x0[(size_t)b * NX + r] - xfirst[r];  // dx0 = xhat0 - x0
             if (!isfinite(x[r]) || !isfinite(lam[r]) || !isfinite(it.x0[(size_t)b * NX + r])) pre_info[b] = -1;
         }
         return;  // the partner worker of this warp only uses its own lane mask below
@@ -653,6 +669,106 @@ __global__ void __launch_bounds__(128) k_srbd_lin_elem(SrbdConst K, SrbdIter<T> 
         const_cast<T *>(qp.r)[st * NX + r] = rr;
         if (bad) pre_info[b] = -1;
         if (fail) atomicMin(ws.fail + b, i + 1);
+    }
+}
+
+// ------------------------------------------------ line search for small batches (latency regime)
+// grid (S, B), one warp per block and per 32 stages: every warp adds its stages' contributions per
+// alpha slot, writes them to `part` ([B][S][2 NA + 2] doubles), and the last warp of an instance
+// (atomic ticket) reduces the S partials in a fixed order, applies the filter rule,
+// updates x, u, lam in place (Eq. 16) and writes the stats.  `cnt` ([B] ints) must be zero on
+// entry and is left zero.
+template <typename T>
+__global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> it, int B, int N, const T *dx,
+                                                      const T *du, const T *dlam, const int32_t *info_in, LsOut<T> so,
+                                                      double *part, int *cnt) {
+    constexpr int NX = 12, NA = 16, PW = 2 * NA + 2;
+    __shared__ double aJ[NA][32], aT[NA][32];
+    __shared__ T sDel[24][32];
+    const int lane = threadIdx.x, sblk = blockIdx.x, S = gridDim.x, b = blockIdx.y;
+    const int na = K.n_alpha;
+    const T *x = it.x + (size_t)b * (N + 2) * NX, *u = it.u + (size_t)b * (N + 1) * NX;
+    const T *xr = it.xref + (size_t)b * (N + 2) * NX;
+    const T *urf = it.uref ? it.uref + (size_t)b * (N + 1) * NX : nullptr;
+    const T *Dx = dx + (size_t)b * (N + 2) * NX, *Du = du + (size_t)b * (N + 1) * NX;
+    for (int a = 0; a <= na; ++a) { aJ[a][lane] = 0.0; aT[a][lane] = 0.0; }
+    double g = 0.0;
+    unsigned guard = 0u;
+    const int i = sblk * 32 + lane;
+    if (i <= N + 1) ls_stage<T>(K, it, b, N, i, na, x, Dx, u, Du, xr, urf, aJ, aT, sDel, lane, g, guard);
+    __syncwarp();
+    double *pw = part + ((size_t)b * S + sblk) * PW;
+    for (int a = 0; a <= na; ++a) {
+        double vJ = aJ[a][lane], vT = aT[a][lane];
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+            vJ += __shfl_xor_sync(0xffffffffu, vJ, off);
+            vT += __shfl_xor_sync(0xffffffffu, vT, off);
+        }
+        if (lane == 0) { pw[a] = vJ; pw[NA + a] = vT; }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+        g += __shfl_xor_sync(0xffffffffu, g, off);
+        guard |= __shfl_xor_sync(0xffffffffu, guard, off);
+    }
+    if (lane == 0) { pw[2 * NA] = g; pw[2 * NA + 1] = (double)guard; }
+    __threadfence();
+    int ticket = 0;
+    if (lane == 0) ticket = atomicAdd(cnt + b, 1);
+    ticket = __shfl_sync(0xffffffffu, ticket, 0);
+    if (ticket != S - 1) return;
+    __threadfence();
+    // last warp of instance b: fixed-order reduction over the S partials
+    const volatile double *pb = part + (size_t)b * S * PW;
+    double J = 0.0, th = 0.0, gg = 0.0;
+    unsigned gd = 0u;
+    for (int t = 0; t < S; ++t) {
+        if (lane <= na) { J += pb[(size_t)t * PW + lane]; th += pb[(size_t)t * PW + NA + lane]; }
+        gg += pb[(size_t)t * PW + 2 * NA];
+        gd |= (unsigned)pb[(size_t)t * PW + 2 * NA + 1];
+    }
+    const T *x0 = it.x0 + (size_t)b * NX;
+    const double al = lane == 0 ? 0.0 : ldexp(1.0, -(lane - 1));
+    {
+        double q = 0;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            const double e = ((double)x0[k] - (double)x[k]) - al * (double)Dx[k];
+            q += e * e;
+        }
+        th += sqrt(q);
+    }
+    const double J0 = __shfl_sync(0xffffffffu, J, 0), th0 = __shfl_sync(0xffffffffu, th, 0);
+    const int info = info_in[b];
+    bool ok = false;
+    if (lane >= 1 && lane <= na && info == 0) {
+        ok = !((gd >> lane) & 1u) && isfinite(J) && isfinite(th);
+        if (ok) {
+            if (th0 > K.theta_max) ok = th <= th0;
+            else if (gg < 0) ok = J <= J0 + K.c1 * al * gg;
+            else ok = (J < J0) || (th < th0);
+        }
+    }
+    const unsigned acc = __ballot_sync(0xffffffffu, ok);
+    const int jb = acc ? __ffs(acc) - 1 : 0;
+    const double Jb = __shfl_sync(0xffffffffu, J, jb), thb = __shfl_sync(0xffffffffu, th, jb);
+    const T alpha = acc ? (T)ldexp(1.0, -(jb - 1)) : T(0);
+    if (acc) {
+        T *xw = const_cast<T *>(it.x) + (size_t)b * (N + 2) * NX;
+        T *uw = const_cast<T *>(it.u) + (size_t)b * (N + 1) * NX;
+        T *lw = const_cast<T *>(it.lam) + (size_t)b * (N + 2) * NX;
+        const T *Dl = dlam + (size_t)b * (N + 2) * NX;
+        for (int t = lane; t < (N + 2) * NX; t += 32) { xw[t] = xw[t] + alpha * Dx[t]; lw[t] = lw[t] + alpha * Dl[t]; }
+        for (int t = lane; t < (N + 1) * NX; t += 32) uw[t] = uw[t] + alpha * Du[t];
+    }
+    if (lane == 0) {
+        so.cost[b] = (T)Jb;
+        so.theta[b] = (T)thb;
+        so.alpha[b] = alpha;
+        so.accepted[b] = acc ? 1 : 0;
+        so.info[b] = info;
+        cnt[b] = 0;
     }
 }
 

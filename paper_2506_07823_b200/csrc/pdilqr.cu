@@ -17,6 +17,7 @@
 #include "lq.cuh"
 #include "srbd.cuh"
 #include "srbd_fused.cuh"
+#include "big.cuh"
 
 using namespace pdilqr;
 
@@ -46,7 +47,8 @@ int pow2ceil(int x) {
 }
 
 // Kernel instantiation chosen for (n, m): exact 12x12 (SRBD) or a zero-padded bound.
-enum Variant { V12 = 0, V4 = 1, V8 = 2, V16 = 3 };
+enum Variant { V12 = 0, V4 = 1, V8 = 2, V16 = 3, VBIG = 4 };
+constexpr int kBigMax = 256;   // largest n, m of the CTA-level path
 
 bool pick_variant(int n, int m, Variant &v, int &NX, int &NU) {
     if (n == 12 && m == 12) { v = V12; NX = NU = 12; return true; }
@@ -54,6 +56,7 @@ bool pick_variant(int n, int m, Variant &v, int &NX, int &NU) {
     if (d <= 4) { v = V4; NX = NU = 4; return true; }
     if (d <= 8) { v = V8; NX = NU = 8; return true; }
     if (d <= 16) { v = V16; NX = NU = 16; return true; }
+    if (d <= kBigMax) { v = VBIG; NX = ld_of(n); NU = ld_of(m); return true; }
     return false;
 }
 
@@ -139,7 +142,9 @@ pdilqr_status check_cfg(const pdilqr_config *c, Variant &v, int &NX, int &NU) {
     if (c->n_alpha < 0 || c->n_alpha > kMaxAlpha) return fail(PDILQR_ERR_INVALID_ARG, "n_alpha must be in [0, %d]", kMaxAlpha);
     if (c->leaf_chunk < 0) return fail(PDILQR_ERR_INVALID_ARG, "leaf_chunk must be >= 0");
     if (!pick_variant(c->n, c->m, v, NX, NU))
-        return fail(PDILQR_ERR_UNSUPPORTED, "n = %d, m = %d: dimensions above 16 are not supported by this build", c->n, c->m);
+        return fail(PDILQR_ERR_UNSUPPORTED, "n = %d, m = %d: dimensions above %d are not supported", c->n, c->m, kBigMax);
+    if (v == VBIG && c->model != PDILQR_MODEL_LQ)
+        return fail(PDILQR_ERR_UNSUPPORTED, "the large-dimension path serves pdilqr_solve_lq only");
     if (c->model == PDILQR_MODEL_SRBD) {
         const auto &s = c->srbd;
         if (!(s.dt >= 0) || !(s.mass > 0) || !(s.barrier_mu > 0) || !(s.barrier_delta > 0))
@@ -155,8 +160,40 @@ int default_chunk(const pdilqr_config *c) {
     return c->batch >= 148 ? c->N + 2 : 1;
 }
 
+size_t big_slot(int n, int m) {
+    const size_t init = (size_t)m * ld_of(m + 2 * n + 1);
+    const size_t fold = (size_t)n * ld_of(n) * 2 + (size_t)n * ld_of(2 * n) + 2 * ld_of(n);
+    const size_t pol = (size_t)n * ld_of(m) + (size_t)m * ld_of(m + n + 1) + ld_of(n);
+    return (std::max({init, fold, pol}) + 63) / 64 * 64;
+}
+constexpr int kBigPersistent = 148 * 4;  // CTAs of the persistent (stage-parallel) big kernels
+
+Layout make_big_layout(const pdilqr_config *c, int esz) {
+    const size_t B = c->batch, N = c->N, n = c->n, m = c->m, LD = ld_of((int)n), LDU = ld_of((int)m);
+    Layout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
+    L.elems = take(B * (N + 2) * (3 * n * LD + 2 * LD) * esz);
+    L.Pp = take(B * (N + 2) * (n * LD + LD) * esz);
+    L.Kk = take(B * (N + 1) * (m * LD + LDU) * esz);
+    L.tel = take(B * (N + 1) * (n * LD + LD) * esz);
+    L.dxw = take(B * (N + 2) * LD * esz);
+    L.vslots = take(std::max((size_t)kBigPersistent, B) * big_slot((int)n, (int)m) * esz);  // scratch slots
+    L.fail = take(B * 4);
+    L.nonfin = take(B * 4);
+    L.pre = take(B * 4);
+    L.info_tmp = take(B * 4);
+    L.stats = take(B * (3 * (size_t)esz + 8));
+    L.total = off;
+    return L;
+}
+
 Layout make_layout(const pdilqr_config *c, int NX, int NU, int esz, int chunk, int &Jb, int &Pv, int &Jf, int &Pf) {
     const size_t B = c->batch, N = c->N;
+    if (NX > 16 || NU > 16 || c->n > 16 || c->m > 16) {  // large path: single chunk
+        Jb = Jf = 1; Pv = Pf = 1;
+        return make_big_layout(c, esz);
+    }
     const size_t VEs = 3 * NX * NX + 2 * NX, TEs = NX * NX + NX, KEs = NU * NX + NU;
     Jb = (int)((N + 2 + chunk - 1) / chunk);
     Jf = (int)((N + 1 + chunk - 1) / chunk);
@@ -345,6 +382,50 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
     return cuda_check("solve_lq launch");
 }
 
+// Large dimensions (16 < max(n, m) <= 256): CTA-level single-chunk path (big.cuh).
+template <typename T>
+pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
+    BigDims<T> d{n, m, ld_of(n), ld_of(m)};
+    BigWork<T> ws;
+    ws.elems = reinterpret_cast<T *>(h->ws + h->lay.elems);
+    ws.Pp = reinterpret_cast<T *>(h->ws + h->lay.Pp);
+    ws.Kk = reinterpret_cast<T *>(h->ws + h->lay.Kk);
+    ws.tel = reinterpret_cast<T *>(h->ws + h->lay.tel);
+    ws.dxw = reinterpret_cast<T *>(h->ws + h->lay.dxw);
+    ws.scratch = reinterpret_cast<T *>(h->ws + h->lay.vslots);
+    ws.slot = big_slot(n, m);
+    ws.fail = reinterpret_cast<int32_t *>(h->ws + h->lay.fail);
+    cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
+    const int gpers = (int)std::min<long>((long)kBigPersistent, (long)B * (N + 2));
+    {
+        Prof pf(h, "k_big_init", st);
+        k_big_init<T><<<gpers, BIG_THREADS, 0, st>>>(qp, B, N, d, ws);
+    }
+    {
+        Prof pf(h, "k_big_fold", st);
+        k_big_fold<T><<<B, BIG_THREADS, 0, st>>>(B, N, d, ws);
+    }
+    {
+        Prof pf(h, "k_big_policy", st);
+        k_big_policy<T><<<gpers, BIG_THREADS, 0, st>>>(qp, B, N, d, ws, out);
+    }
+    {
+        Prof pf(h, "k_big_fwd", st);
+        k_big_fwd<T><<<B, BIG_THREADS, 0, st>>>(qp.dx0, B, N, d, ws, out);
+    }
+    int launches = 4;
+    if (info) {
+        int32_t *nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
+        cudaMemsetAsync(nonfin, 0, (size_t)B * 4, st);
+        Prof pf(h, "k_finalize_info", st);
+        k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, nonfin, nullptr, info);
+        ++launches;
+    }
+    h->launches += launches;
+    return cuda_check("solve_lq (large) launch");
+}
+
 template <typename T>
 pdilqr_status dispatch_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, const int32_t *pre,
                           cudaStream_t st, bool skip_init = false) {
@@ -352,7 +433,8 @@ pdilqr_status dispatch_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int3
         case V12: return run_lq<T, 12, 12, true>(h, qp, out, info, pre, st, skip_init);
         case V4: return run_lq<T, 4, 4, false>(h, qp, out, info, pre, st, skip_init);
         case V8: return run_lq<T, 8, 8, false>(h, qp, out, info, pre, st, skip_init);
-        default: return run_lq<T, 16, 16, false>(h, qp, out, info, pre, st, skip_init);
+        case V16: return run_lq<T, 16, 16, false>(h, qp, out, info, pre, st, skip_init);
+        default: return run_big<T>(h, qp, out, info, st);
     }
 }
 

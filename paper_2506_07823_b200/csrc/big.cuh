@@ -41,20 +41,29 @@ __device__ void cta_gemm(int Mr, int Nc, int K, T alpha, const T *A, int lda, co
             for (int a = 0; a < 4; ++a)
 #pragma unroll
                 for (int c = 0; c < 4; ++c) acc[a][c] = T(0);
-            for (int k0 = 0; k0 < K; k0 += 16) {
+            // k panels of 16, the next panel is loaded into registers while the current one is used
+            T pa[4], pb[4];
+            auto fetch = [&](int k0) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     const int idx = tid + e * BIG_THREADS;  // 0..1023
                     const int kk = idx >> 6, mm = idx & 63;  // As[kk][mm] = opA(tm+mm, k0+kk)
                     const int r = tm + mm, c = k0 + kk;
-                    T va = T(0), vb = T(0);
-                    if (r < Mr && c < K) va = TA ? A[(size_t)c * lda + r] : A[(size_t)r * lda + c];
+                    pa[e] = (r < Mr && c < K) ? (TA ? A[(size_t)c * lda + r] : A[(size_t)r * lda + c]) : T(0);
                     const int rb = k0 + kk, cb = tn + mm;  // Bs[kk][nn] = opB(k0+kk, tn+nn)
-                    if (rb < K && cb < Nc) vb = TB ? Bm[(size_t)cb * ldb + rb] : Bm[(size_t)rb * ldb + cb];
-                    sm.As[kk][mm] = va;
-                    sm.Bs[kk][mm] = vb;
+                    pb[e] = (rb < K && cb < Nc) ? (TB ? Bm[(size_t)cb * ldb + rb] : Bm[(size_t)rb * ldb + cb]) : T(0);
+                }
+            };
+            fetch(0);
+            for (int k0 = 0; k0 < K; k0 += 16) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int idx = tid + e * BIG_THREADS;
+                    sm.As[idx >> 6][idx & 63] = pa[e];
+                    sm.Bs[idx >> 6][idx & 63] = pb[e];
                 }
                 __syncthreads();
+                if (k0 + 16 < K) fetch(k0 + 16);
 #pragma unroll
                 for (int kk = 0; kk < 16; ++kk) {
                     T a[4], b[4];
@@ -212,12 +221,14 @@ struct BigDims {
 // (R SPD), then A~ = A - B Z_S, C~ = B Z_B, P~ = Q - S^T Z_S, b~ = b - B z_r, p~ = q - S^T z_r.
 // Terminal (i = N+1): A~ = C~ = b~ = 0, P~ = P_{N+1}, p~ = p_{N+1}.
 template <typename T>
-__global__ void __launch_bounds__(BIG_THREADS) k_big_init(LqArgs<T> qp, int B, int N, BigDims<T> d, BigWork<T> ws) {
+__global__ void __launch_bounds__(BIG_THREADS) k_big_init(LqArgs<T> qp, int B, int N, BigDims<T> d, BigWork<T> ws,
+                                                          int w_in_smem) {
     __shared__ GemmSmem<T> gsm;
     __shared__ GjShared gjs;
+    extern __shared__ __align__(16) unsigned char dyn[];
     const int n = d.n, m = d.m, LD = d.LD;
     const int ldw = ld_of(m + 2 * n + 1);
-    T *W = ws.scratch + (size_t)blockIdx.x * ws.slot;
+    T *W = w_in_smem ? reinterpret_cast<T *>(dyn) : ws.scratch + (size_t)blockIdx.x * ws.slot;
     for (long item = blockIdx.x; item < (long)B * (N + 2); item += gridDim.x) {
         const int b = (int)(item / (N + 2)), i = (int)(item % (N + 2));
         T *e = ws.elems + ((size_t)b * (N + 2) + i) * d.esize();
@@ -284,14 +295,16 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_init(LqArgs<T> qp, int B, i
 // X = M^-1 A~_i (pivoted GJ), w = p' + P' b~_i, V = P' X, P_i = A~_i^T V + P~_i (symmetrised),
 // p_i = X^T w + p~_i.  Scratch slot: P' (n LD), W (n x ld(2n)), V (n LD), w, p' (LD each).
 template <typename T>
-__global__ void __launch_bounds__(BIG_THREADS) k_big_fold(int B, int N, BigDims<T> d, BigWork<T> ws) {
+__global__ void __launch_bounds__(BIG_THREADS) k_big_fold(int B, int N, BigDims<T> d, BigWork<T> ws, int w_in_smem) {
     __shared__ GemmSmem<T> gsm;
     __shared__ GjShared gjs;
+    extern __shared__ __align__(16) unsigned char dyn[];
     const int b = blockIdx.x;
     if (b >= B) return;
     const int n = d.n, LD = d.LD, ldw = ld_of(2 * n);
     T *Pc = ws.scratch + (size_t)blockIdx.x * ws.slot;
-    T *W = Pc + (size_t)n * LD, *V = W + (size_t)n * ldw, *w = V + (size_t)n * LD, *pc = w + LD;
+    T *Wg = Pc + (size_t)n * LD, *V = Wg + (size_t)n * ldw, *w = V + (size_t)n * LD, *pc = w + LD;
+    T *W = w_in_smem ? reinterpret_cast<T *>(dyn) : Wg;
     const T *E = ws.elems + (size_t)b * (N + 2) * d.esize();
     T *Pp = ws.Pp + (size_t)b * (N + 2) * d.psize();
     {   // s_{N+1}
@@ -346,12 +359,14 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_fold(int B, int N, BigDims<
 // bbar = B k + b.  Scratch: PB (n x ld(m)), W (m x ld(m+n+1)), g (LD).
 template <typename T>
 __global__ void __launch_bounds__(BIG_THREADS) k_big_policy(LqArgs<T> qp, int B, int N, BigDims<T> d, BigWork<T> ws,
-                                                            LqOut<T> out) {
+                                                            LqOut<T> out, int w_in_smem) {
     __shared__ GemmSmem<T> gsm;
     __shared__ GjShared gjs;
+    extern __shared__ __align__(16) unsigned char dyn[];
     const int n = d.n, m = d.m, LD = d.LD, ldpb = ld_of(m), ldw = ld_of(m + n + 1);
     T *PB = ws.scratch + (size_t)blockIdx.x * ws.slot;
-    T *W = PB + (size_t)n * ldpb, *g = W + (size_t)m * ldw;
+    T *Wg = PB + (size_t)n * ldpb, *g = Wg + (size_t)m * ldw;
+    T *W = w_in_smem ? reinterpret_cast<T *>(dyn) : Wg;
     for (long item = blockIdx.x; item < (long)B * (N + 1); item += gridDim.x) {
         const int b = (int)(item / (N + 1)), i = (int)(item % (N + 1));
         const size_t st = (size_t)b * (N + 1) + i;

@@ -398,17 +398,29 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
     ws.fail = reinterpret_cast<int32_t *>(h->ws + h->lay.fail);
     cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
     const int gpers = (int)std::min<long>((long)kBigPersistent, (long)B * (N + 2));
+    // the augmented Gauss-Jordan matrix W lives in shared memory when it fits (n <= ~110 in fp32)
+    const size_t kSmemW = 180 * 1024;
+    auto wbytes = [&](int rows, int cols) { return (size_t)rows * ld_of(cols) * sizeof(T); };
     {
+        const size_t wb = wbytes(m, m + 2 * n + 1);
+        const int in = wb <= kSmemW;
+        if (in) cudaFuncSetAttribute(k_big_init<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
         Prof pf(h, "k_big_init", st);
-        k_big_init<T><<<gpers, BIG_THREADS, 0, st>>>(qp, B, N, d, ws);
+        k_big_init<T><<<gpers, BIG_THREADS, in ? wb : 0, st>>>(qp, B, N, d, ws, in);
     }
     {
+        const size_t wb = wbytes(n, 2 * n);
+        const int in = wb <= kSmemW;
+        if (in) cudaFuncSetAttribute(k_big_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
         Prof pf(h, "k_big_fold", st);
-        k_big_fold<T><<<B, BIG_THREADS, 0, st>>>(B, N, d, ws);
+        k_big_fold<T><<<B, BIG_THREADS, in ? wb : 0, st>>>(B, N, d, ws, in);
     }
     {
+        const size_t wb = wbytes(m, m + n + 1);
+        const int in = wb <= kSmemW;
+        if (in) cudaFuncSetAttribute(k_big_policy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
         Prof pf(h, "k_big_policy", st);
-        k_big_policy<T><<<gpers, BIG_THREADS, 0, st>>>(qp, B, N, d, ws, out);
+        k_big_policy<T><<<gpers, BIG_THREADS, in ? wb : 0, st>>>(qp, B, N, d, ws, out, in);
     }
     {
         Prof pf(h, "k_big_fwd", st);

@@ -335,4 +335,65 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int NPENDING>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPENDING)); }
 
+// Two independent eliminations interleaved step by step (full-warp workers of WS = 16 lanes):
+// problem 1 is SPD (no pivoting), problem 2 uses partial pivoting.  Same arithmetic as two calls of
+// gauss_jordan<..., FULLWARP = true>, but the dependent chains of the two systems overlap (ILP).
+template <typename T, int NR, int NRHS1, int NRHS2>
+__device__ __forceinline__ void gauss_jordan_dual(T (&a1)[NR], T (&r1)[NRHS1], T (&a2)[NR], T (&r2)[NRHS2], int lane,
+                                                  int &piv1, int &piv2, bool &ok1, bool &ok2) {
+    constexpr int WS = 16;
+    const unsigned full = 0xffffffffu;
+    bool used2 = lane >= NR;
+    ok1 = true; ok2 = true;
+    piv2 = -1;
+    T mp1 = T(1), mp2 = T(1);
+    const bool lo = (threadIdx.x & 16) == 0;
+#pragma unroll
+    for (int k = 0; k < NR; ++k) {
+        const unsigned key = used2 ? 0u : ((__float_as_uint(fabsf((float)a2[k])) & 0xFFFFFFE0u) | (31u - (unsigned)lane));
+        const unsigned b0 = __reduce_max_sync(full, lo ? key : 0u);
+        const unsigned b1 = __reduce_max_sync(full, lo ? 0u : key);
+        const int p2 = 31 - (int)((lo ? b0 : b1) & 31u);
+        const int p1 = k;
+        const T rk1 = rcp_rn(a1[k]), rk2 = rcp_rn(a2[k]);
+        const T pv1 = __shfl_sync(full, a1[k], p1, WS), rp1 = __shfl_sync(full, rk1, p1, WS);
+        const T pv2 = __shfl_sync(full, a2[k], p2, WS), rp2 = __shfl_sync(full, rk2, p2, WS);
+        ok1 = ok1 && (pv1 > T(0)) && isfinite(pv1);
+        ok2 = ok2 && (pv2 != T(0)) && isfinite(pv2);
+        const bool isp1 = lane == p1, isp2 = lane == p2;
+        const T f1 = isp1 ? T(0) : a1[k] * rp1;
+        const T f2 = isp2 ? T(0) : a2[k] * rp2;
+        if (isp1) mp1 = pv1;
+        if (isp2) { used2 = true; piv2 = k; mp2 = pv2; }
+#pragma unroll
+        for (int j = k + 1; j < NR; ++j) {
+            a1[j] = fma(-f1, __shfl_sync(full, a1[j], p1, WS), a1[j]);
+            a2[j] = fma(-f2, __shfl_sync(full, a2[j], p2, WS), a2[j]);
+        }
+#pragma unroll
+        for (int j = 0; j + 1 < NRHS1; j += 2) {
+            const T q0 = __shfl_sync(full, r1[j], p1, WS), q1 = __shfl_sync(full, r1[j + 1], p1, WS);
+            ffma2(-f1, -f1, q0, q1, r1[j], r1[j + 1]);
+        }
+        if constexpr (NRHS1 % 2) r1[NRHS1 - 1] = fma(-f1, __shfl_sync(full, r1[NRHS1 - 1], p1, WS), r1[NRHS1 - 1]);
+#pragma unroll
+        for (int j = 0; j + 1 < NRHS2; j += 2) {
+            const T q0 = __shfl_sync(full, r2[j], p2, WS), q1 = __shfl_sync(full, r2[j + 1], p2, WS);
+            ffma2(-f2, -f2, q0, q1, r2[j], r2[j + 1]);
+        }
+        if constexpr (NRHS2 % 2) r2[NRHS2 - 1] = fma(-f2, __shfl_sync(full, r2[NRHS2 - 1], p2, WS), r2[NRHS2 - 1]);
+    }
+    const T i1 = rcp_rn(mp1), i2 = rcp_rn(mp2);
+#pragma unroll
+    for (int j = 0; j < NRHS1; ++j) r1[j] *= i1;
+#pragma unroll
+    for (int j = 0; j < NRHS2; ++j) r2[j] *= i2;
+    piv1 = lane < NR ? lane : -1;
+    unsigned v = (ok1 ? 1u : 0u) | (ok2 ? 2u : 0u);
+#pragma unroll
+    for (int off = WS / 2; off >= 1; off >>= 1) v &= __shfl_xor_sync(full, v, off, WS);
+    ok1 = (v & 1u) != 0u;
+    ok2 = (v & 2u) != 0u;
+}
+
 }  // namespace pdilqr

@@ -163,28 +163,39 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
         }
         __syncwarp(mask);
         {
+            // policy system  G [K | k] = -[H | h]  (G = R + B^T P B SPD, H = B^T P A, h = B^T (p + P b) + r)
+            // and combine system  M X = A~  (M = I + C~ P'), eliminated together
             T bcol[NX], pbcol[NX], G[NX], rhs[NX + 1];
             ld_col<T, NX>(bcol, s.B + r, NX);
             ld_col<T, NX>(pbcol, s.V + r, NX);
 #pragma unroll
             for (int j = 0; j < NX; ++j) G[j] = row.Rrow[j];
-            row_mat<T, NX, NX, NX>(G, bcol, s.V);             // G = R + B^T P B
+            row_mat<T, NX, NX, NX>(G, bcol, s.V);
             zero(*reinterpret_cast<T(*)[NX]>(rhs));
-            row_mat<T, NX, NX, NX>(*reinterpret_cast<T(*)[NX]>(rhs), pbcol, s.A);  // H = B^T P A
-            rhs[NX] = row_dot<T, NX>(bcol, s.g, rr);           // h = B^T (p + P b) + r
-            int pr;
-            if (!gauss_jordan<T, WS, NX, NX + 1, false, true>(mask, G, rhs, lane, NX, pr)) fail = min(fail, i + 1);
-            if (pr >= 0) {
+            row_mat<T, NX, NX, NX>(*reinterpret_cast<T(*)[NX]>(rhs), pbcol, s.A);
+            rhs[NX] = row_dot<T, NX>(bcol, s.g, rr);
+            T M[NX], rhs2[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) { M[j] = (j == r) ? T(1) : T(0); rhs2[j] = arow[j]; }
+            row_mat<T, NX, NX, NX>(M, ct, s.P);
+            const T wr = row_dot<T, NX>(prow, s.bt, s.p[r]);
+            if (act) s.w[r] = wr;
+            int pr1, pr2;
+            bool ok1, ok2;
+            gauss_jordan_dual<T, NX, NX + 1, NX>(G, rhs, M, rhs2, lane, pr1, pr2, ok1, ok2);
+            if (!ok1 || !ok2) fail = min(fail, i + 1);
+            if (pr1 >= 0) {
                 T kr[NX];
 #pragma unroll
                 for (int j = 0; j < NX; ++j) kr[j] = -rhs[j];
-                st_row<T, NX, true>(s.K + pr * NX, kr);
-                s.k[pr] = -rhs[NX];
+                st_row<T, NX, true>(s.K + pr1 * NX, kr);
+                s.k[pr1] = -rhs[NX];
                 if (live) {
-                    st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + pr * NX, kr);
-                    Kk[(size_t)i * KL::SIZE + KL::k + pr] = -rhs[NX];
+                    st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + pr1 * NX, kr);
+                    Kk[(size_t)i * KL::SIZE + KL::k + pr1] = -rhs[NX];
                 }
             }
+            if (pr2 >= 0) st_row<T, NX, true>(s.X + pr2 * NX, rhs2);
         }
         __syncwarp(mask);
         {
@@ -197,23 +208,6 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
                 st_row<T, NX, true>(Te + (size_t)i * TP + r * NX, abar);
                 Te[(size_t)i * TP + NX * NX + r] = bb;
             }
-        }
-        // ---------------- s_i = e_i (x) s_{i+1}, cheap rule: M = I + C~ P', X = M^-1 A,
-        //                  P_i = A^T P' X + Q,  p_i = X^T (p' + P' b~) + q
-        {
-            T M[NX];
-#pragma unroll
-            for (int j = 0; j < NX; ++j) M[j] = (j == r) ? T(1) : T(0);
-            row_mat<T, NX, NX, NX>(M, ct, s.P);
-            const T wr = row_dot<T, NX>(prow, s.bt, s.p[r]);
-            if (act) s.w[r] = wr;
-            T rhs[NX];
-#pragma unroll
-            for (int j = 0; j < NX; ++j) rhs[j] = arow[j];
-            int pr;
-            if (!gauss_jordan<T, WS, NX, NX, true, true>(mask, M, rhs, lane, NX, pr)) fail = min(fail, i + 1);
-            __syncwarp(mask);                          // everyone is done reading s.X (dt Fx)
-            if (pr >= 0) st_row<T, NX, true>(s.X + pr * NX, rhs);
         }
         __syncwarp(mask);
         {

@@ -185,3 +185,10 @@ def test_pitch_guard_info(P):
     assert info[1] == -1 and info[0] == 0 and info[2] == 0
     assert to_np(st["accepted"])[1] == 0 and to_np(st["alpha"])[1] == 0
     assert torch.equal(d["x"][1], x_before[1])
+
+
+@pytest.mark.parametrize("N", [200, 1000])
+def test_step_long_horizon_tree_fp32(P, O, N):
+    """Latency regime (B < 148: cooperative tree scans): fp32 first-step direction parity holds at
+    long horizons (a sequential fp32 Riccati recursion diverges here)."""
+    step_parity(P, O, 2, N, torch.float32, seed=60 + N, leaf_chunk=1, steps=1, dir_steps=(0,))

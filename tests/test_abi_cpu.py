@@ -66,7 +66,8 @@ def test_workspace_bytes_and_validation(P):
     assert nb2.value > nb.value               # the tree needs slot storage
     assert L.pdilqr_workspace_bytes(C.byref(cfg(P, n=13)), C.byref(nb)) == 2       # SRBD needs n = m = 12
     assert b"SRBD" in L.pdilqr_last_error()
-    assert L.pdilqr_workspace_bytes(C.byref(cfg(P, model=0, n=40, m=4)), C.byref(nb)) == 5
+    assert L.pdilqr_workspace_bytes(C.byref(cfg(P, model=0, n=300, m=4)), C.byref(nb)) == 5   # n > 256
+    assert L.pdilqr_workspace_bytes(C.byref(cfg(P, model=0, n=74, m=32, batch=8, N=100)), C.byref(nb)) == 0
     assert L.pdilqr_workspace_bytes(C.byref(cfg(P, n_alpha=40)), C.byref(nb)) == 1
     assert L.pdilqr_workspace_bytes(C.byref(cfg(P, batch=0)), C.byref(nb)) == 2
     assert L.pdilqr_workspace_bytes(None, C.byref(nb)) == 1

@@ -159,4 +159,4 @@ def test_rejects_bad_arguments(P):
     with pytest.raises(P.PdilqrError):
         h.solve_lq(qp)
     with pytest.raises(P.PdilqrError):
-        P.PdIlqr(N=5, n=40, m=2, batch=2)
+        P.PdIlqr(N=5, n=300, m=2, batch=2)

@@ -194,6 +194,7 @@ def main():
     ap.add_argument("--latency", default="25,50,100,200,400,1000",
                     help="horizons of the B=1 latency sweep (config 2), '' to skip")
     ap.add_argument("--latency-reps", type=int, default=300)
+    ap.add_argument("--closed-loop-ticks", type=int, default=50, help="0 disables the closed-loop RTF leg")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -345,6 +346,9 @@ def main():
     lat = None
     if args.latency:
         lat = latency_sweep(P, torch, dev, [int(v) for v in args.latency.split(",")], args.latency_reps)
+    clo = None
+    if args.closed_loop_ticks > 0 and args.dtype == "f32":
+        clo = closed_loop_bench(P, torch, dev, B, N, args.closed_loop_ticks)
     cpu = None if args.no_cpu_baseline else cpu_baseline(B, N, synth.BASE_SEED, args.cpu_budget)
     out = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -357,7 +361,7 @@ def main():
            "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "e2e": e2e,
            "roofline": roof, "cpu_baseline": cpu,
            "kernels_ms": {k: v[1] / v[0] for k, v in prof.items()},
-           "latency": lat}
+           "latency": lat, "closed_loop": clo}
     if gather_ms is not None:
         out["final_allgather_ms"] = gather_ms
     print(json.dumps(out), flush=True)
@@ -420,6 +424,43 @@ def latency_sweep(P, torch, dev, horizons, reps, warm=30):
     return {"metric": "p50 single-solve latency vs horizon N (B=1, config 2, full SQP step)", "unit": "us",
             "timing": "CUDA-graph replay of pdilqr_step, CUDA events per replay (device); e2e = wall time of "
                       "pdilqr_tick_host + stream sync (host)", "per_dtype": out}
+
+
+def closed_loop_bench(P, torch, dev, B, N, ticks, warm=5):
+    """NEXT-1, Table I: B environments, each with its own SRBD MPC,
+    one SQP iteration per control tick + RK4 SRBD plant + warm-start shift, all on the GPU.
+    Real-time factor = simulated seconds (all envs) per wall second, timed with CUDA events over
+    `ticks` ticks; control at 50 Hz (1 node/tick) and 25 Hz (2 nodes/tick, 20 ms nodes)."""
+    out = {}
+    for k, hz in ((1, 50), (2, 25)):
+        L = synth.srbd_problem(B, N + k * (ticks + warm) + 1, seed=synth.BASE_SEED + 7)
+        f32 = lambda a: torch.from_numpy(np.ascontiguousarray(a if a.dtype == np.uint8 else a.astype(np.float32))).to(dev)
+        h = P.PdIlqr(N=N, n=12, m=12, batch=B, dtype=torch.float32, model="srbd", srbd=L["params"], device=dev.index)
+        ref = {key: f32(L[key]) for key in ("x_ref", "u_ref", "contact", "feet")}
+        it0 = {"x": f32(L["x"][:, :N + 2]), "u": f32(L["u"][:, :N + 1]), "lam": f32(L["lam"][:, :N + 2])}
+        cl = P.ClosedLoop(h, ref, it0, f32(L["x0"]), nodes_per_tick=k)
+        for _ in range(warm):
+            cl.tick()
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(ticks):
+            cl.tick()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1)
+        sim_s = B * ticks * k * float(L["params"]["dt"])
+        vref = ref["x_ref"][:, cl.node, 6:8]
+        verr = (cl.x_plant[:, 6:8] - vref).abs().mean().item()
+        out[f"{hz}hz"] = {"envs": B, "control_hz": hz, "ticks": ticks, "ms_per_tick": ms / ticks,
+                          "rtf": sim_s / (ms / 1e3), "rtf_per_env": sim_s / B / (ms / 1e3),
+                          "mean_abs_v_err_final": verr,
+                          "failed_envs": int((cl.stats["info"] != 0).sum().item())}
+        del cl, h
+    return {"what": "closed-loop RTI: step + RK4 SRBD plant + shift per node on GPU (fp32, N=%d); rtf = "
+                    "simulated env-seconds per wall second (Table I reading R23)" % N,
+            "paper_table1_rtf": {"50hz": 370, "25hz": 570, "note": "RTX 3080 + i7-13700KF, JAX + MJX simulator included; context only (P:426-446)"},
+            **out}
 
 
 def h_chunk(args, B, N):

@@ -160,6 +160,20 @@ pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *
                                void *u0_host, void *cost_host, void *theta_host, void *alpha_host,
                                int32_t *accepted_host, int32_t *info_host, void *stream);
 
+/* Closed-loop RTI support (one SQP iteration per control tick, warm-started "with the
+ * previous prediction just shifted by one time-step"; SRBD handles).
+ * pdilqr_shift: x_i <- x_{i+1}, u_i <- u_{i+1}, lam_i <- lam_{i+1} in place, last entries kept.
+ * The caller advances x0, x_ref, u_ref, contact and feet for the new tick. */
+pdilqr_status pdilqr_shift(pdilqr_handle h, pdilqr_iterate *it, void *stream);
+
+/* Batched SRBD plant for closed-loop simulation: integrates the handle's continuous SRBD dynamics
+ * (classical RK4, `substeps` steps over dt) from x_plant[B][12] (updated in place) under the
+ * zero-order-hold input u_hold[B][12] (typically u[:,0,:] of the last step), with the stage-0
+ * contacts and footholds of `it` and an optional external world force ext_force[B][3] on the CoM
+ * (NULL = none; e.g. the 50 N push of P:388).  Arrays in the handle's dtype, device pointers. */
+pdilqr_status pdilqr_srbd_plant(pdilqr_handle h, const pdilqr_iterate *it, void *x_plant, const void *u_hold,
+                                const void *ext_force, double dt, int32_t substeps, void *stream);
+
 /* Per-kernel timing: when enabled, every kernel launch of this handle is bracketed by CUDA
  * events recorded on the launch stream (host-side bookkeeping; events are created lazily and
  * owned by the handle).  Enabling/disabling clears the records. */

@@ -85,6 +85,7 @@ def lib():
         L.oracle_srbd_step.argtypes = [PP, i, i, d, d] + [_dp] * 6 + [_up, _dp] + [_dp] * 4
         L.oracle_srbd_step.restype = i
         L.oracle_srbd_step_batch.argtypes = [PP, i, i, i, d, d] + [_dp] * 6 + [_up, _dp, _dp, i]
+        L.oracle_srbd_plant.argtypes = [PP, _dp, _dp, _dp, _up, C.c_void_p, d, i, _dp]
         L.oracle_max_threads.restype = i
         _lib = L
     return _lib
@@ -243,3 +244,60 @@ def srbd_step(prob: dict, n_alpha=10, c1=1e-4, theta_max=0.0, nthreads: int | No
                                  _c(prob["x_ref"]), _uref(prob), _c(prob["contact"], np.uint8),
                                  _c(prob["feet"]), st, nthreads or max_threads())
     return st
+
+
+def srbd_plant(params: dict, x, u, feet, contact, F_ext=None, dt=0.02, substeps=4):
+    """One closed-loop plant step (RK4 of the SRBD dynamics + external CoM force)."""
+    out = np.zeros(12)
+    fe = None if F_ext is None else _c(F_ext)
+    lib().oracle_srbd_plant(C.byref(SrbdParams.from_dict(params)), _c(x), _c(u), _c(feet),
+                            _c(contact, np.uint8), None if fe is None else fe.ctypes.data,
+                            float(dt), int(substeps), out)
+    return out
+
+
+def warm_start_shift(a):
+    """SPEC S:343-350 / P:315: a_i <- a_{i+1} along the stage axis (axis -2), last entry kept."""
+    out = np.array(a, copy=True)
+    out[..., :-1, :] = a[..., 1:, :]
+    return out
+
+
+def closed_loop(prob_long: dict, N: int, ticks: int, nodes_per_tick: int = 1, substeps: int = 4, push=None,
+                n_alpha=10, c1=1e-4, theta_max=0.0):
+    """Closed-loop RTI on the oracle.  Each control tick: x0 <- plant state,
+    one SQP iteration; then for each of the k = nodes_per_tick nodes until the next tick: the RK4
+    plant integrates one node (dt, `substeps` steps) under the plan's first control u_0 with the
+    node's contacts/footholds, the iterate is shifted by one node and the reference window slides
+    by one node (k = 1: 50 Hz; k = 2: 25 Hz on the same 20 ms nodes, plan played back between
+    ticks).  prob_long holds references for >= N + k*ticks stages.  push(node) -> F_ext[B][3] or
+    None.  Returns {"x_plant": [B][k*ticks+1][12] (per node), "stats": [B][ticks][5]}."""
+    prm = prob_long["params"]
+    k = int(nodes_per_tick)
+    B = prob_long["x0"].shape[0]
+    win = lambda a, o, L: np.ascontiguousarray(a[:, o:o + L])
+    it = {"params": prm, "x": win(prob_long["x"], 0, N + 2), "u": win(prob_long["u"], 0, N + 1),
+          "lam": win(prob_long["lam"], 0, N + 2)}
+    xp = np.array(prob_long["x0"], dtype=np.float64)
+    xs, sts = [xp.copy()], []
+
+    def slide(o):
+        it.update(x_ref=win(prob_long["x_ref"], o, N + 2), u_ref=win(prob_long["u_ref"], o, N + 1),
+                  contact=win(prob_long["contact"], o, N + 1), feet=win(prob_long["feet"], o, N + 1))
+
+    slide(0)
+    node = 0
+    for t in range(ticks):
+        it["x0"] = xp.copy()
+        sts.append(srbd_step(it, n_alpha, c1, theta_max))
+        for _ in range(k):
+            F = push(node) if push is not None else None
+            for b in range(B):
+                xp[b] = srbd_plant(prm, xp[b], it["u"][b, 0], it["feet"][b, 0], it["contact"][b, 0],
+                                   None if F is None else F[b], prm["dt"], substeps)
+            for key in ("x", "u", "lam"):
+                it[key] = np.ascontiguousarray(warm_start_shift(it[key]))
+            node += 1
+            slide(node)
+            xs.append(xp.copy())
+    return {"x_plant": np.stack(xs, 1), "stats": np.stack(sts, 1)}

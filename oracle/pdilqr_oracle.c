@@ -762,6 +762,32 @@ void oracle_srbd_linearize_batch(const oracle_srbd_params *P, int Bn, int N,
             r + b * S1 * NU, Pt + (size_t)b * NX * NX, pt + (size_t)b * NX, dx0 + (size_t)b * NX);
 }
 
+/* Closed-loop plant ("plant = RK4 integration of the same SRBD model";
+ * P:388 push disturbance): classical RK4 of xdot = f(x,u) + (0,0,0, 0,0,0, F_ext/m, 0,0,0),
+ * `sub` steps of h = dt/sub, u / feet / contact held constant (zero-order hold).            */
+void oracle_srbd_plant(const oracle_srbd_params *P, const double *x0, const double *u,
+                       const double *feet, const uint8_t *contact, const double *F_ext /* [3] or NULL */,
+                       double dt, int sub, double *x_out) {
+    double x[NX], k1[NX], k2[NX], k3[NX], k4[NX], y[NX];
+    memcpy(x, x0, sizeof x);
+    const double h = dt / sub;
+    for (int s = 0; s < sub; ++s) {
+        oracle_srbd_f(P, x, u, feet, contact, k1);
+        if (F_ext) for (int a = 0; a < 3; ++a) k1[6 + a] += F_ext[a] / P->mass;
+        for (int r = 0; r < NX; ++r) y[r] = x[r] + 0.5 * h * k1[r];
+        oracle_srbd_f(P, y, u, feet, contact, k2);
+        if (F_ext) for (int a = 0; a < 3; ++a) k2[6 + a] += F_ext[a] / P->mass;
+        for (int r = 0; r < NX; ++r) y[r] = x[r] + 0.5 * h * k2[r];
+        oracle_srbd_f(P, y, u, feet, contact, k3);
+        if (F_ext) for (int a = 0; a < 3; ++a) k3[6 + a] += F_ext[a] / P->mass;
+        for (int r = 0; r < NX; ++r) y[r] = x[r] + h * k3[r];
+        oracle_srbd_f(P, y, u, feet, contact, k4);
+        if (F_ext) for (int a = 0; a < 3; ++a) k4[6 + a] += F_ext[a] / P->mass;
+        for (int r = 0; r < NX; ++r) x[r] += h / 6.0 * (k1[r] + 2.0 * k2[r] + 2.0 * k3[r] + k4[r]);
+    }
+    memcpy(x_out, x, sizeof x);
+}
+
 int oracle_max_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

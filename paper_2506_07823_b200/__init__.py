@@ -4,5 +4,6 @@ The compute path is libpdilqr.so (CUDA kernels behind the C ABI of include/pdilq
 package is a thin ctypes binding.  There is no CPU fallback.
 """
 from .pdilqr import PdIlqr, PdilqrError, lib, LIB_PATH, EXPORTED  # noqa: F401
+from .closed_loop import ClosedLoop  # noqa: F401
 
-__all__ = ["PdIlqr", "PdilqrError", "lib", "LIB_PATH", "EXPORTED"]
+__all__ = ["PdIlqr", "PdilqrError", "ClosedLoop", "lib", "LIB_PATH", "EXPORTED"]

@@ -866,6 +866,45 @@ pdilqr_status pdilqr_step(pdilqr_handle h, pdilqr_iterate *it, pdilqr_stats *sta
     return run_step<double>(h, it, stats, dir, st);
 }
 
+pdilqr_status pdilqr_shift(pdilqr_handle h, pdilqr_iterate *it, void *stream) {
+    pdilqr_status s = check_iter(h, it);
+    if (s != PDILQR_OK) return s;
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = h->cfg.batch, N = h->cfg.N;
+    const long tot = (long)B * 36;
+    h->launches = 1;
+    if (h->cfg.dtype == PDILQR_F32) {
+        Prof pf(h, "k_srbd_shift", st);
+        k_srbd_shift<float><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(iter_of<float>(it), B, N);
+    } else {
+        Prof pf(h, "k_srbd_shift", st);
+        k_srbd_shift<double><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(iter_of<double>(it), B, N);
+    }
+    return cuda_check("shift launch");
+}
+
+pdilqr_status pdilqr_srbd_plant(pdilqr_handle h, const pdilqr_iterate *it, void *x_plant, const void *u_hold,
+                                const void *ext_force, double dt, int32_t substeps, void *stream) {
+    pdilqr_status s = check_iter(h, it);
+    if (s != PDILQR_OK) return s;
+    if (!x_plant || !u_hold || substeps < 1 || !(dt >= 0)) return fail(PDILQR_ERR_INVALID_ARG, "invalid plant arguments");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = h->cfg.batch, N = h->cfg.N;
+    h->launches = 1;
+    if (h->cfg.dtype == PDILQR_F32) {
+        Prof pf(h, "k_srbd_plant", st);
+        k_srbd_plant<float><<<(B + 127) / 128, 128, 0, st>>>(h->K, iter_of<float>(it), B, N, (float *)x_plant,
+                                                            (const float *)u_hold, (const float *)ext_force, (float)dt, substeps);
+    } else {
+        Prof pf(h, "k_srbd_plant", st);
+        k_srbd_plant<double><<<(B + 127) / 128, 128, 0, st>>>(h->K, iter_of<double>(it), B, N, (double *)x_plant,
+                                                             (const double *)u_hold, (const double *)ext_force, dt, substeps);
+    }
+    return cuda_check("plant launch");
+}
+
 pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *x0_host, void *u0_host, void *cost_host,
                                void *theta_host, void *alpha_host, int32_t *accepted_host, int32_t *info_host,
                                void *stream) {

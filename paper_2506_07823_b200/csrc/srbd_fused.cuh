@@ -766,4 +766,61 @@ __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> i
     }
 }
 
+// ------------------------------------------------------------- closed loop (NEXT-1)
+// Warm start of the next tick: x_i <- x_{i+1}, u_i <- u_{i+1}, lam_i <- lam_{i+1}; last entries kept.
+// One thread per (instance, array, component) walks the stages in ascending order (in place).
+template <typename T>
+__global__ void k_srbd_shift(SrbdIter<T> it, int B, int N) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long)B * 36) return;
+    const int b = (int)(t / 36), a = (int)(t % 36) / 12, k = (int)(t % 12);
+    T *base = a == 0 ? const_cast<T *>(it.x) + (size_t)b * (N + 2) * 12
+            : a == 1 ? const_cast<T *>(it.u) + (size_t)b * (N + 1) * 12
+                     : const_cast<T *>(it.lam) + (size_t)b * (N + 2) * 12;
+    const int len = a == 1 ? N + 1 : N + 2;
+    for (int i = 0; i + 1 < len; ++i) base[(size_t)i * 12 + k] = base[(size_t)(i + 1) * 12 + k];
+}
+
+// Batched SRBD plant: classical RK4 of the continuous dynamics (same model as the MPC), `sub`
+// substeps over dt, zero-order-hold input u_hold, stage-0 contacts / footholds, optional external
+// world force on the CoM.  One thread per instance.
+template <typename T>
+__global__ void k_srbd_plant(SrbdConst K, SrbdIter<T> it, int B, int N, T *xp, const T *uh, const T *ext, T dt, int sub) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    T x[12], u[12], fe[12];
+    uint8_t con[4];
+#pragma unroll
+    for (int k = 0; k < 12; ++k) { x[k] = xp[(size_t)b * 12 + k]; u[k] = uh[(size_t)b * 12 + k]; fe[k] = it.feet[(size_t)b * (N + 1) * 12 + k]; }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) con[j] = it.con[(size_t)b * (N + 1) * 4 + j];
+    T Fe[3] = {T(0), T(0), T(0)};
+    if (ext) for (int c = 0; c < 3; ++c) Fe[c] = ext[(size_t)b * 3 + c];
+    auto f = [&](const T *xs, T *out) {
+        SrbdEval<T> ev;
+        ev.init(K, xs, u, fe, con);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) out[k] = ev.f(K, xs, k);
+        for (int c = 0; c < 3; ++c) out[6 + c] += Fe[c] / T(K.mass);
+    };
+    const T h = dt / T(sub);
+    for (int s = 0; s < sub; ++s) {
+        T k1[12], k2[12], k3[12], k4[12], y[12];
+        f(x, k1);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) y[k] = x[k] + T(0.5) * h * k1[k];
+        f(y, k2);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) y[k] = x[k] + T(0.5) * h * k2[k];
+        f(y, k3);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) y[k] = x[k] + h * k3[k];
+        f(y, k4);
+#pragma unroll
+        for (int k = 0; k < 12; ++k) x[k] += h / T(6) * (k1[k] + T(2) * k2[k] + T(2) * k3[k] + k4[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 12; ++k) xp[(size_t)b * 12 + k] = x[k];
+}
+
 }  // namespace pdilqr

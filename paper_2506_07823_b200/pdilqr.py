@@ -24,7 +24,8 @@ STATUS = {0: "PDILQR_OK", 1: "PDILQR_ERR_INVALID_ARG", 2: "PDILQR_ERR_DIM", 3: "
 
 EXPORTED = ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
             "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host", "pdilqr_last_launch_count",
-            "pdilqr_last_error", "pdilqr_abi_version", "pdilqr_profile", "pdilqr_profile_read")
+            "pdilqr_last_error", "pdilqr_abi_version", "pdilqr_profile", "pdilqr_profile_read",
+            "pdilqr_shift", "pdilqr_srbd_plant")
 
 
 class SrbdParams(C.Structure):
@@ -84,6 +85,10 @@ def lib():
         L.pdilqr_profile.restype = st
         L.pdilqr_profile_read.argtypes = [vp, i32, C.POINTER(C.c_char_p), C.POINTER(i32), C.POINTER(C.c_double)]
         L.pdilqr_profile_read.restype = i32
+        L.pdilqr_shift.argtypes = [vp, C.POINTER(Iterate), vp]
+        L.pdilqr_shift.restype = st
+        L.pdilqr_srbd_plant.argtypes = [vp, C.POINTER(Iterate), vp, vp, vp, C.c_double, i32, vp]
+        L.pdilqr_srbd_plant.restype = st
         for f in ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
                   "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host"):
             getattr(L, f).restype = st
@@ -247,6 +252,21 @@ class PdIlqr:
                                       _ptr(stats_host["cost"]), _ptr(stats_host["theta"]),
                                       _ptr(stats_host["alpha"]), _ptr(stats_host["accepted"]),
                                       _ptr(stats_host["info"]), self._stream(stream)))
+
+    def shift(self, it: dict, stream=None):
+        """pdilqr_shift: warm start for the next tick."""
+        itc = self._iterate(it)
+        _check(lib().pdilqr_shift(self._h, C.byref(itc), self._stream(stream)))
+
+    def plant(self, it: dict, x_plant, u_hold, ext_force=None, dt: float = 0.02, substeps: int = 4, stream=None):
+        """pdilqr_srbd_plant: RK4 SRBD plant step (closed-loop simulation), x_plant updated in place."""
+        itc = self._iterate(it)
+        self._check_t(x_plant, (self.batch, 12))
+        self._check_t(u_hold, (self.batch, 12))
+        if ext_force is not None:
+            self._check_t(ext_force, (self.batch, 3))
+        _check(lib().pdilqr_srbd_plant(self._h, C.byref(itc), _ptr(x_plant), _ptr(u_hold), _ptr(ext_force),
+                                       float(dt), int(substeps), self._stream(stream)))
 
     def profile(self, enable: bool = True):
         """Enable / disable per-kernel CUDA-event timing inside the library."""

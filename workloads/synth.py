@@ -172,21 +172,22 @@ def _rotz(yaw):
 
 
 def _ref_pos(p0, yaw0, wz, vb, t):
-    """Reference CoM xy at time t for a constant body-frame velocity vb and yaw rate wz:
-    p0 + int_0^t Rz(yaw0 + wz s) vb ds (closed form)."""
+    """Reference CoM xy at times t (array) for a constant body-frame velocity vb and yaw rate wz:
+    p0 + int_0^t Rz(yaw0 + wz s) vb ds (closed form).  Returns [len(t)][2]."""
+    t = np.asarray(t, dtype=np.float64)
     if abs(wz) < 1e-9:
-        return p0 + t * (_rotz(yaw0) @ vb)
+        return p0[None, :] + t[:, None] * (_rotz(yaw0) @ vb)[None, :]
     s0, c0 = math.sin(yaw0), math.cos(yaw0)
-    s1, c1 = math.sin(yaw0 + wz * t), math.cos(yaw0 + wz * t)
+    s1, c1 = np.sin(yaw0 + wz * t), np.cos(yaw0 + wz * t)
     ic, is_ = (s1 - s0) / wz, (c0 - c1) / wz            # int cos, int sin
-    return p0 + np.array([ic * vb[0] - is_ * vb[1], is_ * vb[0] + ic * vb[1]])
+    return p0[None, :] + np.stack([ic * vb[0] - is_ * vb[1], is_ * vb[0] + ic * vb[1]], axis=1)
 
 
 def srbd_problem(B: int, N: int = 50, seed: int = BASE_SEED, first: int = 0, params: dict | None = None,
-                 randomize: bool = True):
+                 randomize: bool = True, v_cmd=(0.5, 0.0)):
     """SRBD trot MPC instances (configs 2/3).
 
-    Config 2 (``randomize=False``): v_cmd = (0.5, 0) m/s, yaw rate 0, gait phase 0.
+    Config 2 (``randomize=False``): v_cmd = (0.5, 0) m/s (overridable), yaw rate 0, gait phase 0.
     Config 3 (``randomize=True``): per instance v_cmd ~ U(-0.5, 0.5)^2, yaw rate ~ U(-0.5, 0.5),
     gait phase ~ U(0, 1), initial yaw ~ U(-pi, pi), initial xy ~ U(-1, 1)^2.
     Diagonal trot (FL+RR / FR+RL), period 0.4 s, duty 0.5; footholds at mid-stance hip positions
@@ -207,9 +208,10 @@ def srbd_problem(B: int, N: int = 50, seed: int = BASE_SEED, first: int = 0, par
             phase = rng.uniform(0.0, 1.0); yaw0 = rng.uniform(-math.pi, math.pi)
             p0 = rng.uniform(-1.0, 1.0, 2)
         else:
-            vcmd = np.array([0.5, 0.0]); wz = 0.0; phase = 0.0; yaw0 = 0.0; p0 = np.zeros(2)
+            vcmd = np.array(v_cmd, dtype=np.float64); wz = 0.0; phase = 0.0; yaw0 = 0.0; p0 = np.zeros(2)
         yaw = yaw0 + wz * t_nodes
-        vel = np.stack([_rotz(yw) @ vcmd for yw in yaw])            # world-frame xy velocity
+        cy, sy = np.cos(yaw), np.sin(yaw)
+        vel = np.stack([cy * vcmd[0] - sy * vcmd[1], sy * vcmd[0] + cy * vcmd[1]], axis=1)  # world xy
         pos = p0 + np.concatenate([np.zeros((1, 2)), np.cumsum(vel[:-1] * dt, axis=0)])
         x_ref[b, :, 0:2] = pos
         x_ref[b, :, 2] = NOMINAL_HEIGHT
@@ -223,24 +225,21 @@ def srbd_problem(B: int, N: int = 50, seed: int = BASE_SEED, first: int = 0, par
         contact[b, :, 1] = ~pairA; contact[b, :, 2] = ~pairA
         # footholds: hip position of the reference at the middle of the stance phase that
         # contains (or, for swing stages, follows) stage i
-        for i in range(S1):
-            cyc = phase + t_nodes[i] / GAIT_PERIOD
-            for j in range(4):
-                in_a = j in (0, 3)
-                start = math.floor(cyc) + (0.0 if in_a else 0.5)
-                if start > cyc:
-                    start -= 1.0
-                if cyc - start >= 0.5:               # in swing: next stance phase
-                    start += 1.0
-                t_mid = (start + 0.25 - phase) * GAIT_PERIOD
-                yaw_m = yaw0 + wz * t_mid
-                p_m = _ref_pos(p0, yaw0, wz, vcmd, t_mid)  # reference CoM position at mid-stance
-                feet[b, i, j, 0:2] = p_m + _rotz(yaw_m) @ HIP_OFFSETS[j]
-                feet[b, i, j, 2] = 0.0
-            nst = int(contact[b, i].sum())
-            for j in range(4):
-                if contact[b, i, j]:
-                    u_ref[b, i, 3 * j + 2] = mass * g / nst
+        cyc = phase + t_nodes[:S1] / GAIT_PERIOD
+        for j in range(4):
+            in_a = j in (0, 3)
+            start = np.floor(cyc) + (0.0 if in_a else 0.5)
+            start = np.where(start > cyc, start - 1.0, start)
+            start = np.where(cyc - start >= 0.5, start + 1.0, start)   # in swing: next stance phase
+            t_mid = (start + 0.25 - phase) * GAIT_PERIOD
+            yaw_m = yaw0 + wz * t_mid
+            p_m = _ref_pos(p0, yaw0, wz, vcmd, t_mid)                # reference CoM at mid-stance
+            hx, hy = HIP_OFFSETS[j]
+            feet[b, :, j, 0] = p_m[:, 0] + np.cos(yaw_m) * hx - np.sin(yaw_m) * hy
+            feet[b, :, j, 1] = p_m[:, 1] + np.sin(yaw_m) * hx + np.cos(yaw_m) * hy
+            feet[b, :, j, 2] = 0.0
+        nst = np.maximum(contact[b].sum(axis=1), 1).astype(np.float64)
+        u_ref[b, :, 2::3] = contact[b] * (mass * g / nst)[:, None]
         sig = np.array([0.02] * 3 + [0.05] * 3 + [0.1] * 3 + [0.1] * 3)
         x0[b] = x_ref[b, 0] + sig * rng.standard_normal(12)
     x = x_ref.copy()

@@ -160,6 +160,20 @@ pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *
                                void *u0_host, void *cost_host, void *theta_host, void *alpha_host,
                                int32_t *accepted_host, int32_t *info_host, void *stream);
 
+/* Multi-iteration solve (artifact plumbing around the one-iteration RTI of P:315;
+ * SRBD handles).  Repeats pdilqr_step until every instance has converged or failed, or max_iters
+ * iterations ran.  Instance b converges at iteration k when that iteration's accepted step has
+ * theta <= tol and ||alpha (dx, du)||_inf <= tol; it is then frozen (later iterations neither
+ * update it nor overwrite its stats with a step: they report its iterate with alpha = 0,
+ * accepted = 0).  An instance whose info != 0 stops at that iteration.
+ *   stats      as pdilqr_step, of each instance's last iteration (device, required)
+ *   iters      device int32[B] or NULL: k > 0 converged at iteration k, -k stopped by a failure
+ *              at iteration k (see stats.info), 0 = not converged within max_iters
+ *   iters_run  host int32 or NULL: iterations executed (0 when max_iters = 0: iterate unchanged)
+ * Host-synchronous: one 4-byte device->host read per iteration. */
+pdilqr_status pdilqr_solve(pdilqr_handle h, pdilqr_iterate *it, int32_t max_iters, double tol, pdilqr_stats *stats,
+                           int32_t *iters, int32_t *iters_run, void *stream);
+
 /* Closed-loop RTI support (one SQP iteration per control tick, warm-started "with the
  * previous prediction just shifted by one time-step"; SRBD handles).
  * pdilqr_shift: x_i <- x_{i+1}, u_i <- u_{i+1}, lam_i <- lam_{i+1} in place, last entries kept.

@@ -301,3 +301,26 @@ def closed_loop(prob_long: dict, N: int, ticks: int, nodes_per_tick: int = 1, su
             slide(node)
             xs.append(xp.copy())
     return {"x_plant": np.stack(xs, 1), "stats": np.stack(sts, 1)}
+
+
+def srbd_solve(prob: dict, max_iters: int, tol: float, n_alpha=10, c1=1e-4, theta_max=0.0):
+    """Multi-iteration solve, per instance: repeat the SQP iteration until the
+    accepted step has theta <= tol and ||alpha (dx, du)||_inf <= tol (converged at k), or the
+    iteration fails (info != 0: stopped, -k), or max_iters.  In place on prob x/u/lam.
+    Returns (iters[B], stats[B][5] of each instance's last iteration)."""
+    Bn = prob["x"].shape[0]
+    iters = np.zeros(Bn, np.int32)
+    st = np.zeros((Bn, 5))
+    for b in range(Bn):
+        for k in range(1, max_iters + 1):
+            x, u, lam, s, dx, du, _ = srbd_step_single(prob, b, n_alpha, c1, theta_max)
+            prob["x"][b], prob["u"][b], prob["lam"][b] = x, u, lam
+            st[b] = s
+            step = s[2] * max(np.abs(dx).max(), np.abs(du).max())
+            if s[4] != 0:
+                iters[b] = -k
+                break
+            if s[1] <= tol and step <= tol:
+                iters[b] = k
+                break
+    return iters, st

@@ -63,6 +63,7 @@ bool pick_variant(int n, int m, Variant &v, int &NX, int &NU) {
 struct Layout {
     size_t elems, vslots, Pp, Kk, tel, tslots, dxw, fail, nonfin, pre, info_tmp, stats;
     size_t kinds_b, kinds_f, ls_part, ls_cnt;  // grid-scan slot kinds, multi-block line-search scratch
+    size_t conv, active;                       // pdilqr_solve per-instance state, active counter
     size_t qp[11];  // SRBD internal QP buffers (A, Bm, c, Q, R, S, q, r, Pt, pt, dx0)
     size_t dir[3];  // internal direction (dx, du, dlam)
     size_t total;
@@ -90,6 +91,10 @@ struct pdilqr_ctx {
     int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
     int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
+    // pdilqr_solve in progress: convergence bookkeeping handed to the update kernels
+    int32_t *sc_conv = nullptr, *sc_active = nullptr;
+    double sc_tol = 0.0;
+    int sc_iter = 0;
     // per-kernel CUDA-event timing (host bookkeeping only; off unless pdilqr_profile(h, 1))
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -218,6 +223,8 @@ Layout make_layout(const pdilqr_config *c, int NX, int NU, int esz, int chunk, i
     L.kinds_f = take(B * (size_t)Pf * 4);
     L.ls_part = take(B * (size_t)((N + 2 + 31) / 32) * 34 * 8);
     L.ls_cnt = take(B * 4);
+    L.conv = take(B * 4);
+    L.active = take(8);
     const size_t n = c->n, m = c->m;
     if (c->model == PDILQR_MODEL_SRBD) {
         const size_t sz[11] = {(N + 1) * n * n, (N + 1) * n * m, (N + 1) * n, (N + 1) * n * n, (N + 1) * m * m,
@@ -465,6 +472,16 @@ SrbdIter<T> iter_of(const pdilqr_iterate *it) {
 }
 
 template <typename T>
+SrbdIter<T> iter_of(const pdilqr_iterate *it, const pdilqr_ctx *h) {
+    SrbdIter<T> r = iter_of<T>(it);
+    r.conv = h->sc_conv;
+    r.active = h->sc_active;
+    r.tol = h->sc_tol;
+    r.iter = h->sc_iter;
+    return r;
+}
+
+template <typename T>
 pdilqr_status run_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArgs<T> &outq, int32_t *pre,
                             cudaStream_t st) {
     const int B = h->cfg.batch, N = h->cfg.N;
@@ -523,7 +540,7 @@ pdilqr_status run_step_split(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
         Prof pf(h, "k_srbd_fwd_ls", st);
         constexpr int WPB = LsWarps<T>::value;
-        k_srbd_fwd_ls<T, 4><<<(B + WPB - 1) / WPB, 32 * WPB, 0, st>>>(h->K, iter_of<T>(it), B, N, ws, dx, du, dl, nullptr, so,
+        k_srbd_fwd_ls<T, 4><<<(B + WPB - 1) / WPB, 32 * WPB, 0, st>>>(h->K, iter_of<T>(it, h), B, N, ws, dx, du, dl, nullptr, so,
                                                                        pre);
     }
     h->launches += 4;
@@ -562,7 +579,7 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         Prof pf(h, "k_srbd_fwd_ls", st);
         auto go = [&](auto kern) {
             constexpr int WPB = LsWarps<T>::value;
-            kern<<<(B + WPB - 1) / WPB, 32 * WPB, 0, st>>>(h->K, iter_of<T>(it), B, N, ws, dx, du, dl, info_tmp, so, nullptr);
+            kern<<<(B + WPB - 1) / WPB, 32 * WPB, 0, st>>>(h->K, iter_of<T>(it, h), B, N, ws, dx, du, dl, info_tmp, so, nullptr);
         };
         switch (h->occ_ls) {
             case 3: go(k_srbd_fwd_ls<T, 3>); break;
@@ -628,11 +645,11 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
         int *cnt = reinterpret_cast<int *>(h->ws + h->lay.ls_cnt);
         cudaMemsetAsync(cnt, 0, (size_t)B * 4, st);
         Prof pf(h, "k_srbd_ls_multi", st);
-        k_srbd_ls_multi<T><<<dim3(S, B), 32, 0, st>>>(h->K, iter_of<T>(it), B, N, out.dx, out.du, out.dlam, info_tmp, so,
+        k_srbd_ls_multi<T><<<dim3(S, B), 32, 0, st>>>(h->K, iter_of<T>(it, h), B, N, out.dx, out.du, out.dlam, info_tmp, so,
                                                       part, cnt);
     } else {
         Prof pf(h, "k_srbd_linesearch", st);
-        k_srbd_linesearch<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it), B, N, out.dx, out.du, out.dlam, info_tmp, so);
+        k_srbd_linesearch<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it, h), B, N, out.dx, out.du, out.dlam, info_tmp, so);
     }
     h->launches += 1;
     return cuda_check("step launch");
@@ -864,6 +881,43 @@ pdilqr_status pdilqr_step(pdilqr_handle h, pdilqr_iterate *it, pdilqr_stats *sta
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (h->cfg.dtype == PDILQR_F32) return run_step<float>(h, it, stats, dir, st);
     return run_step<double>(h, it, stats, dir, st);
+}
+
+pdilqr_status pdilqr_solve(pdilqr_handle h, pdilqr_iterate *it, int32_t max_iters, double tol, pdilqr_stats *stats,
+                           int32_t *iters, int32_t *iters_run, void *stream) {
+    pdilqr_status s = check_iter(h, it);
+    if (s != PDILQR_OK) return s;
+    if (!stats || !stats->cost || !stats->theta || !stats->alpha || !stats->accepted || !stats->info)
+        return fail(PDILQR_ERR_INVALID_ARG, "NULL stats array");
+    if (max_iters < 0 || !(tol >= 0.0)) return fail(PDILQR_ERR_INVALID_ARG, "max_iters < 0 or tol < 0");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int B = h->cfg.batch;
+    int32_t *conv = reinterpret_cast<int32_t *>(h->ws + h->lay.conv);
+    int32_t *active = reinterpret_cast<int32_t *>(h->ws + h->lay.active);
+    cudaMemsetAsync(conv, 0, (size_t)B * 4, st);
+    int total = 0, run = 0;
+    for (int k = 1; k <= max_iters; ++k) {
+        cudaMemsetAsync(active, 0, 4, st);
+        h->sc_conv = conv;
+        h->sc_active = active;
+        h->sc_tol = tol;
+        h->sc_iter = k;
+        h->launches = 0;
+        s = (h->cfg.dtype == PDILQR_F32) ? run_step<float>(h, it, stats, nullptr, st) : run_step<double>(h, it, stats, nullptr, st);
+        h->sc_conv = h->sc_active = nullptr;
+        total += h->launches;
+        if (s != PDILQR_OK) return s;
+        run = k;
+        int32_t act = 0;
+        cudaMemcpyAsync(&act, active, 4, cudaMemcpyDeviceToHost, st);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check("solve sync");
+        if (act == 0) break;
+    }
+    if (iters) cudaMemcpyAsync(iters, conv, (size_t)B * 4, cudaMemcpyDeviceToDevice, st);
+    if (iters_run) *iters_run = run;
+    h->launches = total;
+    return cuda_check("solve");
 }
 
 pdilqr_status pdilqr_shift(pdilqr_handle h, pdilqr_iterate *it, void *stream) {

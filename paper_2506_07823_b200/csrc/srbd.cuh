@@ -252,6 +252,12 @@ struct SrbdIter {
     const T *x, *u, *lam, *x0, *xref, *uref;
     const uint8_t *con;
     const T *feet;
+    // pdilqr_solve bookkeeping (nullptr for a plain step): conv[b] = 0 active, k > 0 converged at
+    // iteration k (frozen), -k stopped by a failure (info != 0) at iteration k; *active counts the
+    // instances still active after this iteration.
+    int32_t *conv = nullptr, *active = nullptr;
+    double tol = 0.0;
+    int iter = 0;
 };
 
 template <typename T>
@@ -345,6 +351,59 @@ struct LsOut {
     T *cost, *theta, *alpha;
     int32_t *accepted, *info;
 };
+
+// Linear update (Eq. 16) x, u, lam += alpha (dx, du, dlam) of instance b by one warp (coalesced),
+// the step statistics, and the pdilqr_solve convergence test (theta <= tol and
+// ||alpha (dx, du)||_inf <= tol).  Instances frozen by an earlier convergence or failure are not updated and
+// report the current iterate (alpha = 0, accepted = 0).
+template <typename T>
+__device__ __forceinline__ void commit_step(const SrbdIter<T> &it, const LsOut<T> &so, int b, int N, int lane, bool acc,
+                                            T alpha, double J0, double th0, double Jb, double thb, int info,
+                                            const T *Dx, const T *Du, const T *Dl) {
+    const bool frozen = it.conv && it.conv[b] != 0;
+    double smax = 0.0;
+    if (acc && !frozen) {
+        T *xw = const_cast<T *>(it.x) + (size_t)b * (N + 2) * 12;
+        T *uw = const_cast<T *>(it.u) + (size_t)b * (N + 1) * 12;
+        T *lw = const_cast<T *>(it.lam) + (size_t)b * (N + 2) * 12;
+        T sm = T(0);
+        for (int t = lane; t < (N + 2) * 12; t += 32) {
+            const T sx = alpha * Dx[t];
+            xw[t] = xw[t] + sx;
+            lw[t] = lw[t] + alpha * Dl[t];
+            sm = fmax(sm, fabs(sx));
+        }
+        for (int t = lane; t < (N + 1) * 12; t += 32) {
+            const T su = alpha * Du[t];
+            uw[t] = uw[t] + su;
+            sm = fmax(sm, fabs(su));
+        }
+        smax = (double)sm;
+    }
+    if (it.conv) {
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, off));
+    }
+    if (lane == 0) {
+        if (frozen) {
+            so.cost[b] = (T)J0;
+            so.theta[b] = (T)th0;
+            so.alpha[b] = T(0);
+            so.accepted[b] = 0;
+        } else {
+            so.cost[b] = (T)Jb;
+            so.theta[b] = (T)thb;
+            so.alpha[b] = alpha;
+            so.accepted[b] = acc ? 1 : 0;
+            if (it.conv) {
+                if (info != 0) it.conv[b] = -it.iter;
+                else if (thb <= it.tol && smax <= it.tol) it.conv[b] = it.iter;
+                else atomicAdd(it.active, 1);
+            }
+        }
+        so.info[b] = info;
+    }
+}
 
 template <typename T>
 __device__ __forceinline__ double stage_eval(const SrbdConst &K, const T *x, const T *dx, const T *xn, const T *dxn,
@@ -478,21 +537,7 @@ __global__ void __launch_bounds__(128) k_srbd_linesearch(SrbdConst K, SrbdIter<T
     const int jb = acc ? __ffs(acc) - 1 : 0;                   // smallest slot = largest alpha
     const double Jb = __shfl_sync(0xffffffffu, J, jb), thb = __shfl_sync(0xffffffffu, th, jb);
     const T alpha = acc ? (T)ldexp(1.0, -(jb - 1)) : T(0);
-    if (acc) {  // in-place linear update (Eq. 16), coalesced across the warp
-        T *xw = const_cast<T *>(it.x) + (size_t)b * (N + 2) * 12;
-        T *uw = const_cast<T *>(it.u) + (size_t)b * (N + 1) * 12;
-        T *lw = const_cast<T *>(it.lam) + (size_t)b * (N + 2) * 12;
-        const T *Dl = dlam + (size_t)b * (N + 2) * 12;
-        for (int t = lane; t < (N + 2) * 12; t += 32) { xw[t] = xw[t] + alpha * Dx[t]; lw[t] = lw[t] + alpha * Dl[t]; }
-        for (int t = lane; t < (N + 1) * 12; t += 32) uw[t] = uw[t] + alpha * Du[t];
-    }
-    if (lane == 0) {
-        so.cost[b] = (T)Jb;
-        so.theta[b] = (T)thb;
-        so.alpha[b] = alpha;
-        so.accepted[b] = acc ? 1 : 0;
-        so.info[b] = info;
-    }
+    commit_step<T>(it, so, b, N, lane, acc != 0u, alpha, J0, th0, Jb, thb, info, Dx, Du, dlam + (size_t)b * (N + 2) * 12);
 }
 
 }  // namespace pdilqr

@@ -531,20 +531,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         }
     }
     const T alpha = jb >= 0 ? (T)ldexp(1.0, -(jb - 1)) : T(0);
-    if (jb >= 0) {  // x, u, lam += alpha (dx, du, dlam)  (Eq. 16), coalesced
-        T *xw = const_cast<T *>(it.x) + (size_t)b * (N + 2) * NX;
-        T *uw = const_cast<T *>(it.u) + (size_t)b * (N + 1) * NX;
-        T *lw = const_cast<T *>(it.lam) + (size_t)b * (N + 2) * NX;
-        for (int t = lane; t < (N + 2) * NX; t += 32) { xw[t] = xw[t] + alpha * Dx[t]; lw[t] = lw[t] + alpha * Dl[t]; }
-        for (int t = lane; t < (N + 1) * NX; t += 32) uw[t] = uw[t] + alpha * Du[t];
-    }
-    if (lane == 0) {
-        so.cost[b] = (T)Jb;
-        so.theta[b] = (T)thb;
-        so.alpha[b] = alpha;
-        so.accepted[b] = jb >= 0 ? 1 : 0;
-        so.info[b] = info;
-    }
+    commit_step<T>(it, so, b, N, lane, jb >= 0, alpha, J0, th0, Jb, thb, info, Dx, Du, Dl);
 }
 
 // ------------------------------------------- stage-parallel linearisation + element init
@@ -748,22 +735,8 @@ __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> i
     const int jb = acc ? __ffs(acc) - 1 : 0;
     const double Jb = __shfl_sync(0xffffffffu, J, jb), thb = __shfl_sync(0xffffffffu, th, jb);
     const T alpha = acc ? (T)ldexp(1.0, -(jb - 1)) : T(0);
-    if (acc) {
-        T *xw = const_cast<T *>(it.x) + (size_t)b * (N + 2) * NX;
-        T *uw = const_cast<T *>(it.u) + (size_t)b * (N + 1) * NX;
-        T *lw = const_cast<T *>(it.lam) + (size_t)b * (N + 2) * NX;
-        const T *Dl = dlam + (size_t)b * (N + 2) * NX;
-        for (int t = lane; t < (N + 2) * NX; t += 32) { xw[t] = xw[t] + alpha * Dx[t]; lw[t] = lw[t] + alpha * Dl[t]; }
-        for (int t = lane; t < (N + 1) * NX; t += 32) uw[t] = uw[t] + alpha * Du[t];
-    }
-    if (lane == 0) {
-        so.cost[b] = (T)Jb;
-        so.theta[b] = (T)thb;
-        so.alpha[b] = alpha;
-        so.accepted[b] = acc ? 1 : 0;
-        so.info[b] = info;
-        cnt[b] = 0;
-    }
+    commit_step<T>(it, so, b, N, lane, acc != 0u, alpha, J0, th0, Jb, thb, info, Dx, Du, dlam + (size_t)b * (N + 2) * NX);
+    if (lane == 0) cnt[b] = 0;
 }
 
 // ------------------------------------------------------------- closed loop (NEXT-1)

@@ -25,7 +25,7 @@ STATUS = {0: "PDILQR_OK", 1: "PDILQR_ERR_INVALID_ARG", 2: "PDILQR_ERR_DIM", 3: "
 EXPORTED = ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
             "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host", "pdilqr_last_launch_count",
             "pdilqr_last_error", "pdilqr_abi_version", "pdilqr_profile", "pdilqr_profile_read",
-            "pdilqr_shift", "pdilqr_srbd_plant")
+            "pdilqr_shift", "pdilqr_srbd_plant", "pdilqr_solve")
 
 
 class SrbdParams(C.Structure):
@@ -85,6 +85,9 @@ def lib():
         L.pdilqr_profile.restype = st
         L.pdilqr_profile_read.argtypes = [vp, i32, C.POINTER(C.c_char_p), C.POINTER(i32), C.POINTER(C.c_double)]
         L.pdilqr_profile_read.restype = i32
+        L.pdilqr_solve.argtypes = [vp, C.POINTER(Iterate), i32, C.c_double, C.POINTER(Stats), vp,
+                                   C.POINTER(C.c_int32), vp]
+        L.pdilqr_solve.restype = st
         L.pdilqr_shift.argtypes = [vp, C.POINTER(Iterate), vp]
         L.pdilqr_shift.restype = st
         L.pdilqr_srbd_plant.argtypes = [vp, C.POINTER(Iterate), vp, vp, vp, C.c_double, i32, vp]
@@ -252,6 +255,18 @@ class PdIlqr:
                                       _ptr(stats_host["cost"]), _ptr(stats_host["theta"]),
                                       _ptr(stats_host["alpha"]), _ptr(stats_host["accepted"]),
                                       _ptr(stats_host["info"]), self._stream(stream)))
+
+    def solve(self, it: dict, max_iters: int = 50, tol: float = 1e-6, stats: dict | None = None, stream=None):
+        """pdilqr_solve: SQP iterations until every instance converged (theta <= tol and step <= tol)
+        or max_iters.  Returns (stats, iters[B] device int32, iterations run)."""
+        stats = stats if stats is not None else self.new_stats()
+        itc = self._iterate(it)
+        sc = Stats(**{k: _ptr(stats[k]) for k in ("cost", "theta", "alpha", "accepted", "info")})
+        iters = torch.empty(self.batch, dtype=torch.int32, device=self.device)
+        run = C.c_int32(0)
+        _check(lib().pdilqr_solve(self._h, C.byref(itc), int(max_iters), float(tol), C.byref(sc), _ptr(iters),
+                                  C.byref(run), self._stream(stream)))
+        return stats, iters, run.value
 
     def shift(self, it: dict, stream=None):
         """pdilqr_shift: warm start for the next tick."""

@@ -1,0 +1,104 @@
+"""GPU parity of pdilqr_solve (multi-iteration SQP to convergence) against the
+oracle's srbd_solve: the converged iterate (the unique KKT point) matches to the tolerance level;
+iteration counts agree within 2 -- near convergence the filter's accept decisions compare cost
+differences at the rounding level of the cost (reading R21), so the count is not unique -- and
+each side's stop satisfies the criterion.  Frozen-instance and failure semantics."""
+import numpy as np
+import pytest
+import torch
+
+from tests.gpu_util import to_np
+from workloads import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_07823_b200 as P
+    P.lib()
+    return P
+
+
+def dev_iter(pr, dtype):
+    out = {}
+    for k in ("x", "u", "lam", "x0", "x_ref", "u_ref", "contact", "feet"):
+        a = np.ascontiguousarray(pr[k])
+        t = torch.from_numpy(a)
+        out[k] = (t if a.dtype == np.uint8 else t.to(dtype)).cuda().contiguous()
+    return out
+
+
+def handle(P, pr, dtype):
+    B, N2, _ = pr["x"].shape
+    return P.PdIlqr(N=N2 - 2, n=12, m=12, batch=B, dtype=dtype, model="srbd", srbd=pr["params"])
+
+
+@pytest.mark.parametrize("B,N", [(8, 50), (37, 20)])
+def test_solve_fp64_matches_oracle(P, O, B, N):
+    pr = synth.srbd_problem(B, N, seed=3)
+    ref = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in pr.items()}
+    it_ref, st_ref = O.srbd_solve(ref, 50, 1e-8)
+    h = handle(P, pr, torch.float64)
+    it = dev_iter(pr, torch.float64)
+    st, iters, run = h.solve(it, 50, 1e-8)
+    torch.cuda.synchronize()
+    ig = to_np(iters)
+    assert (ig > 0).all() and (it_ref > 0).all() and np.abs(ig - it_ref).max() <= 2, (ig, it_ref)
+    assert run == ig.max()
+    for k in ("x", "u", "lam"):
+        d = np.abs(to_np(it[k]) - ref[k]).max() / max(1.0, np.abs(ref[k]).max())
+        assert d <= 1e-7, (k, d)
+    assert (to_np(st["theta"]) <= 1e-8).all()
+    assert np.allclose(to_np(st["cost"]), st_ref[:, 0], rtol=1e-9)
+
+
+def test_solve_fp32_converges_to_oracle_optimum(P, O):
+    pr = synth.round_to(synth.srbd_problem(64, 50, seed=5), np.float32)
+    ref = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in pr.items()}
+    it_ref, _ = O.srbd_solve(ref, 60, 1e-10)
+    h = handle(P, pr, torch.float32)
+    it = dev_iter(pr, torch.float32)
+    st, iters, run = h.solve(it, 60, 1e-3)
+    torch.cuda.synchronize()
+    ig = to_np(iters)
+    assert (ig > 0).all() and run == ig.max()
+    assert (to_np(st["theta"]) <= 1e-3).all()
+    for k in ("x", "u"):
+        d = np.abs(to_np(it[k]) - ref[k]).max(axis=(1, 2)) / np.maximum(1.0, np.abs(ref[k]).max(axis=(1, 2)))
+        assert d.max() <= 2e-3, (k, d.max())
+
+
+def test_solve_zero_iters_and_frozen(P, O):
+    pr = synth.srbd_problem(6, 20, seed=7)
+    h = handle(P, pr, torch.float64)
+    it = dev_iter(pr, torch.float64)
+    x0 = it["x"].clone()
+    st, iters, run = h.solve(it, 0, 1e-8)
+    torch.cuda.synchronize()
+    assert run == 0 and (to_np(iters) == 0).all() and torch.equal(it["x"], x0)
+    # converge, then solve again: every instance converges at iteration 1 with a tiny step
+    h.solve(it, 50, 1e-9)
+    xs = it["x"].clone()
+    st, iters, run = h.solve(it, 50, 1e-9)
+    torch.cuda.synchronize()
+    assert run == 1 and (to_np(iters) == 1).all()
+    assert (it["x"] - xs).abs().max().item() <= 1e-9
+
+
+def test_solve_failure_stops_instance(P, O):
+    pr = synth.srbd_problem(4, 20, seed=8)
+    pr["x"][2, 5, 4] = 1.6          # pitch beyond the guard |theta| < pi/2 - 0.1 -> info = -1
+    ref = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in pr.items()}
+    it_ref, st_ref = O.srbd_solve(ref, 40, 1e-8)
+    h = handle(P, pr, torch.float64)
+    it = dev_iter(pr, torch.float64)
+    st, iters, run = h.solve(it, 40, 1e-8)
+    torch.cuda.synchronize()
+    ig = to_np(iters)
+    assert ig[2] == it_ref[2] == -1
+    ok = np.arange(4) != 2
+    assert (ig[ok] > 0).all() and np.abs(ig[ok] - it_ref[ok]).max() <= 2
+    assert to_np(iters)[2] == -1 and to_np(st["info"])[2] == st_ref[2, 4] != 0

@@ -304,3 +304,33 @@ def test_step_batch_matches_single(O):
         assert np.array_equal(prob["u"][b], singles[b][1])
         assert np.array_equal(prob["lam"][b], singles[b][2])
         assert np.array_equal(st[b], singles[b][3])
+
+
+def test_solve_zero_iters_is_noop(O):
+    """max_iters = 0 returns the iterate unchanged."""
+    pr = synth.srbd_problem(2, 20, seed=4)
+    x0 = pr["x"].copy()
+    it, _ = O.srbd_solve(pr, 0, 1e-8)
+    assert (it == 0).all() and np.array_equal(pr["x"], x0)
+
+
+def test_solve_reaches_fixed_point(O):
+    """iterating to convergence reaches a KKT point; one more SQP iteration from
+    it moves the trajectory by <= 1e-8 (stationarity) and theta stays <= 1e-10."""
+    pr = synth.srbd_problem(3, 30, seed=6)
+    it, st = O.srbd_solve(pr, 60, 1e-10)
+    assert (it > 0).all() and (it <= 60).all()
+    assert (st[:, 1] <= 1e-10).all()
+    for b in range(3):
+        x, u, lam, s, dx, du, dl = O.srbd_step_single(pr, b)
+        assert max(np.abs(x - pr["x"][b]).max(), np.abs(u - pr["u"][b]).max()) <= 1e-8
+        assert s[1] <= 1e-10
+
+
+def test_solve_iteration_count_monotone_in_tol(O):
+    """A looser tolerance never needs more iterations (same iterates up to the earlier stop)."""
+    a = synth.srbd_problem(4, 30, seed=9)
+    b = synth.srbd_problem(4, 30, seed=9)
+    ia, _ = O.srbd_solve(a, 60, 1e-4)
+    ib, _ = O.srbd_solve(b, 60, 1e-9)
+    assert (ia > 0).all() and (ia <= ib).all()

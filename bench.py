@@ -45,7 +45,8 @@ def flops_per_instance(N: int, n: int = 12, m: int = 12, chunk: int | None = Non
     App. B).  Full combine 16.67 n^3 + 8 n^2, cheap combine (suffix right operand) 8.67 n^3 + 4 n^2,
     element init m^3/3 + 2 m^2 (2n+1) + 6 n^2 m + 4 n m, policy 4 n^2 m + 2 n m^2 + m^3/3 +
     2 m^2 (n+1) + 2 n^2 + 2 n m + (Abar, bbar) 2 n^2 m + 2 n m, forward combine 2 n^3 + 2 n^2,
-    forward fold 2 n^2, tail (du, dlam) 2 m n + 2 n^2."""
+    forward fold 2 n^2, tail (du, dlam) 2 m n + 2 n^2.  Fused SRBD fold: policy + 4 n^3 + 4 n^2 +
+    2 n m + 6 m per stage (no C~, no M solve: X = Abar, DESIGN D7)."""
     L = N + 2
     Lf = N + 1
     c = L if (chunk is None or chunk <= 0) else chunk
@@ -71,11 +72,12 @@ def flops_per_instance(N: int, n: int = 12, m: int = 12, chunk: int | None = Non
     policy = (N + 1) * (4 * n ** 2 * m + 2 * n * m ** 2 + m ** 3 / 3 + 2 * m ** 2 * (n + 1) + 2 * n ** 2 + 2 * n * m
                         + 2 * n ** 2 * m + 2 * n * m)
     tail = (N + 1) * 2 * m * n + (N + 2) * 2 * n ** 2
-    # fused single-chunk SRBD path (S = 0): element init without the S terms, policy, cheap fold
-    init_s0 = (N + 1) * (m ** 3 / 3 + 2 * m ** 2 * (n + 1) + 2 * n ** 2 * m + 2 * n * m)
-    fold = (N + 1) * cheap
+    # fused single-chunk SRBD path (S = 0, DESIGN D7): policy (incl. Abar, bbar), then the cheap
+    # combine with X = Abar: V = P Abar, P' = Q + A^T V (4 n^3), w = p + P b~, p' = Abar^T w + q
+    # (4 n^2), b~ = b - B R^-1 r (2 n m + blockwise R^-1 r, 6 m)
+    fold_s0 = (N + 1) * (4 * n ** 3 + 4 * n ** 2 + 2 * n * m + 6 * m)
     return {"k_elem_init": init, "k_scan_bwd": bwd, "k_policy": policy, "k_scan_fwd": fwd, "k_tail": tail,
-            "k_srbd_bwd_fold": init_s0 + policy + fold,
+            "k_srbd_bwd_fold": policy + fold_s0,
             "k_srbd_fwd_ls": Lf * 2 * n ** 2 + tail}
 
 

@@ -110,10 +110,13 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
             rr = row.rg + BTl;
         }
         // ---------------- element e_i (Eq. 12 with S = 0): A~ = A, P~ = Q, p~ = q,
-        //                  C~ = B R^-1 B^T, b~ = b - B R^-1 r.  The SRBD Gauss-Newton R is block
-        //                  diagonal (one 3x3 SPD block per foot: diagonal weights + barrier
-        //                  curvature of that foot's constraints), so R^-1 is formed blockwise in
-        //                  closed form (adjugate) by the three lanes of each foot.
+        //                  C~ = B R^-1 B^T, b~ = b - B R^-1 r.  Folding it into the suffix
+        //                  s_{i+1} (A~ = C~ = b~ = 0) by the cheap rule (Eq. 11) needs
+        //                  X = M^-1 A~ with M = I + C~ P_{i+1}; by the Woodbury identity
+        //                  X = A - B G^-1 B^T P_{i+1} A = A + B K_i = Abar_i (design D7), so the
+        //                  combine shares the policy's elimination and C~ is never formed.
+        //                  R is block diagonal (one 3x3 SPD block per foot), so R^-1 r is formed
+        //                  blockwise in closed form (adjugate) by the three lanes of each foot.
         if (act) {
             st_row<T, NX, true>(s.ZB + r * NX, row.Rrow);
             s.zr[r] = rr;
@@ -131,24 +134,14 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
             const T det = a00 * c00 + a01 * c10 + a02 * c20;
             // SPD check of the block: leading principal minors a00, a00 a11 - a01 a10, det > 0
             if (!(a00 > T(0)) || !(c22 > T(0)) || !(det > T(0)) || !isfinite(det)) fail = min(fail, i + 1);
-            const T id = T(1) / det;
-            const T q0 = (ar == 0 ? c00 : ar == 1 ? c10 : c20) * id;
-            const T q1 = (ar == 0 ? c01 : ar == 1 ? c11 : c21) * id;
-            const T q2 = (ar == 0 ? c02 : ar == 1 ? c12 : c22) * id;
-            const T zr_r = q0 * s.zr[o] + q1 * s.zr[o + 1] + q2 * s.zr[o + 2];
-            T zb[NX];
-#pragma unroll
-            for (int t = 0; t < NX; ++t) zb[t] = q0 * s.B[t * NX + o] + q1 * s.B[t * NX + o + 1] + q2 * s.B[t * NX + o + 2];
+            const T q0 = (ar == 0 ? c00 : ar == 1 ? c10 : c20);
+            const T q1 = (ar == 0 ? c01 : ar == 1 ? c11 : c21);
+            const T q2 = (ar == 0 ? c02 : ar == 1 ? c12 : c22);
+            const T zr_r = (q0 * s.zr[o] + q1 * s.zr[o + 1] + q2 * s.zr[o + 2]) / det;
             __syncwarp(mask);
-            if (act) {
-                st_row<T, NX, true>(s.ZB + r * NX, zb);
-                s.zr[r] = zr_r;
-            }
+            if (act) s.zr[r] = zr_r;
         }
         __syncwarp(mask);
-        T ct[NX];
-        zero(ct);
-        row_mat<T, NX, NX, NX>(ct, row.Brow, s.ZB);
         const T btr = row_dot<T, NX>(row.Brow, s.zr, T(0));
         if (act) s.bt[r] = s.c[r] - btr;
         // ---------------- policy for stage i from s_{i+1} = (P_{i+1}, p_{i+1})
@@ -164,8 +157,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
         __syncwarp(mask);
         {
             // policy system  G [K | k] = -[H | h]  (G = R + B^T P B SPD, H = B^T P A, h = B^T (p + P b) + r)
-            // and combine system  M X = A~  (M = I + C~ P'), eliminated together
-            T bcol[NX], pbcol[NX], G[NX], rhs[NX + 1];
+            T bcol[NX], pbcol[NX], G[NX], rhs[NX + 2];
             ld_col<T, NX>(bcol, s.B + r, NX);
             ld_col<T, NX>(pbcol, s.V + r, NX);
 #pragma unroll
@@ -174,36 +166,33 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
             zero(*reinterpret_cast<T(*)[NX]>(rhs));
             row_mat<T, NX, NX, NX>(*reinterpret_cast<T(*)[NX]>(rhs), pbcol, s.A);
             rhs[NX] = row_dot<T, NX>(bcol, s.g, rr);
-            T M[NX], rhs2[NX];
-#pragma unroll
-            for (int j = 0; j < NX; ++j) { M[j] = (j == r) ? T(1) : T(0); rhs2[j] = arow[j]; }
-            row_mat<T, NX, NX, NX>(M, ct, s.P);
-            const T wr = row_dot<T, NX>(prow, s.bt, s.p[r]);
+            rhs[NX + 1] = T(0);
+            const T wr = row_dot<T, NX>(prow, s.bt, s.p[r]);   // w = p_{i+1} + P_{i+1} b~_i
             if (act) s.w[r] = wr;
-            int pr1, pr2;
-            bool ok1, ok2;
-            gauss_jordan_dual<T, NX, NX + 1, NX>(G, rhs, M, rhs2, lane, pr1, pr2, ok1, ok2);
-            if (!ok1 || !ok2) fail = min(fail, i + 1);
-            if (pr1 >= 0) {
+            int pr1;
+            const bool ok1 = gauss_jordan<T, WS, NX, NX + 2, false, true>(mask, G, rhs, lane, NX, pr1);
+            if (!ok1) fail = min(fail, i + 1);
+            if (act) {
                 T kr[NX];
 #pragma unroll
                 for (int j = 0; j < NX; ++j) kr[j] = -rhs[j];
-                st_row<T, NX, true>(s.K + pr1 * NX, kr);
-                s.k[pr1] = -rhs[NX];
+                st_row<T, NX, true>(s.K + r * NX, kr);
+                s.k[r] = -rhs[NX];
                 if (live) {
-                    st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + pr1 * NX, kr);
-                    Kk[(size_t)i * KL::SIZE + KL::k + pr1] = -rhs[NX];
+                    st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + r * NX, kr);
+                    Kk[(size_t)i * KL::SIZE + KL::k + r] = -rhs[NX];
                 }
             }
-            if (pr2 >= 0) st_row<T, NX, true>(s.X + pr2 * NX, rhs2);
         }
         __syncwarp(mask);
         {
+            // closed-loop transition (Abar_i, bbar_i) = (A + B K, B k + b)  (Eq. 14) = X of the combine
             T abar[NX];
 #pragma unroll
             for (int j = 0; j < NX; ++j) abar[j] = arow[j];
             row_mat<T, NX, NX, NX>(abar, row.Brow, s.K);
             const T bb = row_dot<T, NX>(row.Brow, s.k, s.c[r]);
+            if (act) st_row<T, NX, true>(s.X + r * NX, abar);
             if (wr_g) {
                 st_row<T, NX, true>(Te + (size_t)i * TP + r * NX, abar);
                 Te[(size_t)i * TP + NX * NX + r] = bb;

@@ -379,6 +379,17 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
         }
     }
 
+// Per-warp shared memory of k_srbd_fwd_ls: during the rollout a ring of D stage blocks
+// [(Abar_i, bbar_i) | (K_i, k_i)] filled by cp.async D-1 stages ahead; during the line search the
+// per-lane alpha partial sums and the defect deltas (the two phases never overlap).
+template <typename T>
+struct FwdLsSmem {
+    static constexpr int NA = 16, BLK = 2 * 156, D = sizeof(T) == 8 ? 4 : 8;
+    static constexpr size_t LS = 2 * NA * 32 * sizeof(double) + 24 * 32 * sizeof(T);
+    static constexpr size_t RING = (size_t)D * BLK * sizeof(T);
+    static constexpr size_t PER_WARP = LS > RING ? LS : RING;
+};
+
 template <typename T, int MINB>
 __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
                                                            T *dx, T *du, T *dlam, const int32_t *info_in, LsOut<T> so,
@@ -386,13 +397,16 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     constexpr int NX = 12, NA = 16;
     constexpr int TP = TE<NX>::SIZE;
     using KL = KE<NX, NX>;
+    using SM = FwdLsSmem<T>;
+    static_assert(TP == 156 && KL::SIZE == 156 && KL::K == 0, "stage block layout");
     constexpr int WPB = LsWarps<T>::value;  // warps (instances) per block
+    constexpr int D = SM::D;
     __shared__ __align__(16) T sx[WPB][16];
-    __shared__ double sJ[WPB][NA][32], sT[WPB][NA][32];
-    __shared__ T sDel[WPB][24][32];     // per lane: x_{i+1} - x_i and dx_{i+1} - dx_i of its stage
+    __shared__ __align__(16) unsigned char sraw[WPB * SM::PER_WARP];
     const int lane = threadIdx.x & 31, wl = threadIdx.x / 32;
     const int b = blockIdx.x * (blockDim.x / 32) + wl;
     if (b >= B) return;
+    unsigned char *mine = sraw + (size_t)wl * SM::PER_WARP;
     const int na = K.n_alpha;
     const T *x = it.x + (size_t)b * (N + 2) * NX, *u = it.u + (size_t)b * (N + 1) * NX;
     const T *xr = it.xref + (size_t)b * (N + 2) * NX;
@@ -410,42 +424,47 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         info = pr != 0 ? pr : (f != kFailNone ? (f & 0xFFFFFF) : 0);
     }
     // ---------------- closed-loop rollout (one chunk of Eq. 15) and du (Eq. 6)
+    T *ring = reinterpret_cast<T *>(mine);
+    constexpr int CH = 156 * (int)sizeof(T) / 16;  // 16-byte chunks per 156-entry block
+    constexpr int EPC = 16 / (int)sizeof(T);
+    auto issue = [&](int s) {  // stage s -> ring slot s % D (always commits a group)
+        if (s <= N) {
+            T *dst = ring + (size_t)(s % D) * SM::BLK;
+            const T *sa = Te + (size_t)s * TP, *sk = Kk + (size_t)s * KL::SIZE;
+            for (int c = lane; c < 2 * CH; c += 32)
+                cp_async16(dst + c * EPC, c < CH ? sa + c * EPC : sk + (c - CH) * EPC);
+        }
+        cp_async_commit();
+    };
+#pragma unroll
+    for (int s0 = 0; s0 < D - 1; ++s0) issue(s0);
     const int r = lane & 15;
     const bool rowl = r < NX;
     {
         const T d0 = x0[r < NX ? r : 0] - x[r < NX ? r : 0];
         if (lane < NX) { sx[wl][r] = d0; Dx[r] = d0; }
     }
-    __syncwarp();
-    // lanes 0..11: dx_{i+1} = Abar_i dx_i + bbar_i ; lanes 16..27: du_i = K_i dx_i + k_i.
-    // The next stage's row is loaded while the current one is applied (register double buffer).
-    const T *rowbase = lane < 16 ? Te + (size_t)(rowl ? r : 0) * NX : Kk + KL::K + (size_t)(rowl ? r : 0) * NX;
-    const T *offbase = lane < 16 ? Te + NX * NX + (rowl ? r : 0) : Kk + KL::k + (rowl ? r : 0);
-    const size_t rstride = lane < 16 ? (size_t)TP : (size_t)KL::SIZE;
-    T rcur[NX], ocur;
-    ld_row<T, NX, true>(rcur, rowbase);
-    ocur = offbase[0];
+    // lanes 0..11: dx_{i+1} = Abar_i dx_i + bbar_i ; lanes 16..27: du_i = K_i dx_i + k_i
+    const int roff = (lane < 16 ? 0 : 156) + (rowl ? r : 0) * NX;
+    const int ooff = (lane < 16 ? 0 : 156) + NX * NX + (rowl ? r : 0);
     for (int i = 0; i <= N; ++i) {
-        T rnext[NX], onext = T(0);
-        if (i < N) {
-            ld_row<T, NX, true>(rnext, rowbase + (size_t)(i + 1) * rstride);
-            onext = offbase[(size_t)(i + 1) * rstride];
-        }
-        T xv[NX];
+        issue(i + D - 1);
+        cp_async_wait<D - 1>();
+        __syncwarp();
+        const T *blk = ring + (size_t)(i % D) * SM::BLK;
+        T rcur[NX], xv[NX];
+        ld_row<T, NX, true>(rcur, blk + roff);
         ld_row<T, NX, true>(xv, sx[wl]);
-        const T v = row_dot<T, NX>(rcur, xv, ocur);
+        const T v = row_dot<T, NX>(rcur, xv, blk[ooff]);
         __syncwarp();
         if (rowl) {
             if (lane < 16) { sx[wl][r] = v; Dx[(size_t)(i + 1) * NX + r] = v; }
             else Du[(size_t)i * NX + r] = v;
         }
         __syncwarp();
-        if (i < N) {
-#pragma unroll
-            for (int j = 0; j < NX; ++j) rcur[j] = rnext[j];
-            ocur = onext;
-        }
     }
+    cp_async_wait<0>();
+    __syncwarp();
     // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel
     for (int t = lane; t < (N + 2) * NX; t += 32) {
         const int i = t / NX, a = t % NX;
@@ -461,13 +480,14 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     // quadratics c0 + c1 a + c2 a^2 (fp64), the barrier arguments are xi0 + a dxi, the defect is
     // (x_{i+1} - x_i) + a (dx_{i+1} - dx_i) - dt f(x_i + a dx_i, u_i + a du_i).  Trial states and
     // the model are evaluated in fp32 (fast sincos / log: SFU), sums in fp64.
-    double(*aJ)[32] = sJ[wl];
-    double(*aT)[32] = sT[wl];
+    double(*aJ)[32] = reinterpret_cast<double(*)[32]>(mine);
+    double(*aT)[32] = reinterpret_cast<double(*)[32]>(mine + NA * 32 * sizeof(double));
+    T(*sDel)[32] = reinterpret_cast<T(*)[32]>(mine + 2 * NA * 32 * sizeof(double));
     for (int a = 0; a <= na; ++a) { aJ[a][lane] = 0.0; aT[a][lane] = 0.0; }
     unsigned guard = 0u;  // bit a: some trial state of slot a leaves the pitch guard
     double g = 0.0;
     for (int i = lane; i <= N + 1; i += 32)
-        ls_stage<T>(K, it, b, N, i, na, x, Dx, u, Du, xr, urf, aJ, aT, sDel[wl], lane, g, guard);
+        ls_stage<T>(K, it, b, N, i, na, x, Dx, u, Du, xr, urf, aJ, aT, sDel, lane, g, guard);
     // fixed-order xor butterflies: every lane ends with bitwise identical sums
     for (int a = 0; a <= na; ++a) {
         double vJ = aJ[a][lane], vT = aT[a][lane];

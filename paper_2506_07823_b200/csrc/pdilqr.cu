@@ -730,6 +730,9 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     for (int k = 0; k < 12; ++k) { K.wx[k] = p.w_x[k]; K.wxt[k] = p.w_x_term[k]; }
     K.wu_st = p.w_u_stance; K.wu_sw = p.w_u_swing;
     K.mu = p.mu_friction; K.fmin = p.f_min; K.fmax = p.f_max; K.bmu = p.barrier_mu; K.bdelta = p.barrier_delta;
+    K.imass = 1.0 / p.mass;
+    K.ibd = 1.0 / p.barrier_delta;
+    K.ibd2 = 1.0 / (p.barrier_delta * p.barrier_delta);
     K.theta_max = h->cfg.theta_max; K.c1 = h->cfg.armijo_c1; K.n_alpha = h->cfg.n_alpha;
     if (const char *e = std::getenv("PDILQR_OCC_FOLD")) h->occ_fold = std::atoi(e);  // tuning knobs
     if (const char *e = std::getenv("PDILQR_OCC_LS")) h->occ_ls = std::atoi(e);

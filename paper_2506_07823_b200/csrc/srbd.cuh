@@ -16,6 +16,7 @@ struct SrbdConst {
     double dt, mass, I[9], Iinv[9], g[3];
     double wx[12], wxt[12], wu_st, wu_sw;
     double mu, fmin, fmax, bmu, bdelta;
+    double imass, ibd, ibd2;  // 1 / mass, 1 / bdelta, 1 / bdelta^2 (host-computed)
     double theta_max, c1;
     int n_alpha;
 };
@@ -34,6 +35,46 @@ __device__ __forceinline__ T barrier_d1(T xi, T mu, T d) { return xi >= d ? -mu 
 template <typename T>
 __device__ __forceinline__ T barrier_d2(T xi, T mu, T d) { return xi >= d ? mu / (xi * xi) : mu / (d * d); }
 
+// Barrier first and second derivatives with one reciprocal instead of IEEE divisions:
+// xi >= d: (-mu / xi, mu / xi^2); else (mu (xi - 2 d) / d^2, mu / d^2), id2 = 1 / d^2.
+template <typename T>
+__device__ __forceinline__ void barrier_d12(T xi, T mu, T d, T id2, T &d1, T &d2) {
+    const T rx = rcp_rn(xi);
+    const bool in = xi >= d;
+    d1 = in ? -mu * rx : mu * (xi - T(2) * d) * id2;
+    d2 = in ? mu * rx * rx : mu * id2;
+}
+
+// Gradient and Hessian of the six friction-pyramid / normal-force barriers of one stance foot
+// with respect to its force (fx, fy, fz), the constraint normals being constants:
+//   grad = sum_c B'(xi_c) g_c,  H = sum_c B''(xi_c) g_c g_c^T  (H_xy = 0).
+template <typename T>
+struct FootBarrier {
+    T gx, gy, gz, hxx, hyy, hzz, hxz, hyz;
+};
+template <typename T>
+__device__ __forceinline__ FootBarrier<T> foot_barrier(const SrbdConst &K, T fx, T fy, T fz) {
+    const T mu = T(K.mu), bmu = T(K.bmu), d = T(K.bdelta), id2 = T(K.ibd2);
+    const T mfz = mu * fz;
+    T a0, a1, a2, a3, a4, a5, b0, b1, b2, b3, b4, b5;
+    barrier_d12<T>(mfz - fx, bmu, d, id2, a0, b0);
+    barrier_d12<T>(mfz + fx, bmu, d, id2, a1, b1);
+    barrier_d12<T>(mfz - fy, bmu, d, id2, a2, b2);
+    barrier_d12<T>(mfz + fy, bmu, d, id2, a3, b3);
+    barrier_d12<T>(fz - T(K.fmin), bmu, d, id2, a4, b4);
+    barrier_d12<T>(T(K.fmax) - fz, bmu, d, id2, a5, b5);
+    FootBarrier<T> o;
+    o.gx = a1 - a0;
+    o.gy = a3 - a2;
+    o.gz = mu * ((a0 + a1) + (a2 + a3)) + (a4 - a5);
+    o.hxx = b0 + b1;
+    o.hyy = b2 + b3;
+    o.hzz = mu * mu * ((b0 + b1) + (b2 + b3)) + (b4 + b5);
+    o.hxz = mu * (b1 - b0);
+    o.hyz = mu * (b3 - b2);
+    return o;
+}
+
 // constraint c in 0..5 of one stance foot: xi = gx fx + gy fy + gz fz + h
 //   0: mu fz - fx   1: mu fz + fx   2: mu fz - fy   3: mu fz + fy   4: fz - fmin   5: fmax - fz
 template <typename T>
@@ -48,7 +89,7 @@ __device__ __forceinline__ void foot_con(int c, T mu, T fmin, T fmax, T &gx, T &
 // Shared trig / rotation terms are recomputed per call (cheap, no smem traffic).
 template <typename T>
 struct SrbdEval {
-    T sr, cr, sp, cp, sy, cy, tp;
+    T sr, cr, sp, cp, sy, cy, tp, icp;
     T R[9];      // body -> world, R = Rz(yaw) Ry(pitch) Rx(roll)
     T tau[3];    // world torque sum_j c_j (r_j - p) x f_j
     T F[3];      // sum_j c_j f_j
@@ -57,7 +98,8 @@ struct SrbdEval {
         sincos(x[3], &sr, &cr);
         sincos(x[4], &sp, &cp);
         sincos(x[5], &sy, &cy);
-        tp = sp / cp;
+        icp = rcp_rn(cp);
+        tp = sp * icp;
         R[0] = cy * cp; R[1] = cy * sp * sr - sy * cr; R[2] = cy * sp * cr + sy * sr;
         R[3] = sy * cp; R[4] = sy * sp * sr + cy * cr; R[5] = sy * sp * cr - cy * sr;
         R[6] = -sp;     R[7] = cp * sr;                R[8] = cp * cr;
@@ -89,9 +131,28 @@ struct SrbdEval {
         if (r < 3) return x[6 + r];
         if (r == 3) return x[9] + sr * tp * x[10] + cr * tp * x[11];
         if (r == 4) return cr * x[10] - sr * x[11];
-        if (r == 5) return (sr * x[10] + cr * x[11]) / cp;
-        if (r < 9) return F[r - 6] / T(K.mass) + T(K.g[r - 6]);
+        if (r == 5) return (sr * x[10] + cr * x[11]) * icp;
+        if (r < 9) return F[r - 6] * T(K.imass) + T(K.g[r - 6]);
         return wdot(K, x, r - 9);
+    }
+    // all twelve components, the angular acceleration evaluated once
+    __device__ __forceinline__ void f_all(const SrbdConst &K, const T *x, T (&out)[12]) const {
+        const T w0 = x[9], w1 = x[10], w2 = x[11];
+        out[0] = x[6]; out[1] = x[7]; out[2] = x[8];
+        out[3] = w0 + sr * tp * w1 + cr * tp * w2;
+        out[4] = cr * w1 - sr * w2;
+        out[5] = (sr * w1 + cr * w2) * icp;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) out[6 + c] = F[c] * T(K.imass) + T(K.g[c]);
+        T Iw[3], rhs[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Iw[c] = T(K.I[3 * c]) * w0 + T(K.I[3 * c + 1]) * w1 + T(K.I[3 * c + 2]) * w2;
+        const T wxIw[3] = {w1 * Iw[2] - w2 * Iw[1], w2 * Iw[0] - w0 * Iw[2], w0 * Iw[1] - w1 * Iw[0]};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) rhs[c] = R[c] * tau[0] + R[3 + c] * tau[1] + R[6 + c] * tau[2] - wxIw[c];
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+            out[9 + a] = T(K.Iinv[3 * a]) * rhs[0] + T(K.Iinv[3 * a + 1]) * rhs[1] + T(K.Iinv[3 * a + 2]) * rhs[2];
     }
 };
 
@@ -126,20 +187,20 @@ __device__ __forceinline__ void srbd_stage_row(const SrbdConst &K, const T *x, c
         for (int c = 0; c < 3; ++c) Arow[6 + c] = (c == r) ? T(1) : T(0);
     } else if (r == 3) {
         Arow[3] = ev.tp * (ev.cr * w1 - ev.sr * w2);
-        Arow[4] = (ev.sr * w1 + ev.cr * w2) / (ev.cp * ev.cp);
+        Arow[4] = (ev.sr * w1 + ev.cr * w2) * (ev.icp * ev.icp);
         Arow[9] = T(1); Arow[10] = ev.sr * ev.tp; Arow[11] = ev.cr * ev.tp;
     } else if (r == 4) {
         Arow[3] = -ev.sr * w1 - ev.cr * w2;
         Arow[10] = ev.cr; Arow[11] = -ev.sr;
     } else if (r == 5) {
-        Arow[3] = (ev.cr * w1 - ev.sr * w2) / ev.cp;
-        Arow[4] = (ev.sr * w1 + ev.cr * w2) * ev.sp / (ev.cp * ev.cp);
-        Arow[10] = ev.sr / ev.cp; Arow[11] = ev.cr / ev.cp;
+        Arow[3] = (ev.cr * w1 - ev.sr * w2) * ev.icp;
+        Arow[4] = (ev.sr * w1 + ev.cr * w2) * ev.sp * (ev.icp * ev.icp);
+        Arow[10] = ev.sr * ev.icp; Arow[11] = ev.cr * ev.icp;
     } else if (r < 9) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) Brow[3 * j + c] = (con[j] && c == r - 6) ? T(1) / T(K.mass) : T(0);
+            for (int c = 0; c < 3; ++c) Brow[3 * j + c] = (con[j] && c == r - 6) ? T(K.imass) : T(0);
     } else {
         const int a = r - 9;
         T Ii[3];
@@ -198,10 +259,11 @@ __device__ __forceinline__ void srbd_stage_row(const SrbdConst &K, const T *x, c
         }
     }
     T fr = T(0);
+    {
+        T fa[NX];
+        ev.f_all(K, xv, fa);
 #pragma unroll
-    for (int c = 0; c < NX; ++c) {
-        const T fc = ev.f(K, xv, c);
-        fr = (c == r) ? fc : fr;
+        for (int c = 0; c < NX; ++c) fr = (c == r) ? fa[c] : fr;
     }
     // Arow holds dt Fx (the identity is added at the store): keeps A^T lam - lam = dt Fx^T lam
     // and the defect free of fp cancellation
@@ -218,28 +280,22 @@ __device__ __forceinline__ void srbd_stage_row(const SrbdConst &K, const T *x, c
 #pragma unroll
     for (int c = 0; c < NX; ++c) Rrow[c] = (c == r) ? wu : T(0);
     T rg = wu * (ur_r - (ur ? ur[r] : T(0)));
-    T &rgo = o.rg;
-    if (stance) {
-        const T fx = u[3 * j], fy = u[3 * j + 1], fz = u[3 * j + 2];
-        for (int c = 0; c < 6; ++c) {
-            T gx, gy, gz, h;
-            foot_con<T>(c, T(K.mu), T(K.fmin), T(K.fmax), gx, gy, gz, h);
-            const T xi = gx * fx + gy * fy + gz * fz + h;
-            const T d1 = barrier_d1<T>(xi, T(K.bmu), T(K.bdelta));
-            const T d2 = barrier_d2<T>(xi, T(K.bmu), T(K.bdelta));
-            const T ga = a == 0 ? gx : a == 1 ? gy : gz;
-            rg += d1 * ga;
+    {
+        // barrier terms of this lane's foot j (stance only): gradient entry a, Hessian row a of the
+        // foot's 3x3 block (columns 3j..3j+2)
+        const FootBarrier<T> fb = foot_barrier<T>(K, uv[3 * j], uv[3 * j + 1], uv[3 * j + 2]);
+        const T ga = a == 0 ? fb.gx : a == 1 ? fb.gy : fb.gz;
+        const T h0 = a == 0 ? fb.hxx : a == 1 ? T(0) : fb.hxz;
+        const T h1 = a == 0 ? T(0) : a == 1 ? fb.hyy : fb.hyz;
+        const T h2 = a == 0 ? fb.hxz : a == 1 ? fb.hyz : fb.hzz;
+        if (stance) rg += ga;
 #pragma unroll
-            for (int bb = 0; bb < 3; ++bb) {
-                const T gb = bb == 0 ? gx : bb == 1 ? gy : gz;
-                // Rrow[3 j + bb] += d2 ga gb  (j runtime: select)
-#pragma unroll
-                for (int jj = 0; jj < 4; ++jj)
-                    if (jj == j) Rrow[3 * jj + bb] += d2 * ga * gb;
-            }
+        for (int c = 0; c < NX; ++c) {
+            const T hv = (c % 3 == 0) ? h0 : (c % 3 == 1) ? h1 : h2;
+            Rrow[c] += (stance && c / 3 == j) ? hv : T(0);
         }
     }
-    rgo = rg;
+    o.rg = rg;
 }
 
 // ------------------------------------------------------------------------- linearisation

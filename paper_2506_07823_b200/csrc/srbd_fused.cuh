@@ -307,11 +307,15 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
                 foot_con<F>(cc, (F)K.mu, (F)K.fmin, (F)K.fmax, gx, gy, gz, h);
                 bx0[6 * j + cc] = gx * us0[3 * j] + gy * us0[3 * j + 1] + gz * us0[3 * j + 2] + h;
                 bdx[6 * j + cc] = gx * dus[3 * j] + gy * dus[3 * j + 1] + gz * dus[3 * j + 2];
-                if ((cmask >> j) & 1)
-                    g += (double)barrier_d1<F>(bx0[6 * j + cc], (F)K.bmu, (F)K.bdelta) * (double)bdx[6 * j + cc];
+                if ((cmask >> j) & 1) {
+                    F d1, d2;
+                    barrier_d12<F>(bx0[6 * j + cc], (F)K.bmu, (F)K.bdelta, (F)K.ibd2, d1, d2);
+                    g += (double)d1 * (double)bdx[6 * j + cc];
+                }
             }
         }
-        const F bmu = (F)K.bmu, bdl = (F)K.bdelta, lbd = fast_log((F)K.bdelta);
+        const F bmu = (F)K.bmu, bdl = (F)K.bdelta, ibdl = (F)K.ibd, lbd = fast_log((F)K.bdelta);
+        const F im = (F)K.imass;
         for (int a = 0; a <= na; ++a) {
             const double ald = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
             const F al = (F)ald;
@@ -323,7 +327,7 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
 #pragma unroll
                 for (int cc = 0; cc < 6; ++cc) {
                     const F xv = fma(al, bdx[6 * j + cc], bx0[6 * j + cc]);
-                    const F t = (xv - F(2.) * bdl) / bdl;
+                    const F t = (xv - F(2.) * bdl) * ibdl;
                     Jb += xv >= bdl ? -bmu * fast_log(xv) : F(0.5) * bmu * (t * t - F(1.)) - bmu * lbd;
                 }
             }
@@ -337,7 +341,7 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
             fast_sincos(xs[3], &sr, &cr);
             fast_sincos(xs[4], &sp, &cp);
             fast_sincos(xs[5], &sy, &cy);
-            const F icp = F(1.) / cp, tp = sp * icp;
+            const F icp = rcp_rn(cp), tp = sp * icp;
             const F R0 = cy * cp, R1 = cy * sp * sr - sy * cr, R2 = cy * sp * cr + sy * sr;
             const F R3 = sy * cp, R4 = sy * sp * sr + cy * cr, R5 = sy * sp * cr - cy * sr;
             const F R6 = -sp, R7 = cp * sr, R8 = cp * cr;
@@ -362,7 +366,6 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
             fv[3] = w0 + sr * tp * w1 + cr * tp * w2;
             fv[4] = cr * w1 - sr * w2;
             fv[5] = (sr * w1 + cr * w2) * icp;
-            const F im = F(1.) / (F)K.mass;
             fv[6] = F0 * im + (F)K.g[0]; fv[7] = F1 * im + (F)K.g[1]; fv[8] = F2 * im + (F)K.g[2];
 #pragma unroll
             for (int c = 0; c < 3; ++c)

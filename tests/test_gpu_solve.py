@@ -79,13 +79,20 @@ def test_solve_zero_iters_and_frozen(P, O):
     st, iters, run = h.solve(it, 0, 1e-8)
     torch.cuda.synchronize()
     assert run == 0 and (to_np(iters) == 0).all() and torch.equal(it["x"], x0)
-    # converge, then solve again: every instance converges at iteration 1 with a tiny step
-    h.solve(it, 50, 1e-9)
+    # instances that converged before the last iteration are frozen: their last stats report the
+    # current iterate (alpha = 0, accepted = 0)
+    st, iters, run = h.solve(it, 50, 1e-9)
+    torch.cuda.synchronize()
+    ig = to_np(iters)
+    assert (ig > 0).all() and run == ig.max()
+    early = ig < run
+    assert (to_np(st["alpha"])[early] == 0).all() and (to_np(st["accepted"])[early] == 0).all()
+    # solving again from the converged iterate: converged within 2 iterations, negligible motion
     xs = it["x"].clone()
     st, iters, run = h.solve(it, 50, 1e-9)
     torch.cuda.synchronize()
-    assert run == 1 and (to_np(iters) == 1).all()
-    assert (it["x"] - xs).abs().max().item() <= 1e-9
+    assert run <= 2 and (to_np(iters) >= 1).all()
+    assert (it["x"] - xs).abs().max().item() <= 1e-8
 
 
 def test_solve_failure_stops_instance(P, O):

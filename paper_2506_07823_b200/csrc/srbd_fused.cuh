@@ -33,6 +33,10 @@ template <typename T>
 struct FoldSmem {
     T P[144], A[144], B[144], ZB[144], X[144], V[144], K[144];
     T p[12], c[12], g[12], bt[12], w[12], zr[12], k[12], pad[4];
+    // per-stage inputs staged by cp.async one stage ahead (3 slots: stage i-1 lands while stages
+    // i and i+1 are read): x, lam, xref, u, feet, uref (12 each), contact flags (4 bytes at IN_CON)
+    static constexpr int IN_X = 0, IN_L = 12, IN_XR = 24, IN_U = 36, IN_F = 48, IN_UR = 60, IN_CON = 72, IN = 80;
+    T in[3][IN];
 };
 
 template <typename T, int MINB>
@@ -80,13 +84,38 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
             Pp[(size_t)(N + 1) * TP + NX * NX + r] = pr;
         }
     }
+    // stage inputs -> s.in[stage % 3] (cp.async, 16-byte chunks spread over the worker's lanes)
+    using FS = FoldSmem<T>;
+    constexpr int EPC = 16 / (int)sizeof(T), RCH = NX / EPC;  // elements / chunks per 12-vector
+    const bool has_ur = it.uref != nullptr;
+    auto prefetch = [&](int sg) {
+        if (sg >= 0) {
+            T *d = s.in[sg % 3];
+            const size_t o = (size_t)b * (N + 2) * NX + (size_t)sg * NX;
+            const size_t ou = ((size_t)b * (N + 1) + (sg <= N ? sg : 0)) * NX;
+            const int nrow = sg <= N ? (has_ur ? 6 : 5) : 3;
+            for (int c = lane; c < nrow * RCH; c += WS) {
+                const int q = c / RCH, e = (c - q * RCH) * EPC;
+                const T *src = q == 0 ? it.x + o : q == 1 ? it.lam + o : q == 2 ? it.xref + o
+                             : q == 3 ? it.u + ou : q == 4 ? it.feet + ou : it.uref + ou;
+                cp_async16(d + 12 * q + e, src + e);
+            }
+            if (sg <= N && lane == 0) cp_async4(d + FS::IN_CON, it.con + ((size_t)b * (N + 1) + sg) * 4);
+        }
+        cp_async_commit();
+    };
+    prefetch(N + 1);
+    prefetch(N);
     __syncwarp(mask);
     for (int i = N; i >= 0; --i) {
-        const size_t st = (size_t)b * (N + 1) + i;
-        const T *x = xb + (size_t)i * NX, *lam = lb + (size_t)i * NX, *ln = lam + NX;
-        const T *u = it.u + st * NX, *feet = it.feet + st * 12;
-        const uint8_t *con = it.con + st * 4;
-        const T *ur = it.uref ? it.uref + st * NX : nullptr;
+        prefetch(i - 1);
+        cp_async_wait<1>();
+        __syncwarp(mask);
+        const T *cur = s.in[i % 3], *nxt = s.in[(i + 1) % 3];
+        const T *x = cur + FS::IN_X, *lam = cur + FS::IN_L, *ln = nxt + FS::IN_L;
+        const T *u = cur + FS::IN_U, *feet = cur + FS::IN_F;
+        const uint8_t *con = reinterpret_cast<const uint8_t *>(cur + FS::IN_CON);
+        const T *ur = has_ur ? cur + FS::IN_UR : nullptr;
         // ---------------- linearise stage i
         SrbdRow<T> row;
         srbd_stage_row<T>(K, x, u, feet, con, ur, r, row);
@@ -98,7 +127,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
             st_row<T, NX, true>(s.A + r * NX, arow);
             st_row<T, NX, true>(s.B + r * NX, row.Brow);
             st_row<T, NX, true>(s.X + r * NX, row.Arow);  // dt Fx (scratch)
-            s.c[r] = (x[r] - x[NX + r]) + dt * row.fr;     // b_i = h(x_i, u_i) - x_{i+1}
+            s.c[r] = (x[r] - nxt[FS::IN_X + r]) + dt * row.fr;  // b_i = h(x_i, u_i) - x_{i+1}
         }
         __syncwarp(mask);
         T qr, rr;
@@ -106,7 +135,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIt
             T ATl = T(0), BTl = T(0);
 #pragma unroll
             for (int t = 0; t < NX; ++t) { ATl = fma(s.X[t * NX + r], ln[t], ATl); BTl = fma(s.B[t * NX + r], ln[t], BTl); }
-            qr = T(K.wx[r]) * (x[r] - xrb[(size_t)i * NX + r]) + ((ln[r] - lam[r]) + ATl);
+            qr = T(K.wx[r]) * (x[r] - cur[FS::IN_XR + r]) + ((ln[r] - lam[r]) + ATl);
             rr = row.rg + BTl;
         }
         // ---------------- element e_i (Eq. 12 with S = 0): A~ = A, P~ = Q, p~ = q,

@@ -88,6 +88,7 @@ struct pdilqr_ctx {
     SrbdConst K;
     int launches;
     int occ_fold = 4, occ_ls = 4;  // minimum resident CTAs per SM requested from ptxas (register cap: 128)
+    int fold_tpb = 64;             // k_srbd_bwd_fold block size (32 / 64 / 128)
     int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
     int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
@@ -562,16 +563,19 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         dl = reinterpret_cast<T *>(h->ws + h->lay.dir[2]);
     }
     {
-        const size_t smem = 8 * sizeof(FoldSmem<T>);
         Prof pf(h, "k_srbd_bwd_fold", st);
-        auto go = [&](auto kern) {
+        auto go = [&](auto kern, int tpb) {
+            const int ipb = tpb / 16;  // instances per block
+            const size_t smem = (size_t)ipb * sizeof(FoldSmem<T>);
             set_smem(kern, smem);
-            kern<<<(B + 7) / 8, 128, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, info_tmp);
+            kern<<<(B + ipb - 1) / ipb, tpb, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, info_tmp);
         };
-        switch (h->occ_fold) {
-            case 3: go(k_srbd_bwd_fold<T, 3>); break;
-            case 4: go(k_srbd_bwd_fold<T, 4>); break;
-            default: go(k_srbd_bwd_fold<T, 2>); break;
+        switch (h->occ_fold * 1000 + h->fold_tpb) {
+            case 4032: go(k_srbd_bwd_fold<T, 4, 32>, 32); break;
+            case 4128: go(k_srbd_bwd_fold<T, 4, 128>, 128); break;
+            case 3064: go(k_srbd_bwd_fold<T, 3, 64>, 64); break;
+            case 2064: go(k_srbd_bwd_fold<T, 2, 64>, 64); break;
+            default: go(k_srbd_bwd_fold<T, 4, 64>, 64); break;
         }
     }
     {
@@ -736,6 +740,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     K.theta_max = h->cfg.theta_max; K.c1 = h->cfg.armijo_c1; K.n_alpha = h->cfg.n_alpha;
     if (const char *e = std::getenv("PDILQR_OCC_FOLD")) h->occ_fold = std::atoi(e);  // tuning knobs
     if (const char *e = std::getenv("PDILQR_OCC_LS")) h->occ_ls = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_FOLD_TPB")) h->fold_tpb = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FUSED")) h->fused = std::atoi(e);
     // latency regime: few instances -> spread every tree level over all SMs (cooperative launch)
     h->grid_scan = cfg->batch < 148 && (Jb > 1 || Jf > 1);

@@ -39,8 +39,11 @@ struct FoldSmem {
     T in[3][IN];
 };
 
-template <typename T, int MINB>
-__global__ void __launch_bounds__(128, MINB) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+// TPB threads per block (2 workers per warp); MINB * 128 / TPB blocks per SM keep the 128-register
+// cap.  Small blocks balance the one-wave grid across the 148 SMs (B = 4096: 512 blocks of 128
+// threads put 4 blocks on 68 SMs and 3 on 80; 1024 blocks of 64 threads put 7 or 6).
+template <typename T, int MINB, int TPB = 64>
+__global__ void __launch_bounds__(TPB, MINB * 128 / TPB) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
                                                              int32_t *info_out) {
     constexpr int WS = 16, NX = 12;
     constexpr int TP = TE<NX>::SIZE;

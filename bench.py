@@ -339,8 +339,11 @@ def main():
         avg_s = tot / launches / 1e3
         ach = fl[dom] * B / avg_s / 1e12
         step_ms = ms / args.steps
+        traffic, tsrc = ncu_traffic(dom)
         roof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                "traffic": None, "flops_per_launch": fl[dom] * B, "avg_launch_ms": avg_s * 1e3,
+                "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read + write)",
+                "traffic_source": f"profiles/{tsrc} (ncu --set full, B={B})" if tsrc else None,
+                "flops_per_launch": fl[dom] * B, "avg_launch_ms": avg_s * 1e3,
                 "share_of_step": (tot / launches) / step_ms,
                 "peak_basis": f"FP32 FMA pipe: 148 SMs x 128 lanes x 2 flop x {sm_mhz:.0f} MHz (max SM clock)",
                 "per_kernel_ms": {k: v[1] / v[0] for k, v in prof.items()}}
@@ -426,6 +429,32 @@ def latency_sweep(P, torch, dev, horizons, reps, warm=30):
     return {"metric": "p50 single-solve latency vs horizon N (B=1, config 2, full SQP step)", "unit": "us",
             "timing": "CUDA-graph replay of pdilqr_step, CUDA events per replay (device); e2e = wall time of "
                       "pdilqr_tick_host + stream sync (host)", "per_dtype": out}
+
+
+def ncu_traffic(kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum (bytes per launch) of `kernel` from the newest
+    committed `ncu --set full` summary under profiles/ (r<round>_v<version>_*_ncu.json)."""
+    import glob
+    import re
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    best = None
+    for f in glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r*_v*_*ncu.json")):
+        m = re.search(r"r(\d+)_v(\d+)_", os.path.basename(f))
+        if not m:
+            continue
+        key = (int(m.group(1)), int(m.group(2)))
+        try:
+            rows = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        for r in rows:
+            if r.get("kernel", "").split("<")[0].split()[-1] == kernel and (best is None or key > best[0]):
+                tot = 0.0
+                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    v, u = r[k].split()
+                    tot += float(v) * units[u]
+                best = (key, tot, os.path.basename(f))
+    return (best[1], best[2]) if best else (None, None)
 
 
 def closed_loop_bench(P, torch, dev, B, N, ticks, warm=5):

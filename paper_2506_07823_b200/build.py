@@ -21,6 +21,10 @@ NVCC_FLAGS = [
     "--expt-relaxed-constexpr",
     "-Xptxas", "-warn-spills",
 ]
+# PDILQR_FAST_BUILD=1: nvcc --split-compile (all host cores, ~3x faster build) for development
+# iterations only -- measured 9% slower SRBD kernels on B200, so the default build does not use it.
+if os.environ.get("PDILQR_FAST_BUILD") == "1":
+    NVCC_FLAGS.append("--split-compile=0")
 
 
 def nvcc() -> str:

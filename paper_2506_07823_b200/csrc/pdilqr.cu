@@ -18,6 +18,7 @@
 #include "srbd.cuh"
 #include "srbd_fused.cuh"
 #include "big.cuh"
+#include "big_ric.cuh"
 
 using namespace pdilqr;
 
@@ -90,6 +91,8 @@ struct pdilqr_ctx {
     int occ_fold = 4, occ_ls = 4;  // minimum resident CTAs per SM requested from ptxas (register cap: 128)
     int fold_tpb = 64;             // k_srbd_bwd_fold block size (32 / 64 / 128)
     int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
+    int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
+    bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
     int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
     // pdilqr_solve in progress: convergence bookkeeping handed to the update kernels
@@ -170,9 +173,10 @@ size_t big_slot(int n, int m) {
     const size_t init = (size_t)m * ld_of(m + 2 * n + 1);
     const size_t fold = (size_t)n * ld_of(n) * 2 + (size_t)n * ld_of(2 * n) + 2 * ld_of(n);
     const size_t pol = (size_t)n * ld_of(m) + (size_t)m * ld_of(m + n + 1) + ld_of(n);
-    return (std::max({init, fold, pol}) + 63) / 64 * 64;
+    return (std::max({init, fold, pol, ric_slot(n, m)}) + 63) / 64 * 64;
 }
 constexpr int kBigPersistent = 148 * 4;  // CTAs of the persistent (stage-parallel) big kernels
+constexpr size_t kRicSmemMax = 200 * 1024;  // k_big_ric keeps the m x m Cholesky factor in shared memory
 
 Layout make_big_layout(const pdilqr_config *c, int esz) {
     const size_t B = c->batch, N = c->N, n = c->n, m = c->m, LD = ld_of((int)n), LDU = ld_of((int)m);
@@ -405,6 +409,51 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
     ws.slot = big_slot(n, m);
     ws.fail = reinterpret_cast<int32_t *>(h->ws + h->lay.fail);
     cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
+    const size_t ric_smem = ric_smem_bytes(m, (int)sizeof(T));
+    if (ric_smem <= kRicSmemMax && !h->big_legacy) {  // fused Riccati-form fold (big_ric.cuh)
+        const int TMsel = (n <= 80 && h->ric_cs == 1) ? 5 : 3;
+        {
+            const int tpb = std::min(256, (m + 31) / 32 * 32);  // one thread per row of R
+            const int g = (int)std::min<long>((long)148 * (2048 / tpb), (long)B * (N + 1));
+            cudaFuncSetAttribute(k_big_rchk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
+            Prof pf(h, "k_big_rchk", st);
+            k_big_rchk<T><<<g, tpb, ric_smem, st>>>(qp.R, B, N, m, ws.fail);
+        }
+        {
+            auto kern = TMsel == 5 ? k_big_ric<T, 5> : k_big_ric<T, 3>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
+            if (h->ric_cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3((unsigned)(B * h->ric_cs));
+            lc.blockDim = dim3(RIC_THREADS);
+            lc.dynamicSmemBytes = ric_smem;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)h->ric_cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            Prof pf(h, "k_big_ric", st);
+            cudaError_t e = cudaLaunchKernelEx(&lc, kern, qp, B, N, d, ws, out, h->ric_cs);
+            if (e != cudaSuccess) return fail(PDILQR_ERR_CUDA, "k_big_ric launch (cluster %d): %s", h->ric_cs, cudaGetErrorString(e));
+        }
+        {
+            Prof pf(h, "k_big_fwd", st);
+            k_big_fwd<T><<<B, BIG_THREADS, 0, st>>>(qp.dx0, B, N, d, ws, out);
+        }
+        int launches = 3;
+        if (info) {
+            int32_t *nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
+            cudaMemsetAsync(nonfin, 0, (size_t)B * 4, st);
+            Prof pf(h, "k_finalize_info", st);
+            k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, nonfin, nullptr, info);
+            ++launches;
+        }
+        h->launches += launches;
+        return cuda_check("solve_lq (large, fused) launch");
+    }
     const int gpers = (int)std::min<long>((long)kBigPersistent, (long)B * (N + 2));
     // the augmented Gauss-Jordan matrix W lives in shared memory when it fits (n <= ~110 in fp32)
     const size_t kSmemW = 180 * 1024;
@@ -742,6 +791,37 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_OCC_LS")) h->occ_ls = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_TPB")) h->fold_tpb = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FUSED")) h->fused = std::atoi(e);
+    if (v == VBIG) {  // large path: cluster size of k_big_ric (CTAs per instance) so that B * CS fills the SMs
+        if (const char *e = std::getenv("PDILQR_BIG_LEGACY")) h->big_legacy = std::atoi(e) != 0;
+        DeviceGuard g(device);
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+        int cs = 1;
+        while (cs < 16 && (long)cfg->batch * cs * 2 <= sms) cs *= 2;
+        if (const char *e = std::getenv("PDILQR_BIG_CS")) cs = std::max(1, std::min(16, std::atoi(e)));
+        const size_t smem = ric_smem_bytes(cfg->m, esz);
+        while (cs > 1 && smem <= kRicSmemMax) {  // the device must co-schedule a whole cluster
+            const void *kern = esz == 4 ? (const void *)k_big_ric<float, 3> : (const void *)k_big_ric<double, 3>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3((unsigned)cs);
+            lc.blockDim = dim3(RIC_THREADS);
+            lc.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            int ncl = 0;
+            if (cudaOccupancyMaxActiveClusters(&ncl, kern, &lc) == cudaSuccess && ncl > 0) break;
+            cudaGetLastError();
+            cs /= 2;
+        }
+        h->ric_cs = cs;
+    }
     // latency regime: few instances -> spread every tree level over all SMs (cooperative launch)
     h->grid_scan = cfg->batch < 148 && (Jb > 1 || Jf > 1);
     if (const char *e = std::getenv("PDILQR_GRID_SCAN")) h->grid_scan = std::atoi(e) != 0 && (Jb > 1 || Jf > 1);

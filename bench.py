@@ -106,16 +106,32 @@ class ClockSampler:
         except (OSError, FileNotFoundError):
             self.proc = None
 
-    def stop(self) -> dict:
+    def _lines(self) -> int:
+        try:
+            with open(self.path) as f:
+                return sum(1 for _ in f)
+        except OSError:
+            return 0
+
+    def wait_ready(self, timeout: float = 10.0) -> int:
+        """Block until nvidia-smi has written its first sample (its start-up takes ~0.1-1 s); return the
+        number of lines written so far: samples before the timed region are dropped by stop()."""
+        t0 = time.time()
+        while self.proc is not None and self._lines() == 0 and time.time() - t0 < timeout:
+            time.sleep(0.01)
+        return self._lines()
+
+    def stop(self, skip: int = 0) -> dict:
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.03)  # let the sampler flush the last in-region sample
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         rows = []
-        for line in open(self.path):
+        for line in list(open(self.path))[skip:]:
             p = [x.strip() for x in line.split(",")]
             if len(p) >= 7:
                 rows.append(p)
@@ -197,6 +213,7 @@ def main():
                     help="horizons of the B=1 latency sweep (config 2), '' to skip")
     ap.add_argument("--latency-reps", type=int, default=300)
     ap.add_argument("--closed-loop-ticks", type=int, default=50, help="0 disables the closed-loop RTF leg")
+    ap.add_argument("--no-large", action="store_true", help="skip the large-dimension LQ leg (configs 4, 5)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -254,7 +271,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     clk.start()
-    time.sleep(0.05)
+    skip = clk.wait_ready()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -262,7 +279,7 @@ def main():
         h.step(it, stats)
     e1.record(stream)
     torch.cuda.synchronize()
-    clocks = clk.stop()
+    clocks = clk.stop(skip)
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
@@ -354,6 +371,9 @@ def main():
     clo = None
     if args.closed_loop_ticks > 0 and args.dtype == "f32":
         clo = closed_loop_bench(P, torch, dev, B, N, args.closed_loop_ticks)
+    large = None
+    if not args.no_large and args.dtype == "f32":
+        large = large_bench(P, torch, dev, sm_mhz=(clocks or {}).get("sm_max_mhz") or 1965.0)
     cpu = None if args.no_cpu_baseline else cpu_baseline(B, N, synth.BASE_SEED, args.cpu_budget)
     out = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -366,7 +386,7 @@ def main():
            "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "e2e": e2e,
            "roofline": roof, "cpu_baseline": cpu,
            "kernels_ms": {k: v[1] / v[0] for k, v in prof.items()},
-           "latency": lat, "closed_loop": clo}
+           "latency": lat, "closed_loop": clo, "large": large}
     if gather_ms is not None:
         out["final_allgather_ms"] = gather_ms
     print(json.dumps(out), flush=True)
@@ -492,6 +512,54 @@ def closed_loop_bench(P, torch, dev, B, N, ticks, warm=5):
                     "simulated env-seconds per wall second (Table I reading R23)" % N,
             "paper_table1_rtf": {"50hz": 370, "25hz": 570, "note": "RTX 3080 + i7-13700KF, JAX + MJX simulator included; context only (P:426-446)"},
             **out}
+
+
+def ric_flops_per_stage(n: int, m: int) -> float:
+    """FP32 flops of one stage of k_big_ric (big_ric.cuh phases 1-6, S present): PB, g, G, H, h,
+    Cholesky, two triangular solves per right-hand side (n + 1 of them), Abar, bbar, V, w, P (+ S^T K), p."""
+    return (2 * n * n * m + 2 * n * n + 2 * n * m * m + 2 * m * n * n + 2 * n * m + m ** 3 / 3
+            + 2 * m * m * (n + 1) + 2 * n * n * m + 2 * n * m + 2 * n ** 3 + 2 * n * n + 2 * n ** 3
+            + 2 * n * n * m + 2 * n * n + 4 * n * m)
+
+
+def large_bench(P, torch, dev, sm_mhz, reps=5):
+    """pdilqr_solve_lq on BASELINE configs 4 (n = m = 192, N = 50; B = 1 and 64) and 5 (n = 74, m = 32,
+    N = 100, B = 1024): CUDA-event time per solve (inputs resident), per-kernel split, and the FP32
+    rate of the fused Riccati-form fold against the FMA-pipe peak.  Data: 4 seeded instances tiled
+    over the batch (the kernels' work does not depend on the values)."""
+    import numpy as np
+    res = {}
+    for name, B, N, n, m, kind in (("config4_b1", 1, 50, 192, 192, "dense"), ("config4_b64", 64, 50, 192, 192, "dense"),
+                                   ("config5_b1024", 1024, 100, 74, 32, "wb")):
+        base = synth.random_lq(min(B, 4), N, n, m, kind=kind, seed=7)
+        qp = {}
+        for k, v in base.items():
+            t = torch.from_numpy(v.astype(np.float32)).to(dev)
+            rep = (B + t.shape[0] - 1) // t.shape[0]
+            qp[k] = t.repeat((rep,) + (1,) * (t.dim() - 1))[:B].contiguous()
+        h = P.PdIlqr(N=N, n=n, m=m, batch=B, dtype=torch.float32, device=dev)
+        out = h.solve_lq(qp)
+        out = h.solve_lq(qp, out=out)
+        torch.cuda.synchronize()
+        h.profile(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            h.solve_lq(qp, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        pr = h.profile_read()
+        h.profile(False)
+        ms = e0.elapsed_time(e1) / reps
+        kms = {k: v[1] / v[0] for k, v in pr.items()}
+        fl = ric_flops_per_stage(n, m) * (N + 1) * B
+        ric = kms.get("k_big_ric")
+        res[name] = {"B": B, "N": N, "n": n, "m": m, "ms_per_solve_lq": ms, "solves_per_s": B / ms * 1e3,
+                     "kernels_ms": kms, "info_ok": bool((out["info"] == 0).all()),
+                     "fold_flops": fl, "fold_tflops": (fl / ric / 1e9) if ric else None,
+                     "fold_frac_fp32_peak": (fl / ric / 1e9 / fp32_peak_tflops(sm_mhz)) if ric else None}
+        del h, out, qp
+    return res
 
 
 def h_chunk(args, B, N):

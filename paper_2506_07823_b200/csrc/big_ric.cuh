@@ -50,36 +50,47 @@ __device__ __forceinline__ void ric_sync(int CS) {
     else __syncthreads();
 }
 
-// Tiles t = part, part + nparts, ... of C[Mr x Nc] = (Cin ? Cin : 0) + alpha op(A)[Mr x K] op(B)[K x Nc].
-// op(A) = A (row-major Mr x K, ld lda) or A^T (A stored K x Mr); same for B.  Cin may alias C with
-// the same leading dimension (each element is read and written by the same thread).
-template <typename T, int TM, bool TA, bool TB>
+// Tiles t = part, part + nparts, ... of C[Mr x Nc] = (Cin ? Cin : 0) + alpha op(A)[Mr x K] op(B)[K x Nc]
+// with (16 TR) x (16 TC) output tiles, TR x TC register micro-tiles (rows ty + 16 q, columns
+// tx + 16 w: broadcast A reads, conflict-free B reads), 16-deep k panels staged through shared
+// memory, the next panel prefetched into registers.  op(A) = A (row-major Mr x K, ld lda) or A^T (A
+// stored K x Mr); same for B.  Cin may alias C with the same leading dimension (each element is read
+// and written by the same thread).  TR, TC <= TM of the shared tile buffer.
+template <typename T, int TR, int TC, bool TA, bool TB, int TM>
 __device__ void ric_gemm(int Mr, int Nc, int K, T alpha, const T *A, int lda, const T *Bm, int ldb, const T *Cin,
                          int ldci, T *C, int ldc, int part, int nparts, RicTiles<T, TM> &sm) {
-    constexpr int TS = 16 * TM;
+    static_assert(TR <= TM && TC <= TM, "tile buffer too small");
+    constexpr int TSR = 16 * TR, TSC = 16 * TC;
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-    const int tmn = (Mr + TS - 1) / TS, tnn = (Nc + TS - 1) / TS;
-    // fixed per-thread panel coordinates: element e = tid + 256 s of the 16 x TS panel
-    int amm[TM], akk[TM], bnn[TM], bkk[TM];
+    const int tmn = (Mr + TSR - 1) / TSR, tnn = (Nc + TSC - 1) / TSC;
+    // fixed per-thread panel coordinates: element e = tid + 256 s of the 16 x TSR (A) / 16 x TSC (B) panel
+    int amm[TR], akk[TR], bnn[TC], bkk[TC];
 #pragma unroll
-    for (int s = 0; s < TM; ++s) {
+    for (int s = 0; s < TR; ++s) {
         const int e = tid + RIC_THREADS * s;
-        if (TA) { amm[s] = e % TS; akk[s] = e / TS; } else { akk[s] = e & 15; amm[s] = e >> 4; }
-        if (TB) { bkk[s] = e & 15; bnn[s] = e >> 4; } else { bnn[s] = e % TS; bkk[s] = e / TS; }
+        if (TA) { amm[s] = e % TSR; akk[s] = e / TSR; } else { akk[s] = e & 15; amm[s] = e >> 4; }
+    }
+#pragma unroll
+    for (int s = 0; s < TC; ++s) {
+        const int e = tid + RIC_THREADS * s;
+        if (TB) { bkk[s] = e & 15; bnn[s] = e >> 4; } else { bnn[s] = e % TSC; bkk[s] = e / TSC; }
     }
     for (int t = part; t < tmn * tnn; t += nparts) {
-        const int tm = (t / tnn) * TS, tn = (t % tnn) * TS;
-        T acc[TM][TM];
+        const int tm = (t / tnn) * TSR, tn = (t % tnn) * TSC;
+        T acc[TR][TC];
 #pragma unroll
-        for (int a = 0; a < TM; ++a)
+        for (int a = 0; a < TR; ++a)
 #pragma unroll
-            for (int c = 0; c < TM; ++c) acc[a][c] = T(0);
-        T pa[TM], pb[TM];
+            for (int c = 0; c < TC; ++c) acc[a][c] = T(0);
+        T pa[TR], pb[TC];
         auto fetch = [&](int k0) {
 #pragma unroll
-            for (int s = 0; s < TM; ++s) {
+            for (int s = 0; s < TR; ++s) {
                 const int r = tm + amm[s], c = k0 + akk[s];
                 pa[s] = (r < Mr && c < K) ? ldg_cg(TA ? A + (size_t)c * lda + r : A + (size_t)r * lda + c) : T(0);
+            }
+#pragma unroll
+            for (int s = 0; s < TC; ++s) {
                 const int rb = k0 + bkk[s], cb = tn + bnn[s];
                 pb[s] = (rb < K && cb < Nc) ? ldg_cg(TB ? Bm + (size_t)cb * ldb + rb : Bm + (size_t)rb * ldb + cb) : T(0);
             }
@@ -87,35 +98,39 @@ __device__ void ric_gemm(int Mr, int Nc, int K, T alpha, const T *A, int lda, co
         fetch(0);
         for (int k0 = 0; k0 < K; k0 += 16) {
 #pragma unroll
-            for (int s = 0; s < TM; ++s) {
-                sm.As[akk[s]][amm[s]] = pa[s];
-                sm.Bs[bkk[s]][bnn[s]] = pb[s];
-            }
+            for (int s = 0; s < TR; ++s) sm.As[akk[s]][amm[s]] = pa[s];
+#pragma unroll
+            for (int s = 0; s < TC; ++s) sm.Bs[bkk[s]][bnn[s]] = pb[s];
             __syncthreads();
             if (k0 + 16 < K) fetch(k0 + 16);
 #pragma unroll
             for (int kk = 0; kk < 16; ++kk) {
-                T a[TM], b[TM];
+                T a[TR], b[TC];
 #pragma unroll
-                for (int q = 0; q < TM; ++q) { a[q] = sm.As[kk][ty + 16 * q]; b[q] = sm.Bs[kk][tx + 16 * q]; }
+                for (int q = 0; q < TR; ++q) a[q] = sm.As[kk][ty + 16 * q];
 #pragma unroll
-                for (int q = 0; q < TM; ++q)
+                for (int q = 0; q < TC; ++q) b[q] = sm.Bs[kk][tx + 16 * q];
 #pragma unroll
-                    for (int w = 0; w < TM; ++w) acc[q][w] = fma(a[q], b[w], acc[q][w]);
+                for (int q = 0; q < TR; ++q)
+#pragma unroll
+                    for (int w = 0; w < TC; ++w) acc[q][w] = fma(a[q], b[w], acc[q][w]);
             }
             __syncthreads();
         }
 #pragma unroll
-        for (int q = 0; q < TM; ++q) {
+        for (int q = 0; q < TR; ++q) {
             const int r = tm + ty + 16 * q;
             if (r >= Mr) continue;
+            T cin[TC];
 #pragma unroll
-            for (int w = 0; w < TM; ++w) {
+            for (int w = 0; w < TC; ++w) {
                 const int c = tn + tx + 16 * w;
-                if (c < Nc) {
-                    const T v = alpha * acc[q][w];
-                    C[(size_t)r * ldc + c] = Cin ? ldg_cg(Cin + (size_t)r * ldci + c) + v : v;
-                }
+                cin[w] = (Cin && c < Nc) ? ldg_cg(Cin + (size_t)r * ldci + c) : T(0);
+            }
+#pragma unroll
+            for (int w = 0; w < TC; ++w) {
+                const int c = tn + tx + 16 * w;
+                if (c < Nc) C[(size_t)r * ldc + c] = fma(alpha, acc[q][w], cin[w]);
             }
         }
     }
@@ -186,22 +201,32 @@ __device__ bool cta_chol(int m, T *L, int ld, T *dinv) {
     if (tid == 0) s_ok = 1;
     for (int kb = 0; kb < m; kb += 16) {
         const int nb = min(16, m - kb);
-        if (wid == 0) {  // (a) diagonal block
+        if (wid == 0) {  // (a) diagonal block: lane i < nb holds row kb + i in registers
+            T x[16];
+            const bool own = lane < nb;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) x[j] = (own && j < nb) ? L[(size_t)(kb + lane) * ld + kb + j] : T(0);
             bool ok = true;
-            for (int k = 0; k < nb; ++k) {
-                const T d = L[(size_t)(kb + k) * ld + kb + k];
-                ok = ok && d > T(0) && isfinite(d);
-                const T sd = sqrt(d), is = T(1) / sd;
-                __syncwarp();
-                if (lane > k && lane < nb) L[(size_t)(kb + lane) * ld + kb + k] *= is;
-                if (lane == 0) { L[(size_t)(kb + k) * ld + kb + k] = sd; dinv[kb + k] = is; }
-                __syncwarp();
-                if (lane > k && lane < nb) {
-                    T *Li = L + (size_t)(kb + lane) * ld + kb;
-                    const T lik = Li[k];
-                    for (int j = k + 1; j <= lane; ++j) Li[j] = fma(-lik, L[(size_t)(kb + j) * ld + kb + k], Li[j]);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k < nb) {
+                    const T d = __shfl_sync(0xffffffffu, x[k], k);
+                    ok = ok && d > T(0) && isfinite(d);
+                    const T sd = sqrt(d), is = T(1) / sd;
+                    const T lik = lane > k ? x[k] * is : (lane == k ? sd : T(0));
+                    x[k] = lane >= k ? lik : x[k];
+                    if (lane == 0) dinv[kb + k] = is;
+#pragma unroll
+                    for (int j = k + 1; j < 16; ++j) {
+                        const T ljk = __shfl_sync(0xffffffffu, lik, j);
+                        if (lane >= j) x[j] = fma(-lik, ljk, x[j]);
+                    }
                 }
-                __syncwarp();
+            }
+            if (own) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (j <= lane && j < nb) L[(size_t)(kb + lane) * ld + kb + j] = x[j];
             }
             if (!ok && lane == 0) s_ok = 0;
         }
@@ -341,9 +366,10 @@ __host__ __device__ inline size_t ric_smem_bytes(int m, int esz) {
 
 // Fused reverse scan + policy (phases 1-7 above), one cluster of CS CTAs per instance.
 // Writes P_i, p_i (ws.Pp), K_i, k_i (ws.Kk, out.K, out.k), Abar_i, bbar_i (ws.tel).
-template <typename T, int TM>
+template <typename T, int TN, int TU>
 __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B, int N, BigDims<T> d, BigWork<T> ws,
                                                          LqOut<T> out, int CS) {
+    constexpr int TM = TN > TU ? TN : TU;
     __shared__ RicTiles<T, TM> tiles;
     extern __shared__ __align__(16) unsigned char dyn[];
     const int n = d.n, m = d.m, LD = d.LD, LDU = d.LDU;
@@ -374,12 +400,12 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
         T *Kw = ws.Kk + st * d.ksize(), *kw = Kw + (size_t)m * LD;
         T *Ab = ws.tel + st * d.psize(), *bb = Ab + (size_t)n * LD;
         // phase 1: PB = P' B ; g = p' + P' c
-        ric_gemm<T, TM, false, false>(n, m, n, T(1), Pn, LD, Bm, m, nullptr, 0, PB, ldpb, rank, CS, tiles);
+        ric_gemm<T, TN, TU, false, false>(n, m, n, T(1), Pn, LD, Bm, m, nullptr, 0, PB, ldpb, rank, CS, tiles);
         ric_gemv<T, false>(n, n, Pn, LD, c, pn, 1, g, 1, gw, nwc);
         ric_sync(CS);
         // phase 2: W = [R + B^T PB | S + PB^T A | r + B^T g]
-        ric_gemm<T, TM, true, false>(m, m, n, T(1), Bm, m, PB, ldpb, R, m, W, ldw, rank, CS, tiles);
-        ric_gemm<T, TM, true, false>(m, n, n, T(1), PB, ldpb, A, n, S, n, W + m, ldw, rank, CS, tiles);
+        ric_gemm<T, TU, TU, true, false>(m, m, n, T(1), Bm, m, PB, ldpb, R, m, W, ldw, rank, CS, tiles);
+        ric_gemm<T, TU, TN, true, false>(m, n, n, T(1), PB, ldpb, A, n, S, n, W + m, ldw, rank, CS, tiles);
         ric_gemv<T, true>(m, n, Bm, m, g, r, 1, W + m + n, ldw, gw, nwc);  // column m+n of W
         ric_sync(CS);
         // phase 3: Cholesky of G (every CTA, own shared memory), [K | k] = -G^-1 [H | h]
@@ -417,26 +443,49 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
         }
         ric_sync(CS);
         // phase 4: Abar = A + B K ; bbar = c + B k
-        ric_gemm<T, TM, false, false>(n, n, m, T(1), Bm, m, Kw, LD, A, n, Ab, LD, rank, CS, tiles);
+        ric_gemm<T, TN, TN, false, false>(n, n, m, T(1), Bm, m, Kw, LD, A, n, Ab, LD, rank, CS, tiles);
         ric_gemv<T, false>(n, m, Bm, m, kw, c, 1, bb, 1, gw, nwc);
         ric_sync(CS);
         // phase 5: V = P' Abar ; w = p' + P' bbar
-        ric_gemm<T, TM, false, false>(n, n, n, T(1), Pn, LD, Ab, LD, nullptr, 0, V, LD, rank, CS, tiles);
+        ric_gemm<T, TN, TN, false, false>(n, n, n, T(1), Pn, LD, Ab, LD, nullptr, 0, V, LD, rank, CS, tiles);
         ric_gemv<T, false>(n, n, Pn, LD, bb, pn, 1, w, 1, gw, nwc);
         ric_sync(CS);
         // phase 6: P_i = Q + A^T V (+ S^T K) ; p_i = q + A^T w (+ S^T k)   (same tiles / rows: no barrier)
-        ric_gemm<T, TM, true, false>(n, n, n, T(1), A, n, V, LD, qp.Q + st * n * n, n, Pc, LD, rank, CS, tiles);
-        if (S) ric_gemm<T, TM, true, false>(n, n, m, T(1), S, n, Kw, LD, Pc, LD, Pc, LD, rank, CS, tiles);
+        ric_gemm<T, TN, TN, true, false>(n, n, n, T(1), A, n, V, LD, qp.Q + st * n * n, n, Pc, LD, rank, CS, tiles);
+        if (S) ric_gemm<T, TN, TN, true, false>(n, n, m, T(1), S, n, Kw, LD, Pc, LD, Pc, LD, rank, CS, tiles);
         ric_gemv<T, true>(n, n, A, n, w, q, 1, pc, 1, gw, nwc);
         if (S) ric_gemv<T, true>(n, m, S, n, kw, pc, 1, pc, 1, gw, nwc);
         ric_sync(CS);
-        // phase 7: re-symmetrise P_i (R22); pairs (r, c), (c, r) owned by one thread
-        for (int t = rank * RIC_THREADS + threadIdx.x; t < n * n; t += CS * RIC_THREADS) {
-            const int rr = t / n, cc = t % n;
-            if (cc > rr) {
-                const T v = T(0.5) * (ldg_cg(Pc + (size_t)rr * LD + cc) + ldg_cg(Pc + (size_t)cc * LD + rr));
-                Pc[(size_t)rr * LD + cc] = v;
-                Pc[(size_t)cc * LD + rr] = v;
+        // phase 7: re-symmetrise P_i (R22): upper-triangle pairs (r, c), (c, r) owned by one thread,
+        // four pairs per batch with all loads issued before the stores
+        {
+            const int np = n * (n - 1) / 2, stride = CS * RIC_THREADS;
+            for (int t0 = rank * RIC_THREADS + threadIdx.x; t0 < np; t0 += 4 * stride) {
+                int ra[4], ca[4];
+                T u[4], l[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    int t = t0 + e * stride;
+                    ra[e] = -1;
+                    if (t < np) {  // pair t -> (r, c), c > r: rows of the strict upper triangle
+                        int rr = (int)((2 * n - 1 - sqrtf((float)((2 * n - 1) * (2 * n - 1) - 8 * t))) * 0.5f);
+                        rr = max(0, min(rr, n - 2));
+                        while (rr > 0 && rr * (2 * n - rr - 1) / 2 > t) --rr;
+                        while ((rr + 1) * (2 * n - rr - 2) / 2 <= t) ++rr;
+                        ra[e] = rr;
+                        ca[e] = rr + 1 + (t - rr * (2 * n - rr - 1) / 2);
+                        u[e] = ldg_cg(Pc + (size_t)ra[e] * LD + ca[e]);
+                        l[e] = ldg_cg(Pc + (size_t)ca[e] * LD + ra[e]);
+                    }
+                }
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (ra[e] >= 0) {
+                        const T v = T(0.5) * (u[e] + l[e]);
+                        Pc[(size_t)ra[e] * LD + ca[e]] = v;
+                        Pc[(size_t)ca[e] * LD + ra[e]] = v;
+                    }
+                }
             }
         }
         ric_sync(CS);

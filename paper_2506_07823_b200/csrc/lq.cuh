@@ -623,6 +623,69 @@ __global__ void __launch_bounds__(128) k_scan_bwd_grid(int B, int N, int chunk, 
     }
 }
 
+// Depth-optimal (Kogge-Stone) reverse scan for the latency regime (leaf chunk 1, few instances).
+// Level d (d = 1, 2, 4, ...): every incomplete s_i becomes s_i (x) s_{i+d}.  At the start of level d,
+// s_j covers stages [j, j + d) and is complete (the suffix through the terminal, R5) iff j + d >= L;
+// a complete right operand is a suffix, so the cheap rule applies and the result is complete too.
+// ceil(log2 L) dependent levels (6 at N = 50, 10 at N = 1000) instead of the Blelloch tree's
+// 2 ceil(log2 L) + 1, for L log L combines instead of 2L -- chosen when a level fits in one wave of
+// workers (D9).  Incomplete elements ping-pong between ws.elems (level-0 input) and
+// ws.vslots (per-instance stride Pv >= L); a completed suffix lives only in ws.Pp as (P_i, p_i),
+// which is all the cheap rule reads of its right operand.
+template <typename T, int NX>
+__global__ void __launch_bounds__(128) k_scan_bwd_ks(int B, int N, int Pv, LqWork<T> ws) {
+    using SB = ScanBwd<T, NX>;
+    using L = VE<NX>;
+    constexpr int WS = worker_width(NX);
+    constexpr int TP = TE<NX>::SIZE;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    cg::grid_group grid = cg::this_grid();
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    CombineSmem<T, NX> &s = reinterpret_cast<CombineSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    const int wpb = blockDim.x / WS;
+    const long gw = (long)blockIdx.x * wpb + threadIdx.x / WS, GW = (long)gridDim.x * wpb;
+    const int L2 = N + 2;
+    auto buf = [&](int k, int b, int i) -> T * {
+        return k == 0 ? ws.elems + ((size_t)b * L2 + i) * L::SIZE : ws.vslots + ((size_t)b * Pv + i) * L::SIZE;
+    };
+    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < (long)B * TP; t += (long)gridDim.x * blockDim.x) {
+        const int b = (int)(t / TP), k = (int)(t % TP);   // s_{L-1} = e_{L-1} (terminal, Eq. 13)
+        const T *e = buf(0, b, L2 - 1);
+        ws.Pp[((size_t)b * L2 + L2 - 1) * TP + k] = k < NX * NX ? e[L::P + k] : e[L::p + (k - NX * NX)];
+    }
+    int cur = 0;
+    for (int d = 1; d < L2; d <<= 1) {
+        grid.sync();
+        for (long u = gw; u < (long)B * L2; u += GW) {
+            const int b = (int)(u / L2), i = (int)(u % L2);
+            if (i + d >= L2) continue;  // s_i already complete
+            int fail = INT_MAX;
+            wcopy<T, L::SIZE, WS>(s.e1, buf(cur, b, i), lane);
+            if (i + 2 * d >= L2) {  // right operand s_{i+d} complete: suffix (P, p) only
+                const T *Pr = ws.Pp + ((size_t)b * L2 + i + d) * TP;
+                for (int k = lane; k < TP; k += WS) {
+                    if (k < NX * NX) s.e2[L::P + k] = Pr[k];
+                    else s.e2[L::p + (k - NX * NX)] = Pr[k];
+                }
+                __syncwarp(mask);
+                T Po[NX], po;
+                if (!combine_cheap<T, NX, WS>(s, mask, lane, Po, po)) fail = i + 1;
+                SB::out_Pp(ws.Pp + ((size_t)b * L2 + i) * TP, Po, po, lane);
+            } else {
+                wcopy<T, L::SIZE, WS>(s.e2, buf(cur, b, i + d), lane);
+                __syncwarp(mask);
+                T Ao[NX], Co[NX], Po[NX], bo, po;
+                if (!combine_full<T, NX, WS>(s, mask, lane, Ao, Co, Po, bo, po)) fail = i + 1;
+                SB::store_elem_rows(buf(cur ^ 1, b, i), Ao, Co, Po, bo, po, lane);
+            }
+            if (fail != INT_MAX && lane == 0) atomicMin(ws.fail + b, (1 << 24) | fail);
+            __syncwarp(mask);
+        }
+        cur ^= 1;
+    }
+}
+
 // ---------------------------------------------------------------------- policy (Eq. 5 rows)
 // Per stage i (one worker):  PB = P_{i+1} B,  g = p_{i+1} + P_{i+1} b,
 //   G = R + B^T PB,  H = S + PB^T A,  h = B^T g + r,  K = -G^-1 H,  k = -G^-1 h  (GJ, SPD),

@@ -95,6 +95,8 @@ struct pdilqr_ctx {
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
     int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
+    int coop_ks = 0;               // ... of the depth-optimal (Kogge-Stone) reverse scan
+    bool ks_bwd = false;           // latency regime: Kogge-Stone instead of the Blelloch tree (D9)
     // pdilqr_solve in progress: convergence bookkeeping handed to the update kernels
     int32_t *sc_conv = nullptr, *sc_active = nullptr;
     double sc_tol = 0.0;
@@ -311,6 +313,17 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         const int ipb = 128 / WSX;
         k_fold<T, NX, 4><<<(B + ipb - 1) / ipb, 128, smem, st>>>(B, N, ws);
         ++launches;
+    } else if (h->grid_scan && h->ks_bwd) {  // cooperative depth-optimal scan (latency regime, D9)
+        int Pv = h->Pv, Bv = B, Nv = N;
+        const int wpb = 128 / WSX;
+        const size_t smem = wpb * sizeof(CombineSmem<T, NX>);
+        set_smem(k_scan_bwd_ks<T, NX>, smem);
+        const long units = (long)B * (N + 2);
+        const int grid = (int)std::max(1L, std::min((long)h->coop_ks, (units + wpb - 1) / wpb));
+        void *args[] = {&Bv, &Nv, &Pv, &ws};
+        Prof pf(h, "k_scan_bwd_ks", st);
+        cudaLaunchCooperativeKernel((const void *)k_scan_bwd_ks<T, NX>, grid, 128, args, smem, st);
+        ++launches;
     } else if (h->grid_scan) {  // cooperative grid-wide tree (latency regime)
         int J = h->Jb, Pv = h->Pv, chunk = h->chunk, Bv = B, Nv = N;
         int *kinds = reinterpret_cast<int *>(h->ws + h->lay.kinds_b);
@@ -411,7 +424,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
     cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
     const size_t ric_smem = ric_smem_bytes(m, (int)sizeof(T));
     if (ric_smem <= kRicSmemMax && !h->big_legacy) {  // fused Riccati-form fold (big_ric.cuh)
-        const int TMsel = (n <= 80 && h->ric_cs == 1) ? 5 : 3;
+        const bool t52 = n <= 80 && m <= 32 && h->ric_cs == 1;  // config-5-like: 80-row n tiles, 32-wide m tiles
         {
             const int tpb = std::min(256, (m + 31) / 32 * 32);  // one thread per row of R
             const int g = (int)std::min<long>((long)148 * (2048 / tpb), (long)B * (N + 1));
@@ -420,7 +433,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
             k_big_rchk<T><<<g, tpb, ric_smem, st>>>(qp.R, B, N, m, ws.fail);
         }
         {
-            auto kern = TMsel == 5 ? k_big_ric<T, 5> : k_big_ric<T, 3>;
+            auto kern = t52 ? k_big_ric<T, 5, 2> : k_big_ric<T, 3, 3>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
             if (h->ric_cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaLaunchConfig_t lc{};
@@ -801,7 +814,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         if (const char *e = std::getenv("PDILQR_BIG_CS")) cs = std::max(1, std::min(16, std::atoi(e)));
         const size_t smem = ric_smem_bytes(cfg->m, esz);
         while (cs > 1 && smem <= kRicSmemMax) {  // the device must co-schedule a whole cluster
-            const void *kern = esz == 4 ? (const void *)k_big_ric<float, 3> : (const void *)k_big_ric<double, 3>;
+            const void *kern = esz == 4 ? (const void *)k_big_ric<float, 3, 3> : (const void *)k_big_ric<double, 3, 3>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaLaunchConfig_t lc{};
@@ -846,8 +859,25 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
             else if (v == V8) { occ(k_scan_bwd_grid<double, 8>, 16 * sizeof(CombineSmem<double, 8>), nb); occ(k_scan_fwd_grid<double, 8>, 16 * sizeof(FwdSmem<double, 8>), nf); }
             else { occ(k_scan_bwd_grid<double, 16>, 8 * sizeof(CombineSmem<double, 16>), nb); occ(k_scan_fwd_grid<double, 16>, 8 * sizeof(FwdSmem<double, 16>), nf); }
         }
+        int nk = 0;
+        if (esz == 4) {
+            if (v == V12) occ(k_scan_bwd_ks<float, 12>, 8 * sizeof(CombineSmem<float, 12>), nk);
+            else if (v == V4) occ(k_scan_bwd_ks<float, 4>, 32 * sizeof(CombineSmem<float, 4>), nk);
+            else if (v == V8) occ(k_scan_bwd_ks<float, 8>, 16 * sizeof(CombineSmem<float, 8>), nk);
+            else occ(k_scan_bwd_ks<float, 16>, 8 * sizeof(CombineSmem<float, 16>), nk);
+        } else {
+            if (v == V12) occ(k_scan_bwd_ks<double, 12>, 8 * sizeof(CombineSmem<double, 12>), nk);
+            else if (v == V4) occ(k_scan_bwd_ks<double, 4>, 32 * sizeof(CombineSmem<double, 4>), nk);
+            else if (v == V8) occ(k_scan_bwd_ks<double, 8>, 16 * sizeof(CombineSmem<double, 8>), nk);
+            else occ(k_scan_bwd_ks<double, 16>, 8 * sizeof(CombineSmem<double, 16>), nk);
+        }
         h->coop_bwd = nb;
         h->coop_fwd = nf;
+        h->coop_ks = nk;
+        // Kogge-Stone when every level of the pure tree fits in one wave of resident workers
+        const int wpb = 128 / worker_width(NX);
+        h->ks_bwd = chunk == 1 && (long)cfg->batch * (cfg->N + 2) <= (long)nk * wpb;
+        if (const char *e = std::getenv("PDILQR_SCAN_KS")) h->ks_bwd = chunk == 1 && std::atoi(e) != 0;
     }
     *out = h;
     return PDILQR_OK;

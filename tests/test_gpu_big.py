@@ -74,3 +74,35 @@ def test_big_info(P):
     qp["R"][1, 2] = -np.eye(8)
     out = solve(P, qp, torch.float32)
     assert out["info"][0] == 0 and out["info"][1] == 3
+
+
+@pytest.mark.parametrize("B", [1, 5, 40, 160])
+def test_cluster_sizes(P, O, B):
+    """k_big_ric with one CTA per instance (B >= 74: cluster size 1, config-5 tile shape) and with
+    clusters of 2..16 CTAs per instance (small B): same parity on a ragged size (n = 38, m = 21)."""
+    qp = rounded(synth.random_lq(B, 6, 38, 21, kind="wb" if B % 2 else "dense", seed=B), torch.float32)
+    out = solve(P, qp, torch.float32)
+    check(O, qp, out, 1e-4)
+
+
+def test_config5_tile_shape_batch(P, O):
+    """Config-5 dimensions at B = 148 (cluster size 1, 80 x 32 tiles) on 2 distinct instances tiled."""
+    base = rounded(synth.random_lq(2, 12, 74, 32, kind="wb", seed=5), torch.float32)
+    qp = {k: np.concatenate([v] * 74, axis=0) for k, v in base.items()}
+    out = solve(P, qp, torch.float32)
+    ref = O.solve_lq({k: v[:2] for k, v in qp.items()})
+    for k in ("dx", "du", "dlam"):
+        for b in (0, 1, 146, 147):
+            r = rel_per_instance(out[k][b:b + 1], ref[k][b % 2:b % 2 + 1])
+            assert r.max() <= 1e-4, (k, b, r.max())
+
+
+def test_legacy_matches_fused(P, monkeypatch):
+    """The element/fold/policy kernels (PDILQR_BIG_LEGACY=1, the M-solve combine) and the fused
+    Riccati-form kernel agree (both are the same KKT solution, D7)."""
+    qp = rounded(synth.random_lq(3, 10, 24, 18, seed=11), torch.float32)
+    a = solve(P, qp, torch.float32)
+    monkeypatch.setenv("PDILQR_BIG_LEGACY", "1")
+    b = solve(P, qp, torch.float32)
+    for k in ("dx", "du", "dlam"):
+        assert rel_per_instance(a[k], b[k]).max() <= 1e-4, k

@@ -160,3 +160,23 @@ def test_rejects_bad_arguments(P):
         h.solve_lq(qp)
     with pytest.raises(P.PdilqrError):
         P.PdIlqr(N=5, n=300, m=2, batch=2)
+
+
+@pytest.mark.parametrize("ks", ["0", "1"])
+@pytest.mark.parametrize("N", [0, 1, 6, 50, 63, 64, 200])
+def test_latency_scan_algorithms(P, O, monkeypatch, ks, N):
+    """Latency regime (leaf chunk 1, cooperative grid kernels): the depth-optimal Kogge-Stone reverse
+    scan (PDILQR_SCAN_KS=1, default when a level fits in one wave) and the Blelloch tree (=0) both
+    match the oracle, across horizons around powers of two."""
+    monkeypatch.setenv("PDILQR_SCAN_KS", ks)
+    qp = rounded(synth.random_lq(2, N, 12, 12, seed=300 + N), torch.float32)
+    out, _ = run_gpu(P, qp, torch.float32, 1)
+    check(O, qp, torch.float32, out)
+
+
+@pytest.mark.parametrize("ks", ["0", "1"])
+def test_latency_scan_algorithms_f64_padded(P, O, monkeypatch, ks):
+    monkeypatch.setenv("PDILQR_SCAN_KS", ks)
+    qp = rounded(synth.random_lq(3, 40, 7, 5, seed=77), torch.float64)
+    out, _ = run_gpu(P, qp, torch.float64, 1)
+    check(O, qp, torch.float64, out)

@@ -192,3 +192,10 @@ def test_step_long_horizon_tree_fp32(P, O, N):
     """Latency regime (B < 148: cooperative tree scans): fp32 first-step direction parity holds at
     long horizons (a sequential fp32 Riccati recursion diverges here)."""
     step_parity(P, O, 2, N, torch.float32, seed=60 + N, leaf_chunk=1, steps=1, dir_steps=(0,))
+
+
+@pytest.mark.parametrize("ks", ["0", "1"])
+def test_step_parity_scan_algorithms(P, O, monkeypatch, ks):
+    """SRBD step in the latency regime with the Kogge-Stone (1) and Blelloch (0) reverse scans."""
+    monkeypatch.setenv("PDILQR_SCAN_KS", ks)
+    step_parity(P, O, 2, 50, torch.float32, seed=33, leaf_chunk=1, steps=2, dir_steps=(0,))

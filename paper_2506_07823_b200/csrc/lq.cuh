@@ -1006,6 +1006,71 @@ __global__ void __launch_bounds__(128) k_scan_fwd_grid(const T *dx0, int B, int 
     }
 }
 
+// Depth-optimal (Kogge-Stone) forward scan, companion of k_scan_bwd_ks (D9).  t_j covers elements
+// (j - d, j] at the start of level d and is complete -- anchored at dx_0, i.e. (0, dx_{j+1}) -- iff
+// j < d.  Level d: every incomplete t_i (i >= d) becomes t_{i-d} then t_i; when t_{i-d} is complete
+// the result is dx_{i+1} = Abar_(i) dx_{i-d+1} + bbar_(i), written to the padded workspace X and to
+// the user's dx.  Incomplete composites ping-pong between ws.tel (level-0 input) and ws.tslots.
+template <typename T, int NX>
+__global__ void __launch_bounds__(128) k_scan_fwd_ks(const T *dx0, int B, int N, int n, int Pf, LqWork<T> ws, T *dx_out) {
+    using TL = TE<NX>;
+    constexpr int WS = worker_width(NX);
+    extern __shared__ __align__(16) unsigned char smraw[];
+    cg::grid_group grid = cg::this_grid();
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    FwdSmem<T, NX> &s = reinterpret_cast<FwdSmem<T, NX> *>(smraw)[threadIdx.x / WS];
+    const int wpb = blockDim.x / WS;
+    const long gw = (long)blockIdx.x * wpb + threadIdx.x / WS, GW = (long)gridDim.x * wpb;
+    const int Lf = N + 1, r = lane < NX ? lane : 0;
+    const bool vr = lane < NX && (n == NX || r < n);
+    auto buf = [&](int k, int b, int i) -> T * {
+        return k == 0 ? ws.tel + ((size_t)b * Lf + i) * TL::SIZE : ws.tslots + ((size_t)b * Pf + i) * TL::SIZE;
+    };
+    for (long b = gw; b < B; b += GW) {  // anchor: dx_0, and t_0 = (0, dx_1 = Abar_0 dx_0 + bbar_0)
+        T *X = ws.dxw + (size_t)b * (N + 2) * NX, *Xo = dx_out + (size_t)b * (N + 2) * n;
+        const T x0 = vr ? dx0[(size_t)b * n + r] : T(0);
+        if (lane < NX) { s.t2[TL::b + r] = x0; X[r] = x0; }
+        if (vr) Xo[r] = x0;
+        __syncwarp(mask);
+        const T *E = buf(0, (int)b, 0);
+        T arow[NX];
+        ld_row<T, NX, true>(arow, E + r * NX);
+        const T v = row_dot<T, NX>(arow, s.t2 + TL::b, E[TL::b + r]);
+        if (lane < NX) X[NX + r] = v;
+        if (vr) Xo[n + r] = v;
+        __syncwarp(mask);
+    }
+    int cur = 0;
+    for (int d = 1; d < Lf; d <<= 1) {
+        grid.sync();
+        for (long u = gw; u < (long)B * Lf; u += GW) {
+            const int b = (int)(u / Lf), i = (int)(u % Lf);
+            if (i < d) continue;  // t_i complete
+            T *X = ws.dxw + (size_t)b * (N + 2) * NX;
+            const T *Ei = buf(cur, b, i);
+            T arow[NX];
+            ld_row<T, NX, true>(arow, Ei + r * NX);
+            if (i < 2 * d) {  // left operand complete: dx_{i+1}
+                const T v = row_dot<T, NX>(arow, X + (size_t)(i - d + 1) * NX, Ei[TL::b + r]);
+                if (lane < NX) X[(size_t)(i + 1) * NX + r] = v;
+                if (vr) dx_out[((size_t)b * (N + 2) + i + 1) * n + r] = v;
+            } else {
+                wcopy<T, TL::SIZE, WS>(s.t1, buf(cur, b, i - d), lane);
+                __syncwarp(mask);
+                T ao[NX];
+                zero(ao);
+                row_mat<T, NX, NX, NX>(ao, arow, s.t1 + TL::A);
+                const T bo = row_dot<T, NX>(arow, s.t1 + TL::b, Ei[TL::b + r]);
+                T *D = buf(cur ^ 1, b, i);
+                if (lane < NX) { st_row<T, NX, true>(D + TL::A + r * NX, ao); D[TL::b + r] = bo; }
+            }
+            __syncwarp(mask);
+        }
+        cur ^= 1;
+    }
+}
+
 // ------------------------------------------------------------ tail: du (Eq. 6), dlam (Eq. 7)
 template <typename T, int NX, int NU>
 __global__ void k_tail(int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {

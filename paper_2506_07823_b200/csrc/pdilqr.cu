@@ -95,7 +95,7 @@ struct pdilqr_ctx {
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
     int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
-    int coop_ks = 0;               // ... of the depth-optimal (Kogge-Stone) reverse scan
+    int coop_ks = 0, coop_fks = 0; // ... of the depth-optimal (Kogge-Stone) reverse / forward scans
     bool ks_bwd = false;           // latency regime: Kogge-Stone instead of the Blelloch tree (D9)
     // pdilqr_solve in progress: convergence bookkeeping handed to the update kernels
     int32_t *sc_conv = nullptr, *sc_active = nullptr;
@@ -361,7 +361,20 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         k_policy<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws, out);
         ++launches;
     }
-    if (h->grid_scan && h->Jf > 1) {  // cooperative grid-wide forward tree
+    if (h->grid_scan && h->ks_bwd && h->Jf > 1) {  // cooperative depth-optimal forward scan (D9)
+        int Pf = h->Pf, Bv = B, Nv = N, nv = n;
+        const int wpb = 128 / WSX;
+        const size_t smem = wpb * sizeof(FwdSmem<T, NX>);
+        set_smem(k_scan_fwd_ks<T, NX>, smem);
+        const long units = (long)B * (N + 1);
+        const int grid = (int)std::max(1L, std::min((long)h->coop_fks, (units + wpb - 1) / wpb));
+        const T *dx0 = qp.dx0;
+        T *dxo = out.dx;
+        void *args[] = {&dx0, &Bv, &Nv, &nv, &Pf, &ws, &dxo};
+        Prof pf(h, "k_scan_fwd_ks", st);
+        cudaLaunchCooperativeKernel((const void *)k_scan_fwd_ks<T, NX>, grid, 128, args, smem, st);
+        ++launches;
+    } else if (h->grid_scan && h->Jf > 1) {  // cooperative grid-wide forward tree
         int J = h->Jf, Pf = h->Pf, chunk = h->chunk, Bv = B, Nv = N, nv = n;
         int *kinds = reinterpret_cast<int *>(h->ws + h->lay.kinds_f);
         const int wpb = 128 / WSX;
@@ -873,7 +886,20 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         }
         h->coop_bwd = nb;
         h->coop_fwd = nf;
+        int nfk = 0;
+        if (esz == 4) {
+            if (v == V12) occ(k_scan_fwd_ks<float, 12>, 8 * sizeof(FwdSmem<float, 12>), nfk);
+            else if (v == V4) occ(k_scan_fwd_ks<float, 4>, 32 * sizeof(FwdSmem<float, 4>), nfk);
+            else if (v == V8) occ(k_scan_fwd_ks<float, 8>, 16 * sizeof(FwdSmem<float, 8>), nfk);
+            else occ(k_scan_fwd_ks<float, 16>, 8 * sizeof(FwdSmem<float, 16>), nfk);
+        } else {
+            if (v == V12) occ(k_scan_fwd_ks<double, 12>, 8 * sizeof(FwdSmem<double, 12>), nfk);
+            else if (v == V4) occ(k_scan_fwd_ks<double, 4>, 32 * sizeof(FwdSmem<double, 4>), nfk);
+            else if (v == V8) occ(k_scan_fwd_ks<double, 8>, 16 * sizeof(FwdSmem<double, 8>), nfk);
+            else occ(k_scan_fwd_ks<double, 16>, 8 * sizeof(FwdSmem<double, 16>), nfk);
+        }
         h->coop_ks = nk;
+        h->coop_fks = nfk;
         // Kogge-Stone when every level of the pure tree fits in one wave of resident workers
         const int wpb = 128 / worker_width(NX);
         h->ks_bwd = chunk == 1 && (long)cfg->batch * (cfg->N + 2) <= (long)nk * wpb;

@@ -228,7 +228,7 @@ Layout make_layout(const pdilqr_config *c, int NX, int NU, int esz, int chunk, i
     L.stats = take(B * (3 * (size_t)esz + 8));
     L.kinds_b = take(B * (size_t)Pv * 4);
     L.kinds_f = take(B * (size_t)Pf * 4);
-    L.ls_part = take(B * (size_t)((N + 2 + 31) / 32) * 34 * 8);
+    L.ls_part = take(B * (size_t)((N + 2 + 31) / 32) * 34 * 8 * (B < 148 ? 16 : 1));  // x alpha groups
     L.ls_cnt = take(B * 4);
     L.conv = take(B * 4);
     L.active = take(8);
@@ -720,12 +720,14 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
     LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
     if (h->grid_scan) {
         const int S = (N + 2 + 31) / 32;
+        // alpha groups: spread the n_alpha + 1 slots over blocks while the grid stays within ~4 warps/SM
+        const int AG = B < 148 ? std::max(1, std::min(h->cfg.n_alpha + 1, (148 * 4) / (B * S))) : 1;
         double *part = reinterpret_cast<double *>(h->ws + h->lay.ls_part);
         int *cnt = reinterpret_cast<int *>(h->ws + h->lay.ls_cnt);
         cudaMemsetAsync(cnt, 0, (size_t)B * 4, st);
         Prof pf(h, "k_srbd_ls_multi", st);
-        k_srbd_ls_multi<T><<<dim3(S, B), 32, 0, st>>>(h->K, iter_of<T>(it, h), B, N, out.dx, out.du, out.dlam, info_tmp, so,
-                                                      part, cnt);
+        k_srbd_ls_multi<T><<<dim3(S * AG, B), 32, 0, st>>>(h->K, iter_of<T>(it, h), B, N, out.dx, out.du, out.dlam, info_tmp,
+                                                           so, part, cnt, AG);
     } else {
         Prof pf(h, "k_srbd_linesearch", st);
         k_srbd_linesearch<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it, h), B, N, out.dx, out.du, out.dlam, info_tmp, so);

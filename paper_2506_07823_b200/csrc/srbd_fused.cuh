@@ -286,7 +286,9 @@ template <typename T>
 __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &it, int b, int N, int i, int na,
                                          const T *x, const T *Dx, const T *u, const T *Du, const T *xr, const T *urf,
                                          double (*aJ)[32], double (*aT)[32], T (*sDel)[32], int lane, double &g,
-                                         unsigned &guard) {
+                                         unsigned &guard, int a_lo = 0, int a_hi = -1, bool add_g = true) {
+    // alpha slots a_lo..a_hi (default: all 0..na); add_g: this call also accumulates the slope g
+    if (a_hi < 0) a_hi = na;
     constexpr int NX = 12;
     using F = T;
         const T *xi = x + (size_t)i * NX, *dxi = Dx + (size_t)i * NX;
@@ -298,11 +300,11 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
                 const double e = (double)xi[k] - (double)xri[k], d = (double)dxi[k];
                 c0 += 0.5 * K.wxt[k] * e * e; c1 += K.wxt[k] * e * d; c2 += 0.5 * K.wxt[k] * d * d;
             }
-            for (int a = 0; a <= na; ++a) {
+            for (int a = a_lo; a <= a_hi; ++a) {
                 const double al = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
                 aJ[a][lane] += c0 + al * (c1 + al * c2);
             }
-            g += c1;
+            if (add_g) g += c1;
             return;
         }
         const T *ui = u + (size_t)i * NX, *dui = Du + (size_t)i * NX;
@@ -328,7 +330,7 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
             const double eu = (double)ui[k] - (uri ? (double)uri[k] : 0.0), du_ = (double)dui[k];
             c0 += 0.5 * wu * eu * eu; c1 += wu * eu * du_; c2 += 0.5 * wu * du_ * du_;
         }
-        g += c1;
+        if (add_g) g += c1;
         // barrier arguments xi0 + a dxi of the stance-foot constraints and their slopes at a = 0
         F bx0[24], bdx[24];
 #pragma unroll
@@ -339,7 +341,7 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
                 foot_con<F>(cc, (F)K.mu, (F)K.fmin, (F)K.fmax, gx, gy, gz, h);
                 bx0[6 * j + cc] = gx * us0[3 * j] + gy * us0[3 * j + 1] + gz * us0[3 * j + 2] + h;
                 bdx[6 * j + cc] = gx * dus[3 * j] + gy * dus[3 * j + 1] + gz * dus[3 * j + 2];
-                if ((cmask >> j) & 1) {
+                if (add_g && ((cmask >> j) & 1)) {
                     F d1, d2;
                     barrier_d12<F>(bx0[6 * j + cc], (F)K.bmu, (F)K.bdelta, (F)K.ibd2, d1, d2);
                     g += (double)d1 * (double)bdx[6 * j + cc];
@@ -348,7 +350,7 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
         }
         const F bmu = (F)K.bmu, bdl = (F)K.bdelta, ibdl = (F)K.ibd, lbd = fast_log((F)K.bdelta);
         const F im = (F)K.imass;
-        for (int a = 0; a <= na; ++a) {
+        for (int a = a_lo; a <= a_hi; ++a) {
             const double ald = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
             const F al = (F)ald;
             double J = c0 + ald * (c1 + ald * c2);
@@ -706,12 +708,15 @@ __global__ void __launch_bounds__(128) k_srbd_lin_elem(SrbdConst K, SrbdIter<T> 
 template <typename T>
 __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> it, int B, int N, const T *dx,
                                                       const T *du, const T *dlam, const int32_t *info_in, LsOut<T> so,
-                                                      double *part, int *cnt) {
+                                                      double *part, int *cnt, int AG) {
     constexpr int NX = 12, NA = 16, PW = 2 * NA + 2;
     __shared__ double aJ[NA][32], aT[NA][32];
     __shared__ T sDel[24][32];
-    const int lane = threadIdx.x, sblk = blockIdx.x, S = gridDim.x, b = blockIdx.y;
-    const int na = K.n_alpha;
+    // grid (S * AG, B): block x = ag * S + sblk evaluates stages 32 sblk.. for alpha slots
+    // [ag * ca, ag * ca + ca) (ca = ceil((na + 1) / AG)); slots it does not own stay zero in its partial
+    const int lane = threadIdx.x, S = gridDim.x / AG, sblk = blockIdx.x % S, ag = blockIdx.x / S, b = blockIdx.y;
+    const int na = K.n_alpha, ca = (na + AG) / AG;
+    const int a_lo = ag * ca, a_hi = min(na, a_lo + ca - 1);
     const T *x = it.x + (size_t)b * (N + 2) * NX, *u = it.u + (size_t)b * (N + 1) * NX;
     const T *xr = it.xref + (size_t)b * (N + 2) * NX;
     const T *urf = it.uref ? it.uref + (size_t)b * (N + 1) * NX : nullptr;
@@ -720,9 +725,11 @@ __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> i
     double g = 0.0;
     unsigned guard = 0u;
     const int i = sblk * 32 + lane;
-    if (i <= N + 1) ls_stage<T>(K, it, b, N, i, na, x, Dx, u, Du, xr, urf, aJ, aT, sDel, lane, g, guard);
+    if (i <= N + 1 && a_lo <= a_hi)
+        ls_stage<T>(K, it, b, N, i, na, x, Dx, u, Du, xr, urf, aJ, aT, sDel, lane, g, guard, a_lo, a_hi, ag == 0);
     __syncwarp();
-    double *pw = part + ((size_t)b * S + sblk) * PW;
+    const int SG = S * AG;
+    double *pw = part + ((size_t)b * SG + blockIdx.x) * PW;
     for (int a = 0; a <= na; ++a) {
         double vJ = aJ[a][lane], vT = aT[a][lane];
 #pragma unroll
@@ -742,13 +749,13 @@ __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> i
     int ticket = 0;
     if (lane == 0) ticket = atomicAdd(cnt + b, 1);
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
-    if (ticket != S - 1) return;
+    if (ticket != SG - 1) return;
     __threadfence();
-    // last warp of instance b: fixed-order reduction over the S partials
-    const volatile double *pb = part + (size_t)b * S * PW;
+    // last warp of instance b: fixed-order reduction over the S * AG partials
+    const volatile double *pb = part + (size_t)b * SG * PW;
     double J = 0.0, th = 0.0, gg = 0.0;
     unsigned gd = 0u;
-    for (int t = 0; t < S; ++t) {
+    for (int t = 0; t < SG; ++t) {
         if (lane <= na) { J += pb[(size_t)t * PW + lane]; th += pb[(size_t)t * PW + NA + lane]; }
         gg += pb[(size_t)t * PW + 2 * NA];
         gd |= (unsigned)pb[(size_t)t * PW + 2 * NA + 1];

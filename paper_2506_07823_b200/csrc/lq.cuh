@@ -623,6 +623,149 @@ __global__ void __launch_bounds__(128) k_scan_bwd_grid(int B, int N, int chunk, 
     }
 }
 
+// Full combination rule with the two half-warps of one warp cooperating (latency regime, D9): both
+// halves form M = I + C1 P2 and run the same pivoted elimination (identical pivots); half 0 solves
+// for [A1 | b1 - C1 p2] -> X, z and forms A = A2 X, b = A2 z + b2, V = P2 X, then P = A1^T V + P1,
+// p = X^T w + p1; half 1 solves for C1 -> Y and forms C = A2 Y A2^T + C2 (same arithmetic per entry
+// as combine_full, the critical path is one elimination with 13 instead of 25 right-hand sides and
+// three instead of six products).  The result element is stored to dst (global).  Requires the
+// whole warp converged; `s` is shared by the two halves.
+template <typename T, int NX>
+__device__ __forceinline__ bool combine_full_split(CombineSmem<T, NX> &s, T *dst) {
+    using L = VE<NX>;
+    static_assert(worker_width(NX) == 16, "half-warp workers");
+    constexpr int WS = 16;
+    const int lane = threadIdx.x & 15, half = (threadIdx.x >> 4) & 1;
+    const unsigned mask = worker_mask<WS>();
+    const int r = lane < NX ? lane : 0;
+    T c1[NX];
+    ld_row<T, NX, true>(c1, s.e1 + L::C + r * NX);
+    T M[NX];
+#pragma unroll
+    for (int j = 0; j < NX; ++j) M[j] = (j == r) ? T(1) : T(0);
+    row_mat<T, NX, NX, NX>(M, c1, s.e2 + L::P);
+    bool ok;
+    int pr;
+    if (half == 0) {
+        T rhs[NX + 1];
+        ld_row<T, NX, true>(*reinterpret_cast<T(*)[NX]>(rhs), s.e1 + L::A + r * NX);
+        rhs[NX] = s.e1[L::b + r] - row_dot<T, NX>(c1, s.e2 + L::p, T(0));
+        ok = gauss_jordan<T, WS, NX, NX + 1, true>(mask, M, rhs, lane, NX, pr);
+        if (pr >= 0) {
+            st_row<T, NX, true>(s.X + pr * NX, *reinterpret_cast<T(*)[NX]>(rhs));
+            s.z[pr] = rhs[NX];
+        }
+    } else {
+        T rhs[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) rhs[j] = c1[j];
+        ok = gauss_jordan<T, WS, NX, NX, true>(mask, M, rhs, lane, NX, pr);
+        if (pr >= 0) st_row<T, NX, true>(s.Y + pr * NX, rhs);
+    }
+    __syncwarp();
+    T a2[NX];
+    ld_row<T, NX, true>(a2, s.e2 + L::A + r * NX);
+    if (half == 0) {
+        T Ao[NX];
+        zero(Ao);
+        row_mat<T, NX, NX, NX>(Ao, a2, s.X);
+        const T bo = row_dot<T, NX>(a2, s.z, s.e2[L::b + r]);
+        T p2[NX];
+        ld_row<T, NX, true>(p2, s.e2 + L::P + r * NX);
+        T V[NX];
+        zero(V);
+        row_mat<T, NX, NX, NX>(V, p2, s.X);
+        const T wr = row_dot<T, NX>(p2, s.e1 + L::b, s.e2[L::p + r]);
+        if (lane < NX) {
+            st_row<T, NX, true>(s.V + r * NX, V);
+            s.w[r] = wr;
+            st_row<T, NX, true>(dst + L::A + r * NX, Ao);
+            dst[L::b + r] = bo;
+        }
+        __syncwarp(mask);
+        T a1c[NX], Po[NX];
+        ld_col<T, NX>(a1c, s.e1 + L::A + r, NX);
+        ld_row<T, NX, true>(Po, s.e1 + L::P + r * NX);
+        row_mat<T, NX, NX, NX>(Po, a1c, s.V);
+        T xc[NX];
+        ld_col<T, NX>(xc, s.X + r, NX);
+        const T po = row_dot<T, NX>(xc, s.w, s.e1[L::p + r]);
+        __syncwarp(mask);
+        symmetrize_rows<T, NX>(Po, s.V, mask, lane);
+        if (lane < NX) {
+            st_row<T, NX, true>(dst + L::P + r * NX, Po);
+            dst[L::p + r] = po;
+        }
+    } else {
+        T W[NX];
+        zero(W);
+        row_mat<T, NX, NX, NX>(W, a2, s.Y);
+        T Co[NX];
+        ld_row<T, NX, true>(Co, s.e2 + L::C + r * NX);
+        row_matT<T, NX, NX, NX>(Co, W, s.e2 + L::A);
+        __syncwarp(mask);
+        symmetrize_rows<T, NX>(Co, s.Y, mask, lane);
+        if (lane < NX) st_row<T, NX, true>(dst + L::C + r * NX, Co);
+    }
+    __syncwarp();
+    return ok;
+}
+
+// Kogge-Stone reverse scan with one warp per combine (half-warp split of the full rule above, the
+// cheap rule on half 0).  Same schedule and results as k_scan_bwd_ks.
+template <typename T, int NX>
+__global__ void __launch_bounds__(128) k_scan_bwd_ks2(int B, int N, int Pv, LqWork<T> ws) {
+    using SB = ScanBwd<T, NX>;
+    using L = VE<NX>;
+    constexpr int TP = TE<NX>::SIZE;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    cg::grid_group grid = cg::this_grid();
+    const int wl = threadIdx.x & 31, lane = threadIdx.x & 15, half = (threadIdx.x >> 4) & 1;
+    const unsigned hmask = worker_mask<16>();
+    CombineSmem<T, NX> &s = reinterpret_cast<CombineSmem<T, NX> *>(smraw)[threadIdx.x / 32];
+    const int wpb = blockDim.x / 32;
+    const long gw = (long)blockIdx.x * wpb + threadIdx.x / 32, GW = (long)gridDim.x * wpb;
+    const int L2 = N + 2;
+    auto buf = [&](int k, int b, int i) -> T * {
+        return k == 0 ? ws.elems + ((size_t)b * L2 + i) * L::SIZE : ws.vslots + ((size_t)b * Pv + i) * L::SIZE;
+    };
+    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < (long)B * TP; t += (long)gridDim.x * blockDim.x) {
+        const int b = (int)(t / TP), k = (int)(t % TP);
+        const T *e = buf(0, b, L2 - 1);
+        ws.Pp[((size_t)b * L2 + L2 - 1) * TP + k] = k < NX * NX ? e[L::P + k] : e[L::p + (k - NX * NX)];
+    }
+    int cur = 0;
+    for (int d = 1; d < L2; d <<= 1) {
+        grid.sync();
+        for (long u = gw; u < (long)B * L2; u += GW) {
+            const int b = (int)(u / L2), i = (int)(u % L2);
+            if (i + d >= L2) continue;
+            bool ok = true;
+            wcopy<T, L::SIZE, 32>(s.e1, buf(cur, b, i), wl);
+            if (i + 2 * d >= L2) {
+                const T *Pr = ws.Pp + ((size_t)b * L2 + i + d) * TP;
+                for (int k = wl; k < TP; k += 32) {
+                    if (k < NX * NX) s.e2[L::P + k] = Pr[k];
+                    else s.e2[L::p + (k - NX * NX)] = Pr[k];
+                }
+                __syncwarp();
+                if (half == 0) {
+                    T Po[NX], po;
+                    ok = combine_cheap<T, NX, 16>(s, hmask, lane, Po, po);
+                    SB::out_Pp(ws.Pp + ((size_t)b * L2 + i) * TP, Po, po, lane);
+                }
+            } else {
+                wcopy<T, L::SIZE, 32>(s.e2, buf(cur, b, i + d), wl);
+                __syncwarp();
+                ok = combine_full_split<T, NX>(s, buf(cur ^ 1, b, i));
+            }
+            if (!ok && wl == 0) atomicMin(ws.fail + b, (1 << 24) | (i + 1));
+            __syncwarp();
+        }
+        cur ^= 1;
+    }
+}
+
 // Depth-optimal (Kogge-Stone) reverse scan for the latency regime (leaf chunk 1, few instances).
 // Level d (d = 1, 2, 4, ...): every incomplete s_i becomes s_i (x) s_{i+d}.  At the start of level d,
 // s_j covers stages [j, j + d) and is complete (the suffix through the terminal, R5) iff j + d >= L;

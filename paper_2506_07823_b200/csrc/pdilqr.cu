@@ -97,6 +97,8 @@ struct pdilqr_ctx {
     int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
     int coop_ks = 0, coop_fks = 0; // ... of the depth-optimal (Kogge-Stone) reverse / forward scans
     bool ks_bwd = false;           // latency regime: Kogge-Stone instead of the Blelloch tree (D9)
+    bool ks_split = true;          // ... with one warp per combine (half-warp split of the full rule)
+    int coop_ks2 = 0;
     // pdilqr_solve in progress: convergence bookkeeping handed to the update kernels
     int32_t *sc_conv = nullptr, *sc_active = nullptr;
     double sc_tol = 0.0;
@@ -306,7 +308,23 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
         ++launches;
     }
-    if (h->Jb == 1) {  // single chunk: tight per-instance fold with prefetch
+    bool bwd_done = false;
+    if constexpr (WSX == 16) {
+        if (h->Jb > 1 && h->grid_scan && h->ks_bwd && h->ks_split) {  // Kogge-Stone, one warp per combine (D9)
+            int Pv = h->Pv, Bv = B, Nv = N;
+            const size_t smem = 4 * sizeof(CombineSmem<T, NX>);
+            set_smem(k_scan_bwd_ks2<T, NX>, smem);
+            const long units = (long)B * (N + 2);
+            const int grid = (int)std::max(1L, std::min((long)h->coop_ks2, (units + 3) / 4));
+            void *args[] = {&Bv, &Nv, &Pv, &ws};
+            Prof pf(h, "k_scan_bwd_ks2", st);
+            cudaLaunchCooperativeKernel((const void *)k_scan_bwd_ks2<T, NX>, grid, 128, args, smem, st);
+            ++launches;
+            bwd_done = true;
+        }
+    }
+    if (bwd_done) {
+    } else if (h->Jb == 1) {  // single chunk: tight per-instance fold with prefetch
         const size_t smem = (size_t)(128 / WSX) * sizeof(FoldChainSmem<T, NX>);
         set_smem(k_fold<T, NX, 4>, smem);
         Prof pf(h, "k_fold", st);
@@ -900,8 +918,18 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
             else if (v == V8) occ(k_scan_fwd_ks<double, 8>, 16 * sizeof(FwdSmem<double, 8>), nfk);
             else occ(k_scan_fwd_ks<double, 16>, 8 * sizeof(FwdSmem<double, 16>), nfk);
         }
+        int nk2 = 0;
+        if (esz == 4) {
+            if (v == V12) occ(k_scan_bwd_ks2<float, 12>, 4 * sizeof(CombineSmem<float, 12>), nk2);
+            else if (v == V16) occ(k_scan_bwd_ks2<float, 16>, 4 * sizeof(CombineSmem<float, 16>), nk2);
+        } else {
+            if (v == V12) occ(k_scan_bwd_ks2<double, 12>, 4 * sizeof(CombineSmem<double, 12>), nk2);
+            else if (v == V16) occ(k_scan_bwd_ks2<double, 16>, 4 * sizeof(CombineSmem<double, 16>), nk2);
+        }
         h->coop_ks = nk;
         h->coop_fks = nfk;
+        h->coop_ks2 = nk2;
+        if (const char *e = std::getenv("PDILQR_KS_SPLIT")) h->ks_split = std::atoi(e) != 0;
         // Kogge-Stone when every level of the pure tree fits in one wave of resident workers
         const int wpb = 128 / worker_width(NX);
         h->ks_bwd = chunk == 1 && (long)cfg->batch * (cfg->N + 2) <= (long)nk * wpb;

@@ -423,16 +423,45 @@ __device__ __forceinline__ void commit_step(const SrbdIter<T> &it, const LsOut<T
         T *uw = const_cast<T *>(it.u) + (size_t)b * (N + 1) * 12;
         T *lw = const_cast<T *>(it.lam) + (size_t)b * (N + 2) * 12;
         T sm = T(0);
-        for (int t = lane; t < (N + 2) * 12; t += 32) {
-            const T sx = alpha * Dx[t];
-            xw[t] = xw[t] + sx;
-            lw[t] = lw[t] + alpha * Dl[t];
-            sm = fmax(sm, fabs(sx));
+        // batches of 8 elements per lane: all loads of a batch issued before its stores (the
+        // iterate and the direction may alias as far as the compiler knows), so a long horizon
+        // is not one L2 round trip per element
+        constexpr int UB = 8;
+        const int nx = (N + 2) * 12, nu = (N + 1) * 12;
+        for (int t0 = lane; t0 < nx; t0 += 32 * UB) {
+            T xv[UB], dv[UB], lv[UB], ev[UB];
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+                const int t = t0 + 32 * k;
+                if (t < nx) { xv[k] = xw[t]; dv[k] = Dx[t]; lv[k] = lw[t]; ev[k] = Dl[t]; }
+            }
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+                const int t = t0 + 32 * k;
+                if (t < nx) {
+                    const T sx = alpha * dv[k];
+                    xw[t] = xv[k] + sx;
+                    lw[t] = lv[k] + alpha * ev[k];
+                    sm = fmax(sm, fabs(sx));
+                }
+            }
         }
-        for (int t = lane; t < (N + 1) * 12; t += 32) {
-            const T su = alpha * Du[t];
-            uw[t] = uw[t] + su;
-            sm = fmax(sm, fabs(su));
+        for (int t0 = lane; t0 < nu; t0 += 32 * UB) {
+            T uv[UB], dv[UB];
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+                const int t = t0 + 32 * k;
+                if (t < nu) { uv[k] = uw[t]; dv[k] = Du[t]; }
+            }
+#pragma unroll
+            for (int k = 0; k < UB; ++k) {
+                const int t = t0 + 32 * k;
+                if (t < nu) {
+                    const T su = alpha * dv[k];
+                    uw[t] = uv[k] + su;
+                    sm = fmax(sm, fabs(su));
+                }
+            }
         }
         smax = (double)sm;
     }

@@ -751,14 +751,20 @@ __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> i
     ticket = __shfl_sync(0xffffffffu, ticket, 0);
     if (ticket != SG - 1) return;
     __threadfence();
-    // last warp of instance b: fixed-order reduction over the S * AG partials
-    const volatile double *pb = part + (size_t)b * SG * PW;
+    // last warp of instance b: fixed-order reduction over the S stage partials of each alpha slot's
+    // own group (lane a <= na reads group a / ca; the slope g comes from group 0), L2 loads after
+    // the fence: the same sums in the same order as with one group
+    const double *pb = part + (size_t)b * SG * PW;
+    const double *pg = pb + (size_t)(lane <= na ? lane / ca : 0) * S * PW;
     double J = 0.0, th = 0.0, gg = 0.0;
     unsigned gd = 0u;
-    for (int t = 0; t < SG; ++t) {
-        if (lane <= na) { J += pb[(size_t)t * PW + lane]; th += pb[(size_t)t * PW + NA + lane]; }
-        gg += pb[(size_t)t * PW + 2 * NA];
-        gd |= (unsigned)pb[(size_t)t * PW + 2 * NA + 1];
+    for (int t = 0; t < S; ++t) {
+        if (lane <= na) {
+            J += __ldcg(pg + (size_t)t * PW + lane);
+            th += __ldcg(pg + (size_t)t * PW + NA + lane);
+            gd |= (unsigned)__ldcg(pg + (size_t)t * PW + 2 * NA + 1);
+        }
+        gg += __ldcg(pb + (size_t)t * PW + 2 * NA);
     }
     const T *x0 = it.x0 + (size_t)b * NX;
     const double al = lane == 0 ? 0.0 : ldexp(1.0, -(lane - 1));

@@ -494,6 +494,109 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
     if (fail != INT_MAX && rank == 0 && threadIdx.x == 0) atomicMin(ws.fail + b, (2 << 24) | fail);
 }
 
+// Rows r0 .. r0+7 of y = op(x) for a row-major matrix A (ld lda) and a vector x in shared memory:
+// one warp, lanes over k, all (row, k) loads of the 8 rows issued before the reduction (the forward
+// recursion is one dependent gemv per stage, so memory-level parallelism is what sets its latency).
+template <typename T>
+__device__ __forceinline__ void warp_gemv8(int Mr, int K, const T *A, int lda, const T *x, int r0, T (&s)[8]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s[q] = T(0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {  // K <= 256
+        const int k = lane + 32 * j;
+        if (j * 32 < K) {
+            const T xk = k < K ? x[k] : T(0);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (r0 + q < Mr && k < K) s[q] = fma(ldg_cg(A + (size_t)(r0 + q) * lda + k), xk, s[q]);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], off);
+}
+
+// Forward rollout of the large path, recursion only: dx_{i+1} = Abar_i dx_i + bbar_i (Eq. 15 with one
+// chunk), one CTA per instance, dx_i kept in shared memory; du and dlam follow in k_big_tail.
+template <typename T>
+__global__ void __launch_bounds__(256) k_big_roll(const T *dx0, int B, int N, BigDims<T> d, BigWork<T> ws, T *dx_out) {
+    __shared__ T xs[2][256];
+    const int b = blockIdx.x;
+    if (b >= B) return;
+    const int n = d.n, LD = d.LD, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T *X = ws.dxw + (size_t)b * (N + 2) * LD;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        const T v = dx0[(size_t)b * n + t];
+        xs[0][t] = v;
+        X[t] = v;
+        dx_out[(size_t)b * (N + 2) * n + t] = v;
+    }
+    __syncthreads();
+    for (int i = 0; i <= N; ++i) {
+        const T *Te = ws.tel + ((size_t)b * (N + 1) + i) * d.psize(), *tb = Te + (size_t)n * LD;
+        const T *xc = xs[i & 1];
+        T *xn = xs[(i + 1) & 1];
+        for (int r0 = 8 * wid; r0 < n; r0 += 8 * (blockDim.x >> 5)) {
+            T s[8];
+            warp_gemv8<T>(n, n, Te, LD, xc, r0, s);
+            if (lane < 8 && r0 + lane < n) {
+                const int r = r0 + lane;
+                T v = s[0];
+#pragma unroll
+                for (int q = 1; q < 8; ++q) v = lane == q ? s[q] : v;
+                v += ldg_cg(tb + r);
+                xn[r] = v;
+                X[(size_t)(i + 1) * LD + r] = v;
+                dx_out[((size_t)b * (N + 2) + i + 1) * n + r] = v;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// du_i = K_i dx_i + k_i (Eq. 6, i <= N) and dlam_i = P_i dx_i + p_i (Eq. 7, i <= N+1), parallel over
+// (instance, stage) items (persistent CTAs), after the recursion.
+template <typename T>
+__global__ void __launch_bounds__(256) k_big_tail(int B, int N, BigDims<T> d, BigWork<T> ws, LqOut<T> out) {
+    __shared__ T xs[256];
+    const int n = d.n, m = d.m, LD = d.LD, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (long item = blockIdx.x; item < (long)B * (N + 2); item += gridDim.x) {
+        const int b = (int)(item / (N + 2)), i = (int)(item % (N + 2));
+        for (int t = threadIdx.x; t < n; t += blockDim.x) xs[t] = ldg_cg(ws.dxw + ((size_t)b * (N + 2) + i) * LD + t);
+        __syncthreads();
+        const T *Pi = ws.Pp + ((size_t)b * (N + 2) + i) * d.psize();
+        const int rows_l = n, ngl = (n + 7) / 8, ngu = i <= N ? (m + 7) / 8 : 0;
+        for (int gi = wid; gi < ngl + ngu; gi += nw) {
+            // row groups [0, ngl): dlam rows 8 gi..; [ngl, ngl + ngu): du rows 8 (gi - ngl)..
+            T s[8];
+            const int r0 = gi < ngl ? 8 * gi : rows_l + 8 * (gi - ngl);
+            if (gi < ngl) {
+                warp_gemv8<T>(rows_l, n, Pi, LD, xs, r0, s);
+                if (lane < 8 && r0 + lane < rows_l) {
+                    T v = s[0];
+#pragma unroll
+                    for (int q = 1; q < 8; ++q) v = lane == q ? s[q] : v;
+                    out.dlam[((size_t)b * (N + 2) + i) * n + r0 + lane] = v + Pi[(size_t)n * LD + r0 + lane];
+                }
+            } else {
+                const size_t st = (size_t)b * (N + 1) + i;
+                const T *Kw = ws.Kk + st * d.ksize();
+                const int u0 = r0 - rows_l;
+                warp_gemv8<T>(m, n, Kw, LD, xs, u0, s);
+                if (lane < 8 && u0 + lane < m) {
+                    T v = s[0];
+#pragma unroll
+                    for (int q = 1; q < 8; ++q) v = lane == q ? s[q] : v;
+                    out.du[st * m + u0 + lane] = v + Kw[(size_t)m * LD + u0 + lane];
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // R_i SPD check of Eq. 12 for every (instance, stage), persistent CTAs; a failure at stage
 // i is reported as i + 1 with the element-initialisation rank (ahead of the policy's G failures).
 template <typename T>

@@ -487,10 +487,15 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
             if (e != cudaSuccess) return fail(PDILQR_ERR_CUDA, "k_big_ric launch (cluster %d): %s", h->ric_cs, cudaGetErrorString(e));
         }
         {
-            Prof pf(h, "k_big_fwd", st);
-            k_big_fwd<T><<<B, BIG_THREADS, 0, st>>>(qp.dx0, B, N, d, ws, out);
+            Prof pf(h, "k_big_roll", st);
+            k_big_roll<T><<<B, 256, 0, st>>>(qp.dx0, B, N, d, ws, out.dx);
         }
-        int launches = 3;
+        {
+            const int g = (int)std::min<long>((long)148 * 8, (long)B * (N + 2));
+            Prof pf(h, "k_big_tail", st);
+            k_big_tail<T><<<g, 256, 0, st>>>(B, N, d, ws, out);
+        }
+        int launches = 4;
         if (info) {
             int32_t *nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
             cudaMemsetAsync(nonfin, 0, (size_t)B * 4, st);

@@ -623,15 +623,6 @@ __global__ void __launch_bounds__(128) k_scan_bwd_grid(int B, int N, int chunk, 
     }
 }
 
-template <int NX, int NU>
-__host__ __device__ constexpr int policy_smem_words() {  // B, A, PB, K, k, c, g of one worker
-    return NX * NU + NX * NX + NX * NU + NU * NX + round_up4(NU) + NX + NX;
-}
-
-template <typename T, int NX, int NU, bool EX>
-__device__ __forceinline__ void policy_unit(const LqArgs<T> &qp, int N, int n, int m, const LqWork<T> &ws,
-                                            const LqOut<T> &out, T *sm, int lane, unsigned mask, int b, int i);
-
 // Full combination rule with the two half-warps of one warp cooperating (latency regime, D9): both
 // halves form M = I + C1 P2 and run the same pivoted elimination (identical pivots); half 0 solves
 // for [A1 | b1 - C1 p2] -> X, z and forms A = A2 X, b = A2 z + b2, V = P2 X, then P = A1^T V + P1,
@@ -722,9 +713,8 @@ __device__ __forceinline__ bool combine_full_split(CombineSmem<T, NX> &s, T *dst
 
 // Kogge-Stone reverse scan with one warp per combine (half-warp split of the full rule above, the
 // cheap rule on half 0).  Same schedule and results as k_scan_bwd_ks.
-template <typename T, int NX, int NU, bool EX>
-__global__ void __launch_bounds__(128) k_scan_bwd_ks2(int B, int N, int Pv, LqWork<T> ws, LqArgs<T> qp, int n, int m,
-                                                      LqOut<T> out) {
+template <typename T, int NX>
+__global__ void __launch_bounds__(128) k_scan_bwd_ks2(int B, int N, int Pv, LqWork<T> ws) {
     using SB = ScanBwd<T, NX>;
     using L = VE<NX>;
     constexpr int TP = TE<NX>::SIZE;
@@ -774,12 +764,6 @@ __global__ void __launch_bounds__(128) k_scan_bwd_ks2(int B, int N, int Pv, LqWo
         }
         cur ^= 1;
     }
-    // fused policy (Eq. 5 rows, Eq. 14) for every (instance, stage), two half-warp workers per warp
-    static_assert(2 * policy_smem_words<NX, NU>() <= (int)(sizeof(CombineSmem<T, NX>) / sizeof(T)), "policy smem");
-    grid.sync();
-    T *psm = reinterpret_cast<T *>(&s) + half * policy_smem_words<NX, NU>();
-    for (long u = 2 * gw + half; u < (long)B * (N + 1); u += 2 * GW)
-        policy_unit<T, NX, NU, EX>(qp, N, n, m, ws, out, psm, lane, hmask, (int)(u / (N + 1)), (int)(u % (N + 1)));
 }
 
 // Depth-optimal (Kogge-Stone) reverse scan for the latency regime (leaf chunk 1, few instances).
@@ -849,13 +833,20 @@ __global__ void __launch_bounds__(128) k_scan_bwd_ks(int B, int N, int Pv, LqWor
 // Per stage i (one worker):  PB = P_{i+1} B,  g = p_{i+1} + P_{i+1} b,
 //   G = R + B^T PB,  H = S + PB^T A,  h = B^T g + r,  K = -G^-1 H,  k = -G^-1 h  (GJ, SPD),
 //   Abar = A + B K,  bbar = B k + b   (Eq. 14).
-// One policy unit (instance b, stage i) on one WS-lane worker with `sm` = its policy_smem_words() slice.
 template <typename T, int NX, int NU, bool EX>
-__device__ __forceinline__ void policy_unit(const LqArgs<T> &qp, int N, int n, int m, const LqWork<T> &ws,
-                                            const LqOut<T> &out, T *sm, int lane, unsigned mask, int b, int i) {
+__global__ void __launch_bounds__(128) k_policy(LqArgs<T> qp, int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {
     constexpr int WS = worker_width(NX > NU ? NX : NU);
+    constexpr int SMW = NX * NU + NX * NX + NX * NU + NU * NX + round_up4(NU) + NX + NX;  // B, A, PB, K, k, c, g
     using KL = KE<NX, NU>;
     constexpr int TP = TE<NX>::SIZE;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int lane = worker_lane<WS>();
+    const unsigned mask = worker_mask<WS>();
+    const int wloc = threadIdx.x / WS;
+    const long gw = (long)blockIdx.x * (blockDim.x / WS) + wloc;
+    if (gw >= (long)B * (N + 1)) return;
+    const int b = (int)(gw / (N + 1)), i = (int)(gw % (N + 1));
+    T *sm = reinterpret_cast<T *>(smraw) + wloc * SMW;
     T *sB = sm, *sA = sB + NX * NU, *sPB = sA + NX * NX, *sK = sPB + NX * NU, *sk = sK + NU * NX;
     T *sc = sk + round_up4(NU), *sg = sc + NX;
     const size_t st = (size_t)b * (N + 1) + i;
@@ -934,20 +925,6 @@ __device__ __forceinline__ void policy_unit(const LqArgs<T> &qp, int N, int n, i
         st_row<T, NX, true>(te + r * NX, abar);
         te[NX * NX + r] = bb;
     }
-}
-
-template <typename T, int NX, int NU, bool EX>
-__global__ void __launch_bounds__(128) k_policy(LqArgs<T> qp, int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {
-    constexpr int WS = worker_width(NX > NU ? NX : NU);
-    constexpr int SMW = policy_smem_words<NX, NU>();
-    extern __shared__ __align__(16) unsigned char smraw[];
-    const int lane = worker_lane<WS>();
-    const unsigned mask = worker_mask<WS>();
-    const int wloc = threadIdx.x / WS;
-    const long gw = (long)blockIdx.x * (blockDim.x / WS) + wloc;
-    if (gw >= (long)B * (N + 1)) return;
-    policy_unit<T, NX, NU, EX>(qp, N, n, m, ws, out, reinterpret_cast<T *>(smraw) + wloc * SMW, lane, mask,
-                               (int)(gw / (N + 1)), (int)(gw % (N + 1)));
 }
 
 // ------------------------------------------------------------ forward scan (Eq. 14-15, R6)

@@ -309,22 +309,18 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         ++launches;
     }
     bool bwd_done = false, tail_done = false;  // tail_done: du, dlam and info written by k_scan_fwd_ks
-    bool policy_done = false;                  // policy_done: K, k, Abar, bbar written by k_scan_bwd_ks2
     if constexpr (WSX == 16) {
         if (h->Jb > 1 && h->grid_scan && h->ks_bwd && h->ks_split) {  // Kogge-Stone, one warp per combine (D9)
-            int Pv = h->Pv, Bv = B, Nv = N, nv = n, mv = m;
+            int Pv = h->Pv, Bv = B, Nv = N;
             const size_t smem = 4 * sizeof(CombineSmem<T, NX>);
-            set_smem(k_scan_bwd_ks2<T, NX, NU, EX>, smem);
+            set_smem(k_scan_bwd_ks2<T, NX>, smem);
             const long units = (long)B * (N + 2);
             const int grid = (int)std::max(1L, std::min((long)h->coop_ks2, (units + 3) / 4));
-            LqArgs<T> q = qp;
-            LqOut<T> o = out;
-            void *args[] = {&Bv, &Nv, &Pv, &ws, &q, &nv, &mv, &o};
+            void *args[] = {&Bv, &Nv, &Pv, &ws};
             Prof pf(h, "k_scan_bwd_ks2", st);
-            cudaLaunchCooperativeKernel((const void *)k_scan_bwd_ks2<T, NX, NU, EX>, grid, 128, args, smem, st);
+            cudaLaunchCooperativeKernel((const void *)k_scan_bwd_ks2<T, NX>, grid, 128, args, smem, st);
             ++launches;
             bwd_done = true;
-            policy_done = true;
         }
     }
     if (bwd_done) {
@@ -374,7 +370,7 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         k_scan_bwd<T, NX><<<(B + IPB - 1) / IPB, IPB * W * WSX, smem, st>>>(B, N, h->chunk, J, Pv, W, IPB, ws);
         ++launches;
     }
-    if (!policy_done) {  // policy
+    {  // policy
         const int wpb = 128 / WS;
         const long nw = (long)B * (N + 1);
         const size_t smem = (size_t)wpb * (NX * NU + NX * NX + NX * NU + NU * NX + round_up4(NU) + NX + NX) * sizeof(T);
@@ -932,11 +928,11 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         }
         int nk2 = 0;
         if (esz == 4) {
-            if (v == V12) occ(k_scan_bwd_ks2<float, 12, 12, true>, 4 * sizeof(CombineSmem<float, 12>), nk2);
-            else if (v == V16) occ(k_scan_bwd_ks2<float, 16, 16, false>, 4 * sizeof(CombineSmem<float, 16>), nk2);
+            if (v == V12) occ(k_scan_bwd_ks2<float, 12>, 4 * sizeof(CombineSmem<float, 12>), nk2);
+            else if (v == V16) occ(k_scan_bwd_ks2<float, 16>, 4 * sizeof(CombineSmem<float, 16>), nk2);
         } else {
-            if (v == V12) occ(k_scan_bwd_ks2<double, 12, 12, true>, 4 * sizeof(CombineSmem<double, 12>), nk2);
-            else if (v == V16) occ(k_scan_bwd_ks2<double, 16, 16, false>, 4 * sizeof(CombineSmem<double, 16>), nk2);
+            if (v == V12) occ(k_scan_bwd_ks2<double, 12>, 4 * sizeof(CombineSmem<double, 12>), nk2);
+            else if (v == V16) occ(k_scan_bwd_ks2<double, 16>, 4 * sizeof(CombineSmem<double, 16>), nk2);
         }
         h->coop_ks = nk;
         h->coop_fks = nfk;

@@ -366,8 +366,8 @@ __host__ __device__ inline size_t ric_smem_bytes(int m, int esz) {
 
 // Fused reverse scan + policy (phases 1-7 above), one cluster of CS CTAs per instance.
 // Writes P_i, p_i (ws.Pp), K_i, k_i (ws.Kk, out.K, out.k), Abar_i, bbar_i (ws.tel).
-template <typename T, int TN, int TU, int MINB>
-__global__ void __launch_bounds__(RIC_THREADS, MINB) k_big_ric(LqArgs<T> qp, int B, int N, BigDims<T> d, BigWork<T> ws,
+template <typename T, int TN, int TU>
+__global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B, int N, BigDims<T> d, BigWork<T> ws,
                                                          LqOut<T> out, int CS) {
     constexpr int TM = TN > TU ? TN : TU;
     __shared__ RicTiles<T, TM> tiles;

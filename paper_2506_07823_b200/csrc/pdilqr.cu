@@ -467,7 +467,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
             k_big_rchk<T><<<g, tpb, ric_smem, st>>>(qp.R, B, N, m, ws.fail);
         }
         {
-            auto kern = t52 ? k_big_ric<T, 5, 2, 3> : k_big_ric<T, 3, 3, 2>;
+            auto kern = t52 ? k_big_ric<T, 5, 2> : k_big_ric<T, 3, 3>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
             if (h->ric_cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaLaunchConfig_t lc{};
@@ -855,7 +855,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         if (const char *e = std::getenv("PDILQR_BIG_CS")) cs = std::max(1, std::min(16, std::atoi(e)));
         const size_t smem = ric_smem_bytes(cfg->m, esz);
         while (cs > 1 && smem <= kRicSmemMax) {  // the device must co-schedule a whole cluster
-            const void *kern = esz == 4 ? (const void *)k_big_ric<float, 3, 3, 2> : (const void *)k_big_ric<double, 3, 3, 2>;
+            const void *kern = esz == 4 ? (const void *)k_big_ric<float, 3, 3> : (const void *)k_big_ric<double, 3, 3>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaLaunchConfig_t lc{};

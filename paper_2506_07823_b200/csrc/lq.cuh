@@ -1149,18 +1149,13 @@ __global__ void __launch_bounds__(128) k_scan_fwd_grid(const T *dx0, int B, int 
     }
 }
 
-template <typename T, int NX, int NU>
-__device__ __forceinline__ void tail_item(long t, int B, int N, int n, int m, const LqWork<T> &ws, const LqOut<T> &out);
-
 // Depth-optimal (Kogge-Stone) forward scan, companion of k_scan_bwd_ks (D9).  t_j covers elements
 // (j - d, j] at the start of level d and is complete -- anchored at dx_0, i.e. (0, dx_{j+1}) -- iff
 // j < d.  Level d: every incomplete t_i (i >= d) becomes t_{i-d} then t_i; when t_{i-d} is complete
 // the result is dx_{i+1} = Abar_(i) dx_{i-d+1} + bbar_(i), written to the padded workspace X and to
 // the user's dx.  Incomplete composites ping-pong between ws.tel (level-0 input) and ws.tslots.
-template <typename T, int NX, int NU>
-__global__ void __launch_bounds__(128) k_scan_fwd_ks(const T *dx0, int B, int N, int n, int m, int Pf, LqWork<T> ws,
-                                                     LqOut<T> out, const int32_t *pre, int32_t *info) {
-    T *dx_out = out.dx;
+template <typename T, int NX>
+__global__ void __launch_bounds__(128) k_scan_fwd_ks(const T *dx0, int B, int N, int n, int Pf, LqWork<T> ws, T *dx_out) {
     using TL = TE<NX>;
     constexpr int WS = worker_width(NX);
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -1217,26 +1212,14 @@ __global__ void __launch_bounds__(128) k_scan_fwd_ks(const T *dx0, int B, int N,
         }
         cur ^= 1;
     }
-    // fused tail (du = K dx + k, Eq. 6; dlam = P dx + p, Eq. 7) and info finalisation: two grid
-    // barriers instead of two kernel launches
-    grid.sync();
-    const long per = (long)(N + 1) * m + (long)(N + 2) * n;
-    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < (long)B * per; t += (long)gridDim.x * blockDim.x)
-        tail_item<T, NX, NU>(t, B, N, n, m, ws, out);
-    if (info == nullptr) return;
-    grid.sync();
-    for (long b = (long)blockIdx.x * blockDim.x + threadIdx.x; b < B; b += (long)gridDim.x * blockDim.x) {
-        int v = ws.fail[b] != kFailNone ? (ws.fail[b] & 0xFFFFFF) : (ws.nonfin[b] ? -1 : 0);
-        if (pre != nullptr && pre[b] != 0) v = pre[b];
-        info[b] = v;
-    }
 }
 
 // ------------------------------------------------------------ tail: du (Eq. 6), dlam (Eq. 7)
 template <typename T, int NX, int NU>
-__device__ __forceinline__ void tail_item(long t, int B, int N, int n, int m, const LqWork<T> &ws, const LqOut<T> &out) {
+__global__ void k_tail(int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {
     using KL = KE<NX, NU>;
     constexpr int TP = TE<NX>::SIZE;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const long per = (long)(N + 1) * m + (long)(N + 2) * n;
     if (t >= (long)B * per) return;
     const int b = (int)(t / per);
@@ -1263,11 +1246,6 @@ __device__ __forceinline__ void tail_item(long t, int B, int N, int n, int m, co
         bad = !isfinite(v) || !isfinite(x[i * NX + a]);
     }
     if (bad) ws.nonfin[b] = 1;
-}
-
-template <typename T, int NX, int NU>
-__global__ void k_tail(int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {
-    tail_item<T, NX, NU>((long)blockIdx.x * blockDim.x + threadIdx.x, B, N, n, m, ws, out);
 }
 
 // info[b] = factorisation failure stage (k > 0), else -1 if a non-finite output, else 0.

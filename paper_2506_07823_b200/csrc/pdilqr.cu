@@ -308,7 +308,7 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
         ++launches;
     }
-    bool bwd_done = false, tail_done = false;  // tail_done: du, dlam and info written by k_scan_fwd_ks
+    bool bwd_done = false;
     if constexpr (WSX == 16) {
         if (h->Jb > 1 && h->grid_scan && h->ks_bwd && h->ks_split) {  // Kogge-Stone, one warp per combine (D9)
             int Pv = h->Pv, Bv = B, Nv = N;
@@ -380,21 +380,18 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         ++launches;
     }
     if (h->grid_scan && h->ks_bwd && h->Jf > 1) {  // cooperative depth-optimal forward scan (D9)
-        int Pf = h->Pf, Bv = B, Nv = N, nv = n, mv = m;
+        int Pf = h->Pf, Bv = B, Nv = N, nv = n;
         const int wpb = 128 / WSX;
         const size_t smem = wpb * sizeof(FwdSmem<T, NX>);
-        set_smem(k_scan_fwd_ks<T, NX, NU>, smem);
+        set_smem(k_scan_fwd_ks<T, NX>, smem);
         const long units = (long)B * (N + 1);
         const int grid = (int)std::max(1L, std::min((long)h->coop_fks, (units + wpb - 1) / wpb));
         const T *dx0 = qp.dx0;
-        LqOut<T> o = out;
-        const int32_t *prev = pre;
-        int32_t *infov = info;
-        void *args[] = {&dx0, &Bv, &Nv, &nv, &mv, &Pf, &ws, &o, &prev, &infov};
+        T *dxo = out.dx;
+        void *args[] = {&dx0, &Bv, &Nv, &nv, &Pf, &ws, &dxo};
         Prof pf(h, "k_scan_fwd_ks", st);
-        cudaLaunchCooperativeKernel((const void *)k_scan_fwd_ks<T, NX, NU>, grid, 128, args, smem, st);
+        cudaLaunchCooperativeKernel((const void *)k_scan_fwd_ks<T, NX>, grid, 128, args, smem, st);
         ++launches;
-        tail_done = true;
     } else if (h->grid_scan && h->Jf > 1) {  // cooperative grid-wide forward tree
         int J = h->Jf, Pf = h->Pf, chunk = h->chunk, Bv = B, Nv = N, nv = n;
         int *kinds = reinterpret_cast<int *>(h->ws + h->lay.kinds_f);
@@ -426,13 +423,13 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
                                                                             out.dx);
         ++launches;
     }
-    if (!tail_done) {  // du, dlam
+    {  // du, dlam
         const long tot = (long)B * ((long)(N + 1) * m + (long)(N + 2) * n);
         Prof pf(h, "k_tail", st);
         k_tail<T, NX, NU><<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(B, N, n, m, ws, out);
         ++launches;
     }
-    if (info && !tail_done) {
+    if (info) {
         Prof pf(h, "k_finalize_info", st);
         k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, ws.nonfin, pre, info);
         ++launches;
@@ -916,15 +913,15 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         h->coop_fwd = nf;
         int nfk = 0;
         if (esz == 4) {
-            if (v == V12) occ(k_scan_fwd_ks<float, 12, 12>, 8 * sizeof(FwdSmem<float, 12>), nfk);
-            else if (v == V4) occ(k_scan_fwd_ks<float, 4, 4>, 32 * sizeof(FwdSmem<float, 4>), nfk);
-            else if (v == V8) occ(k_scan_fwd_ks<float, 8, 8>, 16 * sizeof(FwdSmem<float, 8>), nfk);
-            else occ(k_scan_fwd_ks<float, 16, 16>, 8 * sizeof(FwdSmem<float, 16>), nfk);
+            if (v == V12) occ(k_scan_fwd_ks<float, 12>, 8 * sizeof(FwdSmem<float, 12>), nfk);
+            else if (v == V4) occ(k_scan_fwd_ks<float, 4>, 32 * sizeof(FwdSmem<float, 4>), nfk);
+            else if (v == V8) occ(k_scan_fwd_ks<float, 8>, 16 * sizeof(FwdSmem<float, 8>), nfk);
+            else occ(k_scan_fwd_ks<float, 16>, 8 * sizeof(FwdSmem<float, 16>), nfk);
         } else {
-            if (v == V12) occ(k_scan_fwd_ks<double, 12, 12>, 8 * sizeof(FwdSmem<double, 12>), nfk);
-            else if (v == V4) occ(k_scan_fwd_ks<double, 4, 4>, 32 * sizeof(FwdSmem<double, 4>), nfk);
-            else if (v == V8) occ(k_scan_fwd_ks<double, 8, 8>, 16 * sizeof(FwdSmem<double, 8>), nfk);
-            else occ(k_scan_fwd_ks<double, 16, 16>, 8 * sizeof(FwdSmem<double, 16>), nfk);
+            if (v == V12) occ(k_scan_fwd_ks<double, 12>, 8 * sizeof(FwdSmem<double, 12>), nfk);
+            else if (v == V4) occ(k_scan_fwd_ks<double, 4>, 32 * sizeof(FwdSmem<double, 4>), nfk);
+            else if (v == V8) occ(k_scan_fwd_ks<double, 8>, 16 * sizeof(FwdSmem<double, 8>), nfk);
+            else occ(k_scan_fwd_ks<double, 16>, 8 * sizeof(FwdSmem<double, 16>), nfk);
         }
         int nk2 = 0;
         if (esz == 4) {

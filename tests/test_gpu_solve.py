@@ -87,9 +87,12 @@ def test_solve_zero_iters_and_frozen(P, O):
     assert (ig > 0).all() and run == ig.max()
     early = ig < run
     assert (to_np(st["alpha"])[early] == 0).all() and (to_np(st["accepted"])[early] == 0).all()
-    # solving again from the converged iterate: converged within 2 iterations, negligible motion
+    # solving again from the converged iterate: converged within 2 iterations, negligible motion.
+    # The re-solve uses tol 1e-7: at the solution the fp64 direction is rounding noise of size
+    # cond(KKT) * eps (|du| up to ~6e-8 here, scripts/diag_solve_ks.py), so a 1e-9 step test would
+    # measure the scan's rounding order (Kogge-Stone vs Blelloch, R19/D9), not convergence.
     xs = it["x"].clone()
-    st, iters, run = h.solve(it, 50, 1e-9)
+    st, iters, run = h.solve(it, 50, 1e-7)
     torch.cuda.synchronize()
     assert run <= 2 and (to_np(iters) >= 1).all()
     assert (it["x"] - xs).abs().max().item() <= 1e-8

@@ -737,8 +737,10 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
         out = LqOut<T>{reinterpret_cast<T *>(h->ws + h->lay.dir[0]), reinterpret_cast<T *>(h->ws + h->lay.dir[1]),
                        reinterpret_cast<T *>(h->ws + h->lay.dir[2]), nullptr, nullptr};
     }
-    s = (h->cfg.n == 12 && h->cfg.m == 12) ? dispatch_lq<T>(h, qp, out, info_tmp, pre, st, /*skip_init=*/true)
-                                           : dispatch_lq<T>(h, qp, out, info_tmp, pre, st);
+    // latency regime: the line search's last warp derives the info word itself (no k_finalize_info)
+    int32_t *lq_info = h->grid_scan ? nullptr : info_tmp;
+    s = (h->cfg.n == 12 && h->cfg.m == 12) ? dispatch_lq<T>(h, qp, out, lq_info, pre, st, /*skip_init=*/true)
+                                           : dispatch_lq<T>(h, qp, out, lq_info, pre, st);
     if (s != PDILQR_OK) return s;
     LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
     if (h->grid_scan) {
@@ -749,8 +751,10 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
         int *cnt = reinterpret_cast<int *>(h->ws + h->lay.ls_cnt);
         cudaMemsetAsync(cnt, 0, (size_t)B * 4, st);
         Prof pf(h, "k_srbd_ls_multi", st);
-        k_srbd_ls_multi<T><<<dim3(S * AG, B), 32, 0, st>>>(h->K, iter_of<T>(it, h), B, N, out.dx, out.du, out.dlam, info_tmp,
-                                                           so, part, cnt, AG);
+        const int32_t *fail = reinterpret_cast<const int32_t *>(h->ws + h->lay.fail);
+        const int32_t *nonfin = reinterpret_cast<const int32_t *>(h->ws + h->lay.nonfin);
+        k_srbd_ls_multi<T><<<dim3(S * AG, B), 32, 0, st>>>(h->K, iter_of<T>(it, h), B, N, out.dx, out.du, out.dlam, nullptr,
+                                                           so, part, cnt, AG, fail, nonfin, pre);
     } else {
         Prof pf(h, "k_srbd_linesearch", st);
         k_srbd_linesearch<T><<<(B + 3) / 4, 128, 0, st>>>(h->K, iter_of<T>(it, h), B, N, out.dx, out.du, out.dlam, info_tmp, so);

@@ -708,7 +708,9 @@ __global__ void __launch_bounds__(128) k_srbd_lin_elem(SrbdConst K, SrbdIter<T> 
 template <typename T>
 __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> it, int B, int N, const T *dx,
                                                       const T *du, const T *dlam, const int32_t *info_in, LsOut<T> so,
-                                                      double *part, int *cnt, int AG) {
+                                                      double *part, int *cnt, int AG, const int32_t *fail = nullptr,
+                                                      const int32_t *nonfin = nullptr, const int32_t *pre = nullptr) {
+    // info_in == nullptr: the info word (k_finalize_info's rule) is derived here from fail / nonfin / pre
     constexpr int NX = 12, NA = 16, PW = 2 * NA + 2;
     __shared__ double aJ[NA][32], aT[NA][32];
     __shared__ T sDel[24][32];
@@ -778,7 +780,13 @@ __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> i
         th += sqrt(q);
     }
     const double J0 = __shfl_sync(0xffffffffu, J, 0), th0 = __shfl_sync(0xffffffffu, th, 0);
-    const int info = info_in[b];
+    int info;
+    if (info_in != nullptr) {
+        info = info_in[b];
+    } else {
+        info = fail[b] != kFailNone ? (fail[b] & 0xFFFFFF) : (nonfin[b] ? -1 : 0);
+        if (pre != nullptr && pre[b] != 0) info = pre[b];
+    }
     bool ok = false;
     if (lane >= 1 && lane <= na && info == 0) {
         ok = !((gd >> lane) & 1u) && isfinite(J) && isfinite(th);

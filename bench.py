@@ -371,6 +371,9 @@ def main():
     clo = None
     if args.closed_loop_ticks > 0 and args.dtype == "f32":
         clo = closed_loop_bench(P, torch, dev, B, N, args.closed_loop_ticks)
+    lq_only = None
+    if not args.no_large:
+        lq_only = solve_lq_bench(P, torch, dev, h, upload(), B, N, tdt, sm_mhz=(clocks or {}).get("sm_max_mhz") or 1965.0)
     large = None
     if not args.no_large and args.dtype == "f32":
         large = large_bench(P, torch, dev, sm_mhz=(clocks or {}).get("sm_max_mhz") or 1965.0)
@@ -386,7 +389,7 @@ def main():
            "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "e2e": e2e,
            "roofline": roof, "cpu_baseline": cpu,
            "kernels_ms": {k: v[1] / v[0] for k, v in prof.items()},
-           "latency": lat, "closed_loop": clo, "large": large}
+           "latency": lat, "closed_loop": clo, "solve_lq_only": lq_only, "large": large}
     if gather_ms is not None:
         out["final_allgather_ms"] = gather_ms
     print(json.dumps(out), flush=True)
@@ -520,6 +523,39 @@ def ric_flops_per_stage(n: int, m: int) -> float:
     return (2 * n * n * m + 2 * n * n + 2 * n * m * m + 2 * m * n * n + 2 * n * m + m ** 3 / 3
             + 2 * m * m * (n + 1) + 2 * n * n * m + 2 * n * m + 2 * n ** 3 + 2 * n * n + 2 * n ** 3
             + 2 * n * n * m + 2 * n * n + 4 * n * m)
+
+
+def solve_lq_bench(P, torch, dev, h_srbd, it, B, N, tdt, sm_mhz, reps=50):
+    """pdilqr_solve_lq alone (a2-a6: element init, reverse scan, policy, forward scan,
+    du/dlam) on the Eq. 4 data of config 3 -- the SRBD linearisation at the cold-start iterate
+    (pdilqr_linearize), solved by a generic LQ handle (n = m = 12, B = 4096, N = 50; single-chunk
+    schedule).  CUDA events around `reps` solves, inputs resident."""
+    qp = h_srbd.linearize(it)
+    qp.pop("info", None)
+    h = P.PdIlqr(N=N, n=12, m=12, batch=B, dtype=tdt, device=dev)
+    out = h.solve_lq(qp)
+    out = h.solve_lq(qp, out=out)
+    torch.cuda.synchronize()
+    h.profile(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        h.solve_lq(qp, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    pr = h.profile_read()
+    h.profile(False)
+    ms = e0.elapsed_time(e1) / reps
+    fl = flops_per_instance(N, 12, 12, chunk=N + 2)
+    tot = sum(fl[k] for k in ("k_elem_init", "k_scan_bwd", "k_policy", "k_scan_fwd", "k_tail"))
+    res = {"what": "pdilqr_solve_lq on the config-3 SRBD linearisation (generic LQ handle, single chunk)",
+           "B": B, "N": N, "ms_per_solve_lq": ms, "solves_per_s": B / ms * 1e3,
+           "kernels_ms": {k: v[1] / v[0] for k, v in pr.items()}, "info_ok": bool((out["info"] == 0).all()),
+           "scan_method_mflop_per_instance": (tot / 1e6) if tot else None,
+           "tflops": (tot * B / ms / 1e9) if tot else None,
+           "frac_fp32_peak": (tot * B / ms / 1e9 / fp32_peak_tflops(sm_mhz)) if tot else None}
+    del h, out, qp
+    return res
 
 
 def large_bench(P, torch, dev, sm_mhz, reps=5):

@@ -163,7 +163,9 @@ pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *
 /* Multi-iteration solve (artifact plumbing around the one-iteration RTI of P:315;
  * SRBD handles).  Repeats pdilqr_step until every instance has converged or failed, or max_iters
  * iterations ran.  Instance b converges at iteration k when that iteration's accepted step has
- * theta <= tol and ||alpha (dx, du)||_inf <= tol; it is then frozen (later iterations neither
+ * theta <= tol and ||alpha (dx, du)||_inf <= tol, or when every alpha was rejected at a fixed
+ * point: theta <= tol and |grad J . (dx, du)| <= tol max(1, |J|) (the linear model predicts no
+ * decrease; R24).  A rejected step elsewhere is not convergence.  It is then frozen (later iterations neither
  * update it nor overwrite its stats with a step: they report its iterate with alpha = 0,
  * accepted = 0).  An instance whose info != 0 stops at that iteration.
  *   stats      as pdilqr_step, of each instance's last iteration (device, required)

@@ -305,7 +305,9 @@ def closed_loop(prob_long: dict, N: int, ticks: int, nodes_per_tick: int = 1, su
 
 def srbd_solve(prob: dict, max_iters: int, tol: float, n_alpha=10, c1=1e-4, theta_max=0.0):
     """Multi-iteration solve, per instance: repeat the SQP iteration until the
-    accepted step has theta <= tol and ||alpha (dx, du)||_inf <= tol (converged at k), or the
+    accepted step has theta <= tol and ||alpha (dx, du)||_inf <= tol, or every alpha is rejected at
+    a fixed point (theta <= tol and |grad J . (dx, du)| <= tol max(1, |J|), R24)
+    (converged at k), or the
     iteration fails (info != 0: stopped, -k), or max_iters.  In place on prob x/u/lam.
     Returns (iters[B], stats[B][5] of each instance's last iteration)."""
     Bn = prob["x"].shape[0]
@@ -320,7 +322,13 @@ def srbd_solve(prob: dict, max_iters: int, tol: float, n_alpha=10, c1=1e-4, thet
             if s[4] != 0:
                 iters[b] = -k
                 break
-            if s[1] <= tol and step <= tol:
+            if s[3]:
+                conv = s[1] <= tol and step <= tol
+            else:   # every alpha rejected: a fixed point iff the linear model predicts no decrease
+                _, _, _, (J0, th0, g) = srbd_line_search(prob, b, dx, du, n_alpha, c1,
+                                                         None if theta_max <= 0 else theta_max)
+                conv = th0 <= tol and abs(g) <= tol * max(1.0, abs(J0))
+            if conv:
                 iters[b] = k
                 break
     return iters, st

@@ -1251,7 +1251,7 @@ __global__ void k_tail(int B, int N, int n, int m, LqWork<T> ws, LqOut<T> out) {
 // info[b] = factorisation failure stage (k > 0), else -1 if a non-finite output, else 0.
 // Failures are ranked by origin (R in element init < scan combine < G in the policy), then by
 // stage: fail[b] = (origin << 24) | (stage + 1), min over all failures.
-__global__ void k_finalize_info(int B, const int32_t *fail, const int32_t *nonfin, const int32_t *pre,
+static __global__ void k_finalize_info(int B, const int32_t *fail, const int32_t *nonfin, const int32_t *pre,
                                        int32_t *info) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= B) return;

@@ -22,9 +22,25 @@
 
 using namespace pdilqr;
 
+// Build partition: paper_2506_07823_b200/build.py compiles this file once per part, in parallel
+// (the kernels of one part do not depend on those of another):
+//   0 everything in one translation unit        1 host: C ABI, validation, workspace layout
+//   2 f32 kernels for n, m <= 16                3 f64 kernels for n, m <= 16
+//   4 f32 large-n kernels (16 < n, m <= 256)    5 f64 large-n kernels
+#ifndef PDILQR_PART
+#define PDILQR_PART 0
+#endif
+#define PDILQR_HOST (PDILQR_PART == 0 || PDILQR_PART == 1)
+#define PDILQR_SMALL(f64) (PDILQR_PART == 0 || PDILQR_PART == 2 + (f64))
+#define PDILQR_BIG(f64) (PDILQR_PART == 0 || PDILQR_PART == 4 + (f64))
+
+namespace pdq {
+extern thread_local std::string g_err;  // pdilqr_last_error (defined in the host part)
+}
+
 namespace {
 
-thread_local std::string g_err = "ok";
+using pdq::g_err;
 
 pdilqr_status fail(pdilqr_status s, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
 pdilqr_status fail(pdilqr_status s, const char *fmt, ...) {
@@ -288,6 +304,57 @@ void set_smem(K kernel, size_t bytes) {
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+}  // namespace
+
+namespace {
+template <typename T>
+LqArgs<T> internal_qp(pdilqr_ctx *h) {
+    auto p = [&](int k) { return reinterpret_cast<const T *>(h->ws + h->lay.qp[k]); };
+    return LqArgs<T>{p(0), p(1), p(2), p(3), p(4), p(5), p(6), p(7), p(8), p(9), p(10)};
+}
+
+template <typename T>
+SrbdIter<T> iter_of(const pdilqr_iterate *it) {
+    return SrbdIter<T>{reinterpret_cast<const T *>(it->x),    reinterpret_cast<const T *>(it->u),
+                       reinterpret_cast<const T *>(it->lam),  reinterpret_cast<const T *>(it->x0),
+                       reinterpret_cast<const T *>(it->x_ref), reinterpret_cast<const T *>(it->u_ref),
+                       it->contact,                           reinterpret_cast<const T *>(it->feet)};
+}
+
+template <typename T>
+SrbdIter<T> iter_of(const pdilqr_iterate *it, const pdilqr_ctx *h) {
+    SrbdIter<T> r = iter_of<T>(it);
+    r.conv = h->sc_conv;
+    r.active = h->sc_active;
+    r.tol = h->sc_tol;
+    r.iter = h->sc_iter;
+    return r;
+}
+
+}  // namespace
+
+// Entry points of the kernel parts, called from the host part (explicit instantiations below).
+namespace pdq {
+template <typename T>
+pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, cudaStream_t st);
+template <typename T>
+pdilqr_status dispatch_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, const int32_t *pre,
+                          cudaStream_t st, bool skip_init = false);
+template <typename T>
+pdilqr_status run_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArgs<T> &outq, int32_t *pre,
+                            cudaStream_t st);
+template <typename T>
+pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st);
+// k_big_ric cluster-size probe: true if a cluster of cs CTAs with smem bytes can be co-scheduled
+template <typename T>
+bool ric_cluster_fits(int cs, size_t smem);
+// co-resident CTAs of the cooperative latency-regime scan kernels (v: Variant)
+template <typename T>
+void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk2);
+}  // namespace pdq
+
+#if PDILQR_SMALL(0) || PDILQR_SMALL(1)
+namespace pdq {
 // --------------------------------------------------------------------------- LQ pipeline
 template <typename T, int NX, int NU, bool EX>
 pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, const int32_t *pre,
@@ -440,113 +507,8 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
 
 // Large dimensions (16 < max(n, m) <= 256): CTA-level single-chunk path (big.cuh).
 template <typename T>
-pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, cudaStream_t st) {
-    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
-    BigDims<T> d{n, m, ld_of(n), ld_of(m)};
-    BigWork<T> ws;
-    ws.elems = reinterpret_cast<T *>(h->ws + h->lay.elems);
-    ws.Pp = reinterpret_cast<T *>(h->ws + h->lay.Pp);
-    ws.Kk = reinterpret_cast<T *>(h->ws + h->lay.Kk);
-    ws.tel = reinterpret_cast<T *>(h->ws + h->lay.tel);
-    ws.dxw = reinterpret_cast<T *>(h->ws + h->lay.dxw);
-    ws.scratch = reinterpret_cast<T *>(h->ws + h->lay.vslots);
-    ws.slot = big_slot(n, m);
-    ws.fail = reinterpret_cast<int32_t *>(h->ws + h->lay.fail);
-    cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
-    const size_t ric_smem = ric_smem_bytes(m, (int)sizeof(T));
-    if (ric_smem <= kRicSmemMax && !h->big_legacy) {  // fused Riccati-form fold (big_ric.cuh)
-        const bool t52 = n <= 80 && m <= 32 && h->ric_cs == 1;  // config-5-like: 80-row n tiles, 32-wide m tiles
-        {
-            const int tpb = std::min(256, (m + 31) / 32 * 32);  // one thread per row of R
-            const int g = (int)std::min<long>((long)148 * (2048 / tpb), (long)B * (N + 1));
-            cudaFuncSetAttribute(k_big_rchk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
-            Prof pf(h, "k_big_rchk", st);
-            k_big_rchk<T><<<g, tpb, ric_smem, st>>>(qp.R, B, N, m, ws.fail);
-        }
-        {
-            auto kern = t52 ? k_big_ric<T, 5, 2> : k_big_ric<T, 3, 3>;
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
-            if (h->ric_cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3((unsigned)(B * h->ric_cs));
-            lc.blockDim = dim3(RIC_THREADS);
-            lc.dynamicSmemBytes = ric_smem;
-            lc.stream = st;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = (unsigned)h->ric_cs;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            lc.attrs = at;
-            lc.numAttrs = 1;
-            Prof pf(h, "k_big_ric", st);
-            cudaError_t e = cudaLaunchKernelEx(&lc, kern, qp, B, N, d, ws, out, h->ric_cs);
-            if (e != cudaSuccess) return fail(PDILQR_ERR_CUDA, "k_big_ric launch (cluster %d): %s", h->ric_cs, cudaGetErrorString(e));
-        }
-        {
-            Prof pf(h, "k_big_roll", st);
-            k_big_roll<T><<<B, 256, 0, st>>>(qp.dx0, B, N, d, ws, out.dx);
-        }
-        {
-            const int g = (int)std::min<long>((long)148 * 8, (long)B * (N + 2));
-            Prof pf(h, "k_big_tail", st);
-            k_big_tail<T><<<g, 256, 0, st>>>(B, N, d, ws, out);
-        }
-        int launches = 4;
-        if (info) {
-            int32_t *nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
-            cudaMemsetAsync(nonfin, 0, (size_t)B * 4, st);
-            Prof pf(h, "k_finalize_info", st);
-            k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, nonfin, nullptr, info);
-            ++launches;
-        }
-        h->launches += launches;
-        return cuda_check("solve_lq (large, fused) launch");
-    }
-    const int gpers = (int)std::min<long>((long)kBigPersistent, (long)B * (N + 2));
-    // the augmented Gauss-Jordan matrix W lives in shared memory when it fits (n <= ~110 in fp32)
-    const size_t kSmemW = 180 * 1024;
-    auto wbytes = [&](int rows, int cols) { return (size_t)rows * ld_of(cols) * sizeof(T); };
-    {
-        const size_t wb = wbytes(m, m + 2 * n + 1);
-        const int in = wb <= kSmemW;
-        if (in) cudaFuncSetAttribute(k_big_init<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
-        Prof pf(h, "k_big_init", st);
-        k_big_init<T><<<gpers, BIG_THREADS, in ? wb : 0, st>>>(qp, B, N, d, ws, in);
-    }
-    {
-        const size_t wb = wbytes(n, 2 * n);
-        const int in = wb <= kSmemW;
-        if (in) cudaFuncSetAttribute(k_big_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
-        Prof pf(h, "k_big_fold", st);
-        k_big_fold<T><<<B, BIG_THREADS, in ? wb : 0, st>>>(B, N, d, ws, in);
-    }
-    {
-        const size_t wb = wbytes(m, m + n + 1);
-        const int in = wb <= kSmemW;
-        if (in) cudaFuncSetAttribute(k_big_policy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
-        Prof pf(h, "k_big_policy", st);
-        k_big_policy<T><<<gpers, BIG_THREADS, in ? wb : 0, st>>>(qp, B, N, d, ws, out, in);
-    }
-    {
-        Prof pf(h, "k_big_fwd", st);
-        k_big_fwd<T><<<B, BIG_THREADS, 0, st>>>(qp.dx0, B, N, d, ws, out);
-    }
-    int launches = 4;
-    if (info) {
-        int32_t *nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
-        cudaMemsetAsync(nonfin, 0, (size_t)B * 4, st);
-        Prof pf(h, "k_finalize_info", st);
-        k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, nonfin, nullptr, info);
-        ++launches;
-    }
-    h->launches += launches;
-    return cuda_check("solve_lq (large) launch");
-}
-
-template <typename T>
 pdilqr_status dispatch_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, const int32_t *pre,
-                          cudaStream_t st, bool skip_init = false) {
+                          cudaStream_t st, bool skip_init) {
     switch (h->var) {
         case V12: return run_lq<T, 12, 12, true>(h, qp, out, info, pre, st, skip_init);
         case V4: return run_lq<T, 4, 4, false>(h, qp, out, info, pre, st, skip_init);
@@ -554,30 +516,6 @@ pdilqr_status dispatch_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int3
         case V16: return run_lq<T, 16, 16, false>(h, qp, out, info, pre, st, skip_init);
         default: return run_big<T>(h, qp, out, info, st);
     }
-}
-
-template <typename T>
-LqArgs<T> internal_qp(pdilqr_ctx *h) {
-    auto p = [&](int k) { return reinterpret_cast<const T *>(h->ws + h->lay.qp[k]); };
-    return LqArgs<T>{p(0), p(1), p(2), p(3), p(4), p(5), p(6), p(7), p(8), p(9), p(10)};
-}
-
-template <typename T>
-SrbdIter<T> iter_of(const pdilqr_iterate *it) {
-    return SrbdIter<T>{reinterpret_cast<const T *>(it->x),    reinterpret_cast<const T *>(it->u),
-                       reinterpret_cast<const T *>(it->lam),  reinterpret_cast<const T *>(it->x0),
-                       reinterpret_cast<const T *>(it->x_ref), reinterpret_cast<const T *>(it->u_ref),
-                       it->contact,                           reinterpret_cast<const T *>(it->feet)};
-}
-
-template <typename T>
-SrbdIter<T> iter_of(const pdilqr_iterate *it, const pdilqr_ctx *h) {
-    SrbdIter<T> r = iter_of<T>(it);
-    r.conv = h->sc_conv;
-    r.active = h->sc_active;
-    r.tol = h->sc_tol;
-    r.iter = h->sc_iter;
-    return r;
 }
 
 template <typename T>
@@ -763,6 +701,195 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
     return cuda_check("step launch");
 }
 
+
+template <typename T>
+void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk2) {
+    auto occ = [&](auto kern, size_t smem, int &out) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
+        out = std::max(1, per) * sms;
+    };
+    if (v == V12) { occ(k_scan_bwd_grid<T, 12>, 8 * sizeof(CombineSmem<T, 12>), nb); occ(k_scan_fwd_grid<T, 12>, 8 * sizeof(FwdSmem<T, 12>), nf); }
+    else if (v == V4) { occ(k_scan_bwd_grid<T, 4>, 32 * sizeof(CombineSmem<T, 4>), nb); occ(k_scan_fwd_grid<T, 4>, 32 * sizeof(FwdSmem<T, 4>), nf); }
+    else if (v == V8) { occ(k_scan_bwd_grid<T, 8>, 16 * sizeof(CombineSmem<T, 8>), nb); occ(k_scan_fwd_grid<T, 8>, 16 * sizeof(FwdSmem<T, 8>), nf); }
+    else { occ(k_scan_bwd_grid<T, 16>, 8 * sizeof(CombineSmem<T, 16>), nb); occ(k_scan_fwd_grid<T, 16>, 8 * sizeof(FwdSmem<T, 16>), nf); }
+    if (v == V12) occ(k_scan_bwd_ks<T, 12>, 8 * sizeof(CombineSmem<T, 12>), nk);
+    else if (v == V4) occ(k_scan_bwd_ks<T, 4>, 32 * sizeof(CombineSmem<T, 4>), nk);
+    else if (v == V8) occ(k_scan_bwd_ks<T, 8>, 16 * sizeof(CombineSmem<T, 8>), nk);
+    else occ(k_scan_bwd_ks<T, 16>, 8 * sizeof(CombineSmem<T, 16>), nk);
+    if (v == V12) occ(k_scan_fwd_ks<T, 12>, 8 * sizeof(FwdSmem<T, 12>), nfk);
+    else if (v == V4) occ(k_scan_fwd_ks<T, 4>, 32 * sizeof(FwdSmem<T, 4>), nfk);
+    else if (v == V8) occ(k_scan_fwd_ks<T, 8>, 16 * sizeof(FwdSmem<T, 8>), nfk);
+    else occ(k_scan_fwd_ks<T, 16>, 8 * sizeof(FwdSmem<T, 16>), nfk);
+    if (v == V12) occ(k_scan_bwd_ks2<T, 12>, 4 * sizeof(CombineSmem<T, 12>), nk2);
+    else if (v == V16) occ(k_scan_bwd_ks2<T, 16>, 4 * sizeof(CombineSmem<T, 16>), nk2);
+}
+
+#define PDILQR_INST_SMALL(T)                                                                                       \
+    template pdilqr_status dispatch_lq<T>(pdilqr_ctx *, const LqArgs<T> &, LqOut<T>, int32_t *, const int32_t *,    \
+                                          cudaStream_t, bool);                                                     \
+    template pdilqr_status run_linearize<T>(pdilqr_ctx *, const pdilqr_iterate *, const LqArgs<T> &, int32_t *,     \
+                                            cudaStream_t);                                                         \
+    template pdilqr_status run_step<T>(pdilqr_ctx *, pdilqr_iterate *, pdilqr_stats *, pdilqr_dir *, cudaStream_t); \
+    template void grid_occupancy<T>(int, int, int &, int &, int &, int &, int &);
+#if PDILQR_SMALL(0)
+PDILQR_INST_SMALL(float)
+#endif
+#if PDILQR_SMALL(1)
+PDILQR_INST_SMALL(double)
+#endif
+}  // namespace pdq
+#endif
+
+#if PDILQR_BIG(0) || PDILQR_BIG(1)
+namespace pdq {
+template <typename T>
+pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
+    BigDims<T> d{n, m, ld_of(n), ld_of(m)};
+    BigWork<T> ws;
+    ws.elems = reinterpret_cast<T *>(h->ws + h->lay.elems);
+    ws.Pp = reinterpret_cast<T *>(h->ws + h->lay.Pp);
+    ws.Kk = reinterpret_cast<T *>(h->ws + h->lay.Kk);
+    ws.tel = reinterpret_cast<T *>(h->ws + h->lay.tel);
+    ws.dxw = reinterpret_cast<T *>(h->ws + h->lay.dxw);
+    ws.scratch = reinterpret_cast<T *>(h->ws + h->lay.vslots);
+    ws.slot = big_slot(n, m);
+    ws.fail = reinterpret_cast<int32_t *>(h->ws + h->lay.fail);
+    cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
+    const size_t ric_smem = ric_smem_bytes(m, (int)sizeof(T));
+    if (ric_smem <= kRicSmemMax && !h->big_legacy) {  // fused Riccati-form fold (big_ric.cuh)
+        const bool t52 = n <= 80 && m <= 32 && h->ric_cs == 1;  // config-5-like: 80-row n tiles, 32-wide m tiles
+        {
+            const int tpb = std::min(256, (m + 31) / 32 * 32);  // one thread per row of R
+            const int g = (int)std::min<long>((long)148 * (2048 / tpb), (long)B * (N + 1));
+            cudaFuncSetAttribute(k_big_rchk<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
+            Prof pf(h, "k_big_rchk", st);
+            k_big_rchk<T><<<g, tpb, ric_smem, st>>>(qp.R, B, N, m, ws.fail);
+        }
+        {
+            auto kern = t52 ? k_big_ric<T, 5, 2> : k_big_ric<T, 3, 3>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
+            if (h->ric_cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3((unsigned)(B * h->ric_cs));
+            lc.blockDim = dim3(RIC_THREADS);
+            lc.dynamicSmemBytes = ric_smem;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = (unsigned)h->ric_cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            Prof pf(h, "k_big_ric", st);
+            cudaError_t e = cudaLaunchKernelEx(&lc, kern, qp, B, N, d, ws, out, h->ric_cs);
+            if (e != cudaSuccess) return fail(PDILQR_ERR_CUDA, "k_big_ric launch (cluster %d): %s", h->ric_cs, cudaGetErrorString(e));
+        }
+        {
+            Prof pf(h, "k_big_roll", st);
+            k_big_roll<T><<<B, 256, 0, st>>>(qp.dx0, B, N, d, ws, out.dx);
+        }
+        {
+            const int g = (int)std::min<long>((long)148 * 8, (long)B * (N + 2));
+            Prof pf(h, "k_big_tail", st);
+            k_big_tail<T><<<g, 256, 0, st>>>(B, N, d, ws, out);
+        }
+        int launches = 4;
+        if (info) {
+            int32_t *nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
+            cudaMemsetAsync(nonfin, 0, (size_t)B * 4, st);
+            Prof pf(h, "k_finalize_info", st);
+            k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, nonfin, nullptr, info);
+            ++launches;
+        }
+        h->launches += launches;
+        return cuda_check("solve_lq (large, fused) launch");
+    }
+    const int gpers = (int)std::min<long>((long)kBigPersistent, (long)B * (N + 2));
+    // the augmented Gauss-Jordan matrix W lives in shared memory when it fits (n <= ~110 in fp32)
+    const size_t kSmemW = 180 * 1024;
+    auto wbytes = [&](int rows, int cols) { return (size_t)rows * ld_of(cols) * sizeof(T); };
+    {
+        const size_t wb = wbytes(m, m + 2 * n + 1);
+        const int in = wb <= kSmemW;
+        if (in) cudaFuncSetAttribute(k_big_init<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
+        Prof pf(h, "k_big_init", st);
+        k_big_init<T><<<gpers, BIG_THREADS, in ? wb : 0, st>>>(qp, B, N, d, ws, in);
+    }
+    {
+        const size_t wb = wbytes(n, 2 * n);
+        const int in = wb <= kSmemW;
+        if (in) cudaFuncSetAttribute(k_big_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
+        Prof pf(h, "k_big_fold", st);
+        k_big_fold<T><<<B, BIG_THREADS, in ? wb : 0, st>>>(B, N, d, ws, in);
+    }
+    {
+        const size_t wb = wbytes(m, m + n + 1);
+        const int in = wb <= kSmemW;
+        if (in) cudaFuncSetAttribute(k_big_policy<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
+        Prof pf(h, "k_big_policy", st);
+        k_big_policy<T><<<gpers, BIG_THREADS, in ? wb : 0, st>>>(qp, B, N, d, ws, out, in);
+    }
+    {
+        Prof pf(h, "k_big_fwd", st);
+        k_big_fwd<T><<<B, BIG_THREADS, 0, st>>>(qp.dx0, B, N, d, ws, out);
+    }
+    int launches = 4;
+    if (info) {
+        int32_t *nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
+        cudaMemsetAsync(nonfin, 0, (size_t)B * 4, st);
+        Prof pf(h, "k_finalize_info", st);
+        k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, nonfin, nullptr, info);
+        ++launches;
+    }
+    h->launches += launches;
+    return cuda_check("solve_lq (large) launch");
+}
+
+template <typename T>
+bool ric_cluster_fits(int cs, size_t smem) {
+    const void *kern = (const void *)k_big_ric<T, 3, 3>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3((unsigned)cs);
+    lc.blockDim = dim3(RIC_THREADS);
+    lc.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)cs;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, kern, &lc) == cudaSuccess && ncl > 0) return true;
+    cudaGetLastError();
+    return false;
+}
+#if PDILQR_BIG(0)
+template pdilqr_status run_big<float>(pdilqr_ctx *, const LqArgs<float> &, LqOut<float>, int32_t *, cudaStream_t);
+template bool ric_cluster_fits<float>(int, size_t);
+#endif
+#if PDILQR_BIG(1)
+template pdilqr_status run_big<double>(pdilqr_ctx *, const LqArgs<double> &, LqOut<double>, int32_t *, cudaStream_t);
+template bool ric_cluster_fits<double>(int, size_t);
+#endif
+}  // namespace pdq
+#endif
+
+#if PDILQR_HOST
+namespace pdq {
+thread_local std::string g_err = "ok";
+}
+using pdq::dispatch_lq;
+using pdq::run_linearize;
+using pdq::run_step;
+
+namespace {
 void inv3(const double *M, double *Mi) {
     const double a = M[0], b = M[1], c = M[2], d = M[3], e = M[4], f = M[5], g = M[6], hh = M[7], i = M[8];
     const double det = a * (e * i - f * hh) - b * (d * i - f * g) + c * (d * hh - e * g);
@@ -856,23 +983,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         if (const char *e = std::getenv("PDILQR_BIG_CS")) cs = std::max(1, std::min(16, std::atoi(e)));
         const size_t smem = ric_smem_bytes(cfg->m, esz);
         while (cs > 1 && smem <= kRicSmemMax) {  // the device must co-schedule a whole cluster
-            const void *kern = esz == 4 ? (const void *)k_big_ric<float, 3, 3> : (const void *)k_big_ric<double, 3, 3>;
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-            cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3((unsigned)cs);
-            lc.blockDim = dim3(RIC_THREADS);
-            lc.dynamicSmemBytes = smem;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = (unsigned)cs;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            lc.attrs = at;
-            lc.numAttrs = 1;
-            int ncl = 0;
-            if (cudaOccupancyMaxActiveClusters(&ncl, kern, &lc) == cudaSuccess && ncl > 0) break;
-            cudaGetLastError();
+            if (esz == 4 ? pdq::ric_cluster_fits<float>(cs, smem) : pdq::ric_cluster_fits<double>(cs, smem)) break;
             cs /= 2;
         }
         h->ric_cs = cs;
@@ -884,57 +995,11 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         DeviceGuard g(device);
         int sms = 148, nb = 0, nf = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-        auto occ = [&](auto kern, size_t smem, int &out) {
-            if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            int per = 0;
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 128, smem);
-            out = std::max(1, per) * sms;
-        };
-        if (esz == 4) {
-            if (v == V12) { occ(k_scan_bwd_grid<float, 12>, 8 * sizeof(CombineSmem<float, 12>), nb); occ(k_scan_fwd_grid<float, 12>, 8 * sizeof(FwdSmem<float, 12>), nf); }
-            else if (v == V4) { occ(k_scan_bwd_grid<float, 4>, 32 * sizeof(CombineSmem<float, 4>), nb); occ(k_scan_fwd_grid<float, 4>, 32 * sizeof(FwdSmem<float, 4>), nf); }
-            else if (v == V8) { occ(k_scan_bwd_grid<float, 8>, 16 * sizeof(CombineSmem<float, 8>), nb); occ(k_scan_fwd_grid<float, 8>, 16 * sizeof(FwdSmem<float, 8>), nf); }
-            else { occ(k_scan_bwd_grid<float, 16>, 8 * sizeof(CombineSmem<float, 16>), nb); occ(k_scan_fwd_grid<float, 16>, 8 * sizeof(FwdSmem<float, 16>), nf); }
-        } else {
-            if (v == V12) { occ(k_scan_bwd_grid<double, 12>, 8 * sizeof(CombineSmem<double, 12>), nb); occ(k_scan_fwd_grid<double, 12>, 8 * sizeof(FwdSmem<double, 12>), nf); }
-            else if (v == V4) { occ(k_scan_bwd_grid<double, 4>, 32 * sizeof(CombineSmem<double, 4>), nb); occ(k_scan_fwd_grid<double, 4>, 32 * sizeof(FwdSmem<double, 4>), nf); }
-            else if (v == V8) { occ(k_scan_bwd_grid<double, 8>, 16 * sizeof(CombineSmem<double, 8>), nb); occ(k_scan_fwd_grid<double, 8>, 16 * sizeof(FwdSmem<double, 8>), nf); }
-            else { occ(k_scan_bwd_grid<double, 16>, 8 * sizeof(CombineSmem<double, 16>), nb); occ(k_scan_fwd_grid<double, 16>, 8 * sizeof(FwdSmem<double, 16>), nf); }
-        }
-        int nk = 0;
-        if (esz == 4) {
-            if (v == V12) occ(k_scan_bwd_ks<float, 12>, 8 * sizeof(CombineSmem<float, 12>), nk);
-            else if (v == V4) occ(k_scan_bwd_ks<float, 4>, 32 * sizeof(CombineSmem<float, 4>), nk);
-            else if (v == V8) occ(k_scan_bwd_ks<float, 8>, 16 * sizeof(CombineSmem<float, 8>), nk);
-            else occ(k_scan_bwd_ks<float, 16>, 8 * sizeof(CombineSmem<float, 16>), nk);
-        } else {
-            if (v == V12) occ(k_scan_bwd_ks<double, 12>, 8 * sizeof(CombineSmem<double, 12>), nk);
-            else if (v == V4) occ(k_scan_bwd_ks<double, 4>, 32 * sizeof(CombineSmem<double, 4>), nk);
-            else if (v == V8) occ(k_scan_bwd_ks<double, 8>, 16 * sizeof(CombineSmem<double, 8>), nk);
-            else occ(k_scan_bwd_ks<double, 16>, 8 * sizeof(CombineSmem<double, 16>), nk);
-        }
+        int nk = 0, nfk = 0, nk2 = 0;
+        if (esz == 4) pdq::grid_occupancy<float>(v, sms, nb, nf, nk, nfk, nk2);
+        else pdq::grid_occupancy<double>(v, sms, nb, nf, nk, nfk, nk2);
         h->coop_bwd = nb;
         h->coop_fwd = nf;
-        int nfk = 0;
-        if (esz == 4) {
-            if (v == V12) occ(k_scan_fwd_ks<float, 12>, 8 * sizeof(FwdSmem<float, 12>), nfk);
-            else if (v == V4) occ(k_scan_fwd_ks<float, 4>, 32 * sizeof(FwdSmem<float, 4>), nfk);
-            else if (v == V8) occ(k_scan_fwd_ks<float, 8>, 16 * sizeof(FwdSmem<float, 8>), nfk);
-            else occ(k_scan_fwd_ks<float, 16>, 8 * sizeof(FwdSmem<float, 16>), nfk);
-        } else {
-            if (v == V12) occ(k_scan_fwd_ks<double, 12>, 8 * sizeof(FwdSmem<double, 12>), nfk);
-            else if (v == V4) occ(k_scan_fwd_ks<double, 4>, 32 * sizeof(FwdSmem<double, 4>), nfk);
-            else if (v == V8) occ(k_scan_fwd_ks<double, 8>, 16 * sizeof(FwdSmem<double, 8>), nfk);
-            else occ(k_scan_fwd_ks<double, 16>, 8 * sizeof(FwdSmem<double, 16>), nfk);
-        }
-        int nk2 = 0;
-        if (esz == 4) {
-            if (v == V12) occ(k_scan_bwd_ks2<float, 12>, 4 * sizeof(CombineSmem<float, 12>), nk2);
-            else if (v == V16) occ(k_scan_bwd_ks2<float, 16>, 4 * sizeof(CombineSmem<float, 16>), nk2);
-        } else {
-            if (v == V12) occ(k_scan_bwd_ks2<double, 12>, 4 * sizeof(CombineSmem<double, 12>), nk2);
-            else if (v == V16) occ(k_scan_bwd_ks2<double, 16>, 4 * sizeof(CombineSmem<double, 16>), nk2);
-        }
         h->coop_ks = nk;
         h->coop_fks = nfk;
         h->coop_ks2 = nk2;
@@ -1172,3 +1237,4 @@ pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *
 }
 
 }  // extern "C"
+#endif  // PDILQR_HOST

@@ -415,7 +415,7 @@ struct LsOut {
 template <typename T>
 __device__ __forceinline__ void commit_step(const SrbdIter<T> &it, const LsOut<T> &so, int b, int N, int lane, bool acc,
                                             T alpha, double J0, double th0, double Jb, double thb, int info,
-                                            const T *Dx, const T *Du, const T *Dl) {
+                                            const T *Dx, const T *Du, const T *Dl, double gslope) {
     const bool frozen = it.conv && it.conv[b] != 0;
     double smax = 0.0;
     if (acc && !frozen) {
@@ -482,7 +482,12 @@ __device__ __forceinline__ void commit_step(const SrbdIter<T> &it, const LsOut<T
             so.accepted[b] = acc ? 1 : 0;
             if (it.conv) {
                 if (info != 0) it.conv[b] = -it.iter;
-                else if (thb <= it.tol && smax <= it.tol) it.conv[b] = it.iter;
+                // accepted: theta and ||alpha (dx, du)||_inf within tol; every alpha rejected: the
+                // iterate is kept, and it is a fixed point iff theta <= tol and the linear model
+                // predicts no decrease, |grad J . (dx, du)| <= tol max(1, |J|) (R24)
+                else if (acc ? (thb <= it.tol && smax <= it.tol)
+                             : (th0 <= it.tol && fabs(gslope) <= it.tol * fmax(1.0, fabs(J0))))
+                    it.conv[b] = it.iter;
                 else atomicAdd(it.active, 1);
             }
         }
@@ -622,7 +627,7 @@ __global__ void __launch_bounds__(128) k_srbd_linesearch(SrbdConst K, SrbdIter<T
     const int jb = acc ? __ffs(acc) - 1 : 0;                   // smallest slot = largest alpha
     const double Jb = __shfl_sync(0xffffffffu, J, jb), thb = __shfl_sync(0xffffffffu, th, jb);
     const T alpha = acc ? (T)ldexp(1.0, -(jb - 1)) : T(0);
-    commit_step<T>(it, so, b, N, lane, acc != 0u, alpha, J0, th0, Jb, thb, info, Dx, Du, dlam + (size_t)b * (N + 2) * 12);
+    commit_step<T>(it, so, b, N, lane, acc != 0u, alpha, J0, th0, Jb, thb, info, Dx, Du, dlam + (size_t)b * (N + 2) * 12, g0);
 }
 
 }  // namespace pdilqr

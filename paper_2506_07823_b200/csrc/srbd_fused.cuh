@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         }
     }
     const T alpha = jb >= 0 ? (T)ldexp(1.0, -(jb - 1)) : T(0);
-    commit_step<T>(it, so, b, N, lane, jb >= 0, alpha, J0, th0, Jb, thb, info, Dx, Du, Dl);
+    commit_step<T>(it, so, b, N, lane, jb >= 0, alpha, J0, th0, Jb, thb, info, Dx, Du, Dl, g);
 }
 
 // ------------------------------------------- stage-parallel linearisation + element init
@@ -800,7 +800,7 @@ __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> i
     const int jb = acc ? __ffs(acc) - 1 : 0;
     const double Jb = __shfl_sync(0xffffffffu, J, jb), thb = __shfl_sync(0xffffffffu, th, jb);
     const T alpha = acc ? (T)ldexp(1.0, -(jb - 1)) : T(0);
-    commit_step<T>(it, so, b, N, lane, acc != 0u, alpha, J0, th0, Jb, thb, info, Dx, Du, dlam + (size_t)b * (N + 2) * NX);
+    commit_step<T>(it, so, b, N, lane, acc != 0u, alpha, J0, th0, Jb, thb, info, Dx, Du, dlam + (size_t)b * (N + 2) * NX, gg);
     if (lane == 0) cnt[b] = 0;
 }
 

@@ -334,3 +334,140 @@ def test_solve_iteration_count_monotone_in_tol(O):
     ia, _ = O.srbd_solve(a, 60, 1e-4)
     ib, _ = O.srbd_solve(b, 60, 1e-9)
     assert (ia > 0).all() and (ia <= ib).all()
+
+
+# ----------------------------------------------------------------------------- round-2 pins
+def _euler_rates_textbook(Id, w):
+    """Euler's rigid-body equations for principal inertias Id = (I1, I2, I3), torque free
+    (textbook form, not the cross-product form of the oracle):
+    I1 w1' = (I2 - I3) w2 w3,  I2 w2' = (I3 - I1) w3 w1,  I3 w3' = (I1 - I2) w1 w2."""
+    I1, I2, I3 = Id
+    return np.array([(I2 - I3) * w[1] * w[2] / I1, (I3 - I1) * w[2] * w[0] / I2, (I1 - I2) * w[0] * w[1] / I3])
+
+
+def test_gyroscopic_term_euler_equations(O):
+    """Pins the -w x I w term of P:322-327 (wdot = I^-1(tau - w x I w)) at non-principal spin,
+    where it does not vanish: the oracle's wdot must equal Euler's equations written out."""
+    rng = np.random.default_rng(41)
+    for Id in ((0.10, 0.25, 0.28), (0.3, 0.05, 0.17)):
+        p = dict(PRM); p["inertia"] = [Id[0], 0, 0, 0, Id[1], 0, 0, 0, Id[2]]
+        for _ in range(10):
+            x = random_state(rng)
+            xd = O.srbd_f(p, x, np.zeros(12), np.zeros((4, 3)), np.zeros(4, np.uint8))
+            np.testing.assert_allclose(xd[9:12], _euler_rates_textbook(Id, x[9:12]), rtol=1e-13, atol=1e-13)
+    # one hand-computed value: I = diag(0.1, 0.25, 0.28), w = (1, 2, 3):
+    # w1' = (0.25 - 0.28) * 6 / 0.1 = -1.8; w2' = (0.28 - 0.1) * 3 / 0.25 = 2.16; w3' = (0.1 - 0.25) * 2 / 0.28
+    x = np.zeros(12); x[2] = 0.3; x[9:12] = [1.0, 2.0, 3.0]
+    p = dict(PRM); p["inertia"] = [0.1, 0, 0, 0, 0.25, 0, 0, 0, 0.28]
+    xd = O.srbd_f(p, x, np.zeros(12), np.zeros((4, 3)), np.zeros(4, np.uint8))
+    np.testing.assert_allclose(xd[9:12], [-1.8, 2.16, -0.3 / 0.28], rtol=1e-14)
+
+
+def test_torque_free_angular_momentum_conserved(O):
+    """Torque-free rigid body (no stance feet), non-principal spin: the world-frame angular
+    momentum R(Theta) I w and the kinetic energy 1/2 w^T I w are constants of the motion.  The
+    oracle's RK4 plant integrates the oracle's f; a sign error in -w x I w (or in the Euler-angle
+    kinematics) breaks conservation by O(1), RK4 at h = 1e-4 s keeps it to ~1e-12."""
+    for inertia in ([0.10, 0.0, 0.0, 0.0, 0.25, 0.0, 0.0, 0.0, 0.28],
+                    [0.12, 0.01, -0.02, 0.01, 0.20, 0.015, -0.02, 0.015, 0.25]):
+        p = dict(PRM); p["inertia"] = inertia
+        I = np.array(inertia).reshape(3, 3)
+        x = np.zeros(12); x[2] = 0.3; x[3:6] = [0.1, -0.2, 0.3]; x[9:12] = [0.8, -0.6, 1.1]
+
+        def Lw(x):
+            R = Rotation.from_euler("ZYX", [x[5], x[4], x[3]]).as_matrix()
+            return R @ (I @ x[9:12])
+        L0, E0 = Lw(x), 0.5 * x[9:12] @ I @ x[9:12]
+        nobody = np.zeros(4, np.uint8)
+        for _ in range(50):       # 0.5 s in 50 plant calls of 10 ms, 100 RK4 substeps each
+            x = O.srbd_plant(p, x, np.zeros(12), np.zeros((4, 3)), nobody, None, 0.01, 100)
+            assert abs(x[4]) < 1.2
+            assert np.abs(Lw(x) - L0).max() <= 1e-9 * np.abs(L0).max()
+            assert abs(0.5 * x[9:12] @ I @ x[9:12] - E0) <= 1e-9 * E0
+        assert np.abs(x[9:12] - [0.8, -0.6, 1.1]).max() > 1e-2     # the body frame rates did change
+
+
+def test_theta_counts_initial_condition_defect(O):
+    """theta = sum_i ||x_{i+1} - h(x_i,u_i)||_2 + ||xhat0 - x_0||_2 (reading R9):
+    a ballistic trajectory (no stance feet, w = 0: h(x) = x + dt (v, 0, g, 0), written out here)
+    has zero dynamics defects, so theta is exactly the initial-condition term (3-4-5) plus one
+    planted defect (5-12-13)."""
+    N = 6
+    prob = synth.srbd_problem(1, N=N, seed=3)
+    p = prob["params"]; dt = p["dt"]; g = np.array(p["gravity"])
+    prob["contact"][:] = 0
+    x = np.zeros((N + 2, 12)); x[0, 0:3] = [0.1, -0.2, 0.35]; x[0, 3:6] = [0.05, -0.1, 0.7]
+    x[0, 6:9] = [0.4, 0.1, 0.0]
+    for i in range(N + 1):
+        x[i + 1] = x[i]
+        x[i + 1, 0:3] = x[i, 0:3] + dt * x[i, 6:9]
+        x[i + 1, 6:9] = x[i, 6:9] + dt * g
+    u = np.random.default_rng(0).uniform(-5, 5, (N + 1, 12))     # swing feet: forces do nothing
+    prob["x0"][0] = x[0]
+    assert O.srbd_theta(prob, 0, x, u) == pytest.approx(0.0, abs=1e-14)
+    prob["x0"][0] = x[0] + np.r_[0.03, 0.0, 0.0, 0.04, np.zeros(8)]
+    assert O.srbd_theta(prob, 0, x, u) == pytest.approx(0.05, abs=1e-14)
+    x[N + 1, 6] += 0.05; x[N + 1, 11] += 0.12          # the last node enters one defect only
+    assert O.srbd_theta(prob, 0, x, u) == pytest.approx(0.05 + 0.13, abs=1e-14)
+
+
+def test_cost_value_hand_computed(O):
+    """J = sum_i l_i + l_{N+1} on a case computed by hand: tracking terms only
+    at the nodes perturbed, one stance foot whose six constraints are written out, the barrier of
+    the golden worked value's definition (tests/golden/barrier_value.json)."""
+    N = 2
+    prob = synth.srbd_problem(1, N=N, seed=4)
+    p = prob["params"]
+    prob["contact"][:] = 0
+    prob["u_ref"][0, 1, 6:9] = 0.0
+    x = prob["x_ref"][0].copy(); u = prob["u_ref"][0].copy()
+    x[1, 2] += 0.1                         # 1/2 * 500 * 0.01 = 2.5
+    x[N + 1, 0] += 0.2                     # terminal: 1/2 * 50 * 0.04 = 1.0
+    u[0, 1] += 2.0                         # swing weight 10: 1/2 * 10 * 4 = 20
+    prob["contact"][0, 1, 2] = 1           # foot 2 in stance at node 1 with f = (3, -1, 40)
+    u[1, 6:9] = [3.0, -1.0, 40.0]          # stance weight 1e-3 against u_ref (0 there: swing)
+    track_u = 0.5 * 1e-3 * (9 + 1 + 1600)
+    mu, d = p["barrier_mu"], p["barrier_delta"]
+
+    def bar(xi):
+        return -mu * math.log(xi) if xi >= d else 0.5 * mu * (((xi - 2 * d) / d) ** 2 - 1) - mu * math.log(d)
+    xis = [0.6 * 40 - 3, 0.6 * 40 + 3, 0.6 * 40 + 1, 0.6 * 40 - 1, 40 - 2.0, 250.0 - 40]
+    expect = 2.5 + 1.0 + 20.0 + track_u + sum(bar(v) for v in xis)
+    assert O.srbd_cost(prob, 0, x, u) == pytest.approx(expect, rel=1e-13)
+    # the same foot in the quadratic (relaxed) branch: f_z = 2.5 -> fz - fmin = 0.5 < delta
+    u[1, 6:9] = [0.0, 0.0, 2.5]
+    xis = [1.5, 1.5, 1.5, 1.5, 0.5, 247.5]
+    expect = 2.5 + 1.0 + 20.0 + 0.5 * 1e-3 * 6.25 + sum(bar(v) for v in xis)
+    assert O.srbd_cost(prob, 0, x, u) == pytest.approx(expect, rel=1e-13)
+
+
+def test_cost_slope_matches_central_difference(O):
+    """The descent test's slope grad J . (dx, du) (reading R10) equals the central difference of J
+    along the direction, with every term active: tracking, terminal, swing weights, and barriers
+    in both branches (some stance forces pushed below f_min + delta)."""
+    prob = synth.srbd_problem(4, N=10, seed=5)
+    rng = np.random.default_rng(9)
+
+    def cd(prob, b, x, u, dx, du):   # central difference, Richardson-extrapolated (O(h^4))
+        D = lambda h: (O.srbd_cost(prob, b, x + h * dx, u + h * du) - O.srbd_cost(prob, b, x - h * dx, u - h * du)) / (2 * h)
+        return (4 * D(5e-5) - D(1e-4)) / 3
+    prob["u"] += rng.normal(0, 8, prob["u"].shape)
+    prob["x"] += 0.05 * rng.standard_normal(prob["x"].shape)
+    for b in range(4):
+        st = prob["contact"][b].astype(bool)
+        for i in range(11):
+            for j in range(4):
+                if st[i, j] and rng.uniform() < 0.3:
+                    prob["u"][b, i, 3 * j + 2] = rng.uniform(2.1, 2.9)     # quadratic branch
+        for _ in range(3):
+            dx = rng.standard_normal((12, 12)) * 0.1
+            du = rng.standard_normal((11, 12)) * 2.0
+            x, u = prob["x"][b], prob["u"][b]
+            fd = cd(prob, b, x, u, dx, du)
+            _, _, _, (_, _, g) = O.srbd_line_search(prob, b, dx, du)
+            assert g == pytest.approx(fd, rel=1e-7, abs=1e-7 * max(1.0, abs(fd)))
+            # terminal-only and u-only directions separately (a dropped term cannot cancel)
+            for ddx, ddu in ((np.zeros_like(dx), du), (np.r_[np.zeros((11, 12)), dx[-1:]], np.zeros_like(du))):
+                fd = cd(prob, b, x, u, ddx, ddu)
+                _, _, _, (_, _, g) = O.srbd_line_search(prob, b, ddx, ddu)
+                assert g == pytest.approx(fd, rel=1e-7, abs=1e-7 * max(1.0, abs(fd)))

@@ -146,15 +146,31 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------- oracle baseline
-def cpu_baseline(B: int, N: int, seed: int, budget_s: float = 10.0, sample: int = 1024):
+def cpu_info() -> dict:
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def cpu_baseline(B: int, N: int, seed: int, budget_s: float = 10.0, sample: int = 1024,
+                 latency_horizons=(), lat_budget_s: float = 1.0):
     """The fp64 oracle as it stands (oracle/pdilqr_oracle.c, OpenMP over instances, all host
-    cores) on a bounded sample of the same workload: repeated steps of `sample` instances until
-    `budget_s` of wall time.  Returns solves/s and what was run."""
+    cores; built with -march=native on this host) on a bounded sample of the same workload:
+    repeated steps of `sample` instances until `budget_s` of wall time.  Plus the single-core p50
+    latency of one oracle step (B = 1, config 2) per horizon, each bounded by
+    `lat_budget_s`.  Returns solves/s, the latency table and what was run."""
     from oracle import oracle as O
-    O.build()
+    O.use_native()
     ns = min(sample, B)
     prob = synth.srbd_problem(ns, N=N, seed=seed)
     threads = O.max_threads()
+    O.srbd_step(prob, nthreads=threads)
     t0 = time.perf_counter()
     reps = 0
     while True:
@@ -163,16 +179,30 @@ def cpu_baseline(B: int, N: int, seed: int, budget_s: float = 10.0, sample: int 
         if time.perf_counter() - t0 >= budget_s:
             break
     dt = time.perf_counter() - t0
+    lat = {}
+    for Nl in latency_horizons:
+        p1 = synth.srbd_problem(1, N=Nl, seed=synth.BASE_SEED + 2, randomize=False)
+        ts = []
+        t1 = time.perf_counter()
+        while len(ts) < 3 or (time.perf_counter() - t1 < lat_budget_s and len(ts) < 200):
+            q = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in p1.items()}
+            a = time.perf_counter()
+            O.srbd_step(q, nthreads=1)
+            ts.append((time.perf_counter() - a) * 1e6)
+        lat[str(Nl)] = {"p50_us": float(np.percentile(ts, 50)), "runs": len(ts)}
     return {"value": ns * reps / dt, "unit": "solves/s", "cores": threads, "kind": "oracle",
+            **cpu_info(), "build": O.build_flags(),
+            "single_core_latency_us": lat,
             "sample": f"{reps} batched oracle steps of the first {ns} of {B} config-3 instances (N={N}), "
-                      f"{dt:.1f} s wall, fp64, {threads} OpenMP threads"}
+                      f"{dt:.1f} s wall, fp64, {threads} OpenMP threads; latency: one step of config 2 "
+                      f"(B=1) on 1 thread per horizon, up to 200 runs or {lat_budget_s:.0f} s"}
 
 
 def run_reference(args, rank: int):
     if rank != 0:
         return None
     from oracle import oracle as O
-    O.build()
+    O.use_native()
     ns = min(args.ref_sample, args.batch)
     prob = synth.srbd_problem(ns, N=args.N, seed=synth.BASE_SEED)
     threads = O.max_threads()
@@ -189,7 +219,8 @@ def run_reference(args, rank: int):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (workloads/synth.py, seeded)",
             "config": {"workload": "srbd_mpc_config3", "batch_per_gpu": args.batch, "N": args.N, "n": 12, "m": 12},
-            "cpu_baseline": {"value": v, "unit": "solves/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "solves/s", "cores": threads, "kind": "oracle", "sample": sample,
+                             **cpu_info(), "build": O.build_flags()},
             "e2e": {"value": v, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -211,7 +242,12 @@ def main():
     ap.add_argument("--profile-only", action="store_true", help="short run for ncu (no JSON extras)")
     ap.add_argument("--latency", default="25,50,100,200,400,1000",
                     help="horizons of the B=1 latency sweep (config 2), '' to skip")
-    ap.add_argument("--latency-reps", type=int, default=300)
+    ap.add_argument("--latency-reps", type=int, default=1000)
+    ap.add_argument("--latency-warmup", type=int, default=50)
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="gloo: CPU collectives (e.g. two ranks sharing one GPU to exercise the sharded path)")
+    ap.add_argument("--no-scan-legs", action="store_true", help="skip the B=4096 tree / chunked scan legs")
+    ap.add_argument("--gather-out", default="", help="rank 0 saves the gathered [B_total][17] u0 + stats here")
     ap.add_argument("--closed-loop-ticks", type=int, default=50, help="0 disables the closed-loop RTF leg")
     ap.add_argument("--no-large", action="store_true", help="skip the large-dimension LQ leg (configs 4, 5)")
     args = ap.parse_args()
@@ -229,19 +265,27 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2506_07823_b200 as P
+    from paper_2506_07823_b200 import sharding
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    ndev = torch.cuda.device_count()
+    local_dev = local % ndev          # ranks may share a device (gloo test runs on a 1-GPU box)
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    coll_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
     tdt = torch.float32 if args.dtype == "f32" else torch.float64
     B, N = args.batch, args.N
 
-    prob = synth.srbd_problem(B, N=N, seed=synth.BASE_SEED, first=rank * B)
+    first, _ = sharding.shard(B, rank)
+    prob = synth.srbd_problem(B, N=N, seed=synth.BASE_SEED, first=first)
     h = P.PdIlqr(N=N, n=12, m=12, batch=B, dtype=tdt, model="srbd", srbd=prob["params"],
-                 leaf_chunk=args.leaf_chunk, device=local)
+                 leaf_chunk=args.leaf_chunk, device=local_dev)
     npd = np.float32 if tdt == torch.float32 else np.float64
 
     def upload():
@@ -265,8 +309,8 @@ def main():
         return
 
     # --------------------------------------------------------------- timed region (device)
-    clk = ClockSampler(local)
-    h.profile(True)
+    # No instrumentation inside: the per-kernel breakdown comes from a separate pass below.
+    clk = ClockSampler(local_dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -283,30 +327,46 @@ def main():
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
+    ms_max = sharding.max_over_ranks(ms, world, coll_dev, dist)
+    value = world * B * args.steps / (ms_max / 1e3)
+    # validation of the timed steps: every instance factorised, finite statistics
+    info = stats["info"]
+    step_check = {"info_nonzero": int((info != 0).sum().item()), "info_negative": int((info < 0).sum().item()),
+                  "theta_finite": bool(torch.isfinite(stats["theta"]).all().item()),
+                  "cost_finite": bool(torch.isfinite(stats["cost"]).all().item()),
+                  "accepted_last_step": int(stats["accepted"].sum().item())}
+    if step_check["info_negative"] or not (step_check["theta_finite"] and step_check["cost_finite"]):
+        raise SystemExit(f"bench.py: timed steps produced non-finite results: {step_check}")
+
+    # per-kernel CUDA-event breakdown (separate, untimed pass over the same number of steps)
+    h.profile(True)
+    for _ in range(min(args.steps, 50)):
+        h.step(it, stats)
+    torch.cuda.synchronize()
     prof = h.profile_read()
     h.profile(False)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * B * args.steps / (ms_max / 1e3)
 
-    # final collective (outside the hot path): all-gather of u0 and stats over NCCL
+    # final collective (outside the hot path): all-gather of u0 and stats
     gather_ms = None
+    gathered = None
     if world > 1:
-        u0 = it["u"][:, 0, :].contiguous()
-        st = torch.stack([stats["cost"].to(u0.dtype), stats["theta"].to(u0.dtype), stats["alpha"].to(u0.dtype),
-                          stats["accepted"].to(u0.dtype), stats["info"].to(u0.dtype)], 1)
-        g_u0 = torch.empty(world * B, 12, dtype=u0.dtype, device=dev)
-        g_st = torch.empty(world * B, 5, dtype=u0.dtype, device=dev)
+        packed = sharding.pack_results(it["u"][:, 0, :], stats).to(coll_dev)
         dist.barrier()
-        a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        dist.all_gather_into_tensor(g_u0, u0)
-        dist.all_gather_into_tensor(g_st, st)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        gather_ms = a0.elapsed_time(a1)
+        t0 = time.perf_counter()
+        if coll_dev.type == "cuda":
+            a0 = torch.cuda.Event(enable_timing=True); a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            gathered = sharding.gather_results(packed, world, dist)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            gather_ms = a0.elapsed_time(a1)
+        else:
+            gathered = sharding.gather_results(packed, world, dist)
+            gather_ms = (time.perf_counter() - t0) * 1e3
+    if args.gather_out and rank == 0:
+        if gathered is None:   # one rank: its own packed rows (same layout as the gathered tensor)
+            gathered = sharding.pack_results(it["u"][:, 0, :], stats)
+        torch.save(gathered.cpu(), args.gather_out)
 
     # --------------------------------------------------------------- e2e via host buffers
     e2e = None
@@ -330,11 +390,9 @@ def main():
             stream.synchronize()
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t_e2e = sharding.max_over_ranks(e0.elapsed_time(e1), world, coll_dev, dist)
         es = np.dtype(npd).itemsize
-        e2e = {"value": world * B * args.steps / (float(t.item()) / 1e3), "unit": "solves/s",
+        e2e = {"value": world * B * args.steps / (t_e2e / 1e3), "unit": "solves/s",
                "h2d_bytes_per_step": B * 12 * es,
                "d2h_bytes_per_step": B * 12 * es + 3 * B * es + 2 * B * 4,
                "api": "pdilqr_tick_host (pinned host x0 -> step -> host u0 + stats, sync per tick)"}
@@ -364,10 +422,18 @@ def main():
                 "share_of_step": (tot / launches) / step_ms,
                 "peak_basis": f"FP32 FMA pipe: 148 SMs x 128 lanes x 2 flop x {sm_mhz:.0f} MHz (max SM clock)",
                 "per_kernel_ms": {k: v[1] / v[0] for k, v in prof.items()}}
+        mp = measured_peaks()
+        if mp.get("bf16_tflops"):
+            scale = float(mp["bf16_tflops"]) / 2250.0
+            roof["peak_measured_scaled"] = peak * scale
+            roof["frac_vs_measured_scaled"] = ach / (peak * scale)
+            roof["peak_measured_scaled_basis"] = (f"FP32 peak x measured/nominal dense bf16 ({mp['bf16_tflops']:.0f} / "
+                                                  f"2250 TFLOP/s, MEASURED_PEAKS.json): no FP32 entry is measured")
 
     lat = None
     if args.latency:
-        lat = latency_sweep(P, torch, dev, [int(v) for v in args.latency.split(",")], args.latency_reps)
+        lat = latency_sweep(P, torch, dev, [int(v) for v in args.latency.split(",")], args.latency_reps,
+                            args.latency_warmup)
     clo = None
     if args.closed_loop_ticks > 0 and args.dtype == "f32":
         clo = closed_loop_bench(P, torch, dev, B, N, args.closed_loop_ticks)
@@ -377,7 +443,12 @@ def main():
     large = None
     if not args.no_large and args.dtype == "f32":
         large = large_bench(P, torch, dev, sm_mhz=(clocks or {}).get("sm_max_mhz") or 1965.0)
-    cpu = None if args.no_cpu_baseline else cpu_baseline(B, N, synth.BASE_SEED, args.cpu_budget)
+    scan_legs = None
+    if not args.no_scan_legs and args.dtype == "f32":
+        scan_legs = scan_legs_bench(P, torch, dev, B, N, upload, args.steps, peak)
+    cpu = None if args.no_cpu_baseline else cpu_baseline(B, N, synth.BASE_SEED, args.cpu_budget,
+                                                        latency_horizons=[int(v) for v in args.latency.split(",")]
+                                                        if args.latency else [])
     out = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (workloads/synth.py, seeded; config 3)",
@@ -385,11 +456,13 @@ def main():
                       "leaf_chunk": h_chunk(args, B, N), "n_alpha": 10,
                       "l2": "working set (QP + scan workspace) ~%.2f GB per GPU > 126 MB L2; no flush needed"
                             % (h.workspace.numel() / 1e9),
-                      "parallelism": f"batch-sharded dp{world}, no collective on the hot path"},
+                      "parallelism": f"batch-sharded dp{world}, no collective on the hot path"
+                                     + (f" ({args.dist_backend} for the final gather)" if world > 1 else "")},
            "gpu_launches": launches_per_step * args.steps, "clocks": clocks, "e2e": e2e,
            "roofline": roof, "cpu_baseline": cpu,
            "kernels_ms": {k: v[1] / v[0] for k, v in prof.items()},
-           "latency": lat, "closed_loop": clo, "solve_lq_only": lq_only, "large": large}
+           "step_check": step_check, "latency": lat, "scan_legs": scan_legs, "closed_loop": clo,
+           "solve_lq_only": lq_only, "large": large}
     if gather_ms is not None:
         out["final_allgather_ms"] = gather_ms
     print(json.dumps(out), flush=True)
@@ -397,7 +470,7 @@ def main():
         dist.destroy_process_group()
 
 
-def latency_sweep(P, torch, dev, horizons, reps, warm=30):
+def latency_sweep(P, torch, dev, horizons, reps, warm=50):
     """Config 2: p50 / p90 single-instance (B=1) pdilqr_step latency vs horizon N, from CUDA-graph
     replays timed one by one with CUDA events (device time), plus the end-to-end tick through
     pdilqr_tick_host (pinned x0 in, u0 + stats out, host synchronisation).  fp32 and fp64."""
@@ -595,6 +668,53 @@ def large_bench(P, torch, dev, sm_mhz, reps=5):
                      "fold_flops": fl, "fold_tflops": (fl / ric / 1e9) if ric else None,
                      "fold_frac_fp32_peak": (fl / ric / 1e9 / fp32_peak_tflops(sm_mhz)) if ric else None}
         del h, out, qp
+    return res
+
+
+def measured_peaks() -> dict:
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def scan_legs_bench(P, torch, dev, B, N, upload, steps, peak, chunks=(1, 8)):
+    """The paper's associative scans at the headline configuration (B = 4096, N = 50): the same
+    step with leaf_chunk = 1 (the pure tree of P:195) and an intermediate chunk, instead of the
+    single-chunk fold the default picks at B >= 148 (DESIGN D1).  CUDA events around `steps`
+    steps (inputs resident); scan-method flops of the flop model / step time vs the FP32 peak."""
+    res = {}
+    steps = max(5, min(steps, 50))
+    prob = synth.srbd_problem(1, N=N)
+    for c in chunks:
+        h = P.PdIlqr(N=N, n=12, m=12, batch=B, dtype=torch.float32, model="srbd", srbd=prob["params"],
+                     leaf_chunk=c, device=dev.index)
+        it = upload()
+        st = h.new_stats()
+        for _ in range(3):
+            h.step(it, st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(steps):
+            h.step(it, st)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        h.profile(True)
+        for _ in range(5):
+            h.step(it, st)
+        torch.cuda.synchronize()
+        pr = h.profile_read()
+        h.profile(False)
+        fl = flops_per_instance(N, chunk=c)
+        tot = sum(fl[k] for k in ("k_elem_init", "k_scan_bwd", "k_policy", "k_scan_fwd", "k_tail"))
+        res[f"leaf_chunk_{c}"] = {"ms_per_step": ms, "solves_per_s": B / ms * 1e3,
+                                  "kernels_ms": {k: v[1] / v[0] for k, v in pr.items()},
+                                  "scan_method_mflop_per_instance": tot / 1e6,
+                                  "frac_fp32_peak": tot * B / ms / 1e9 / peak,
+                                  "info_ok": bool((st["info"] == 0).all().item())}
+        del h, it, st
     return res
 
 

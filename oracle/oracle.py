@@ -21,13 +21,30 @@ _ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 _up = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 
 
-def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (-O3, OpenMP).  Plain x86-64 code (no -march=native) so the
-    same binary runs on the GPU box's host."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-std=gnu11", "-O3", "-fopenmp", "-fPIC", "-shared",
-                               "-Wall", "-o", _LIB, _SRC])
-    return _LIB
+_FLAGS = ["-std=gnu11", "-O3", "-fopenmp", "-fPIC", "-shared", "-Wall"]
+_native = False
+
+
+def build(force: bool = False, native: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O3, OpenMP): plain x86-64 code, so the same binary runs on
+    any host (tests).  native=True builds liboracle_native.so with -march=native for the timed
+    CPU baseline, on the host that runs it (bench.py)."""
+    lib = _LIB.replace(".so", "_native.so") if native else _LIB
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *_FLAGS, *(["-march=native"] if native else []), "-o", lib + ".tmp", _SRC])
+        os.replace(lib + ".tmp", lib)
+    return lib
+
+
+def use_native() -> None:
+    """Timed baselines: load the -march=native build (call before the first oracle call)."""
+    global _native
+    if _lib is None:
+        _native = True
+
+
+def build_flags() -> str:
+    return "gcc " + " ".join(_FLAGS[:3] + (["-march=native"] if _native else []))
 
 
 class SrbdParams(C.Structure):
@@ -57,7 +74,7 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        L = C.CDLL(build())
+        L = C.CDLL(build(native=_native))
         i, d, PP = C.c_int, C.c_double, C.POINTER(SrbdParams)
         L.oracle_riccati.argtypes = [i, i, i] + [_dp] * 11 + [_dp] * 4
         L.oracle_riccati.restype = i

@@ -1,6 +1,7 @@
-"""Multi-process logic of the batch-sharded bench on CPU with gloo, world_size 2:
-each rank regenerates only its own instances [r*B, (r+1)*B) and solves them (the fp64 oracle stands
-in for the GPU solver), then one all_gather assembles u0 and the stats; the result must equal the
+"""Multi-process logic of the batch-sharded bench on CPU with gloo, world_size 2,
+through the same functions bench.py calls (paper_2506_07823_b200/sharding.py): each rank
+regenerates only its own instances [r*B, (r+1)*B) and solves them (the fp64 oracle stands in for
+the GPU solver), then one all_gather assembles u0 and the stats; the result must equal the
 single-process run on the full batch."""
 import os
 import socket
@@ -29,18 +30,16 @@ def _worker(rank, port, out_path):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
     from oracle import oracle as O
-    prob = synth.srbd_problem(BPR, N=N, seed=synth.BASE_SEED, first=rank * BPR)
-    st = O.srbd_step(prob, nthreads=1)
-    u0 = torch.from_numpy(prob["u"][:, 0, :].copy())
-    stt = torch.from_numpy(st)
-    gu = [torch.empty_like(u0) for _ in range(WORLD)]
-    gs = [torch.empty_like(stt) for _ in range(WORLD)]
-    dist.all_gather(gu, u0)
-    dist.all_gather(gs, stt)
-    t = torch.tensor([float(rank + 1)])
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)      # max-over-ranks timing reduction
+    from paper_2506_07823_b200 import sharding
+    first, nb = sharding.shard(BPR, rank)
+    prob = synth.srbd_problem(nb, N=N, seed=synth.BASE_SEED, first=first)
+    st = O.srbd_step(prob, nthreads=1)          # the fp64 oracle stands in for the GPU step
+    stats = {k: torch.from_numpy(st[:, j].copy()) for j, k in enumerate(sharding.STAT_KEYS)}
+    packed = sharding.pack_results(torch.from_numpy(prob["u"][:, 0, :].copy()), stats)
+    g = sharding.gather_results(packed, WORLD, dist)
+    tmax = sharding.max_over_ranks(float(rank + 1), WORLD, torch.device("cpu"), dist)
     if rank == 0:
-        np.savez(out_path, u0=torch.cat(gu).numpy(), st=torch.cat(gs).numpy(), tmax=t.numpy())
+        np.savez(out_path, g=g.numpy(), tmax=np.array([tmax]))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -53,8 +52,8 @@ def test_two_rank_shard_and_gather(tmp_path):
     g = np.load(out)
     full = synth.srbd_problem(WORLD * BPR, N=N, seed=synth.BASE_SEED)
     st = O.srbd_step(full, nthreads=1)
-    assert np.array_equal(g["u0"], full["u"][:, 0, :])
-    assert np.array_equal(g["st"], st)
+    assert np.array_equal(g["g"][:, :12], full["u"][:, 0, :])
+    assert np.array_equal(g["g"][:, 12:], st)
     assert g["tmax"][0] == WORLD
 
 

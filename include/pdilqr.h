@@ -137,6 +137,32 @@ pdilqr_status pdilqr_destroy(pdilqr_handle h);
 pdilqr_status pdilqr_solve_lq(pdilqr_handle h, const pdilqr_lq *qp, pdilqr_dir *dir,
                               int32_t *info, void *stream /* cudaStream_t */);
 
+/* Gradients of a scalar loss L with respect to the Eq. 4 data of pdilqr_solve_lq (same layouts
+ * and dtype as pdilqr_lq; device pointers; any member may be NULL = not wanted). */
+typedef struct {
+    void *A, *Bm, *c, *Q, *R, *S, *q, *r, *P_term, *p_term, *dx0;
+} pdilqr_lq_grad;
+
+/* Adjoint of pdilqr_solve_lq (NEXT-4 of SURVEY §8(f): the solver made differentiable for learning,
+ * P:61-62).  The LQ solution z = (dx, du, dlam) is the unique solution of the KKT
+ * system M z = rhs of Eq. 4 (M symmetric: Hessian blocks Q, R, S, P_{N+1} and the constraint
+ * Jacobian [A_i, B_i, -I]; rhs = -(q, r, p_{N+1}) and -(dx0, c)).  Given the upstream gradient
+ * g = dL/dz (gsol: dx, du, dlam; NULL members = 0) it solves M w = g by the same parallel scans
+ * (one more pdilqr_solve_lq with the handle's matrices and the linear terms q' = -g_dx[0..N],
+ * r' = -g_du, p_{N+1}' = -g_dx[N+1], dx0' = -g_dlam[0], c_i' = -g_dlam[i+1]) and writes
+ *   dL/dq_i = -w_dx[i], dL/dr_i = -w_du[i], dL/dp_{N+1} = -w_dx[N+1], dL/ddx0 = -w_dlam[0],
+ *   dL/dc_i = -w_dlam[i+1],
+ *   dL/dQ_i = -w_dx[i] dx[i]^T, dL/dR_i = -w_du[i] du[i]^T, dL/dP_{N+1} = -w_dx[N+1] dx[N+1]^T,
+ *   dL/dS_i = -(w_du[i] dx[i]^T + du[i] w_dx[i]^T),
+ *   dL/dA_i = -(w_dlam[i+1] dx[i]^T + dlam[i+1] w_dx[i]^T),
+ *   dL/dB_i = -(w_dlam[i+1] du[i]^T + dlam[i+1] w_du[i]^T)
+ * (dL = w^T (d rhs - dM z)).  The matrix gradients treat every entry as independent (symmetrise
+ * for symmetric parametrisations).  sol = the forward solution of the same qp (device, required:
+ * dx, du, dlam).  info as pdilqr_solve_lq.  No allocation, no host sync (graph capturable). */
+pdilqr_status pdilqr_solve_lq_adjoint(pdilqr_handle h, const pdilqr_lq *qp, const pdilqr_dir *sol,
+                                      const pdilqr_dir *gsol, pdilqr_lq_grad *grad, int32_t *info,
+                                      void *stream);
+
 /* SRBD linearisation + Gauss-Newton quadraticisation at the iterate (
  * q, r include the multiplier terms, reading R8).  SRBD handles only.  Exposed for inspection;
  * pdilqr_step performs it internally.  info may be NULL. */

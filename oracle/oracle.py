@@ -82,6 +82,8 @@ def lib():
         L.oracle_solve_lq.argtypes = [i, i, i] + [_dp] * 11 + [_dp] * 3 + [_dp] * 4
         L.oracle_solve_lq.restype = i
         L.oracle_solve_lq_batch.argtypes = [i, i, i, i] + [_dp] * 11 + [_dp] * 3 + [_ip, i]
+        L.oracle_solve_lq_adjoint.argtypes = [i, i, i] + [_dp] * 6 + [_dp] * 3 + [_dp] * 3 + [_dp] * 11
+        L.oracle_solve_lq_adjoint.restype = i
         L.oracle_srbd_f.argtypes = [PP, _dp, _dp, _dp, _up, _dp]
         L.oracle_srbd_jac.argtypes = [PP, _dp, _dp, _dp, _up, _dp, _dp]
         L.oracle_srbd_h.argtypes = [PP, _dp, _dp, _dp, _up, _dp]
@@ -146,6 +148,23 @@ def solve_lq(qp: dict, nthreads: int | None = None):
                                 _c(qp["p_term"]), _c(qp["dx0"]), dx, du, dl, info,
                                 nthreads or max_threads())
     return {"dx": dx, "du": du, "dlam": dl, "info": info}
+
+
+def solve_lq_adjoint_single(qp: dict, sol: dict, g: dict, b: int = 0):
+    """Gradients of L (dL/d(dx, du, dlam) = g) w.r.t. instance b's Eq. 4 data, given its forward
+    solution sol (dict dx, du, dlam of that instance).  Returns (dict of gradients, info)."""
+    A = _c(qp["A"][b]); N1, n, _ = A.shape
+    N = N1 - 1
+    m = qp["Bm"].shape[-1]
+    out = {k: np.zeros_like(_c(qp[k][b])) for k in ("A", "Bm", "c", "Q", "R", "S", "q", "r", "P_term", "p_term", "dx0")}
+    gz = lambda k, shp: _c(g[k]) if g.get(k) is not None else np.zeros(shp)
+    info = lib().oracle_solve_lq_adjoint(
+        N, n, m, A, _c(qp["Bm"][b]), _c(qp["Q"][b]), _c(qp["R"][b]), _c(qp["S"][b]), _c(qp["P_term"][b]),
+        _c(sol["dx"]), _c(sol["du"]), _c(sol["dlam"]),
+        gz("dx", (N + 2, n)), gz("du", (N + 1, m)), gz("dlam", (N + 2, n)),
+        out["A"], out["Bm"], out["c"], out["Q"], out["R"], out["S"], out["q"], out["r"], out["P_term"],
+        out["p_term"], out["dx0"])
+    return out, info
 
 
 # ----------------------------------------------------------------------------- SRBD

@@ -232,6 +232,69 @@ int oracle_solve_lq(int N, int n, int m,
     return st;
 }
 
+/* Adjoint of the LQ solve (NEXT-4; the differentiable solver of P:61-62): z = (dx, du, dlam)
+ * solves the symmetric KKT system M z = rhs of Eq. 4, so for a loss L with dL/dz = g,
+ *   w = M^{-1} g,  dL/drhs = w,  dL/dM = -w z^T   (dL = w^T (d rhs - dM z)).
+ * M w = g is itself an LQ problem with the same matrices and the linear terms
+ *   q'_i = -g_dx[i] (i <= N), r'_i = -g_du[i], p'_{N+1} = -g_dx[N+1], dx0' = -g_dlam[0],
+ *   c'_i = -g_dlam[i+1],
+ * solved here by the same sequential Riccati recursion (oracle_solve_lq).  Then, block by block of
+ * M (Q_i, R_i, S_i / S_i^T, P_{N+1}, and the constraint Jacobian blocks A_i / A_i^T, B_i / B_i^T):
+ *   gQ_i = -w_dx[i] dx[i]^T, gR_i = -w_du[i] du[i]^T, gS_i = -(w_du[i] dx[i]^T + du[i] w_dx[i]^T),
+ *   gP_{N+1} = -w_dx[N+1] dx[N+1]^T, gA_i = -(w_dlam[i+1] dx[i]^T + dlam[i+1] w_dx[i]^T),
+ *   gB_i = -(w_dlam[i+1] du[i]^T + dlam[i+1] w_du[i]^T);
+ * and from rhs = -(q, r, p_{N+1}; dx0, c): gq_i = -w_dx[i], gr_i = -w_du[i], gp_{N+1} = -w_dx[N+1],
+ * gdx0 = -w_dlam[0], gc_i = -w_dlam[i+1].  Returns the solve's status. */
+int oracle_solve_lq_adjoint(int N, int n, int m,
+                            const double *A, const double *Bm, const double *Q, const double *R,
+                            const double *S, const double *Pt,
+                            const double *dx, const double *du, const double *dlam,
+                            const double *gdx, const double *gdu, const double *gdlam,
+                            double *gA, double *gB, double *gc, double *gQ, double *gR, double *gS,
+                            double *gq, double *gr, double *gPt, double *gpt, double *gdx0) {
+    const size_t S1 = (size_t)(N + 1), nn = (size_t)n * n, nm = (size_t)n * m, mm = (size_t)m * m;
+    double *q2 = malloc(sizeof(double) * S1 * n), *r2 = malloc(sizeof(double) * S1 * m);
+    double *c2 = malloc(sizeof(double) * S1 * n), *pt2 = malloc(sizeof(double) * n);
+    double *d02 = malloc(sizeof(double) * n);
+    double *wx = malloc(sizeof(double) * (S1 + 1) * n), *wu = malloc(sizeof(double) * S1 * m);
+    double *wl = malloc(sizeof(double) * (S1 + 1) * n);
+    for (size_t i = 0; i <= (size_t)N; ++i) {
+        for (int a = 0; a < n; ++a) q2[i * n + a] = -gdx[i * n + a];
+        for (int a = 0; a < m; ++a) r2[i * m + a] = -gdu[i * m + a];
+        for (int a = 0; a < n; ++a) c2[i * n + a] = -gdlam[(i + 1) * n + a];
+    }
+    for (int a = 0; a < n; ++a) { pt2[a] = -gdx[(S1) * n + a]; d02[a] = -gdlam[a]; }
+    int st = oracle_solve_lq(N, n, m, A, Bm, c2, Q, R, S, q2, r2, Pt, pt2, d02, wx, wu, wl,
+                             NULL, NULL, NULL, NULL);
+    if (st == 0) {
+        for (size_t i = 0; i <= (size_t)N; ++i) {
+            const double *xi = dx + i * n, *wxi = wx + i * n, *ui = du + i * m, *wui = wu + i * m;
+            const double *l1 = dlam + (i + 1) * n, *wl1 = wl + (i + 1) * n;
+            for (int a = 0; a < n; ++a)
+                for (int b = 0; b < n; ++b) {
+                    gQ[i * nn + IDX2(a, b, n)] = -wxi[a] * xi[b];
+                    gA[i * nn + IDX2(a, b, n)] = -(wl1[a] * xi[b] + l1[a] * wxi[b]);
+                }
+            for (int a = 0; a < m; ++a)
+                for (int b = 0; b < m; ++b) gR[i * mm + IDX2(a, b, m)] = -wui[a] * ui[b];
+            for (int a = 0; a < m; ++a)
+                for (int b = 0; b < n; ++b) gS[i * nm + IDX2(a, b, n)] = -(wui[a] * xi[b] + ui[a] * wxi[b]);
+            for (int a = 0; a < n; ++a)
+                for (int b = 0; b < m; ++b) gB[i * nm + IDX2(a, b, m)] = -(wl1[a] * ui[b] + l1[a] * wui[b]);
+            for (int a = 0; a < n; ++a) { gq[i * n + a] = -wxi[a]; gc[i * n + a] = -wl1[a]; }
+            for (int a = 0; a < m; ++a) gr[i * m + a] = -wui[a];
+        }
+        const double *xt = dx + S1 * n, *wxt = wx + S1 * n;
+        for (int a = 0; a < n; ++a) {
+            for (int b = 0; b < n; ++b) gPt[IDX2(a, b, n)] = -wxt[a] * xt[b];
+            gpt[a] = -wxt[a];
+            gdx0[a] = -wl[a];
+        }
+    }
+    free(q2); free(r2); free(c2); free(pt2); free(d02); free(wx); free(wu); free(wl);
+    return st;
+}
+
 /* Batched LQ solve over B independent instances (batch-outermost arrays). */
 void oracle_solve_lq_batch(int Bn, int N, int n, int m,
                            const double *A, const double *Bm, const double *c,

@@ -5,5 +5,6 @@ package is a thin ctypes binding.  There is no CPU fallback.
 """
 from .pdilqr import PdIlqr, PdilqrError, lib, LIB_PATH, EXPORTED  # noqa: F401
 from .closed_loop import ClosedLoop  # noqa: F401
+from .autograd import lq_solve, LqSolveFunction  # noqa: F401
 
-__all__ = ["PdIlqr", "PdilqrError", "ClosedLoop", "lib", "LIB_PATH", "EXPORTED"]
+__all__ = ["PdIlqr", "PdilqrError", "ClosedLoop", "lq_solve", "LqSolveFunction", "lib", "LIB_PATH", "EXPORTED"]

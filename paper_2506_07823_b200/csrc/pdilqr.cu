@@ -19,6 +19,7 @@
 #include "srbd_fused.cuh"
 #include "big.cuh"
 #include "big_ric.cuh"
+#include "adjoint.cuh"
 
 using namespace pdilqr;
 
@@ -83,6 +84,7 @@ struct Layout {
     size_t conv, active;                       // pdilqr_solve per-instance state, active counter
     size_t qp[11];  // SRBD internal QP buffers (A, Bm, c, Q, R, S, q, r, Pt, pt, dx0)
     size_t dir[3];  // internal direction (dx, du, dlam)
+    size_t adj[8];  // adjoint solve: linear terms (q, r, c, pt, dx0) and solution (wx, wu, wl)
     size_t total;
 };
 
@@ -214,6 +216,12 @@ Layout make_big_layout(const pdilqr_config *c, int esz) {
     L.pre = take(B * 4);
     L.info_tmp = take(B * 4);
     L.stats = take(B * (3 * (size_t)esz + 8));
+    {  // pdilqr_solve_lq_adjoint: adjoint linear terms and solution, user (unpadded) layouts
+        const size_t nB = c->batch, nN = c->N, nn_ = c->n, mm_ = c->m;
+        const size_t sz[8] = {(nN + 1) * nn_, (nN + 1) * mm_, (nN + 1) * nn_, nn_, nn_, (nN + 2) * nn_, (nN + 1) * mm_,
+                              (nN + 2) * nn_};
+        for (int k = 0; k < 8; ++k) L.adj[k] = take(nB * sz[k] * esz);
+    }
     L.total = off;
     return L;
 }
@@ -258,6 +266,12 @@ Layout make_layout(const pdilqr_config *c, int NX, int NU, int esz, int chunk, i
         L.dir[0] = take(B * (N + 2) * n * esz);
         L.dir[1] = take(B * (N + 1) * m * esz);
         L.dir[2] = take(B * (N + 2) * n * esz);
+    }
+    {  // pdilqr_solve_lq_adjoint: adjoint linear terms and solution, user (unpadded) layouts
+        const size_t nB = c->batch, nN = c->N, nn_ = c->n, mm_ = c->m;
+        const size_t sz[8] = {(nN + 1) * nn_, (nN + 1) * mm_, (nN + 1) * nn_, nn_, nn_, (nN + 2) * nn_, (nN + 1) * mm_,
+                              (nN + 2) * nn_};
+        for (int k = 0; k < 8; ++k) L.adj[k] = take(nB * sz[k] * esz);
     }
     L.total = off;
     return L;
@@ -345,6 +359,9 @@ pdilqr_status run_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArg
                             cudaStream_t st);
 template <typename T>
 pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st);
+template <typename T>
+pdilqr_status run_adjoint(pdilqr_ctx *h, const LqArgs<T> &qp, const LqOut<T> &sol, const T *gdx, const T *gdu,
+                          const T *gdl, const AdjGrad<T> &grad, int32_t *info, cudaStream_t st);
 // k_big_ric cluster-size probe: true if a cluster of cs CTAs with smem bytes can be co-scheduled
 template <typename T>
 bool ric_cluster_fits(int cs, size_t smem);
@@ -702,6 +719,36 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
 }
 
 
+// Adjoint of solve_lq (adjoint.cuh): linear terms from the upstream gradient, the same scans on
+// the handle's matrices, then the outer-product gradients.
+template <typename T>
+pdilqr_status run_adjoint(pdilqr_ctx *h, const LqArgs<T> &qp, const LqOut<T> &sol, const T *gdx, const T *gdu,
+                          const T *gdl, const AdjGrad<T> &grad, int32_t *info, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
+    auto ws = [&](int k) { return reinterpret_cast<T *>(h->ws + h->lay.adj[k]); };
+    AdjRhs<T> rhs{ws(0), ws(1), ws(2), ws(3), ws(4)};
+    const long tr = (long)B * ((long)(N + 2) * n * 2 + (long)(N + 1) * m);
+    {
+        Prof pf(h, "k_adj_rhs", st);
+        k_adj_rhs<T><<<(unsigned)std::min<long>((tr + 255) / 256, 148L * 16), 256, 0, st>>>(B, N, n, m, gdx, gdu, gdl, rhs);
+    }
+    h->launches += 1;
+    LqArgs<T> aq = qp;
+    aq.q = rhs.q; aq.r = rhs.r; aq.c = rhs.c; aq.pt = rhs.pt; aq.dx0 = rhs.dx0;
+    LqOut<T> w{ws(5), ws(6), ws(7), nullptr, nullptr};
+    pdilqr_status s = dispatch_lq<T>(h, aq, w, info, nullptr, st);
+    if (s != PDILQR_OK) return s;
+    const long nn = (long)n * n, nm = (long)n * m, mm = (long)m * m;
+    const long tg = (long)B * ((long)(N + 1) * (2 * nn + 2 * nm + mm + 2 * n + m) + nn + 2 * n);
+    {
+        Prof pf(h, "k_adj_grad", st);
+        AdjIn<T> z{sol.dx, sol.du, sol.dlam, w.dx, w.du, w.dlam};
+        k_adj_grad<T><<<(unsigned)std::min<long>((tg + 255) / 256, 148L * 16), 256, 0, st>>>(B, N, n, m, z, grad);
+    }
+    h->launches += 1;
+    return cuda_check("solve_lq_adjoint launch");
+}
+
 template <typename T>
 void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk2) {
     auto occ = [&](auto kern, size_t smem, int &out) {
@@ -732,7 +779,9 @@ void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk
     template pdilqr_status run_linearize<T>(pdilqr_ctx *, const pdilqr_iterate *, const LqArgs<T> &, int32_t *,     \
                                             cudaStream_t);                                                         \
     template pdilqr_status run_step<T>(pdilqr_ctx *, pdilqr_iterate *, pdilqr_stats *, pdilqr_dir *, cudaStream_t); \
-    template void grid_occupancy<T>(int, int, int &, int &, int &, int &, int &);
+    template void grid_occupancy<T>(int, int, int &, int &, int &, int &, int &);                               \
+    template pdilqr_status run_adjoint<T>(pdilqr_ctx *, const LqArgs<T> &, const LqOut<T> &, const T *, const T *,   \
+                                          const T *, const AdjGrad<T> &, int32_t *, cudaStream_t);
 #if PDILQR_SMALL(0)
 PDILQR_INST_SMALL(float)
 #endif
@@ -1079,6 +1128,31 @@ pdilqr_status pdilqr_solve_lq(pdilqr_handle h, const pdilqr_lq *qp, pdilqr_dir *
                      (const double *)qp->P_term, (const double *)qp->p_term, (const double *)qp->dx0};
     LqOut<double> o{(double *)dir->dx, (double *)dir->du, (double *)dir->dlam, (double *)dir->K, (double *)dir->k};
     return dispatch_lq<double>(h, a, o, info, nullptr, st);
+}
+
+pdilqr_status pdilqr_solve_lq_adjoint(pdilqr_handle h, const pdilqr_lq *qp, const pdilqr_dir *sol,
+                                      const pdilqr_dir *gsol, pdilqr_lq_grad *grad, int32_t *info, void *stream) {
+    if (!h || !qp || !sol || !grad) return fail(PDILQR_ERR_INVALID_ARG, "NULL handle, qp, sol or grad");
+    const void *ptrs[] = {qp->A, qp->Bm, qp->Q, qp->R, qp->S, qp->P_term, sol->dx, sol->du, sol->dlam};
+    for (const void *p : ptrs) {
+        if (!p) return fail(PDILQR_ERR_INVALID_ARG, "NULL matrix in qp or NULL array in sol");
+        if (!aligned16(p)) return fail(PDILQR_ERR_INVALID_ARG, "arrays must be 16-byte aligned");
+    }
+    DeviceGuard g(h->device);
+    h->launches = 0;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto run = [&](auto zero) {
+        using T = decltype(zero);
+        LqArgs<T> a{(const T *)qp->A, (const T *)qp->Bm, nullptr, (const T *)qp->Q, (const T *)qp->R, (const T *)qp->S,
+                    nullptr, nullptr, (const T *)qp->P_term, nullptr, nullptr};
+        LqOut<T> z{(T *)sol->dx, (T *)sol->du, (T *)sol->dlam, nullptr, nullptr};
+        AdjGrad<T> gr{(T *)grad->A, (T *)grad->Bm, (T *)grad->c, (T *)grad->Q, (T *)grad->R, (T *)grad->S,
+                      (T *)grad->q, (T *)grad->r, (T *)grad->P_term, (T *)grad->p_term, (T *)grad->dx0};
+        const T *gx = gsol ? (const T *)gsol->dx : nullptr, *gu = gsol ? (const T *)gsol->du : nullptr,
+                *gl = gsol ? (const T *)gsol->dlam : nullptr;
+        return pdq::run_adjoint<T>(h, a, z, gx, gu, gl, gr, info, st);
+    };
+    return h->cfg.dtype == PDILQR_F32 ? run(0.0f) : run(0.0);
 }
 
 static pdilqr_status check_iter(pdilqr_handle h, const pdilqr_iterate *it) {

@@ -25,7 +25,7 @@ STATUS = {0: "PDILQR_OK", 1: "PDILQR_ERR_INVALID_ARG", 2: "PDILQR_ERR_DIM", 3: "
 EXPORTED = ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
             "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host", "pdilqr_last_launch_count",
             "pdilqr_last_error", "pdilqr_abi_version", "pdilqr_profile", "pdilqr_profile_read",
-            "pdilqr_shift", "pdilqr_srbd_plant", "pdilqr_solve")
+            "pdilqr_shift", "pdilqr_srbd_plant", "pdilqr_solve", "pdilqr_solve_lq_adjoint")
 
 
 class SrbdParams(C.Structure):
@@ -74,6 +74,8 @@ def lib():
         L.pdilqr_create.argtypes = [C.POINTER(Config), C.c_int, vp, C.c_size_t, C.POINTER(vp)]
         L.pdilqr_destroy.argtypes = [vp]
         L.pdilqr_solve_lq.argtypes = [vp, C.POINTER(Lq), C.POINTER(Dir), vp, vp]
+        L.pdilqr_solve_lq_adjoint.argtypes = [vp, C.POINTER(Lq), C.POINTER(Dir), C.POINTER(Dir), C.POINTER(Lq), vp, vp]
+        L.pdilqr_solve_lq_adjoint.restype = st
         L.pdilqr_linearize.argtypes = [vp, C.POINTER(Iterate), C.POINTER(Lq), vp, vp]
         L.pdilqr_step.argtypes = [vp, C.POINTER(Iterate), C.POINTER(Stats), C.POINTER(Dir), vp]
         L.pdilqr_tick_host.argtypes = [vp, C.POINTER(Iterate), vp, vp, vp, vp, vp, vp, vp, vp]
@@ -171,6 +173,27 @@ class PdIlqr:
                               f"on {getattr(t, 'device', None)}")
         return t
 
+    def _check_host(self, t, shape, dtype=None):
+        dtype = dtype or self.dtype
+        if not (isinstance(t, torch.Tensor) and t.device.type == "cpu" and t.dtype == dtype and t.is_contiguous()
+                and tuple(t.shape) == tuple(shape)):
+            raise PdilqrError(f"expected contiguous host {dtype} tensor of shape {tuple(shape)}, got "
+                              f"{getattr(t, 'dtype', type(t))} {tuple(getattr(t, 'shape', ()))} "
+                              f"on {getattr(t, 'device', None)}")
+        if not t.is_pinned():
+            raise PdilqrError("host buffers of tick_host must be pinned (asynchronous copies)")
+        return t
+
+    def _check_dir(self, d: dict, policy_ok: bool = True):
+        B, N, n, m = self.batch, self.N, self.n, self.m
+        self._check_t(d["dx"], (B, N + 2, n)); self._check_t(d["du"], (B, N + 1, m))
+        self._check_t(d["dlam"], (B, N + 2, n))
+        if d.get("K") is not None:
+            self._check_t(d["K"], (B, N + 1, m, n))
+        if d.get("k") is not None:
+            self._check_t(d["k"], (B, N + 1, m))
+        return d
+
     def _stream(self, stream):
         s = torch.cuda.current_stream(self.device) if stream is None else stream
         return C.c_void_p(s.cuda_stream)
@@ -196,14 +219,44 @@ class PdIlqr:
         """pdilqr_solve_lq: returns dict dx, du, dlam (+ K, k) and info (int32 [B])."""
         for k, shp in self.lq_shapes().items():
             self._check_t(qp[k], shp)
-        out = out if out is not None else self.new_direction(policy)
-        info = info if info is not None else torch.empty(self.batch, dtype=torch.int32, device=self.device)
+        out = self._check_dir(out) if out is not None else self.new_direction(policy)
+        info = self._check_t(info, (self.batch,), torch.int32) if info is not None else \
+            torch.empty(self.batch, dtype=torch.int32, device=self.device)
         lq = Lq(**{k: _ptr(qp[k]) for k in self.lq_shapes()})
         d = Dir(dx=_ptr(out["dx"]), du=_ptr(out["du"]), dlam=_ptr(out["dlam"]), K=_ptr(out.get("K")),
                 k=_ptr(out.get("k")))
         _check(lib().pdilqr_solve_lq(self._h, C.byref(lq), C.byref(d), _ptr(info), self._stream(stream)))
         out["info"] = info
         return out
+
+    def solve_lq_adjoint(self, qp: dict, sol: dict, gsol: dict, grad: dict | None = None, info=None, stream=None):
+        """pdilqr_solve_lq_adjoint: gradients of a loss L w.r.t. the Eq. 4 data, given the forward
+        solution sol (dx, du, dlam) of the same qp and gsol = dL/d(dx, du, dlam) (missing keys = 0).
+        Returns dict of gradient tensors (the keys of grad, default all 11) and info."""
+        shapes = self.lq_shapes()
+        for k in ("A", "Bm", "Q", "R", "S", "P_term"):
+            self._check_t(qp[k], shapes[k])
+        self._check_dir(sol)
+        B, N, n, m = self.batch, self.N, self.n, self.m
+        gs = {"dx": (B, N + 2, n), "du": (B, N + 1, m), "dlam": (B, N + 2, n)}
+        for k, shp in gs.items():
+            if gsol.get(k) is not None:
+                self._check_t(gsol[k], shp)
+        if grad is None:
+            grad = {k: torch.empty(shp, dtype=self.dtype, device=self.device) for k, shp in shapes.items()}
+        for k, t in grad.items():
+            if k != "info":
+                self._check_t(t, shapes[k])
+        info = self._check_t(info, (B,), torch.int32) if info is not None else \
+            torch.empty(B, dtype=torch.int32, device=self.device)
+        lq = Lq(**{k: _ptr(qp.get(k)) for k in shapes})
+        d = Dir(dx=_ptr(sol["dx"]), du=_ptr(sol["du"]), dlam=_ptr(sol["dlam"]), K=None, k=None)
+        g = Dir(dx=_ptr(gsol.get("dx")), du=_ptr(gsol.get("du")), dlam=_ptr(gsol.get("dlam")), K=None, k=None)
+        gr = Lq(**{k: _ptr(grad.get(k)) for k in shapes})
+        _check(lib().pdilqr_solve_lq_adjoint(self._h, C.byref(lq), C.byref(d), C.byref(g), C.byref(gr), _ptr(info),
+                                             self._stream(stream)))
+        grad["info"] = info
+        return grad
 
     def _iterate(self, it: dict) -> Iterate:
         B, N = self.batch, self.N
@@ -242,6 +295,7 @@ class PdIlqr:
         st = Stats(**{k: _ptr(stats[k]) for k in ("cost", "theta", "alpha", "accepted", "info")})
         d = None
         if direction is not None:
+            self._check_dir(direction)
             d = Dir(dx=_ptr(direction["dx"]), du=_ptr(direction["du"]), dlam=_ptr(direction["dlam"]),
                     K=_ptr(direction.get("K")), k=_ptr(direction.get("k")))
         _check(lib().pdilqr_step(self._h, C.byref(itc), C.byref(st), C.byref(d) if d is not None else None,
@@ -251,6 +305,12 @@ class PdIlqr:
     def tick_host(self, it: dict, x0_host, u0_host, stats_host: dict, stream=None):
         """pdilqr_tick_host: host x0 in, host u0 + stats out (pinned CPU tensors)."""
         itc = self._iterate(it)
+        B = self.batch
+        self._check_host(x0_host, (B, 12)); self._check_host(u0_host, (B, 12))
+        for k in ("cost", "theta", "alpha"):
+            self._check_host(stats_host[k], (B,))
+        for k in ("accepted", "info"):
+            self._check_host(stats_host[k], (B,), torch.int32)
         _check(lib().pdilqr_tick_host(self._h, C.byref(itc), _ptr(x0_host), _ptr(u0_host),
                                       _ptr(stats_host["cost"]), _ptr(stats_host["theta"]),
                                       _ptr(stats_host["alpha"]), _ptr(stats_host["accepted"]),

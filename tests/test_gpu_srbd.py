@@ -5,6 +5,7 @@ import numpy as np
 import pytest
 import torch
 
+from tests import kkt_dense
 from tests.gpu_util import rel, rel_per_instance, rounded, to_device, to_np
 from workloads import synth
 
@@ -76,18 +77,24 @@ def alpha_ambiguous(O, prob, b, alpha_gpu):
 
 
 def step_parity(P, O, B, N, dtype, seed, perturb=0.0, leaf_chunk=0, steps=1, sample=None, dir_steps=(0,),
-                tol=None):
-    """Per step: the search direction (for the steps in dir_steps) and the updated iterate
-    x, u, lam must match the oracle's step from the same iterate (rel <= 1e-4 f32 / 1e-9 f64,
-    relative to the reference's max magnitude), and alpha must agree unless the oracle's decision
-    is ambiguous.  Later steps only check the iterate: near convergence the direction is at the
-    fp32 noise floor of the residuals."""
+                tol=None, eta_tol=None):
+    """Per step and sampled instance:
+    - the KKT backward error eta of the GPU search direction on the oracle's QP at the same iterate
+      (SURVEY §8(c-5)) is <= 1e-5 (f32) / 1e-12 (f64) at every step;
+    - for the steps in dir_steps the direction (dx, du, dlam) and the iterate change
+      (x, u, lam)_new - (x, u, lam)_old match the oracle's (rel <= 1e-4 f32 / 1e-9 f64, relative to
+      the reference's max magnitude); at the other steps the iterate matches relative to max|x|
+      (near convergence the fp32 direction sits at the noise floor of the residuals, DESIGN.md
+      "Precision", while eta stays bounded);
+    - alpha agrees unless the oracle's decision is ambiguous (§8(c-5))."""
     prob = problem(B, N, seed, dtype, perturb)
     h = handle(P, prob, dtype, B, N, leaf_chunk)
     dev = to_device({k: prob[k] for k in ITER_KEYS}, dtype)
     dirn = h.new_direction()
     tol = tol or (1e-4 if dtype == torch.float32 else 1e-9)
+    eta_tol = eta_tol or (1e-5 if dtype == torch.float32 else 1e-12)
     idx = list(range(B)) if sample is None else list(sample)
+    worst = {"eta": 0.0, "dir": 0.0, "delta": 0.0}
     for s in range(steps):
         rp = dict(prob)
         rp.update({k: to_np(dev[k]) for k in ("x", "u", "lam")})
@@ -95,19 +102,31 @@ def step_parity(P, O, B, N, dtype, seed, perturb=0.0, leaf_chunk=0, steps=1, sam
         torch.cuda.synchronize()
         a_gpu, info = to_np(st["alpha"]), to_np(st["info"])
         assert (info[idx] == 0).all()
+        lin = O.srbd_linearize(rp)
         for b in idx:
             x, u, lam, st_r, dx, du, dl = O.srbd_step_single(rp, b)
+            eta = kkt_dense.backward_error_blockwise(lin, b, to_np(dirn["dx"][b]), to_np(dirn["du"][b]),
+                                                     to_np(dirn["dlam"][b]))
+            worst["eta"] = max(worst["eta"], eta)
+            assert eta <= eta_tol, (s, b, eta)
             if s in dir_steps:
                 for k, ref in (("dx", dx), ("du", du), ("dlam", dl)):
-                    assert rel(to_np(dirn[k][b]), ref) <= tol, (s, k, b, rel(to_np(dirn[k][b]), ref))
+                    e = rel(to_np(dirn[k][b]), ref)
+                    worst["dir"] = max(worst["dir"], e)
+                    assert e <= tol, (s, k, b, e)
             if a_gpu[b] != st_r[2]:
                 assert alpha_ambiguous(O, rp, b, a_gpu[b]), (s, b, a_gpu[b], st_r[2])
                 continue
             for k, ref in (("x", x), ("u", u), ("lam", lam)):
-                assert rel(to_np(dev[k][b]), ref) <= tol, (s, k, b, rel(to_np(dev[k][b]), ref))
+                if s in dir_steps and st_r[3]:
+                    e = rel(to_np(dev[k][b]) - rp[k][b], ref - rp[k][b])
+                    worst["delta"] = max(worst["delta"], e)
+                    assert e <= tol, (s, k, b, "step", e)
+                else:
+                    assert rel(to_np(dev[k][b]), ref) <= tol, (s, k, b, rel(to_np(dev[k][b]), ref))
             assert to_np(st["accepted"])[b] == st_r[3]
             assert abs(to_np(st["cost"])[b] - st_r[0]) <= 10 * tol * max(1.0, abs(st_r[0]))
-    return prob
+    return prob, worst
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
@@ -119,12 +138,12 @@ def test_step_parity_config2(P, O, dtype, chunk):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 def test_step_parity_perturbed_batch(P, O, dtype):
-    """Stress: random multipliers and controls (not the paper's workload).  f64 checks the
-    direction to 1e-9; f32 checks the iterate to 3e-4: with random lam the combine systems reach
-    cond(I + C~P~) ~ 1e3 and fp32 costates lose ~1e-4."""
+    """Stress: random multipliers and controls (not the paper's workload), latency regime (B = 64,
+    tree scans with the M-solve combine).  The first-step direction and iterate change are held to
+    the north-star 1e-4 (f32; measured worst 4e-5 with cond(KKT) ~ 6e8) and 1e-9 (f64), eta to 1e-5
+    at every step."""
     step_parity(P, O, 64, 50, dtype, seed=32, perturb=1.0, steps=2,
-                dir_steps=(0, 1) if dtype == torch.float64 else (),
-                tol=3e-4 if dtype == torch.float32 else None)
+                dir_steps=(0, 1) if dtype == torch.float64 else (0,))
 
 
 @pytest.mark.parametrize("N", [0, 1, 7, 100])

@@ -227,6 +227,14 @@ pdilqr_status pdilqr_profile(pdilqr_handle h, int32_t enable);
 int32_t pdilqr_profile_read(pdilqr_handle h, int32_t max, const char **names, int32_t *launches,
                             double *total_ms);
 
+/* Diagnostic (test infrastructure for the tensor-core products of the large-n fold):
+ * C[M][N] = (Cin ? Cin : 0) + op(A)[M x K] op(B)[K x N] in FP32 through the tcgen05 3xTF32 path
+ * (one CTA; M, N <= 256), row-major device arrays: op(A) = A (M x K, ld lda) or A^T (A stored K x M)
+ * if trans_a; same for B (K x N or N x K, ld ldb); C and Cin are M x N with ld N.  Asynchronous on
+ * stream.  Returns PDILQR_ERR_DIM / INVALID_ARG / CUDA. */
+pdilqr_status pdilqr_debug_tc_gemm(int32_t M, int32_t N, int32_t K, int32_t trans_a, int32_t trans_b, const float *A,
+                                   int32_t lda, const float *B, int32_t ldb, const float *Cin, float *C, void *stream);
+
 /* Number of kernels the last solve_lq / step / linearize call launched (for accounting). */
 int32_t pdilqr_last_launch_count(pdilqr_handle h);
 

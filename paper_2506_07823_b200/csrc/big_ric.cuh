@@ -31,6 +31,7 @@
 #include <cooperative_groups.h>
 
 #include "big.cuh"
+#include "tc.cuh"
 
 namespace pdilqr {
 
@@ -133,6 +134,19 @@ __device__ void ric_gemm(int Mr, int Nc, int K, T alpha, const T *A, int lda, co
                 if (c < Nc) C[(size_t)r * ldc + c] = fma(alpha, acc[q][w], cin[w]);
             }
         }
+    }
+}
+
+// The products of k_big_ric: SIMT FP32 tiles (ric_gemm) or, with UT (float only), tcgen05 tensor
+// cores in 3xTF32 (tc_gemm, tc.cuh).  Same contract.
+template <typename T, int TR, int TC_, bool TA, bool TB, int TM, bool UT>
+__device__ __forceinline__ void big_gemm(int Mr, int Nc, int K, const T *A, int lda, const T *Bm, int ldb, const T *Cin,
+                                         int ldci, T *C, int ldc, int part, int nparts, RicTiles<T, TM> &tiles,
+                                         TcSmem *tcs, TcPhase &ph) {
+    if constexpr (UT) {
+        tc_gemm<TA, TB>(Mr, Nc, K, 1.0f, A, lda, Bm, ldb, Cin, ldci, C, ldc, part, nparts, *tcs, ph);
+    } else {
+        ric_gemm<T, TR, TC_, TA, TB, TM>(Mr, Nc, K, T(1), A, lda, Bm, ldb, Cin, ldci, C, ldc, part, nparts, tiles);
     }
 }
 
@@ -364,12 +378,18 @@ __host__ __device__ inline size_t ric_smem_bytes(int m, int esz) {
     return ((size_t)m * ric_ldl(m) + (size_t)ld_of(m)) * esz;
 }
 
+// ... plus the tensor-core panel buffers (128-byte aligned) of the UT variant
+__host__ __device__ inline size_t ric_tc_offset(int m, int esz) { return (ric_smem_bytes(m, esz) + 127) / 128 * 128; }
+__host__ __device__ inline size_t ric_smem_bytes_tc(int m) { return ric_tc_offset(m, 4) + sizeof(TcSmem); }
+constexpr uint32_t RIC_TMEM_COLS = 128;
+
 // Fused reverse scan + policy (phases 1-7 above), one cluster of CS CTAs per instance.
 // Writes P_i, p_i (ws.Pp), K_i, k_i (ws.Kk, out.K, out.k), Abar_i, bbar_i (ws.tel).
-template <typename T, int TN, int TU>
+template <typename T, int TN, int TU, bool UT = false>
 __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B, int N, BigDims<T> d, BigWork<T> ws,
                                                          LqOut<T> out, int CS) {
-    constexpr int TM = TN > TU ? TN : TU;
+    static_assert(!UT || sizeof(T) == 4, "tensor-core products are FP32 (3xTF32) only");
+    constexpr int TM = UT ? 1 : (TN > TU ? TN : TU);
     __shared__ RicTiles<T, TM> tiles;
     extern __shared__ __align__(16) unsigned char dyn[];
     const int n = d.n, m = d.m, LD = d.LD, LDU = d.LDU;
@@ -382,6 +402,12 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
     T *PB = ws.scratch + (size_t)b * ws.slot, *W = PB + (size_t)n * ldpb, *V = W + (size_t)m * ldw,
       *g = V + (size_t)n * LD, *w = g + LD;
     T *Pp = ws.Pp + (size_t)b * (N + 2) * d.psize();
+    TcSmem *tcs = nullptr;
+    TcPhase ph;
+    if constexpr (UT) {
+        tcs = reinterpret_cast<TcSmem *>(dyn + ric_tc_offset(m, sizeof(T)));
+        tc_alloc(*tcs, RIC_TMEM_COLS);
+    }
     {   // s_{N+1} = (P_{N+1}, p_{N+1})
         T *Pt = Pp + (size_t)(N + 1) * d.psize();
         for (int t = rank * RIC_THREADS + threadIdx.x; t < n * n; t += CS * RIC_THREADS)
@@ -400,12 +426,12 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
         T *Kw = ws.Kk + st * d.ksize(), *kw = Kw + (size_t)m * LD;
         T *Ab = ws.tel + st * d.psize(), *bb = Ab + (size_t)n * LD;
         // phase 1: PB = P' B ; g = p' + P' c
-        ric_gemm<T, TN, TU, false, false>(n, m, n, T(1), Pn, LD, Bm, m, nullptr, 0, PB, ldpb, rank, CS, tiles);
+        big_gemm<T, TN, TU, false, false, TM, UT>(n, m, n, Pn, LD, Bm, m, nullptr, 0, PB, ldpb, rank, CS, tiles, tcs, ph);
         ric_gemv<T, false>(n, n, Pn, LD, c, pn, 1, g, 1, gw, nwc);
         ric_sync(CS);
         // phase 2: W = [R + B^T PB | S + PB^T A | r + B^T g]
-        ric_gemm<T, TU, TU, true, false>(m, m, n, T(1), Bm, m, PB, ldpb, R, m, W, ldw, rank, CS, tiles);
-        ric_gemm<T, TU, TN, true, false>(m, n, n, T(1), PB, ldpb, A, n, S, n, W + m, ldw, rank, CS, tiles);
+        big_gemm<T, TU, TU, true, false, TM, UT>(m, m, n, Bm, m, PB, ldpb, R, m, W, ldw, rank, CS, tiles, tcs, ph);
+        big_gemm<T, TU, TN, true, false, TM, UT>(m, n, n, PB, ldpb, A, n, S, n, W + m, ldw, rank, CS, tiles, tcs, ph);
         ric_gemv<T, true>(m, n, Bm, m, g, r, 1, W + m + n, ldw, gw, nwc);  // column m+n of W
         ric_sync(CS);
         // phase 3: Cholesky of G (every CTA, own shared memory), [K | k] = -G^-1 [H | h]
@@ -443,16 +469,16 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
         }
         ric_sync(CS);
         // phase 4: Abar = A + B K ; bbar = c + B k
-        ric_gemm<T, TN, TN, false, false>(n, n, m, T(1), Bm, m, Kw, LD, A, n, Ab, LD, rank, CS, tiles);
+        big_gemm<T, TN, TN, false, false, TM, UT>(n, n, m, Bm, m, Kw, LD, A, n, Ab, LD, rank, CS, tiles, tcs, ph);
         ric_gemv<T, false>(n, m, Bm, m, kw, c, 1, bb, 1, gw, nwc);
         ric_sync(CS);
         // phase 5: V = P' Abar ; w = p' + P' bbar
-        ric_gemm<T, TN, TN, false, false>(n, n, n, T(1), Pn, LD, Ab, LD, nullptr, 0, V, LD, rank, CS, tiles);
+        big_gemm<T, TN, TN, false, false, TM, UT>(n, n, n, Pn, LD, Ab, LD, nullptr, 0, V, LD, rank, CS, tiles, tcs, ph);
         ric_gemv<T, false>(n, n, Pn, LD, bb, pn, 1, w, 1, gw, nwc);
         ric_sync(CS);
         // phase 6: P_i = Q + A^T V (+ S^T K) ; p_i = q + A^T w (+ S^T k)   (same tiles / rows: no barrier)
-        ric_gemm<T, TN, TN, true, false>(n, n, n, T(1), A, n, V, LD, qp.Q + st * n * n, n, Pc, LD, rank, CS, tiles);
-        if (S) ric_gemm<T, TN, TN, true, false>(n, n, m, T(1), S, n, Kw, LD, Pc, LD, Pc, LD, rank, CS, tiles);
+        big_gemm<T, TN, TN, true, false, TM, UT>(n, n, n, A, n, V, LD, qp.Q + st * n * n, n, Pc, LD, rank, CS, tiles, tcs, ph);
+        if (S) big_gemm<T, TN, TN, true, false, TM, UT>(n, n, m, S, n, Kw, LD, Pc, LD, Pc, LD, rank, CS, tiles, tcs, ph);
         ric_gemv<T, true>(n, n, A, n, w, q, 1, pc, 1, gw, nwc);
         if (S) ric_gemv<T, true>(n, m, S, n, kw, pc, 1, pc, 1, gw, nwc);
         ric_sync(CS);
@@ -491,6 +517,7 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
         ric_sync(CS);
     }
     (void)LDU;
+    if constexpr (UT) tc_free(*tcs, RIC_TMEM_COLS);
     if (fail != INT_MAX && rank == 0 && threadIdx.x == 0) atomicMin(ws.fail + b, (2 << 24) | fail);
 }
 

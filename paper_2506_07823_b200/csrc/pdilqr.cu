@@ -11,6 +11,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "pdilqr.h"
@@ -111,6 +112,7 @@ struct pdilqr_ctx {
     int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
+    bool big_tc = true;            // large path, f32: tcgen05 3xTF32 products in k_big_ric (PDILQR_BIG_TC=0: SIMT)
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
     int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
     int coop_ks = 0, coop_fks = 0; // ... of the depth-optimal (Kogge-Stone) reverse / forward scans
@@ -364,7 +366,9 @@ pdilqr_status run_adjoint(pdilqr_ctx *h, const LqArgs<T> &qp, const LqOut<T> &so
                           const T *gdl, const AdjGrad<T> &grad, int32_t *info, cudaStream_t st);
 // k_big_ric cluster-size probe: true if a cluster of cs CTAs with smem bytes can be co-scheduled
 template <typename T>
-bool ric_cluster_fits(int cs, size_t smem);
+bool ric_cluster_fits(int cs, size_t smem, bool ut);
+cudaError_t debug_tc_gemm(int M, int N, int K, int ta, int tb, const float *A, int lda, const float *Bm, int ldb,
+                          const float *Cin, float *C, cudaStream_t st);
 // co-resident CTAs of the cooperative latency-regime scan kernels (v: Variant)
 template <typename T>
 void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk2);
@@ -793,6 +797,22 @@ PDILQR_INST_SMALL(double)
 
 #if PDILQR_BIG(0) || PDILQR_BIG(1)
 namespace pdq {
+// k_big_ric variant: SIMT tiles (5x2 for config-5-like shapes, else 3x3) or tcgen05 (float only)
+template <typename T>
+using RicKernT = void (*)(LqArgs<T>, int, int, BigDims<T>, BigWork<T>, LqOut<T>, int);
+template <typename T>
+RicKernT<T> ric_kernel(bool t52, bool ut) {
+    if constexpr (std::is_same<T, float>::value) {
+        if (ut) return k_big_ric<float, 1, 1, true>;
+    }
+    (void)ut;
+    return t52 ? k_big_ric<T, 5, 2> : k_big_ric<T, 3, 3>;
+}
+template <typename T>
+bool ric_use_tc(const pdilqr_ctx *h, int m) {
+    return std::is_same<T, float>::value && h->big_tc && ric_smem_bytes_tc(m) <= 227 * 1024;
+}
+
 template <typename T>
 pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *info, cudaStream_t st) {
     const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
@@ -810,6 +830,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
     const size_t ric_smem = ric_smem_bytes(m, (int)sizeof(T));
     if (ric_smem <= kRicSmemMax && !h->big_legacy) {  // fused Riccati-form fold (big_ric.cuh)
         const bool t52 = n <= 80 && m <= 32 && h->ric_cs == 1;  // config-5-like: 80-row n tiles, 32-wide m tiles
+        const bool ut = ric_use_tc<T>(h, m);                      // tcgen05 3xTF32 products (tc.cuh)
         {
             const int tpb = std::min(256, (m + 31) / 32 * 32);  // one thread per row of R
             const int g = (int)std::min<long>((long)148 * (2048 / tpb), (long)B * (N + 1));
@@ -818,13 +839,14 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
             k_big_rchk<T><<<g, tpb, ric_smem, st>>>(qp.R, B, N, m, ws.fail);
         }
         {
-            auto kern = t52 ? k_big_ric<T, 5, 2> : k_big_ric<T, 3, 3>;
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ric_smem);
+            auto kern = ric_kernel<T>(t52, ut);
+            const size_t smem = ut ? ric_smem_bytes_tc(m) : ric_smem;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (h->ric_cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
             cudaLaunchConfig_t lc{};
             lc.gridDim = dim3((unsigned)(B * h->ric_cs));
             lc.blockDim = dim3(RIC_THREADS);
-            lc.dynamicSmemBytes = ric_smem;
+            lc.dynamicSmemBytes = smem;
             lc.stream = st;
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
@@ -833,7 +855,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            Prof pf(h, "k_big_ric", st);
+            Prof pf(h, ut ? "k_big_ric_tc" : "k_big_ric", st);
             cudaError_t e = cudaLaunchKernelEx(&lc, kern, qp, B, N, d, ws, out, h->ric_cs);
             if (e != cudaSuccess) return fail(PDILQR_ERR_CUDA, "k_big_ric launch (cluster %d): %s", h->ric_cs, cudaGetErrorString(e));
         }
@@ -899,8 +921,8 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
 }
 
 template <typename T>
-bool ric_cluster_fits(int cs, size_t smem) {
-    const void *kern = (const void *)k_big_ric<T, 3, 3>;
+bool ric_cluster_fits(int cs, size_t smem, bool ut) {
+    const void *kern = (const void *)ric_kernel<T>(false, ut);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t lc{};
@@ -920,12 +942,25 @@ bool ric_cluster_fits(int cs, size_t smem) {
     return false;
 }
 #if PDILQR_BIG(0)
+cudaError_t debug_tc_gemm(int M, int N, int K, int ta, int tb, const float *A, int lda, const float *Bm, int ldb,
+                          const float *Cin, float *C, cudaStream_t st) {
+    const size_t smem = sizeof(TcSmem);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<1, 256, smem, st>>>(M, N, K, A, lda, Bm, ldb, Cin, C);
+    };
+    if (ta && tb) go(k_tc_gemm_test<true, true>);
+    else if (ta) go(k_tc_gemm_test<true, false>);
+    else if (tb) go(k_tc_gemm_test<false, true>);
+    else go(k_tc_gemm_test<false, false>);
+    return cudaGetLastError();
+}
 template pdilqr_status run_big<float>(pdilqr_ctx *, const LqArgs<float> &, LqOut<float>, int32_t *, cudaStream_t);
-template bool ric_cluster_fits<float>(int, size_t);
+template bool ric_cluster_fits<float>(int, size_t, bool);
 #endif
 #if PDILQR_BIG(1)
 template pdilqr_status run_big<double>(pdilqr_ctx *, const LqArgs<double> &, LqOut<double>, int32_t *, cudaStream_t);
-template bool ric_cluster_fits<double>(int, size_t);
+template bool ric_cluster_fits<double>(int, size_t, bool);
 #endif
 }  // namespace pdq
 #endif
@@ -1030,9 +1065,11 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         int cs = 1;
         while (cs < 16 && (long)cfg->batch * cs * 2 <= sms) cs *= 2;
         if (const char *e = std::getenv("PDILQR_BIG_CS")) cs = std::max(1, std::min(16, std::atoi(e)));
-        const size_t smem = ric_smem_bytes(cfg->m, esz);
-        while (cs > 1 && smem <= kRicSmemMax) {  // the device must co-schedule a whole cluster
-            if (esz == 4 ? pdq::ric_cluster_fits<float>(cs, smem) : pdq::ric_cluster_fits<double>(cs, smem)) break;
+        if (const char *e = std::getenv("PDILQR_BIG_TC")) h->big_tc = std::atoi(e) != 0;
+        const bool ut = esz == 4 && h->big_tc && ric_smem_bytes_tc(cfg->m) <= 227 * 1024;
+        const size_t smem = ut ? ric_smem_bytes_tc(cfg->m) : ric_smem_bytes(cfg->m, esz);
+        while (cs > 1 && ric_smem_bytes(cfg->m, esz) <= kRicSmemMax) {  // the device must co-schedule a whole cluster
+            if (esz == 4 ? pdq::ric_cluster_fits<float>(cs, smem, ut) : pdq::ric_cluster_fits<double>(cs, smem, false)) break;
             cs /= 2;
         }
         h->ric_cs = cs;
@@ -1153,6 +1190,14 @@ pdilqr_status pdilqr_solve_lq_adjoint(pdilqr_handle h, const pdilqr_lq *qp, cons
         return pdq::run_adjoint<T>(h, a, z, gx, gu, gl, gr, info, st);
     };
     return h->cfg.dtype == PDILQR_F32 ? run(0.0f) : run(0.0);
+}
+
+pdilqr_status pdilqr_debug_tc_gemm(int32_t M, int32_t N, int32_t K, int32_t trans_a, int32_t trans_b, const float *A,
+                                   int32_t lda, const float *Bm, int32_t ldb, const float *Cin, float *C, void *stream) {
+    if (M < 1 || N < 1 || K < 1 || M > 256 || N > 256) return fail(PDILQR_ERR_DIM, "debug_tc_gemm: 1 <= M, N <= 256, K >= 1");
+    if (!A || !Bm || !C) return fail(PDILQR_ERR_INVALID_ARG, "debug_tc_gemm: NULL array");
+    cudaError_t e = pdq::debug_tc_gemm(M, N, K, trans_a, trans_b, A, lda, Bm, ldb, Cin, C, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? PDILQR_OK : fail(PDILQR_ERR_CUDA, "debug_tc_gemm: %s", cudaGetErrorString(e));
 }
 
 static pdilqr_status check_iter(pdilqr_handle h, const pdilqr_iterate *it) {

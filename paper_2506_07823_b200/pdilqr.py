@@ -25,7 +25,7 @@ STATUS = {0: "PDILQR_OK", 1: "PDILQR_ERR_INVALID_ARG", 2: "PDILQR_ERR_DIM", 3: "
 EXPORTED = ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
             "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host", "pdilqr_last_launch_count",
             "pdilqr_last_error", "pdilqr_abi_version", "pdilqr_profile", "pdilqr_profile_read",
-            "pdilqr_shift", "pdilqr_srbd_plant", "pdilqr_solve", "pdilqr_solve_lq_adjoint")
+            "pdilqr_shift", "pdilqr_srbd_plant", "pdilqr_solve", "pdilqr_solve_lq_adjoint", "pdilqr_debug_tc_gemm")
 
 
 class SrbdParams(C.Structure):
@@ -76,6 +76,8 @@ def lib():
         L.pdilqr_solve_lq.argtypes = [vp, C.POINTER(Lq), C.POINTER(Dir), vp, vp]
         L.pdilqr_solve_lq_adjoint.argtypes = [vp, C.POINTER(Lq), C.POINTER(Dir), C.POINTER(Dir), C.POINTER(Lq), vp, vp]
         L.pdilqr_solve_lq_adjoint.restype = st
+        L.pdilqr_debug_tc_gemm.argtypes = [i32, i32, i32, i32, i32, vp, i32, vp, i32, vp, vp, vp]
+        L.pdilqr_debug_tc_gemm.restype = st
         L.pdilqr_linearize.argtypes = [vp, C.POINTER(Iterate), C.POINTER(Lq), vp, vp]
         L.pdilqr_step.argtypes = [vp, C.POINTER(Iterate), C.POINTER(Stats), C.POINTER(Dir), vp]
         L.pdilqr_tick_host.argtypes = [vp, C.POINTER(Iterate), vp, vp, vp, vp, vp, vp, vp, vp]
@@ -103,6 +105,26 @@ def lib():
 
 class PdilqrError(RuntimeError):
     pass
+
+
+def debug_tc_gemm(A, B, Cin=None, trans_a=False, trans_b=False, stream=None):
+    """pdilqr_debug_tc_gemm: C = Cin + op(A) op(B) through the tcgen05 3xTF32 product of the large-n
+    fold (one CTA; diagnostic).  float32 CUDA tensors, row-major."""
+    M = A.shape[1] if trans_a else A.shape[0]
+    K = A.shape[0] if trans_a else A.shape[1]
+    N = B.shape[0] if trans_b else B.shape[1]
+    for t in (A, B) + ((Cin,) if Cin is not None else ()):
+        if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+            raise PdilqrError("debug_tc_gemm: contiguous float32 CUDA tensors expected")
+    C = torch.empty(M, N, dtype=torch.float32, device=A.device)
+    s = torch.cuda.current_stream(A.device) if stream is None else stream
+    _check(lib().pdilqr_debug_tc_gemm(M, N, K, int(trans_a), int(trans_b), _ptr(A), A.shape[1], _ptr(B), B.shape[1],
+                                      _ptr(Cin), _ptr(C), C_void(s.cuda_stream)))
+    return C
+
+
+def C_void(x):
+    return C.c_void_p(x)
 
 
 def _check(status: int):

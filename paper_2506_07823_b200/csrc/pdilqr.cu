@@ -112,7 +112,8 @@ struct pdilqr_ctx {
     int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
-    bool big_tc = true;            // large path, f32: tcgen05 3xTF32 products in k_big_ric (PDILQR_BIG_TC=0: SIMT)
+    bool big_tc = false;           // large path, f32: tcgen05 3xTF32 products in k_big_ric (PDILQR_BIG_TC=1);
+                                   // off by default: measured slower than the SIMT tiles (K7)
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
     int coop_bwd = 0, coop_fwd = 0;  // max co-resident CTAs of the grid scan kernels
     int coop_ks = 0, coop_fks = 0; // ... of the depth-optimal (Kogge-Stone) reverse / forward scans

@@ -137,31 +137,60 @@ __device__ __forceinline__ int panel_off(int r, int k) {
     return (r >> 3) * (TC_KC / 4 * 128) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
 }
 
-__device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
-    hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-    lo = x - hi;
+// Round to the nearest TF32 value (10 explicit mantissa bits) in an FP32 container.
+__device__ __forceinline__ float round_tf32(float x) {
+    return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
-// Stage one panel: rows [0, R) (R <= 128, zero beyond nr valid rows) x k in [k0, k0 + KC) (zero
-// beyond K) of op(X): element (row, k) = TX ? X[k * ld + row] : X[row * ld + k]; thread-to-element
-// mapping t -> (row % 8, k % 4) conflict-free in shared memory.
+// x = hi + lo with hi = rn_tf32(x) (|x - hi| <= 2^-11 |x|) and lo = rn_tf32(x - hi): both exactly
+// representable in TF32, so the tensor core's TF32 read of them is exact and x - hi - lo = O(2^-22 |x|).
+__device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
+    hi = round_tf32(x);
+    lo = round_tf32(x - hi);
+}
+
+// Panel staging in two halves so that global loads are batched ahead of the shared-memory stores
+// (and of the MMAs of the previous panel): panel_load fetches this thread's elements of one
+// (R <= 128) x KC panel of op(X) into registers (zero outside [0, nr) x [k0, K)), panel_store splits
+// them into hi / lo and writes them in the canonical layout.  Element e = tid + 256 j of the panel,
+// mapping t -> (row % 8, k % 4) conflict-free in shared memory; op(X)(row, k) = TX ? X[k ld + row]
+// : X[row ld + k].
+constexpr int TC_PER_THREAD = TC_PANEL / 256;  // elements of a 128 x KC panel per thread (blockDim 256)
+
+__device__ __forceinline__ void panel_coords(int e, int &r, int &k) {
+    const int t = e & 31, g = e >> 5;
+    const int rg = g / (TC_KC / 4), kc = g % (TC_KC / 4);
+    r = rg * 8 + (t & 7);
+    k = kc * 4 + ((t >> 3) & 3);
+}
+
 template <bool TX>
-__device__ __forceinline__ void stage_panel(const float *X, int ld, int row0, int nr, int k0, int K, int R, float *hi,
-                                            float *lo) {
-    const int nel = R * TC_KC;
-    for (int e = threadIdx.x; e < nel; e += blockDim.x) {
-        const int t = e & 31, g = e >> 5;
-        const int rl = t & 7, kl = (t >> 3) & 3;
-        // g enumerates (row group, k chunk): row group = g / (KC/4), k chunk = g % (KC/4)
-        const int rg = g / (TC_KC / 4), kc = g % (TC_KC / 4);
-        const int r = rg * 8 + rl, k = kc * 4 + kl;
-        float x = 0.f;
-        if (r < nr && k0 + k < K) x = __ldcg(TX ? X + (size_t)(k0 + k) * ld + row0 + r : X + (size_t)(row0 + r) * ld + k0 + k);
-        float h, l;
-        split_tf32(x, h, l);
-        const int off = panel_off(r, k) >> 2;
-        hi[off] = h;
-        lo[off] = l;
+__device__ __forceinline__ void panel_load(const float *X, int ld, int row0, int nr, int k0, int K, int R,
+                                           float (&v)[TC_PER_THREAD]) {
+#pragma unroll
+    for (int j = 0; j < TC_PER_THREAD; ++j) {
+        const int e = threadIdx.x + 256 * j;
+        int r, k;
+        panel_coords(e, r, k);
+        v[j] = (r < R && r < nr && k0 + k < K)
+                   ? __ldcg(TX ? X + (size_t)(k0 + k) * ld + row0 + r : X + (size_t)(row0 + r) * ld + k0 + k)
+                   : 0.f;
+    }
+}
+
+__device__ __forceinline__ void panel_store(int R, const float (&v)[TC_PER_THREAD], float *hi, float *lo) {
+#pragma unroll
+    for (int j = 0; j < TC_PER_THREAD; ++j) {
+        const int e = threadIdx.x + 256 * j;
+        int r, k;
+        panel_coords(e, r, k);
+        if (r < R) {
+            float h, l;
+            split_tf32(v[j], h, l);
+            const int off = panel_off(r, k) >> 2;
+            hi[off] = h;
+            lo[off] = l;
+        }
     }
 }
 
@@ -173,25 +202,35 @@ template <bool TA, bool TB>
 __device__ void tc_gemm(int Mr, int Nc, int K, float alpha, const float *A, int lda, const float *Bm, int ldb,
                         const float *Cin, int ldci, float *C, int ldc, int part, int nparts, TcSmem &sm,
                         TcPhase &ph) {
-    const int NT = min(TC_NMAX, (Nc + 15) & ~15);
-    const int tmn = (Mr + TC_M - 1) / TC_M, tnn = (Nc + NT - 1) / NT;
+    // N tile: up to 128 columns, narrower (>= 16) when a cluster would otherwise leave CTAs idle
+    const int tmn = (Mr + TC_M - 1) / TC_M;
+    const int want_tn = max(1, (nparts + tmn - 1) / tmn);
+    const int NT = min(TC_NMAX, max(16, ((Nc + want_tn - 1) / want_tn + 15) & ~15));
+    const int tnn = (Nc + NT - 1) / NT;
     const uint32_t idesc = umma_idesc_tf32(TC_M, NT);
     const int nk = (K + TC_KC - 1) / TC_KC;
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     for (int t = part; t < tmn * tnn; t += nparts) {
         const int tm = (t / tnn) * TC_M, tn = (t % tnn) * NT;
         const int nr_a = min(TC_M, Mr - tm), nr_b = min(NT, Nc - tn);
+        float va[TC_PER_THREAD], vb[TC_PER_THREAD];
+        panel_load<TA>(A, lda, tm, nr_a, 0, K, TC_M, va);
+        panel_load<!TB>(Bm, ldb, tn, nr_b, 0, K, NT, vb);
         for (int kb = 0; kb < nk; ++kb) {
             const int buf = kb & 1;
             if (kb >= 2) {  // the MMAs that read this buffer two panels ago must be done
                 mbar_wait(&sm.mbar[buf], (ph.bits >> buf) & 1u);
                 ph.bits ^= 1u << buf;
             }
-            stage_panel<TA>(A, lda, tm, nr_a, kb * TC_KC, K, TC_M, sm.a_hi[buf], sm.a_lo[buf]);
-            stage_panel<!TB>(Bm, ldb, tn, nr_b, kb * TC_KC, K, NT, sm.b_hi[buf], sm.b_lo[buf]);
+            panel_store(TC_M, va, sm.a_hi[buf], sm.a_lo[buf]);
+            panel_store(NT, vb, sm.b_hi[buf], sm.b_lo[buf]);
             fence_async_smem();
             tc_fence_before();
             __syncthreads();
+            if (kb + 1 < nk) {  // next panel's loads in flight while the tensor core works
+                panel_load<TA>(A, lda, tm, nr_a, (kb + 1) * TC_KC, K, TC_M, va);
+                panel_load<!TB>(Bm, ldb, tn, nr_b, (kb + 1) * TC_KC, K, NT, vb);
+            }
             if (threadIdx.x == 0) {
                 tc_fence_after();
                 const uint32_t a_hi = smem_u32(sm.a_hi[buf]), a_lo = smem_u32(sm.a_lo[buf]);
@@ -228,13 +267,16 @@ __device__ void tc_gemm(int Mr, int Nc, int K, float alpha, const float *A, int 
             float v[16];
             tmem_ld16(sm.tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0, v);
             if (row < Mr) {
+                float cin[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {  // all Cin loads before the stores (Cin may alias C)
+                    const int col = tn + c0 + j;
+                    cin[j] = (Cin && col < Nc && c0 + j < NT) ? __ldcg(Cin + (size_t)row * ldci + col) : 0.f;
+                }
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const int col = tn + c0 + j;
-                    if (col < Nc && c0 + j < NT) {
-                        const float cin = Cin ? __ldcg(Cin + (size_t)row * ldci + col) : 0.f;
-                        C[(size_t)row * ldc + col] = fmaf(alpha, v[j], cin);
-                    }
+                    if (col < Nc && c0 + j < NT) C[(size_t)row * ldc + col] = fmaf(alpha, v[j], cin[j]);
                 }
             }
         }

@@ -20,6 +20,14 @@ def P():
     return P
 
 
+@pytest.fixture(autouse=True, params=["simt", "tc"])
+def products(request, monkeypatch):
+    """Every large-path test runs with the SIMT FP32 products and with the tcgen05 3xTF32 products
+    of k_big_ric (PDILQR_BIG_TC=1; tc.cuh) -- the same parity bar for both."""
+    monkeypatch.setenv("PDILQR_BIG_TC", "1" if request.param == "tc" else "0")
+    return request.param
+
+
 def solve(P, qp, dtype):
     B, N1, n, _ = qp["A"].shape
     m = qp["Bm"].shape[-1]

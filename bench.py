@@ -632,14 +632,54 @@ def solve_lq_bench(P, torch, dev, h_srbd, it, B, N, tdt, sm_mhz, reps=50):
 
 
 def large_bench(P, torch, dev, sm_mhz, reps=5):
-    """pdilqr_solve_lq on BASELINE configs 4 (n = m = 192, N = 50; B = 1 and 64) and 5 (n = 74, m = 32,
-    N = 100, B = 1024): CUDA-event time per solve (inputs resident), per-kernel split, and the FP32
-    rate of the fused Riccati-form fold against the FMA-pipe peak.  Data: 4 seeded instances tiled
-    over the batch (the kernels' work does not depend on the values)."""
+    """BASELINE configs 4 and 5 on the large-n path.
+    Config 4: the centralized controller for 16 quadrupeds (NEXT-3 model, n = m = 192, N = 50;
+    workloads.synth.multi_srbd_problem: 16 config-3 robots on a 4 x 4 grid 1.5 m apart, collision
+    penalty), one full SQP step (pdilqr_step: multi-robot linearisation, LQ solve, line search,
+    update) at B = 1 and B = 64 -- the paper's "< 25 ms for 16 robots" unit (one iteration,
+    P:375).  Config 5: pdilqr_solve_lq on the whole-body-sized LQ (n = 74, m = 32, N = 100,
+    B = 1024; 4 seeded instances tiled, the kernels' work does not depend on the values).
+    CUDA events around `reps` calls (inputs resident; the config-4 iterate restored before each
+    step so every rep solves the cold-start problem), per-kernel split from a separate pass."""
     import numpy as np
     res = {}
-    for name, B, N, n, m, kind in (("config4_b1", 1, 50, 192, 192, "dense"), ("config4_b64", 64, 50, 192, 192, "dense"),
-                                   ("config5_b1024", 1024, 100, 74, 32, "wb")):
+    keys = ("x", "u", "lam", "x0", "x_ref", "u_ref", "contact", "feet")
+    for name, B in (("config4_b1", 1), ("config4_b64", 64)):
+        N, R = 50, 16
+        prob = synth.multi_srbd_problem(B, R, N=N, seed=synth.BASE_SEED)
+        it = {k: torch.from_numpy(np.ascontiguousarray(prob[k] if prob[k].dtype == np.uint8 else prob[k].astype(np.float32)))
+              .to(dev) for k in keys}
+        pristine = {k: it[k].clone() for k in ("x", "u", "lam")}
+        h = P.PdIlqr(N=N, n=12 * R, m=12 * R, batch=B, dtype=torch.float32, model="multi_srbd", srbd=prob["params"],
+                     multi=prob["multi"], device=dev)
+        st = h.new_stats()
+        h.step(it, st)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            for k in pristine:
+                it[k].copy_(pristine[k])
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(); h.step(it, st); e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        h.profile(True)
+        h.step(it, st)
+        torch.cuda.synchronize()
+        pr = h.profile_read()
+        h.profile(False)
+        ms = float(np.median(ts))
+        kms = {k: v[1] / v[0] for k, v in pr.items()}
+        fl = ric_flops_per_stage(12 * R, 12 * R) * (N + 1) * B
+        ric = kms.get("k_big_ric") or kms.get("k_big_ric_tc")
+        res[name] = {"B": B, "N": N, "n": 12 * R, "m": 12 * R, "robots": R, "ms_per_step": ms,
+                     "solves_per_s": B / ms * 1e3, "kernels_ms": kms, "launches": h.last_launch_count(),
+                     "info_ok": bool((st["info"] == 0).all().item()), "alpha": float(st["alpha"][0].item()),
+                     "fold_flops": fl, "fold_tflops": (fl / ric / 1e9) if ric else None,
+                     "fold_frac_fp32_peak": (fl / ric / 1e9 / fp32_peak_tflops(sm_mhz)) if ric else None,
+                     "paper": "< 25 ms per solve for 16 robots on an RTX 3080 (P:18, P:417; context)"}
+        del h, it
+    for name, B, N, n, m, kind in (("config5_b1024", 1024, 100, 74, 32, "wb"),):
         base = synth.random_lq(min(B, 4), N, n, m, kind=kind, seed=7)
         qp = {}
         for k, v in base.items():
@@ -650,19 +690,21 @@ def large_bench(P, torch, dev, sm_mhz, reps=5):
         out = h.solve_lq(qp)
         out = h.solve_lq(qp, out=out)
         torch.cuda.synchronize()
-        h.profile(True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(reps):
             h.solve_lq(qp, out=out)
         e1.record()
         torch.cuda.synchronize()
+        h.profile(True)
+        h.solve_lq(qp, out=out)
+        torch.cuda.synchronize()
         pr = h.profile_read()
         h.profile(False)
         ms = e0.elapsed_time(e1) / reps
         kms = {k: v[1] / v[0] for k, v in pr.items()}
         fl = ric_flops_per_stage(n, m) * (N + 1) * B
-        ric = kms.get("k_big_ric")
+        ric = kms.get("k_big_ric") or kms.get("k_big_ric_tc")
         res[name] = {"B": B, "N": N, "n": n, "m": m, "ms_per_solve_lq": ms, "solves_per_s": B / ms * 1e3,
                      "kernels_ms": kms, "info_ok": bool((out["info"] == 0).all()),
                      "fold_flops": fl, "fold_tflops": (fl / ric / 1e9) if ric else None,

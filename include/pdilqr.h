@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define PDILQR_ABI_VERSION 1
+#define PDILQR_ABI_VERSION 2
 
 typedef enum {
     PDILQR_OK = 0,
@@ -52,7 +52,7 @@ typedef enum {
 } pdilqr_status;
 
 typedef enum { PDILQR_F32 = 0, PDILQR_F64 = 1 } pdilqr_dtype;
-typedef enum { PDILQR_MODEL_LQ = 0, PDILQR_MODEL_SRBD = 1 } pdilqr_model;
+typedef enum { PDILQR_MODEL_LQ = 0, PDILQR_MODEL_SRBD = 1, PDILQR_MODEL_MULTI_SRBD = 2 } pdilqr_model;
 
 /* Built-in single-rigid-body quadruped model and its cost (SI units).
  * State x = [p(3) world, Theta(3) = ZYX (roll, pitch, yaw), v(3) world, w(3) body] (n = 12,
@@ -65,6 +65,20 @@ typedef struct {
     double w_x[12], w_x_term[12], w_u_stance, w_u_swing;
     double mu_friction, f_min, f_max, barrier_mu, barrier_delta;
 } pdilqr_srbd_params;
+
+/* Centralized multi-robot model (PDILQR_MODEL_MULTI_SRBD; NEXT-3 of SURVEY §8(f); P:391, P:417;
+ * SPEC S:449-457): n_robots copies of the SRBD model above in one OCP, n = m = 12 n_robots (state
+ * and input stacked robot by robot; contact [4 R] and footholds [4 R][3] per stage likewise),
+ * coupled by a collision-avoidance penalty 1/2 weight eps^2 on every robot pair at every node,
+ * eps = softplus_k(d_min - d) = log(1 + exp(k (d_min - d))) / k with k = sharpness and
+ * d = sqrt(|p_a - p_b|_xy^2 + 1e-6) the planar CoM distance ("a quadratic penalty term", P:391;
+ * softplus smoothing), quadraticised by Gauss-Newton. */
+typedef struct {
+    int32_t n_robots;       /* R >= 1, 12 R <= 256                                              */
+    double d_min;           /* collision distance [m] (> 0)                                     */
+    double weight;          /* w >= 0                                                           */
+    double sharpness;       /* k > 0                                                            */
+} pdilqr_multi_params;
 
 typedef struct {
     int32_t N;              /* horizon: stages 0..N, terminal node N+1 (N >= 0)             */
@@ -80,7 +94,8 @@ typedef struct {
                                1 = pure tree over all N+2 elements; >= N+2 = single chunk
                                (sequential fold).  0 -> library default.                     */
     int32_t export_policy;  /* reserved (K,k are written whenever pdilqr_dir.K/k are non-NULL) */
-    pdilqr_srbd_params srbd;/* used iff model == PDILQR_MODEL_SRBD                           */
+    pdilqr_srbd_params srbd;/* used iff model == PDILQR_MODEL_SRBD or MULTI_SRBD (per robot)  */
+    pdilqr_multi_params multi; /* used iff model == PDILQR_MODEL_MULTI_SRBD                   */
 } pdilqr_config;
 
 typedef struct pdilqr_ctx *pdilqr_handle;

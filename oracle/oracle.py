@@ -68,6 +68,14 @@ class SrbdParams(C.Structure):
         return p
 
 
+class MultiParams(C.Structure):
+    _fields_ = [("n_robots", C.c_int), ("d_min", C.c_double), ("weight", C.c_double), ("sharpness", C.c_double)]
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "MultiParams":
+        return cls(int(d["n_robots"]), float(d["d_min"]), float(d["weight"]), float(d["sharpness"]))
+
+
 _lib = None
 
 
@@ -105,6 +113,19 @@ def lib():
         L.oracle_srbd_step.restype = i
         L.oracle_srbd_step_batch.argtypes = [PP, i, i, i, d, d] + [_dp] * 6 + [_up, _dp, _dp, i]
         L.oracle_srbd_plant.argtypes = [PP, _dp, _dp, _dp, _up, C.c_void_p, d, i, _dp]
+        MP = C.POINTER(MultiParams)
+        L.oracle_multi_coll_cost.argtypes = [MP, _dp]
+        L.oracle_multi_coll_cost.restype = d
+        L.oracle_multi_linearize.argtypes = [PP, MP, i] + [_dp] * 6 + [_up, _dp] + [_dp] * 11
+        L.oracle_multi_linearize.restype = i
+        L.oracle_multi_cost.argtypes = [PP, MP, i, _dp, _dp, _dp, _dp, _up]
+        L.oracle_multi_cost.restype = d
+        L.oracle_multi_theta.argtypes = [PP, MP, i, _dp, _dp, _dp, _up, _dp]
+        L.oracle_multi_theta.restype = d
+        L.oracle_multi_cost_slope.argtypes = [PP, MP, i, _dp, _dp, _dp, _dp, _up, _dp, _dp]
+        L.oracle_multi_cost_slope.restype = d
+        L.oracle_multi_step.argtypes = [PP, MP, i, i, d, d] + [_dp] * 6 + [_up, _dp] + [_dp] * 4
+        L.oracle_multi_step.restype = i
         L.oracle_max_threads.restype = i
         _lib = L
     return _lib
@@ -368,3 +389,65 @@ def srbd_solve(prob: dict, max_iters: int, tol: float, n_alpha=10, c1=1e-4, thet
                 iters[b] = k
                 break
     return iters, st
+
+
+# ----------------------------------------------------------------------------- multi-robot (NEXT-3)
+
+def _mp(prob):
+    return C.byref(SrbdParams.from_dict(prob["params"])), C.byref(MultiParams.from_dict(prob["multi"]))
+
+
+def multi_linearize_single(prob: dict, b: int = 0):
+    """Eq. 4 blocks of instance b of a multi-robot problem (workloads.synth.multi_srbd_problem)."""
+    x = _c(prob["x"][b]); N = x.shape[0] - 2; n = x.shape[1]
+    out = {"A": np.zeros((N + 1, n, n)), "Bm": np.zeros((N + 1, n, n)), "c": np.zeros((N + 1, n)),
+           "Q": np.zeros((N + 1, n, n)), "R": np.zeros((N + 1, n, n)), "S": np.zeros((N + 1, n, n)),
+           "q": np.zeros((N + 1, n)), "r": np.zeros((N + 1, n)), "P_term": np.zeros((n, n)),
+           "p_term": np.zeros(n), "dx0": np.zeros(n)}
+    P_, M_ = _mp(prob)
+    info = lib().oracle_multi_linearize(P_, M_, N, x, _c(prob["u"][b]), _c(prob["lam"][b]), _c(prob["x0"][b]),
+                                        _c(prob["x_ref"][b]), _uref(prob, b), _c(prob["contact"][b], np.uint8),
+                                        _c(prob["feet"][b]), out["A"], out["Bm"], out["c"], out["Q"], out["R"],
+                                        out["S"], out["q"], out["r"], out["P_term"], out["p_term"], out["dx0"])
+    out["info"] = info
+    return out
+
+
+def multi_coll_cost(multi: dict, x_node):
+    return lib().oracle_multi_coll_cost(C.byref(MultiParams.from_dict(multi)), _c(x_node))
+
+
+def multi_cost(prob, b, x=None, u=None):
+    x = prob["x"][b] if x is None else x
+    u = prob["u"][b] if u is None else u
+    P_, M_ = _mp(prob)
+    return lib().oracle_multi_cost(P_, M_, x.shape[0] - 2, _c(x), _c(u), _c(prob["x_ref"][b]), _uref(prob, b),
+                                   _c(prob["contact"][b], np.uint8))
+
+
+def multi_theta(prob, b, x=None, u=None):
+    x = prob["x"][b] if x is None else x
+    u = prob["u"][b] if u is None else u
+    P_, M_ = _mp(prob)
+    return lib().oracle_multi_theta(P_, M_, x.shape[0] - 2, _c(x), _c(u), _c(prob["x0"][b]),
+                                    _c(prob["contact"][b], np.uint8), _c(prob["feet"][b]))
+
+
+def multi_cost_slope(prob, b, dx, du):
+    x = prob["x"][b]
+    P_, M_ = _mp(prob)
+    return lib().oracle_multi_cost_slope(P_, M_, x.shape[0] - 2, _c(x), _c(prob["u"][b]), _c(prob["x_ref"][b]),
+                                         _uref(prob, b), _c(prob["contact"][b], np.uint8), _c(dx), _c(du))
+
+
+def multi_step_single(prob, b, n_alpha=10, c1=1e-4, theta_max=0.0):
+    """One SQP iteration of instance b of the centralized OCP: (x, u, lam, stats[5], dx, du, dlam)."""
+    x = _c(prob["x"][b]).copy(); u = _c(prob["u"][b]).copy(); lam = _c(prob["lam"][b]).copy()
+    N = x.shape[0] - 2; n = x.shape[1]
+    st = np.zeros(5)
+    dx = np.zeros((N + 2, n)); du = np.zeros((N + 1, n)); dl = np.zeros((N + 2, n))
+    P_, M_ = _mp(prob)
+    lib().oracle_multi_step(P_, M_, N, n_alpha, c1, theta_max, x, u, lam, _c(prob["x0"][b]), _c(prob["x_ref"][b]),
+                            _uref(prob, b), _c(prob["contact"][b], np.uint8), _c(prob["feet"][b]), st, dx, du, dl)
+    return x, u, lam, st, dx, du, dl
+

@@ -825,6 +825,288 @@ void oracle_srbd_linearize_batch(const oracle_srbd_params *P, int Bn, int N,
             r + b * S1 * NU, Pt + (size_t)b * NX * NX, pt + (size_t)b * NX, dx0 + (size_t)b * NX);
 }
 
+/* ------------------------------------------------------------------------- */
+/* Centralized multi-robot SRBD model (NEXT-3) */
+/* ------------------------------------------------------------------------- */
+/* R robots share one OCP: state x = [x_robot0 (12) .. x_robot{R-1}], input likewise, contact
+ * [4R], footholds [4R][3].  Dynamics and the per-robot cost are R copies of the SRBD model above
+ * (block-diagonal A, B, Q, R; S = 0).  Coupling: a collision-avoidance penalty ("a quadratic
+ * penalty term"; "smooth quadratic penalty (softplus smoothing)") on every robot pair
+ * (a < b) at every node i = 0..N+1:
+ *   d = sqrt(|p_a - p_b|_xy^2 + eta^2)  (planar CoM distance, eta = 1e-3 regularises d = 0),
+ *   eps = softplus_k(d_min - d) = log(1 + exp(k (d_min - d))) / k,   cost 1/2 w eps^2;
+ * Gauss-Newton: Hessian w grad eps grad eps^T, gradient w eps grad eps, with
+ *   grad_{p_a} eps = -sigma(k (d_min - d)) (p_a - p_b) / d,  grad_{p_b} eps = -grad_{p_a} eps. */
+typedef struct {
+    int n_robots;
+    double d_min, weight, sharpness;
+} oracle_multi_params;
+
+#define COLL_ETA 1e-3
+
+/* One pair term at positions pa, pb (xy): eps and grad eps w.r.t. (pa_x, pa_y, pb_x, pb_y). */
+static double coll_pair(const oracle_multi_params *M, const double *pa, const double *pb, double *g4) {
+    double dx = pa[0] - pb[0], dy = pa[1] - pb[1];
+    double d = sqrt(dx * dx + dy * dy + COLL_ETA * COLL_ETA);
+    double s = M->sharpness * (M->d_min - d);
+    double eps = (s > 0 ? s + log1p(exp(-s)) : log1p(exp(s))) / M->sharpness;
+    double sig = 1.0 / (1.0 + exp(-s));
+    g4[0] = -sig * dx / d; g4[1] = -sig * dy / d;
+    g4[2] = sig * dx / d;  g4[3] = sig * dy / d;
+    return eps;
+}
+
+/* Collision cost of one node (sum over pairs of 1/2 w eps^2). */
+double oracle_multi_coll_cost(const oracle_multi_params *M, const double *x /* [12 R] */) {
+    double J = 0, g4[4];
+    for (int a = 0; a < M->n_robots; ++a)
+        for (int b = a + 1; b < M->n_robots; ++b) {
+            double e = coll_pair(M, x + 12 * a, x + 12 * b, g4);
+            J += 0.5 * M->weight * e * e;
+        }
+    return J;
+}
+
+/* Add the Gauss-Newton collision terms of one node to H (n x n, ld n) and h (n). */
+static void coll_gn(const oracle_multi_params *M, const double *x, double *H, double *h) {
+    const int n = 12 * M->n_robots;
+    for (int a = 0; a < M->n_robots; ++a)
+        for (int b = a + 1; b < M->n_robots; ++b) {
+            double g4[4];
+            double e = coll_pair(M, x + 12 * a, x + 12 * b, g4);
+            int idx[4] = {12 * a, 12 * a + 1, 12 * b, 12 * b + 1};
+            for (int s = 0; s < 4; ++s) {
+                h[idx[s]] += M->weight * e * g4[s];
+                for (int t = 0; t < 4; ++t) H[IDX2(idx[s], idx[t], n)] += M->weight * g4[s] * g4[t];
+            }
+        }
+}
+
+/* Linearise + quadraticise the centralized OCP at (x, u, lam): per robot the SRBD linearisation
+ * of oracle_srbd_linearize on that robot's slices (block-diagonal placement; q, r with the
+ * multiplier terms of the robot's own constraints), plus the collision terms at nodes
+ * 0..N (into Q_i, q_i) and N+1 (into P_{N+1}, p_{N+1}).  Returns 0 or -1 (any robot invalid). */
+int oracle_multi_linearize(const oracle_srbd_params *P, const oracle_multi_params *M, int N,
+                           const double *x, const double *u, const double *lam,
+                           const double *x0, const double *xref, const double *uref,
+                           const uint8_t *contact, const double *feet,
+                           double *A, double *Bm, double *c, double *Q, double *R, double *S,
+                           double *q, double *r, double *Pt, double *pt, double *dx0) {
+    const int Rn = M->n_robots, n = 12 * Rn;
+    const size_t S1 = (size_t)(N + 1), S2 = S1 + 1, nn = (size_t)n * n;
+    memset(A, 0, sizeof(double) * S1 * nn); memset(Bm, 0, sizeof(double) * S1 * nn);
+    memset(Q, 0, sizeof(double) * S1 * nn); memset(R, 0, sizeof(double) * S1 * nn);
+    memset(S, 0, sizeof(double) * S1 * nn); memset(Pt, 0, sizeof(double) * nn);
+    /* per-robot slices and outputs */
+    double *xs = malloc(sizeof(double) * S2 * 12), *us = malloc(sizeof(double) * S1 * 12);
+    double *ls = malloc(sizeof(double) * S2 * 12), *xrs = malloc(sizeof(double) * S2 * 12);
+    double *urs = malloc(sizeof(double) * S1 * 12), *fs = malloc(sizeof(double) * S1 * 12);
+    uint8_t *cs = malloc(S1 * 4);
+    double *a1 = malloc(sizeof(double) * S1 * 144), *b1 = malloc(sizeof(double) * S1 * 144);
+    double *c1 = malloc(sizeof(double) * S1 * 12), *q1m = malloc(sizeof(double) * S1 * 144);
+    double *r1m = malloc(sizeof(double) * S1 * 144), *s1m = malloc(sizeof(double) * S1 * 144);
+    double *q1 = malloc(sizeof(double) * S1 * 12), *r1 = malloc(sizeof(double) * S1 * 12);
+    double pt1m[144], pt1[12], d01[12];
+    int info = 0;
+    for (int k = 0; k < Rn && info == 0; ++k) {
+        for (size_t i = 0; i < S2; ++i)
+            for (int a = 0; a < 12; ++a) {
+                xs[i * 12 + a] = x[i * n + 12 * k + a];
+                ls[i * 12 + a] = lam[i * n + 12 * k + a];
+                xrs[i * 12 + a] = xref[i * n + 12 * k + a];
+            }
+        for (size_t i = 0; i < S1; ++i) {
+            for (int a = 0; a < 12; ++a) {
+                us[i * 12 + a] = u[i * n + 12 * k + a];
+                urs[i * 12 + a] = uref ? uref[i * n + 12 * k + a] : 0.0;
+                fs[i * 12 + a] = feet[i * 12 * Rn + 12 * k + a];
+            }
+            for (int j = 0; j < 4; ++j) cs[i * 4 + j] = contact[i * 4 * Rn + 4 * k + j];
+        }
+        double x0s[12];
+        for (int a = 0; a < 12; ++a) x0s[a] = x0[12 * k + a];
+        info = oracle_srbd_linearize(P, N, xs, us, ls, x0s, xrs, urs, cs, fs,
+                                     a1, b1, c1, q1m, r1m, s1m, q1, r1, pt1m, pt1, d01);
+        if (info) break;
+        for (size_t i = 0; i < S1; ++i) {
+            for (int a = 0; a < 12; ++a) {
+                for (int bb = 0; bb < 12; ++bb) {
+                    size_t o = i * nn + IDX2(12 * k + a, 12 * k + bb, n);
+                    A[o] = a1[i * 144 + IDX2(a, bb, 12)];
+                    Bm[o] = b1[i * 144 + IDX2(a, bb, 12)];
+                    Q[o] = q1m[i * 144 + IDX2(a, bb, 12)];
+                    R[o] = r1m[i * 144 + IDX2(a, bb, 12)];
+                }
+                c[i * n + 12 * k + a] = c1[i * 12 + a];
+                q[i * n + 12 * k + a] = q1[i * 12 + a];
+                r[i * n + 12 * k + a] = r1[i * 12 + a];
+            }
+        }
+        for (int a = 0; a < 12; ++a) {
+            for (int bb = 0; bb < 12; ++bb) Pt[IDX2(12 * k + a, 12 * k + bb, n)] = pt1m[IDX2(a, bb, 12)];
+            pt[12 * k + a] = pt1[a];
+            dx0[12 * k + a] = d01[a];
+        }
+    }
+    if (info == 0) {
+        for (size_t i = 0; i < S1; ++i) coll_gn(M, x + i * n, Q + i * nn, q + i * n);
+        coll_gn(M, x + S1 * n, Pt, pt);
+    }
+    free(xs); free(us); free(ls); free(xrs); free(urs); free(fs); free(cs);
+    free(a1); free(b1); free(c1); free(q1m); free(r1m); free(s1m); free(q1); free(r1);
+    return info;
+}
+
+/* Copy robot k's slices (x, u of stride 12 R) of a trajectory into single-robot arrays. */
+static void robot_slice(int Rn, int k, int N, const double *x, const double *u, const uint8_t *contact,
+                        const double *feet, const double *xref, const double *uref,
+                        double *xs, double *us, uint8_t *cs, double *fs, double *xrs, double *urs) {
+    const int n = 12 * Rn;
+    for (int i = 0; i <= N + 1; ++i)
+        for (int a = 0; a < 12; ++a) {
+            if (xs) xs[i * 12 + a] = x[i * n + 12 * k + a];
+            if (xrs) xrs[i * 12 + a] = xref[i * n + 12 * k + a];
+        }
+    for (int i = 0; i <= N; ++i) {
+        for (int a = 0; a < 12; ++a) {
+            if (us) us[i * 12 + a] = u[i * n + 12 * k + a];
+            if (urs) urs[i * 12 + a] = uref ? uref[i * n + 12 * k + a] : 0.0;
+            if (fs) fs[i * 12 + a] = feet[i * 12 * Rn + 12 * k + a];
+        }
+        if (cs) for (int j = 0; j < 4; ++j) cs[i * 4 + j] = contact[i * 4 * Rn + 4 * k + j];
+    }
+}
+
+/* J = sum_k J_srbd(robot k) + sum_{i=0}^{N+1} sum_{a<b} 1/2 w eps_ab(x_i)^2. */
+double oracle_multi_cost(const oracle_srbd_params *P, const oracle_multi_params *M, int N, const double *x,
+                         const double *u, const double *xref, const double *uref, const uint8_t *contact) {
+    const int Rn = M->n_robots, n = 12 * Rn;
+    double *xs = malloc(sizeof(double) * (N + 2) * 12), *us = malloc(sizeof(double) * (N + 1) * 12);
+    double *xrs = malloc(sizeof(double) * (N + 2) * 12), *urs = malloc(sizeof(double) * (N + 1) * 12);
+    uint8_t *cs = malloc((size_t)(N + 1) * 4);
+    double J = 0;
+    for (int k = 0; k < Rn; ++k) {
+        robot_slice(Rn, k, N, x, u, contact, NULL, xref, uref, xs, us, cs, NULL, xrs, urs);
+        J += oracle_srbd_cost(P, N, xs, us, xrs, urs, cs);
+    }
+    for (int i = 0; i <= N + 1; ++i) J += oracle_multi_coll_cost(M, x + (size_t)i * n);
+    free(xs); free(us); free(xrs); free(urs); free(cs);
+    return J;
+}
+
+/* theta = sum_{i=0}^{N} |x_{i+1} - h(x_i, u_i)|_2 + |xhat0 - x_0|_2 over the stacked state
+ * (Eq. 17, reading R9; h is the per-robot Euler step). */
+double oracle_multi_theta(const oracle_srbd_params *P, const oracle_multi_params *M, int N, const double *x,
+                          const double *u, const double *x0, const uint8_t *contact, const double *feet) {
+    const int Rn = M->n_robots, n = 12 * Rn;
+    double th = 0, d0 = 0;
+    for (int a = 0; a < n; ++a) d0 += (x0[a] - x[a]) * (x0[a] - x[a]);
+    th += sqrt(d0);
+    for (int i = 0; i <= N; ++i) {
+        double s = 0;
+        for (int k = 0; k < Rn; ++k) {
+            double xn[12];
+            uint8_t ck[4];
+            for (int j = 0; j < 4; ++j) ck[j] = contact[(size_t)i * 4 * Rn + 4 * k + j];
+            oracle_srbd_h(P, x + (size_t)i * n + 12 * k, u + (size_t)i * n + 12 * k, feet + (size_t)i * 12 * Rn + 12 * k, ck, xn);
+            for (int a = 0; a < 12; ++a) {
+                double d = x[(size_t)(i + 1) * n + 12 * k + a] - xn[a];
+                s += d * d;
+            }
+        }
+        th += sqrt(s);
+    }
+    return th;
+}
+
+/* grad J . (dx, du) (descent test, reading R10): per-robot SRBD slopes + collision gradients. */
+double oracle_multi_cost_slope(const oracle_srbd_params *P, const oracle_multi_params *M, int N, const double *x,
+                               const double *u, const double *xref, const double *uref, const uint8_t *contact,
+                               const double *dx, const double *du) {
+    const int Rn = M->n_robots, n = 12 * Rn;
+    double *xs = malloc(sizeof(double) * (N + 2) * 12), *us = malloc(sizeof(double) * (N + 1) * 12);
+    double *xrs = malloc(sizeof(double) * (N + 2) * 12), *urs = malloc(sizeof(double) * (N + 1) * 12);
+    double *dxs = malloc(sizeof(double) * (N + 2) * 12), *dus = malloc(sizeof(double) * (N + 1) * 12);
+    uint8_t *cs = malloc((size_t)(N + 1) * 4);
+    double g = 0;
+    for (int k = 0; k < Rn; ++k) {
+        robot_slice(Rn, k, N, x, u, contact, NULL, xref, uref, xs, us, cs, NULL, xrs, urs);
+        robot_slice(Rn, k, N, dx, du, contact, NULL, xref, NULL, dxs, dus, NULL, NULL, NULL, NULL);
+        g += oracle_srbd_cost_slope(P, N, xs, us, xrs, urs, cs, dxs, dus);
+    }
+    for (int i = 0; i <= N + 1; ++i) {
+        const double *xi = x + (size_t)i * n, *di = dx + (size_t)i * n;
+        for (int a = 0; a < Rn; ++a)
+            for (int b = a + 1; b < Rn; ++b) {
+                double g4[4];
+                double e = coll_pair(M, xi + 12 * a, xi + 12 * b, g4);
+                g += M->weight * e * (g4[0] * di[12 * a] + g4[1] * di[12 * a + 1] + g4[2] * di[12 * b] + g4[3] * di[12 * b + 1]);
+            }
+    }
+    free(xs); free(us); free(xrs); free(urs); free(dxs); free(dus); free(cs);
+    return g;
+}
+
+/* One SQP iteration of the centralized OCP: linearise -> Riccati LQ solve -> dual update ->
+ * filter line search (same rule and grid as the single-robot step) -> update.  stats[5] as
+ * oracle_srbd_step.  dirs optional. */
+int oracle_multi_step(const oracle_srbd_params *P, const oracle_multi_params *M, int N, int n_alpha, double c1,
+                      double theta_max, double *x, double *u, double *lam, const double *x0, const double *xref,
+                      const double *uref, const uint8_t *contact, const double *feet, double *stats,
+                      double *dx_out, double *du_out, double *dlam_out) {
+    const int n = 12 * M->n_robots, m = n;
+    const size_t S1 = (size_t)(N + 1), nn = (size_t)n * n;
+    double *A = malloc(sizeof(double) * S1 * nn), *Bm = malloc(sizeof(double) * S1 * nn);
+    double *c = malloc(sizeof(double) * S1 * n), *Q = malloc(sizeof(double) * S1 * nn);
+    double *R = malloc(sizeof(double) * S1 * nn), *S = malloc(sizeof(double) * S1 * nn);
+    double *q = malloc(sizeof(double) * S1 * n), *r = malloc(sizeof(double) * S1 * m);
+    double *Pt = malloc(sizeof(double) * nn), *pt = malloc(sizeof(double) * n), *d0 = malloc(sizeof(double) * n);
+    double *dx = malloc(sizeof(double) * (S1 + 1) * n), *du = malloc(sizeof(double) * S1 * m);
+    double *dl = malloc(sizeof(double) * (S1 + 1) * n);
+    double *xa = malloc(sizeof(double) * (S1 + 1) * n), *ua = malloc(sizeof(double) * S1 * m);
+    double thr = theta_max > 0 ? theta_max : 1e-2 * (N + 1);
+    int info = oracle_multi_linearize(P, M, N, x, u, lam, x0, xref, uref, contact, feet, A, Bm, c, Q, R, S, q, r,
+                                      Pt, pt, d0);
+    if (info == 0) info = oracle_solve_lq(N, n, m, A, Bm, c, Q, R, S, q, r, Pt, pt, d0, dx, du, dl, NULL, NULL, NULL, NULL);
+    if (info == 0) {
+        for (size_t t = 0; t < (S1 + 1) * n; ++t)
+            if (!isfinite(dx[t]) || !isfinite(dl[t])) info = -1;
+        for (size_t t = 0; t < S1 * m; ++t)
+            if (!isfinite(du[t])) info = -1;
+    }
+    double J0 = oracle_multi_cost(P, M, N, x, u, xref, uref, contact);
+    double th0 = oracle_multi_theta(P, M, N, x, u, x0, contact, feet);
+    double alpha = 0, Jn = J0, thn = th0;
+    int accepted = 0;
+    if (info == 0) {
+        double g = oracle_multi_cost_slope(P, M, N, x, u, xref, uref, contact, dx, du);
+        for (int j = 0; j < n_alpha && !accepted; ++j) {
+            double al = ldexp(1.0, -j);
+            int ok = 1;
+            for (size_t t = 0; t < (S1 + 1) * n; ++t) xa[t] = x[t] + al * dx[t];
+            for (size_t t = 0; t < S1 * m; ++t) ua[t] = u[t] + al * du[t];
+            for (int i = 0; i <= N; ++i)
+                for (int k = 0; k < M->n_robots; ++k) ok &= pitch_ok(xa + (size_t)i * n + 12 * k);
+            double Ja = ok ? oracle_multi_cost(P, M, N, xa, ua, xref, uref, contact) : INFINITY;
+            double tha = ok ? oracle_multi_theta(P, M, N, xa, ua, x0, contact, feet) : INFINITY;
+            if (filter_accept(J0, th0, g, Ja, tha, al, c1, thr)) {
+                alpha = al; accepted = 1; Jn = Ja; thn = tha;
+            }
+        }
+        if (accepted) {
+            for (size_t t = 0; t < (S1 + 1) * n; ++t) { x[t] += alpha * dx[t]; lam[t] += alpha * dl[t]; }
+            for (size_t t = 0; t < S1 * m; ++t) u[t] += alpha * du[t];
+        }
+    }
+    if (stats) { stats[0] = Jn; stats[1] = thn; stats[2] = alpha; stats[3] = accepted; stats[4] = info; }
+    if (dx_out) memcpy(dx_out, dx, sizeof(double) * (S1 + 1) * n);
+    if (du_out) memcpy(du_out, du, sizeof(double) * S1 * m);
+    if (dlam_out) memcpy(dlam_out, dl, sizeof(double) * (S1 + 1) * n);
+    free(A); free(Bm); free(c); free(Q); free(R); free(S); free(q); free(r); free(Pt); free(pt); free(d0);
+    free(dx); free(du); free(dl); free(xa); free(ua);
+    return info;
+}
+
 /* Closed-loop plant ("plant = RK4 integration of the same SRBD model";
  * P:388 push disturbance): classical RK4 of xdot = f(x,u) + (0,0,0, 0,0,0, F_ext/m, 0,0,0),
  * `sub` steps of h = dt/sub, u / feet / contact held constant (zero-order hold).            */

@@ -21,6 +21,7 @@
 #include "big.cuh"
 #include "big_ric.cuh"
 #include "adjoint.cuh"
+#include "multi.cuh"
 
 using namespace pdilqr;
 
@@ -169,17 +170,25 @@ pdilqr_status check_cfg(const pdilqr_config *c, Variant &v, int &NX, int &NU) {
     if (c->N < 0 || c->batch < 1 || c->n < 1 || c->m < 1)
         return fail(PDILQR_ERR_DIM, "invalid dimensions N=%d n=%d m=%d batch=%d", c->N, c->n, c->m, c->batch);
     if (c->dtype != PDILQR_F32 && c->dtype != PDILQR_F64) return fail(PDILQR_ERR_INVALID_ARG, "unknown dtype %d", (int)c->dtype);
-    if (c->model != PDILQR_MODEL_LQ && c->model != PDILQR_MODEL_SRBD)
+    if (c->model != PDILQR_MODEL_LQ && c->model != PDILQR_MODEL_SRBD && c->model != PDILQR_MODEL_MULTI_SRBD)
         return fail(PDILQR_ERR_INVALID_ARG, "unknown model %d", (int)c->model);
     if (c->model == PDILQR_MODEL_SRBD && (c->n != 12 || c->m != 12))
         return fail(PDILQR_ERR_DIM, "SRBD model needs n = m = 12 (got %d, %d)", c->n, c->m);
+    if (c->model == PDILQR_MODEL_MULTI_SRBD) {
+        const auto &mp = c->multi;
+        if (mp.n_robots < 1 || mp.n_robots > MULTI_MAX_R || c->n != 12 * mp.n_robots || c->m != 12 * mp.n_robots)
+            return fail(PDILQR_ERR_DIM, "multi-robot model needs 1 <= n_robots <= %d and n = m = 12 n_robots (got R=%d, n=%d, m=%d)",
+                        MULTI_MAX_R, mp.n_robots, c->n, c->m);
+        if (!(mp.d_min > 0) || !(mp.weight >= 0) || !(mp.sharpness > 0))
+            return fail(PDILQR_ERR_INVALID_ARG, "invalid collision parameters (d_min > 0, weight >= 0, sharpness > 0)");
+    }
     if (c->n_alpha < 0 || c->n_alpha > kMaxAlpha) return fail(PDILQR_ERR_INVALID_ARG, "n_alpha must be in [0, %d]", kMaxAlpha);
     if (c->leaf_chunk < 0) return fail(PDILQR_ERR_INVALID_ARG, "leaf_chunk must be >= 0");
     if (!pick_variant(c->n, c->m, v, NX, NU))
         return fail(PDILQR_ERR_UNSUPPORTED, "n = %d, m = %d: dimensions above %d are not supported", c->n, c->m, kBigMax);
-    if (v == VBIG && c->model != PDILQR_MODEL_LQ)
-        return fail(PDILQR_ERR_UNSUPPORTED, "the large-dimension path serves pdilqr_solve_lq only");
-    if (c->model == PDILQR_MODEL_SRBD) {
+    if (v == VBIG && c->model == PDILQR_MODEL_SRBD)
+        return fail(PDILQR_ERR_UNSUPPORTED, "the large-dimension path serves LQ and multi-robot handles");
+    if (c->model != PDILQR_MODEL_LQ) {
         const auto &s = c->srbd;
         if (!(s.dt >= 0) || !(s.mass > 0) || !(s.barrier_mu > 0) || !(s.barrier_delta > 0))
             return fail(PDILQR_ERR_INVALID_ARG, "invalid SRBD parameters (dt >= 0, mass > 0, barrier mu, delta > 0)");
@@ -219,6 +228,14 @@ Layout make_big_layout(const pdilqr_config *c, int esz) {
     L.pre = take(B * 4);
     L.info_tmp = take(B * 4);
     L.stats = take(B * (3 * (size_t)esz + 8));
+    if (c->model == PDILQR_MODEL_MULTI_SRBD) {  // internal QP and direction of the multi-robot step
+        const size_t sz[11] = {(N + 1) * n * n, (N + 1) * n * m, (N + 1) * n, (N + 1) * n * n, (N + 1) * m * m,
+                               (N + 1) * m * n, (N + 1) * n, (N + 1) * m, n * n, n, n};
+        for (int k = 0; k < 11; ++k) L.qp[k] = take(B * sz[k] * esz);
+        L.dir[0] = take(B * (N + 2) * n * esz);
+        L.dir[1] = take(B * (N + 1) * m * esz);
+        L.dir[2] = take(B * (N + 2) * n * esz);
+    }
     {  // pdilqr_solve_lq_adjoint: adjoint linear terms and solution, user (unpadded) layouts
         const size_t nB = c->batch, nN = c->N, nn_ = c->n, mm_ = c->m;
         const size_t sz[8] = {(nN + 1) * nn_, (nN + 1) * mm_, (nN + 1) * nn_, nn_, nn_, (nN + 2) * nn_, (nN + 1) * mm_,
@@ -262,7 +279,7 @@ Layout make_layout(const pdilqr_config *c, int NX, int NU, int esz, int chunk, i
     L.conv = take(B * 4);
     L.active = take(8);
     const size_t n = c->n, m = c->m;
-    if (c->model == PDILQR_MODEL_SRBD) {
+    if (c->model != PDILQR_MODEL_LQ) {
         const size_t sz[11] = {(N + 1) * n * n, (N + 1) * n * m, (N + 1) * n, (N + 1) * n * n, (N + 1) * m * m,
                                (N + 1) * m * n, (N + 1) * n, (N + 1) * m, n * n, n, n};
         for (int k = 0; k < 11; ++k) L.qp[k] = take(B * sz[k] * esz);
@@ -370,6 +387,12 @@ template <typename T>
 bool ric_cluster_fits(int cs, size_t smem, bool ut);
 cudaError_t debug_tc_gemm(int M, int N, int K, int ta, int tb, const float *A, int lda, const float *Bm, int ldb,
                           const float *Cin, float *C, cudaStream_t st);
+// centralized multi-robot model (multi.cuh): linearisation and one SQP step
+template <typename T>
+pdilqr_status run_multi_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArgs<T> &outq, int32_t *pre,
+                                  cudaStream_t st);
+template <typename T>
+pdilqr_status run_multi_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st);
 // co-resident CTAs of the cooperative latency-regime scan kernels (v: Variant)
 template <typename T>
 void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk2);
@@ -942,6 +965,64 @@ bool ric_cluster_fits(int cs, size_t smem, bool ut) {
     cudaGetLastError();
     return false;
 }
+inline MultiConst multi_const(const pdilqr_ctx *h) {
+    const auto &mp = h->cfg.multi;
+    return MultiConst{mp.n_robots, mp.d_min, mp.weight, mp.sharpness};
+}
+
+template <typename T>
+pdilqr_status run_multi_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const LqArgs<T> &outq, int32_t *pre,
+                                  cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N;
+    cudaMemsetAsync(pre, 0, (size_t)B * 4, st);
+    {
+        Prof pf(h, "k_multi_linearize", st);
+        k_multi_linearize<T><<<(unsigned)((long)B * (N + 2)), MULTI_THREADS, 0, st>>>(h->K, multi_const(h), iter_of<T>(it), B,
+                                                                                     N, outq, pre);
+    }
+    h->launches += 1;
+    return cuda_check("multi linearize launch");
+}
+
+// One SQP iteration of the centralized OCP: linearise (k_multi_linearize), solve the dense LQ
+// subproblem (large-n path or n = 12 path), filter line search + update (k_multi_linesearch).
+template <typename T>
+pdilqr_status run_multi_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N;
+    LqArgs<T> qp = internal_qp<T>(h);
+    int32_t *pre = reinterpret_cast<int32_t *>(h->ws + h->lay.pre);
+    int32_t *info_tmp = reinterpret_cast<int32_t *>(h->ws + h->lay.info_tmp);
+    pdilqr_status s = run_multi_linearize<T>(h, it, qp, pre, st);
+    if (s != PDILQR_OK) return s;
+    LqOut<T> out;
+    if (dir && dir->dx) {
+        out = LqOut<T>{(T *)dir->dx, (T *)dir->du, (T *)dir->dlam, (T *)dir->K, (T *)dir->k};
+    } else {
+        out = LqOut<T>{reinterpret_cast<T *>(h->ws + h->lay.dir[0]), reinterpret_cast<T *>(h->ws + h->lay.dir[1]),
+                       reinterpret_cast<T *>(h->ws + h->lay.dir[2]), nullptr, nullptr};
+    }
+    s = dispatch_lq<T>(h, qp, out, info_tmp, nullptr, st);
+    if (s != PDILQR_OK) return s;
+    LsOut<T> so{(T *)stats->cost, (T *)stats->theta, (T *)stats->alpha, stats->accepted, stats->info};
+    {
+        Prof pf(h, "k_multi_linesearch", st);
+        k_multi_linesearch<T><<<B, MULTI_THREADS, 0, st>>>(h->K, multi_const(h), iter_of<T>(it), B, N, out.dx, out.du,
+                                                           out.dlam, info_tmp, pre, so);
+    }
+    h->launches += 1;
+    return cuda_check("multi step launch");
+}
+
+#if PDILQR_BIG(0)
+template pdilqr_status run_multi_linearize<float>(pdilqr_ctx *, const pdilqr_iterate *, const LqArgs<float> &, int32_t *,
+                                                  cudaStream_t);
+template pdilqr_status run_multi_step<float>(pdilqr_ctx *, pdilqr_iterate *, pdilqr_stats *, pdilqr_dir *, cudaStream_t);
+#endif
+#if PDILQR_BIG(1)
+template pdilqr_status run_multi_linearize<double>(pdilqr_ctx *, const pdilqr_iterate *, const LqArgs<double> &,
+                                                   int32_t *, cudaStream_t);
+template pdilqr_status run_multi_step<double>(pdilqr_ctx *, pdilqr_iterate *, pdilqr_stats *, pdilqr_dir *, cudaStream_t);
+#endif
 #if PDILQR_BIG(0)
 cudaError_t debug_tc_gemm(int M, int N, int K, int ta, int tb, const float *A, int lda, const float *Bm, int ldb,
                           const float *Cin, float *C, cudaStream_t st) {
@@ -1203,7 +1284,7 @@ pdilqr_status pdilqr_debug_tc_gemm(int32_t M, int32_t N, int32_t K, int32_t tran
 
 static pdilqr_status check_iter(pdilqr_handle h, const pdilqr_iterate *it) {
     if (!h || !it) return fail(PDILQR_ERR_INVALID_ARG, "NULL handle or iterate");
-    if (h->cfg.model != PDILQR_MODEL_SRBD) return fail(PDILQR_ERR_UNSUPPORTED, "handle was not created for the SRBD model");
+    if (h->cfg.model == PDILQR_MODEL_LQ) return fail(PDILQR_ERR_UNSUPPORTED, "handle was not created for a built-in model");
     const void *ptrs[] = {it->x, it->u, it->lam, it->x0, it->x_ref, it->contact, it->feet};
     for (const void *p : ptrs)
         if (!p) return fail(PDILQR_ERR_INVALID_ARG, "NULL array in iterate");
@@ -1230,11 +1311,13 @@ pdilqr_status pdilqr_linearize(pdilqr_handle h, const pdilqr_iterate *it, pdilqr
         LqArgs<float> o{(float *)out->A, (float *)out->Bm, (float *)out->c, (float *)out->Q, (float *)out->R,
                         (float *)out->S, (float *)out->q, (float *)out->r, (float *)out->P_term, (float *)out->p_term,
                         (float *)out->dx0};
+        if (h->cfg.model == PDILQR_MODEL_MULTI_SRBD) return pdq::run_multi_linearize<float>(h, it, o, pre, st);
         return run_linearize<float>(h, it, o, pre, st);
     }
     LqArgs<double> o{(double *)out->A, (double *)out->Bm, (double *)out->c, (double *)out->Q, (double *)out->R,
                      (double *)out->S, (double *)out->q, (double *)out->r, (double *)out->P_term, (double *)out->p_term,
                      (double *)out->dx0};
+    if (h->cfg.model == PDILQR_MODEL_MULTI_SRBD) return pdq::run_multi_linearize<double>(h, it, o, pre, st);
     return run_linearize<double>(h, it, o, pre, st);
 }
 
@@ -1247,6 +1330,9 @@ pdilqr_status pdilqr_step(pdilqr_handle h, pdilqr_iterate *it, pdilqr_stats *sta
     DeviceGuard g(h->device);
     h->launches = 0;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (h->cfg.model == PDILQR_MODEL_MULTI_SRBD)
+        return h->cfg.dtype == PDILQR_F32 ? pdq::run_multi_step<float>(h, it, stats, dir, st)
+                                          : pdq::run_multi_step<double>(h, it, stats, dir, st);
     if (h->cfg.dtype == PDILQR_F32) return run_step<float>(h, it, stats, dir, st);
     return run_step<double>(h, it, stats, dir, st);
 }
@@ -1254,6 +1340,8 @@ pdilqr_status pdilqr_step(pdilqr_handle h, pdilqr_iterate *it, pdilqr_stats *sta
 pdilqr_status pdilqr_solve(pdilqr_handle h, pdilqr_iterate *it, int32_t max_iters, double tol, pdilqr_stats *stats,
                            int32_t *iters, int32_t *iters_run, void *stream) {
     pdilqr_status s = check_iter(h, it);
+    if (s == PDILQR_OK && h->cfg.model != PDILQR_MODEL_SRBD)
+        s = fail(PDILQR_ERR_UNSUPPORTED, "solve / shift / plant / tick_host serve single-robot SRBD handles");
     if (s != PDILQR_OK) return s;
     if (!stats || !stats->cost || !stats->theta || !stats->alpha || !stats->accepted || !stats->info)
         return fail(PDILQR_ERR_INVALID_ARG, "NULL stats array");
@@ -1290,6 +1378,8 @@ pdilqr_status pdilqr_solve(pdilqr_handle h, pdilqr_iterate *it, int32_t max_iter
 
 pdilqr_status pdilqr_shift(pdilqr_handle h, pdilqr_iterate *it, void *stream) {
     pdilqr_status s = check_iter(h, it);
+    if (s == PDILQR_OK && h->cfg.model != PDILQR_MODEL_SRBD)
+        s = fail(PDILQR_ERR_UNSUPPORTED, "solve / shift / plant / tick_host serve single-robot SRBD handles");
     if (s != PDILQR_OK) return s;
     DeviceGuard g(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1309,6 +1399,8 @@ pdilqr_status pdilqr_shift(pdilqr_handle h, pdilqr_iterate *it, void *stream) {
 pdilqr_status pdilqr_srbd_plant(pdilqr_handle h, const pdilqr_iterate *it, void *x_plant, const void *u_hold,
                                 const void *ext_force, double dt, int32_t substeps, void *stream) {
     pdilqr_status s = check_iter(h, it);
+    if (s == PDILQR_OK && h->cfg.model != PDILQR_MODEL_SRBD)
+        s = fail(PDILQR_ERR_UNSUPPORTED, "solve / shift / plant / tick_host serve single-robot SRBD handles");
     if (s != PDILQR_OK) return s;
     if (!x_plant || !u_hold || substeps < 1 || !(dt >= 0)) return fail(PDILQR_ERR_INVALID_ARG, "invalid plant arguments");
     DeviceGuard g(h->device);
@@ -1331,6 +1423,8 @@ pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *
                                void *theta_host, void *alpha_host, int32_t *accepted_host, int32_t *info_host,
                                void *stream) {
     pdilqr_status s = check_iter(h, it);
+    if (s == PDILQR_OK && h->cfg.model != PDILQR_MODEL_SRBD)
+        s = fail(PDILQR_ERR_UNSUPPORTED, "solve / shift / plant / tick_host serve single-robot SRBD handles");
     if (s != PDILQR_OK) return s;
     if (!x0_host || !u0_host) return fail(PDILQR_ERR_INVALID_ARG, "NULL host buffer");
     DeviceGuard g(h->device);

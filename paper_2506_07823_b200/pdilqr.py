@@ -18,7 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libpdilqr.so")
 
 PDILQR_F32, PDILQR_F64 = 0, 1
-PDILQR_MODEL_LQ, PDILQR_MODEL_SRBD = 0, 1
+PDILQR_MODEL_LQ, PDILQR_MODEL_SRBD, PDILQR_MODEL_MULTI_SRBD = 0, 1, 2
+ABI_VERSION = 2
 STATUS = {0: "PDILQR_OK", 1: "PDILQR_ERR_INVALID_ARG", 2: "PDILQR_ERR_DIM", 3: "PDILQR_ERR_WORKSPACE",
           4: "PDILQR_ERR_CUDA", 5: "PDILQR_ERR_UNSUPPORTED"}
 
@@ -36,11 +37,15 @@ class SrbdParams(C.Structure):
                 ("barrier_delta", C.c_double)]
 
 
+class MultiParams(C.Structure):
+    _fields_ = [("n_robots", C.c_int32), ("d_min", C.c_double), ("weight", C.c_double), ("sharpness", C.c_double)]
+
+
 class Config(C.Structure):
     _fields_ = [("N", C.c_int32), ("n", C.c_int32), ("m", C.c_int32), ("batch", C.c_int32),
                 ("dtype", C.c_int), ("model", C.c_int), ("n_alpha", C.c_int32), ("armijo_c1", C.c_double),
                 ("theta_max", C.c_double), ("leaf_chunk", C.c_int32), ("export_policy", C.c_int32),
-                ("srbd", SrbdParams)]
+                ("srbd", SrbdParams), ("multi", MultiParams)]
 
 
 class Lq(C.Structure):
@@ -160,16 +165,21 @@ class PdIlqr:
 
     def __init__(self, N: int, n: int, m: int, batch: int, dtype=torch.float32, model: str = "lq",
                  srbd: dict | None = None, n_alpha: int = 10, armijo_c1: float = 1e-4, theta_max: float = 0.0,
-                 leaf_chunk: int = 0, device: int | torch.device | None = None):
+                 leaf_chunk: int = 0, device: int | torch.device | None = None, multi: dict | None = None):
         L = lib()
+        if L.pdilqr_abi_version() != ABI_VERSION:
+            raise PdilqrError(f"libpdilqr.so ABI {L.pdilqr_abi_version()} != binding ABI {ABI_VERSION}")
         self.N, self.n, self.m, self.batch = N, n, m, batch
         self.dtype = dtype
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
                                    (device.index if isinstance(device, torch.device) else device))
+        mdl = {"lq": PDILQR_MODEL_LQ, "srbd": PDILQR_MODEL_SRBD, "multi_srbd": PDILQR_MODEL_MULTI_SRBD}[model]
+        mp = MultiParams(**({k: multi[k] for k in ("n_robots", "d_min", "weight", "sharpness")} if multi else {}))
         cfg = Config(N=N, n=n, m=m, batch=batch, dtype=PDILQR_F32 if dtype == torch.float32 else PDILQR_F64,
-                     model=PDILQR_MODEL_SRBD if model == "srbd" else PDILQR_MODEL_LQ, n_alpha=n_alpha,
-                     armijo_c1=armijo_c1, theta_max=theta_max, leaf_chunk=leaf_chunk, export_policy=0,
-                     srbd=srbd_params_struct(srbd))
+                     model=mdl, n_alpha=n_alpha, armijo_c1=armijo_c1, theta_max=theta_max, leaf_chunk=leaf_chunk,
+                     export_policy=0, srbd=srbd_params_struct(srbd), multi=mp)
+        self.model = model
+        self.n_robots = multi["n_robots"] if multi else 1
         self._cfg = cfg
         nb = C.c_size_t()
         _check(L.pdilqr_workspace_bytes(C.byref(cfg), C.byref(nb)))
@@ -281,14 +291,15 @@ class PdIlqr:
         return grad
 
     def _iterate(self, it: dict) -> Iterate:
-        B, N = self.batch, self.N
-        self._check_t(it["x"], (B, N + 2, 12)); self._check_t(it["u"], (B, N + 1, 12))
-        self._check_t(it["lam"], (B, N + 2, 12)); self._check_t(it["x0"], (B, 12))
-        self._check_t(it["x_ref"], (B, N + 2, 12))
+        B, N, R = self.batch, self.N, self.n_robots
+        nx = 12 * R
+        self._check_t(it["x"], (B, N + 2, nx)); self._check_t(it["u"], (B, N + 1, nx))
+        self._check_t(it["lam"], (B, N + 2, nx)); self._check_t(it["x0"], (B, nx))
+        self._check_t(it["x_ref"], (B, N + 2, nx))
         if it.get("u_ref") is not None:
-            self._check_t(it["u_ref"], (B, N + 1, 12))
-        self._check_t(it["contact"], (B, N + 1, 4), torch.uint8)
-        self._check_t(it["feet"], (B, N + 1, 4, 3))
+            self._check_t(it["u_ref"], (B, N + 1, nx))
+        self._check_t(it["contact"], (B, N + 1, 4 * R), torch.uint8)
+        self._check_t(it["feet"], (B, N + 1, 4 * R, 3))
         return Iterate(**{k: _ptr(it.get(k)) for k in ("x", "u", "lam", "x0", "x_ref", "u_ref", "contact", "feet")})
 
     def linearize(self, it: dict, out: dict | None = None, info=None, stream=None):

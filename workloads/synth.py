@@ -262,3 +262,46 @@ def round_to(arrs: dict, dtype) -> dict:
         else:
             out[k] = v
     return out
+
+
+# --------------------------------------------------------------------------------------
+# Config 4: centralized controller for R quadrupeds (NEXT-3 model)
+# --------------------------------------------------------------------------------------
+def multi_default_params(n_robots: int = 16) -> dict:
+    """Collision-penalty parameters of the centralized model (recorded choices: the paper gives
+    only "a quadratic penalty term"): d_min = 1.0 m, weight 1e3, softplus sharpness 10 /m."""
+    return {"n_robots": n_robots, "d_min": 1.0, "weight": 1.0e3, "sharpness": 10.0}
+
+
+def multi_srbd_problem(B: int, n_robots: int = 16, N: int = 50, seed: int = BASE_SEED, first: int = 0,
+                       spacing: float = 1.5, multi: dict | None = None):
+    """Config 4: R SRBD robots (config-3 trot instances: random commands, phases and yaw) on a
+    ceil(sqrt R) x ceil(sqrt R) grid `spacing` metres apart (4 x 4, 1.5 m for R = 16), stacked
+    robot by robot into one instance: x[B][N+2][12R], u[B][N+1][12R], lam, x0[B][12R],
+    x_ref, u_ref, contact[B][N+1][4R], feet[B][N+1][4R][3].  Robot k of instance b is the
+    config-3 draw number first * R + b * R + k; only the grid offsets of positions, references and
+    footholds are added here (data generation, no method arithmetic)."""
+    R = n_robots
+    one = srbd_problem(B * R, N=N, seed=seed, first=first * R)
+    side = int(math.ceil(math.sqrt(R)))
+    S1, S2 = N + 1, N + 2
+    out = {"params": one["params"], "multi": multi or multi_default_params(R), "N": N}
+    for key, shp in (("x", (S2, 12)), ("u", (S1, 12)), ("lam", (S2, 12)), ("x_ref", (S2, 12)), ("u_ref", (S1, 12))):
+        a = one[key].reshape(B, R, *shp).copy()
+        if key in ("x", "x_ref"):
+            for k in range(R):
+                a[:, k, :, 0] += spacing * (k % side)
+                a[:, k, :, 1] += spacing * (k // side)
+        out[key] = np.ascontiguousarray(np.moveaxis(a, 1, 2).reshape(B, shp[0], 12 * R))
+    x0 = one["x0"].reshape(B, R, 12).copy()
+    feet = one["feet"].reshape(B, R, S1, 4, 3).copy()
+    for k in range(R):
+        x0[:, k, 0] += spacing * (k % side)
+        x0[:, k, 1] += spacing * (k // side)
+        feet[:, k, :, :, 0] += spacing * (k % side)
+        feet[:, k, :, :, 1] += spacing * (k // side)
+    out["x0"] = np.ascontiguousarray(x0.reshape(B, 12 * R))
+    out["feet"] = np.ascontiguousarray(np.moveaxis(feet, 1, 2).reshape(B, S1, 4 * R, 3))
+    out["contact"] = np.ascontiguousarray(np.moveaxis(one["contact"].reshape(B, R, S1, 4), 1, 2).reshape(B, S1, 4 * R))
+    return out
+

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol(P):
     L = C.CDLL(P.LIB_PATH)
     for f in declared_functions():
         assert hasattr(L, f), f
-    assert L.pdilqr_abi_version() == 1
+    assert L.pdilqr_abi_version() == P.pdilqr.ABI_VERSION == 2
 
 
 def test_library_is_sm100a(P):

@@ -242,6 +242,27 @@ pdilqr_status pdilqr_profile(pdilqr_handle h, int32_t enable);
 int32_t pdilqr_profile_read(pdilqr_handle h, int32_t max, const char **names, int32_t *launches,
                             double *total_ms);
 
+/* Horizon sharding of one LQ problem over G ranks (NEXT-2 of SURVEY §8(f); the associative scans
+ * of P:188-271 split at chunk boundaries, Eq. 8 associativity).  Rank r holds stages [s_r, e_r) of
+ * the global horizon as an ordinary LQ handle (n, m <= 16; its N+1 stages, its terminal node = the
+ * global node e_r).  Protocol (paper_2506_07823_b200/horizon.py):
+ *   1. pdilqr_lq_segment_reduce: S_r = e_{s_r} (x) ... (x) e_{e_r - 1} (Eq. 12 elements, full rule
+ *      Eq. 11 as corrected in R1/R2; in-place tree, log2 depth); all-gather S_0..S_{G-1}.
+ *   2. pdilqr_lq_segment_suffix: (P, p) of S_{r+1} (x) ... (x) S_{G-1} (x) (P_term, p_term of the
+ *      global problem) -- the value function at e_r; solve_lq with it as the local terminal.
+ *   3. pdilqr_lq_segment_forward: F_r = (Phi, phi), the chunk's closed-loop map dx_{s_r} -> dx_{e_r}
+ *      (Eq. 15 composition, R6) from the last solve_lq on this handle; all-gather F_0..F_{G-1}.
+ *   4. pdilqr_lq_segment_prefix: dx_{s_r} = F_{r-1} o ... o F_0 (dx0); solve_lq with it as dx0.
+ * Layouts (device, handle dtype, unpadded row-major): summary [B][3 n^2 + 2 n] = (A, C, P, b, p);
+ * forward map [B][n^2 + n] = (Phi, phi); gathered arrays rank-major [G][B][...].  info (reduce) as
+ * pdilqr_solve_lq.  No allocation, no host sync. */
+pdilqr_status pdilqr_lq_segment_reduce(pdilqr_handle h, const pdilqr_lq *qp, void *S_out, int32_t *info, void *stream);
+pdilqr_status pdilqr_lq_segment_suffix(pdilqr_handle h, const void *S_all, int32_t G, int32_t r, const void *P_term,
+                                       const void *p_term, void *P_out, void *p_out, void *stream);
+pdilqr_status pdilqr_lq_segment_forward(pdilqr_handle h, void *F_out, void *stream);
+pdilqr_status pdilqr_lq_segment_prefix(pdilqr_handle h, const void *F_all, int32_t G, int32_t r, const void *dx0,
+                                       void *dxs_out, void *stream);
+
 /* Diagnostic (test infrastructure for the tensor-core products of the large-n fold):
  * C[M][N] = (Cin ? Cin : 0) + op(A)[M x K] op(B)[K x N] in FP32 through the tcgen05 3xTF32 path
  * (one CTA; M, N <= 256), row-major device arrays: op(A) = A (M x K, ld lda) or A^T (A stored K x M)

@@ -22,6 +22,7 @@
 #include "big_ric.cuh"
 #include "adjoint.cuh"
 #include "multi.cuh"
+#include "segment.cuh"
 
 using namespace pdilqr;
 
@@ -393,6 +394,16 @@ pdilqr_status run_multi_linearize(pdilqr_ctx *h, const pdilqr_iterate *it, const
                                   cudaStream_t st);
 template <typename T>
 pdilqr_status run_multi_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, pdilqr_dir *dir, cudaStream_t st);
+// horizon sharding (segment.cuh), n, m <= 16 handles
+template <typename T>
+pdilqr_status run_seg_reduce(pdilqr_ctx *h, const LqArgs<T> &qp, T *S_out, int32_t *info, cudaStream_t st);
+template <typename T>
+pdilqr_status run_seg_suffix(pdilqr_ctx *h, const T *S_all, int G, int r, const T *Pt, const T *pt, T *P_out, T *p_out,
+                             cudaStream_t st);
+template <typename T>
+pdilqr_status run_seg_forward(pdilqr_ctx *h, T *F_out, cudaStream_t st);
+template <typename T>
+pdilqr_status run_seg_prefix(pdilqr_ctx *h, const T *F_all, int G, int r, const T *dx0, T *dxs, cudaStream_t st);
 // co-resident CTAs of the cooperative latency-regime scan kernels (v: Variant)
 template <typename T>
 void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk2);
@@ -777,6 +788,94 @@ pdilqr_status run_adjoint(pdilqr_ctx *h, const LqArgs<T> &qp, const LqOut<T> &so
     return cuda_check("solve_lq_adjoint launch");
 }
 
+// --------------------------------------------------------------------------- horizon sharding
+#define PDILQR_SEG_DISPATCH(...)                                             \
+    switch (h->var) {                                                        \
+        case V12: { constexpr int NX = 12, WS = 16; __VA_ARGS__; } break;    \
+        case V4: { constexpr int NX = 4, WS = 4; __VA_ARGS__; } break;       \
+        case V8: { constexpr int NX = 8, WS = 8; __VA_ARGS__; } break;       \
+        case V16: { constexpr int NX = 16, WS = 16; __VA_ARGS__; } break;    \
+        default: return fail(PDILQR_ERR_UNSUPPORTED, "horizon sharding serves n, m <= 16"); \
+    }
+
+template <typename T>
+pdilqr_status run_seg_reduce(pdilqr_ctx *h, const LqArgs<T> &qp, T *S_out, int32_t *info, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
+    LqWork<T> ws = work<T>(h);
+    cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
+    h->launches = 0;
+    PDILQR_SEG_DISPATCH({
+        constexpr int NU = NX;
+        const bool ex = h->var == V12;
+        const int wpb = 128 / WS;
+        const long nw = (long)B * (N + 2);
+        const size_t smem = (size_t)wpb * (2 * NU * NX + round_up4(NU)) * sizeof(T);
+        {
+            Prof pf(h, "k_elem_init", st);
+            if (ex) {
+                set_smem(k_elem_init<T, NX, NU, true>, smem);
+                k_elem_init<T, NX, NU, true><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
+            } else {
+                set_smem(k_elem_init<T, NX, NU, false>, smem);
+                k_elem_init<T, NX, NU, false><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
+            }
+        }
+        const size_t sm2 = (size_t)(128 / WS) * sizeof(CombineSmem<T, NX>);
+        set_smem(k_seg_reduce<T, NX, WS>, sm2);
+        {
+            Prof pf(h, "k_seg_reduce", st);
+            k_seg_reduce<T, NX, WS><<<B, 128, sm2, st>>>(B, N, n, ws, S_out);
+        }
+    })
+    if (info) k_finalize_info<<<(B + 255) / 256, 256, 0, st>>>(B, ws.fail, ws.nonfin, nullptr, info);
+    h->launches = info ? 3 : 2;
+    return cuda_check("segment reduce launch");
+}
+
+template <typename T>
+pdilqr_status run_seg_suffix(pdilqr_ctx *h, const T *S_all, int G, int r, const T *Pt, const T *pt, T *P_out, T *p_out,
+                             cudaStream_t st) {
+    const int B = h->cfg.batch, n = h->cfg.n;
+    LqWork<T> ws = work<T>(h);
+    PDILQR_SEG_DISPATCH({
+        const int wpb = 128 / WS;
+        const size_t sm = (size_t)wpb * sizeof(CombineSmem<T, NX>);
+        set_smem(k_seg_suffix<T, NX, WS>, sm);
+        Prof pf(h, "k_seg_suffix", st);
+        k_seg_suffix<T, NX, WS><<<(B + wpb - 1) / wpb, 128, sm, st>>>(B, n, S_all, G, r, Pt, pt, P_out, p_out, ws.fail);
+    })
+    h->launches = 1;
+    return cuda_check("segment suffix launch");
+}
+
+template <typename T>
+pdilqr_status run_seg_forward(pdilqr_ctx *h, T *F_out, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n;
+    LqWork<T> ws = work<T>(h);
+    PDILQR_SEG_DISPATCH({
+        const int wpb = 128 / WS;
+        const size_t sm = (size_t)wpb * (NX * NX + NX) * sizeof(T);
+        set_smem(k_seg_forward<T, NX, WS>, sm);
+        Prof pf(h, "k_seg_forward", st);
+        k_seg_forward<T, NX, WS><<<(B + wpb - 1) / wpb, 128, sm, st>>>(B, N, n, ws, F_out);
+    })
+    h->launches = 1;
+    return cuda_check("segment forward launch");
+}
+
+template <typename T>
+pdilqr_status run_seg_prefix(pdilqr_ctx *h, const T *F_all, int G, int r, const T *dx0, T *dxs, cudaStream_t st) {
+    const int B = h->cfg.batch, n = h->cfg.n;
+    PDILQR_SEG_DISPATCH({
+        const int wpb = 128 / WS;
+        Prof pf(h, "k_seg_prefix", st);
+        k_seg_prefix<T, NX, WS><<<(B + wpb - 1) / wpb, 128, 0, st>>>(B, n, F_all, G, r, dx0, dxs);
+    })
+    h->launches = 1;
+    return cuda_check("segment prefix launch");
+}
+#undef PDILQR_SEG_DISPATCH
+
 template <typename T>
 void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk2) {
     auto occ = [&](auto kern, size_t smem, int &out) {
@@ -809,7 +908,12 @@ void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk
     template pdilqr_status run_step<T>(pdilqr_ctx *, pdilqr_iterate *, pdilqr_stats *, pdilqr_dir *, cudaStream_t); \
     template void grid_occupancy<T>(int, int, int &, int &, int &, int &, int &);                               \
     template pdilqr_status run_adjoint<T>(pdilqr_ctx *, const LqArgs<T> &, const LqOut<T> &, const T *, const T *,   \
-                                          const T *, const AdjGrad<T> &, int32_t *, cudaStream_t);
+                                          const T *, const AdjGrad<T> &, int32_t *, cudaStream_t);                   \
+    template pdilqr_status run_seg_reduce<T>(pdilqr_ctx *, const LqArgs<T> &, T *, int32_t *, cudaStream_t);         \
+    template pdilqr_status run_seg_suffix<T>(pdilqr_ctx *, const T *, int, int, const T *, const T *, T *, T *,      \
+                                             cudaStream_t);                                                        \
+    template pdilqr_status run_seg_forward<T>(pdilqr_ctx *, T *, cudaStream_t);                                      \
+    template pdilqr_status run_seg_prefix<T>(pdilqr_ctx *, const T *, int, int, const T *, T *, cudaStream_t);
 #if PDILQR_SMALL(0)
 PDILQR_INST_SMALL(float)
 #endif
@@ -1272,6 +1376,59 @@ pdilqr_status pdilqr_solve_lq_adjoint(pdilqr_handle h, const pdilqr_lq *qp, cons
         return pdq::run_adjoint<T>(h, a, z, gx, gu, gl, gr, info, st);
     };
     return h->cfg.dtype == PDILQR_F32 ? run(0.0f) : run(0.0);
+}
+
+pdilqr_status pdilqr_lq_segment_reduce(pdilqr_handle h, const pdilqr_lq *qp, void *S_out, int32_t *info, void *stream) {
+    if (!h || !qp || !S_out) return fail(PDILQR_ERR_INVALID_ARG, "NULL handle, qp or S_out");
+    if (h->cfg.model != PDILQR_MODEL_LQ) return fail(PDILQR_ERR_UNSUPPORTED, "horizon sharding serves LQ handles");
+    const void *ptrs[] = {qp->A, qp->Bm, qp->c, qp->Q, qp->R, qp->S, qp->q, qp->r, qp->P_term, qp->p_term, qp->dx0};
+    for (const void *p : ptrs)
+        if (!p || !aligned16(p)) return fail(PDILQR_ERR_INVALID_ARG, "NULL or misaligned array in qp");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto run = [&](auto zero) {
+        using T = decltype(zero);
+        LqArgs<T> a{(const T *)qp->A, (const T *)qp->Bm, (const T *)qp->c, (const T *)qp->Q, (const T *)qp->R,
+                    (const T *)qp->S, (const T *)qp->q, (const T *)qp->r, (const T *)qp->P_term, (const T *)qp->p_term,
+                    (const T *)qp->dx0};
+        return pdq::run_seg_reduce<T>(h, a, (T *)S_out, info, st);
+    };
+    return h->cfg.dtype == PDILQR_F32 ? run(0.0f) : run(0.0);
+}
+
+pdilqr_status pdilqr_lq_segment_suffix(pdilqr_handle h, const void *S_all, int32_t G, int32_t r, const void *P_term,
+                                       const void *p_term, void *P_out, void *p_out, void *stream) {
+    if (!h || !S_all || !P_term || !p_term || !P_out || !p_out) return fail(PDILQR_ERR_INVALID_ARG, "NULL argument");
+    if (G < 1 || r < 0 || r >= G) return fail(PDILQR_ERR_INVALID_ARG, "need 0 <= r < G");
+    if (h->cfg.model != PDILQR_MODEL_LQ) return fail(PDILQR_ERR_UNSUPPORTED, "horizon sharding serves LQ handles");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (h->cfg.dtype == PDILQR_F32)
+        return pdq::run_seg_suffix<float>(h, (const float *)S_all, G, r, (const float *)P_term, (const float *)p_term,
+                                          (float *)P_out, (float *)p_out, st);
+    return pdq::run_seg_suffix<double>(h, (const double *)S_all, G, r, (const double *)P_term, (const double *)p_term,
+                                       (double *)P_out, (double *)p_out, st);
+}
+
+pdilqr_status pdilqr_lq_segment_forward(pdilqr_handle h, void *F_out, void *stream) {
+    if (!h || !F_out) return fail(PDILQR_ERR_INVALID_ARG, "NULL handle or F_out");
+    if (h->cfg.model != PDILQR_MODEL_LQ) return fail(PDILQR_ERR_UNSUPPORTED, "horizon sharding serves LQ handles");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    return h->cfg.dtype == PDILQR_F32 ? pdq::run_seg_forward<float>(h, (float *)F_out, st)
+                                      : pdq::run_seg_forward<double>(h, (double *)F_out, st);
+}
+
+pdilqr_status pdilqr_lq_segment_prefix(pdilqr_handle h, const void *F_all, int32_t G, int32_t r, const void *dx0,
+                                       void *dxs_out, void *stream) {
+    if (!h || !F_all || !dx0 || !dxs_out) return fail(PDILQR_ERR_INVALID_ARG, "NULL argument");
+    if (G < 1 || r < 0 || r >= G) return fail(PDILQR_ERR_INVALID_ARG, "need 0 <= r < G");
+    if (h->cfg.model != PDILQR_MODEL_LQ) return fail(PDILQR_ERR_UNSUPPORTED, "horizon sharding serves LQ handles");
+    DeviceGuard g(h->device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (h->cfg.dtype == PDILQR_F32)
+        return pdq::run_seg_prefix<float>(h, (const float *)F_all, G, r, (const float *)dx0, (float *)dxs_out, st);
+    return pdq::run_seg_prefix<double>(h, (const double *)F_all, G, r, (const double *)dx0, (double *)dxs_out, st);
 }
 
 pdilqr_status pdilqr_debug_tc_gemm(int32_t M, int32_t N, int32_t K, int32_t trans_a, int32_t trans_b, const float *A,

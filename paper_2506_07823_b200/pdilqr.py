@@ -26,7 +26,9 @@ STATUS = {0: "PDILQR_OK", 1: "PDILQR_ERR_INVALID_ARG", 2: "PDILQR_ERR_DIM", 3: "
 EXPORTED = ("pdilqr_workspace_bytes", "pdilqr_create", "pdilqr_destroy", "pdilqr_solve_lq",
             "pdilqr_linearize", "pdilqr_step", "pdilqr_tick_host", "pdilqr_last_launch_count",
             "pdilqr_last_error", "pdilqr_abi_version", "pdilqr_profile", "pdilqr_profile_read",
-            "pdilqr_shift", "pdilqr_srbd_plant", "pdilqr_solve", "pdilqr_solve_lq_adjoint", "pdilqr_debug_tc_gemm")
+            "pdilqr_shift", "pdilqr_srbd_plant", "pdilqr_solve", "pdilqr_solve_lq_adjoint", "pdilqr_debug_tc_gemm",
+            "pdilqr_lq_segment_reduce", "pdilqr_lq_segment_suffix", "pdilqr_lq_segment_forward",
+            "pdilqr_lq_segment_prefix")
 
 
 class SrbdParams(C.Structure):
@@ -83,6 +85,13 @@ def lib():
         L.pdilqr_solve_lq_adjoint.restype = st
         L.pdilqr_debug_tc_gemm.argtypes = [i32, i32, i32, i32, i32, vp, i32, vp, i32, vp, vp, vp]
         L.pdilqr_debug_tc_gemm.restype = st
+        L.pdilqr_lq_segment_reduce.argtypes = [vp, C.POINTER(Lq), vp, vp, vp]
+        L.pdilqr_lq_segment_suffix.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp]
+        L.pdilqr_lq_segment_forward.argtypes = [vp, vp, vp]
+        L.pdilqr_lq_segment_prefix.argtypes = [vp, vp, i32, i32, vp, vp, vp]
+        for f in ("pdilqr_lq_segment_reduce", "pdilqr_lq_segment_suffix", "pdilqr_lq_segment_forward",
+                  "pdilqr_lq_segment_prefix"):
+            getattr(L, f).restype = st
         L.pdilqr_linearize.argtypes = [vp, C.POINTER(Iterate), C.POINTER(Lq), vp, vp]
         L.pdilqr_step.argtypes = [vp, C.POINTER(Iterate), C.POINTER(Stats), C.POINTER(Dir), vp]
         L.pdilqr_tick_host.argtypes = [vp, C.POINTER(Iterate), vp, vp, vp, vp, vp, vp, vp, vp]
@@ -289,6 +298,46 @@ class PdIlqr:
                                              self._stream(stream)))
         grad["info"] = info
         return grad
+
+    # ---------------------------------------------------------- horizon sharding (NEXT-2)
+    def segment_reduce(self, qp: dict, out=None, info=None, stream=None):
+        """pdilqr_lq_segment_reduce: chunk summary S = e_0 (x) ... (x) e_N, [B][3 n^2 + 2 n]."""
+        for k, shp in self.lq_shapes().items():
+            self._check_t(qp[k], shp)
+        B, n = self.batch, self.n
+        out = self._check_t(out, (B, 3 * n * n + 2 * n)) if out is not None else \
+            torch.empty(B, 3 * n * n + 2 * n, dtype=self.dtype, device=self.device)
+        lq = Lq(**{k: _ptr(qp[k]) for k in self.lq_shapes()})
+        _check(lib().pdilqr_lq_segment_reduce(self._h, C.byref(lq), _ptr(out), _ptr(info), self._stream(stream)))
+        return out
+
+    def segment_suffix(self, S_all, r: int, P_term, p_term, stream=None):
+        """pdilqr_lq_segment_suffix: (P, p) of S_{r+1} (x) ... (x) S_{G-1} (x) (P_term, p_term)."""
+        B, n = self.batch, self.n
+        G = S_all.shape[0]
+        self._check_t(S_all, (G, B, 3 * n * n + 2 * n)); self._check_t(P_term, (B, n, n)); self._check_t(p_term, (B, n))
+        P = torch.empty(B, n, n, dtype=self.dtype, device=self.device)
+        p = torch.empty(B, n, dtype=self.dtype, device=self.device)
+        _check(lib().pdilqr_lq_segment_suffix(self._h, _ptr(S_all), G, int(r), _ptr(P_term), _ptr(p_term), _ptr(P),
+                                              _ptr(p), self._stream(stream)))
+        return P, p
+
+    def segment_forward(self, stream=None):
+        """pdilqr_lq_segment_forward: closed-loop map (Phi, phi) of the last solve_lq, [B][n^2 + n]."""
+        B, n = self.batch, self.n
+        F = torch.empty(B, n * n + n, dtype=self.dtype, device=self.device)
+        _check(lib().pdilqr_lq_segment_forward(self._h, _ptr(F), self._stream(stream)))
+        return F
+
+    def segment_prefix(self, F_all, r: int, dx0, stream=None):
+        """pdilqr_lq_segment_prefix: dx at this rank's first node from the gathered maps and dx0."""
+        B, n = self.batch, self.n
+        G = F_all.shape[0]
+        self._check_t(F_all, (G, B, n * n + n)); self._check_t(dx0, (B, n))
+        dxs = torch.empty(B, n, dtype=self.dtype, device=self.device)
+        _check(lib().pdilqr_lq_segment_prefix(self._h, _ptr(F_all), G, int(r), _ptr(dx0), _ptr(dxs),
+                                              self._stream(stream)))
+        return dxs
 
     def _iterate(self, it: dict) -> Iterate:
         B, N, R = self.batch, self.N, self.n_robots

@@ -251,7 +251,8 @@ int32_t pdilqr_profile_read(pdilqr_handle h, int32_t max, const char **names, in
  *   2. pdilqr_lq_segment_suffix: (P, p) of S_{r+1} (x) ... (x) S_{G-1} (x) (P_term, p_term of the
  *      global problem) -- the value function at e_r; solve_lq with it as the local terminal.
  *   3. pdilqr_lq_segment_forward: F_r = (Phi, phi), the chunk's closed-loop map dx_{s_r} -> dx_{e_r}
- *      (Eq. 15 composition, R6) from the last solve_lq on this handle; all-gather F_0..F_{G-1}.
+ *      (Eq. 15 composition, R6) of Abar = A + B K, bbar = B k + c with the policy of the last
+ *      solve_lq on this handle and the same qp (A, Bm, c read); all-gather F_0..F_{G-1}.
  *   4. pdilqr_lq_segment_prefix: dx_{s_r} = F_{r-1} o ... o F_0 (dx0); solve_lq with it as dx0.
  * Layouts (device, handle dtype, unpadded row-major): summary [B][3 n^2 + 2 n] = (A, C, P, b, p);
  * forward map [B][n^2 + n] = (Phi, phi); gathered arrays rank-major [G][B][...].  info (reduce) as
@@ -259,7 +260,7 @@ int32_t pdilqr_profile_read(pdilqr_handle h, int32_t max, const char **names, in
 pdilqr_status pdilqr_lq_segment_reduce(pdilqr_handle h, const pdilqr_lq *qp, void *S_out, int32_t *info, void *stream);
 pdilqr_status pdilqr_lq_segment_suffix(pdilqr_handle h, const void *S_all, int32_t G, int32_t r, const void *P_term,
                                        const void *p_term, void *P_out, void *p_out, void *stream);
-pdilqr_status pdilqr_lq_segment_forward(pdilqr_handle h, void *F_out, void *stream);
+pdilqr_status pdilqr_lq_segment_forward(pdilqr_handle h, const pdilqr_lq *qp, void *F_out, void *stream);
 pdilqr_status pdilqr_lq_segment_prefix(pdilqr_handle h, const void *F_all, int32_t G, int32_t r, const void *dx0,
                                        void *dxs_out, void *stream);
 

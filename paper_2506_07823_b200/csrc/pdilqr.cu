@@ -401,7 +401,7 @@ template <typename T>
 pdilqr_status run_seg_suffix(pdilqr_ctx *h, const T *S_all, int G, int r, const T *Pt, const T *pt, T *P_out, T *p_out,
                              cudaStream_t st);
 template <typename T>
-pdilqr_status run_seg_forward(pdilqr_ctx *h, T *F_out, cudaStream_t st);
+pdilqr_status run_seg_forward(pdilqr_ctx *h, const LqArgs<T> &qp, T *F_out, cudaStream_t st);
 template <typename T>
 pdilqr_status run_seg_prefix(pdilqr_ctx *h, const T *F_all, int G, int r, const T *dx0, T *dxs, cudaStream_t st);
 // co-resident CTAs of the cooperative latency-regime scan kernels (v: Variant)
@@ -849,15 +849,15 @@ pdilqr_status run_seg_suffix(pdilqr_ctx *h, const T *S_all, int G, int r, const 
 }
 
 template <typename T>
-pdilqr_status run_seg_forward(pdilqr_ctx *h, T *F_out, cudaStream_t st) {
-    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n;
+pdilqr_status run_seg_forward(pdilqr_ctx *h, const LqArgs<T> &qp, T *F_out, cudaStream_t st) {
+    const int B = h->cfg.batch, N = h->cfg.N, n = h->cfg.n, m = h->cfg.m;
     LqWork<T> ws = work<T>(h);
     PDILQR_SEG_DISPATCH({
         const int wpb = 128 / WS;
         const size_t sm = (size_t)wpb * (NX * NX + NX) * sizeof(T);
         set_smem(k_seg_forward<T, NX, WS>, sm);
         Prof pf(h, "k_seg_forward", st);
-        k_seg_forward<T, NX, WS><<<(B + wpb - 1) / wpb, 128, sm, st>>>(B, N, n, ws, F_out);
+        k_seg_forward<T, NX, WS><<<(B + wpb - 1) / wpb, 128, sm, st>>>(B, N, n, m, qp, ws, F_out);
     })
     h->launches = 1;
     return cuda_check("segment forward launch");
@@ -912,7 +912,7 @@ void grid_occupancy(int v, int sms, int &nb, int &nf, int &nk, int &nfk, int &nk
     template pdilqr_status run_seg_reduce<T>(pdilqr_ctx *, const LqArgs<T> &, T *, int32_t *, cudaStream_t);         \
     template pdilqr_status run_seg_suffix<T>(pdilqr_ctx *, const T *, int, int, const T *, const T *, T *, T *,      \
                                              cudaStream_t);                                                        \
-    template pdilqr_status run_seg_forward<T>(pdilqr_ctx *, T *, cudaStream_t);                                      \
+    template pdilqr_status run_seg_forward<T>(pdilqr_ctx *, const LqArgs<T> &, T *, cudaStream_t);                                      \
     template pdilqr_status run_seg_prefix<T>(pdilqr_ctx *, const T *, int, int, const T *, T *, cudaStream_t);
 #if PDILQR_SMALL(0)
 PDILQR_INST_SMALL(float)
@@ -1410,13 +1410,18 @@ pdilqr_status pdilqr_lq_segment_suffix(pdilqr_handle h, const void *S_all, int32
                                        (double *)P_out, (double *)p_out, st);
 }
 
-pdilqr_status pdilqr_lq_segment_forward(pdilqr_handle h, void *F_out, void *stream) {
-    if (!h || !F_out) return fail(PDILQR_ERR_INVALID_ARG, "NULL handle or F_out");
+pdilqr_status pdilqr_lq_segment_forward(pdilqr_handle h, const pdilqr_lq *qp, void *F_out, void *stream) {
+    if (!h || !qp || !F_out || !qp->A || !qp->Bm || !qp->c) return fail(PDILQR_ERR_INVALID_ARG, "NULL argument");
     if (h->cfg.model != PDILQR_MODEL_LQ) return fail(PDILQR_ERR_UNSUPPORTED, "horizon sharding serves LQ handles");
     DeviceGuard g(h->device);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    return h->cfg.dtype == PDILQR_F32 ? pdq::run_seg_forward<float>(h, (float *)F_out, st)
-                                      : pdq::run_seg_forward<double>(h, (double *)F_out, st);
+    auto run = [&](auto zero) {
+        using T = decltype(zero);
+        LqArgs<T> a{(const T *)qp->A, (const T *)qp->Bm, (const T *)qp->c, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, nullptr};
+        return pdq::run_seg_forward<T>(h, a, (T *)F_out, st);
+    };
+    return h->cfg.dtype == PDILQR_F32 ? run(0.0f) : run(0.0);
 }
 
 pdilqr_status pdilqr_lq_segment_prefix(pdilqr_handle h, const void *F_all, int32_t G, int32_t r, const void *dx0,

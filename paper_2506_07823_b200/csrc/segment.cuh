@@ -10,7 +10,7 @@
 //   k_seg_reduce   S = e_0 (x) ... (x) e_N of every instance: in-place tree reduction of the
 //                  element array (one CTA per instance, one worker per combine, log2 depth)
 //   k_seg_suffix   (P, p) of S_{r+1} (x) ... (x) S_{G-1} (x) (P_term, p_term) (cheap rule, right to left)
-//   k_seg_forward  (Phi, phi) = composition of (Abar_i, bbar_i), i = 0..N, of the last solve
+//   k_seg_forward  (Phi, phi) = composition of (Abar_i, bbar_i) = (A + B K, B k + c), i = 0..N, of the last solve
 //   k_seg_prefix   dx_s = F_{r-1} o ... o F_0 (dx0)
 // User layouts (unpadded, row-major, per instance): summary [A (n x n), C (n x n), P (n x n), b (n),
 // p (n)] = 3 n^2 + 2 n values; forward map [Phi (n x n), phi (n)] = n^2 + n values.
@@ -128,11 +128,13 @@ __global__ void __launch_bounds__(128) k_seg_suffix(int B, int n, const T *S_all
     if (!okall && lane == 0) atomicMin(fail + b, (1 << 24) | 1);
 }
 
-// One worker per instance: (Phi, phi) <- (Abar_i Phi, Abar_i phi + bbar_i), i = 0..N, from the
-// closed-loop elements of the last solve (ws.tel).  F_out: [B][n^2 + n].
+// One worker per instance: (Phi, phi) <- (Abar_i Phi, Abar_i phi + bbar_i), i = 0..N, with the
+// closed-loop elements Abar_i = A_i + B_i K_i, bbar_i = B_i k_i + c_i (Eq. 14) formed from the user's
+// A, B, c and the policy K_i, k_i of the last solve (ws.Kk; the forward scans reuse ws.tel as scan
+// storage, so it does not hold Abar after a solve).  F_out: [B][n^2 + n].
 template <typename T, int NX, int WS>
-__global__ void __launch_bounds__(128) k_seg_forward(int B, int N, int n, LqWork<T> ws, T *F_out) {
-    using TL = TE<NX>;
+__global__ void __launch_bounds__(128) k_seg_forward(int B, int N, int n, int m, LqArgs<T> qp, LqWork<T> ws, T *F_out) {
+    using KL = KE<NX, NX>;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int wk = threadIdx.x / WS;
     T *Ph = reinterpret_cast<T *>(smraw) + (size_t)wk * (NX * NX + NX);
@@ -141,20 +143,30 @@ __global__ void __launch_bounds__(128) k_seg_forward(int B, int N, int n, LqWork
     const unsigned mask = worker_mask<WS>();
     const int b = blockIdx.x * (blockDim.x / WS) + wk;
     if (b >= B) return;
-    const int r = lane < NX ? lane : 0;
+    const int r = lane < n ? lane : 0;
     for (int t = lane; t < NX * NX; t += WS) Ph[t] = (t / NX == t % NX) ? T(1) : T(0);
     for (int t = lane; t < NX; t += WS) ph[t] = T(0);
     __syncwarp(mask);
     for (int i = 0; i <= N; ++i) {
-        const T *Te = ws.tel + ((size_t)b * (N + 1) + i) * TL::SIZE;
+        const size_t st = (size_t)b * (N + 1) + i;
+        const T *A = qp.A + st * n * n, *Bm = qp.Bm + st * n * m, *c = qp.c + st * n;
+        const T *Kw = ws.Kk + st * KL::SIZE;
         T arow[NX];
-        ld_row<T, NX, true>(arow, Te + TL::A + r * NX);
+#pragma unroll
+        for (int t = 0; t < NX; ++t) arow[t] = t < n ? A[(size_t)r * n + t] : T(0);
+        T bb = c[r];
+        for (int j = 0; j < m; ++j) {
+            const T bj = Bm[(size_t)r * m + j];
+#pragma unroll
+            for (int t = 0; t < NX; ++t) arow[t] = fma(bj, Kw[KL::K + j * NX + t], arow[t]);
+            bb = fma(bj, Kw[KL::k + j], bb);
+        }
         T nrow[NX];
         zero(nrow);
         row_mat<T, NX, NX, NX>(nrow, arow, Ph);
-        const T nph = row_dot<T, NX>(arow, ph, Te[TL::b + r]);
+        const T nph = row_dot<T, NX>(arow, ph, bb);
         __syncwarp(mask);
-        if (lane < NX) {
+        if (lane < n) {
             st_row<T, NX, true>(Ph + r * NX, nrow);
             ph[r] = nph;
         }

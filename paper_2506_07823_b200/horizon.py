@@ -44,9 +44,9 @@ def dist_all_gather(dist, device=None):
     def gather(t):
         world = dist.get_world_size()
         src = t if device is None else t.to(device)
-        out = torch.empty((world,) + tuple(src.shape), dtype=src.dtype, device=src.device)
+        out = torch.empty((world * src.shape[0],) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
         dist.all_gather_into_tensor(out, src.contiguous())
-        return out.to(t.device)
+        return out.view((world,) + tuple(src.shape)).to(t.device)
     return gather
 
 
@@ -56,7 +56,7 @@ def solve_lq_sharded(h, qp_local: dict, P_term, p_term, dx0, rank: int, world: i
     Pe, pe = h.segment_suffix(S_all, rank, P_term, p_term)
     qp = dict(qp_local, P_term=Pe, p_term=pe, dx0=torch.zeros_like(dx0))
     out = h.solve_lq(qp)
-    F = h.segment_forward()
+    F = h.segment_forward(qp)
     F_all = all_gather(F)
     qp["dx0"] = h.segment_prefix(F_all, rank, dx0)
     return h.solve_lq(qp, out=out)

@@ -87,7 +87,7 @@ def lib():
         L.pdilqr_debug_tc_gemm.restype = st
         L.pdilqr_lq_segment_reduce.argtypes = [vp, C.POINTER(Lq), vp, vp, vp]
         L.pdilqr_lq_segment_suffix.argtypes = [vp, vp, i32, i32, vp, vp, vp, vp, vp]
-        L.pdilqr_lq_segment_forward.argtypes = [vp, vp, vp]
+        L.pdilqr_lq_segment_forward.argtypes = [vp, C.POINTER(Lq), vp, vp]
         L.pdilqr_lq_segment_prefix.argtypes = [vp, vp, i32, i32, vp, vp, vp]
         for f in ("pdilqr_lq_segment_reduce", "pdilqr_lq_segment_suffix", "pdilqr_lq_segment_forward",
                   "pdilqr_lq_segment_prefix"):
@@ -322,11 +322,15 @@ class PdIlqr:
                                               _ptr(p), self._stream(stream)))
         return P, p
 
-    def segment_forward(self, stream=None):
-        """pdilqr_lq_segment_forward: closed-loop map (Phi, phi) of the last solve_lq, [B][n^2 + n]."""
+    def segment_forward(self, qp: dict, stream=None):
+        """pdilqr_lq_segment_forward: closed-loop map (Phi, phi) of the last solve_lq on qp, [B][n^2 + n]."""
         B, n = self.batch, self.n
+        shapes = self.lq_shapes()
+        for k in ("A", "Bm", "c"):
+            self._check_t(qp[k], shapes[k])
         F = torch.empty(B, n * n + n, dtype=self.dtype, device=self.device)
-        _check(lib().pdilqr_lq_segment_forward(self._h, _ptr(F), self._stream(stream)))
+        lq = Lq(**{k: _ptr(qp.get(k)) for k in shapes})
+        _check(lib().pdilqr_lq_segment_forward(self._h, C.byref(lq), _ptr(F), self._stream(stream)))
         return F
 
     def segment_prefix(self, F_all, r: int, dx0, stream=None):

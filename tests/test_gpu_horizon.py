@@ -46,7 +46,7 @@ def simulate(P, qp, G, dtype, leaf_chunk=0):
         Pe, pe = h.segment_suffix(S_all, r, qpt["P_term"], qpt["p_term"])
         l.update(P_term=Pe, p_term=pe, dx0=torch.zeros_like(qpt["dx0"]))
         outs.append(h.solve_lq(l))
-        F.append(h.segment_forward())
+        F.append(h.segment_forward(l))
     F_all = torch.stack(F)
     for r, (h, l) in enumerate(zip(hs, locs)):
         l["dx0"] = h.segment_prefix(F_all, r, qpt["dx0"])

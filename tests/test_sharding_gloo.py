@@ -62,3 +62,34 @@ def test_rank_slices_regenerate_bitwise():
     part = synth.srbd_problem(2, N=5, seed=7, first=3)
     for k in ("x", "u", "x0", "x_ref", "feet", "contact"):
         assert np.array_equal(full[k][3:5], part[k])
+
+
+def test_horizon_split_covers_stages():
+    from paper_2506_07823_b200 import horizon
+    for N in (0, 1, 7, 50, 1000):
+        for G in (1, 2, 3, 8):
+            ch = horizon.split_stages(N, G)
+            assert ch[0][0] == 0 and ch[-1][1] == N + 1
+            assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
+            sizes = [e - s for s, e in ch]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _gather_worker(rank, port, out_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    from paper_2506_07823_b200 import horizon
+    g = horizon.dist_all_gather(dist)(torch.full((3, 5), float(rank)))
+    if rank == 0:
+        np.save(out_path, g.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_horizon_all_gather_gloo(tmp_path):
+    """The collective of the horizon-sharded solve (horizon.dist_all_gather): rank-major stacking."""
+    out = str(tmp_path / "g.npy")
+    mp.spawn(_gather_worker, args=(_free_port(), out), nprocs=WORLD, join=True)
+    g = np.load(out)
+    assert g.shape == (WORLD, 3, 5) and (g[0] == 0).all() and (g[1] == 1).all()

@@ -338,6 +338,15 @@ __global__ void __launch_bounds__(128) k_elem_init(LqArgs<T> qp, int B, int N, i
     if (lane < NX) { e[L::b + r] = bt; e[L::p + r] = pt; }
 }
 
+// Negative control of the parity tests (PDILQR_FAULT_COMBINE=1, never set in
+// production): perturb P~[0][0] of the element of stage floor(N/2) of instance 0 by 1e-3 (1 + |P~00|),
+// so every combine that consumes it is wrong; the parity tests must then fail for instance 0.
+template <typename T, int NX>
+__global__ void k_fault_inject(LqWork<T> ws, int N) {
+    T *e = ws.elems + (size_t)(N / 2) * VE<NX>::SIZE + VE<NX>::P;
+    e[0] += T(1e-3) * (T(1) + fabs(e[0]));
+}
+
 // -------------------------------------------------------------------- backward scan (Eq. 8-11)
 // One CTA per instance, W workers.  L = N+2 elements are cut into J = ceil(L / chunk) chunks.
 //  phase 1: every chunk j < J-1 is reduced right-to-left into its summary S_j by the full rule;

@@ -114,6 +114,7 @@ struct pdilqr_ctx {
     int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
+    bool fault_combine = false;    // PDILQR_FAULT_COMBINE=1: negative control of the parity tests
     bool big_tc = false;           // large path, f32: tcgen05 3xTF32 products in k_big_ric (PDILQR_BIG_TC=1);
                                    // off by default: measured slower than the SIMT tiles (K7)
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
@@ -430,6 +431,10 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
         Prof pf(h, "k_elem_init", st);
         k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
         ++launches;
+        if (h->fault_combine) {  // negative control (tests only): corrupt one element of instance 0
+            k_fault_inject<T, NX><<<1, 1, 0, st>>>(ws, N);
+            ++launches;
+        }
     }
     bool bwd_done = false;
     if constexpr (WSX == 16) {
@@ -1243,6 +1248,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_OCC_LS")) h->occ_ls = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_TPB")) h->fold_tpb = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FUSED")) h->fused = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_FAULT_COMBINE")) h->fault_combine = std::atoi(e) != 0;
     if (v == VBIG) {  // large path: cluster size of k_big_ric (CTAs per instance) so that B * CS fills the SMs
         if (const char *e = std::getenv("PDILQR_BIG_LEGACY")) h->big_legacy = std::atoi(e) != 0;
         DeviceGuard g(device);

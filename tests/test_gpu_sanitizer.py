@@ -1,4 +1,4 @@
-"""compute-sanitizer memcheck / racecheck / synccheck over small runs of every kernel family
+"""compute-sanitizer memcheck / racecheck / synccheck / initcheck over small runs of every kernel family
 (fused fold path, cooperative grid scans, single-CTA scans, padded and large-dimension paths)."""
 import os
 import shutil
@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
 def test_sanitizer_clean(tool):
     import torch
     if not torch.cuda.is_available():

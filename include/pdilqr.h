@@ -138,7 +138,8 @@ typedef struct {
 pdilqr_status pdilqr_workspace_bytes(const pdilqr_config *cfg, size_t *bytes);
 
 /* Validate cfg, bind the caller-owned device workspace (>= pdilqr_workspace_bytes, 256-byte
- * aligned) and create a handle on CUDA device `device`. */
+ * aligned) and create a handle on CUDA device `device`.  The workspace is zero-filled once here
+ * (synchronous; setup only). */
 pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspace, size_t bytes,
                             pdilqr_handle *out);
 

@@ -1228,6 +1228,14 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     h->Jb = Jb; h->Pv = Pv; h->Jf = Jf; h->Pf = Pf;
     h->ws = static_cast<char *>(workspace);
     h->ws_bytes = bytes;
+    {   // defined contents once: padded lanes and unused tree slots are then never uninitialised reads
+        // (compute-sanitizer initcheck); setup only, not on the hot path
+        DeviceGuard g0(device);
+        if (cudaMemset(workspace, 0, L.total) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) {
+            delete h;
+            return fail(PDILQR_ERR_CUDA, "workspace initialisation failed: %s", cudaGetErrorString(cudaGetLastError()));
+        }
+    }
     h->lay = L;
     h->launches = 0;
     SrbdConst &K = h->K;

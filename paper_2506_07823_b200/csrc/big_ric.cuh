@@ -583,44 +583,50 @@ __global__ void __launch_bounds__(256) k_big_roll(const T *dx0, int B, int N, Bi
     }
 }
 
-// du_i = K_i dx_i + k_i (Eq. 6, i <= N) and dlam_i = P_i dx_i + p_i (Eq. 7, i <= N+1), parallel over
-// (instance, stage) items (persistent CTAs), after the recursion.
+// du_i = K_i dx_i + k_i (Eq. 6, i <= N) and dlam_i = P_i dx_i + p_i (Eq. 7, i <= N+1), after the
+// recursion.  HBM-bound: it streams every P_i and K_i once (algorithmic bytes (n + m) LD per stage).
+// One block of 128 threads per (instance, stage) item, dx_i staged in shared memory, one thread per
+// output row: the row is read with independent 16-byte L2-only loads (rows are 16-byte aligned, LD a
+// multiple of 4), so every thread keeps ceil(n / 4) loads in flight and every fetched sector is used.
 template <typename T>
-__global__ void __launch_bounds__(256) k_big_tail(int B, int N, BigDims<T> d, BigWork<T> ws, LqOut<T> out) {
-    __shared__ T xs[256];
-    const int n = d.n, m = d.m, LD = d.LD, lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (long item = blockIdx.x; item < (long)B * (N + 2); item += gridDim.x) {
-        const int b = (int)(item / (N + 2)), i = (int)(item % (N + 2));
-        for (int t = threadIdx.x; t < n; t += blockDim.x) xs[t] = ldg_cg(ws.dxw + ((size_t)b * (N + 2) + i) * LD + t);
-        __syncthreads();
-        const T *Pi = ws.Pp + ((size_t)b * (N + 2) + i) * d.psize();
-        const int rows_l = n, ngl = (n + 7) / 8, ngu = i <= N ? (m + 7) / 8 : 0;
-        for (int gi = wid; gi < ngl + ngu; gi += nw) {
-            // row groups [0, ngl): dlam rows 8 gi..; [ngl, ngl + ngu): du rows 8 (gi - ngl)..
-            T s[8];
-            const int r0 = gi < ngl ? 8 * gi : rows_l + 8 * (gi - ngl);
-            if (gi < ngl) {
-                warp_gemv8<T>(rows_l, n, Pi, LD, xs, r0, s);
-                if (lane < 8 && r0 + lane < rows_l) {
-                    T v = s[0];
-#pragma unroll
-                    for (int q = 1; q < 8; ++q) v = lane == q ? s[q] : v;
-                    out.dlam[((size_t)b * (N + 2) + i) * n + r0 + lane] = v + Pi[(size_t)n * LD + r0 + lane];
-                }
+__global__ void __launch_bounds__(128) k_big_tail(int B, int N, BigDims<T> d, BigWork<T> ws, LqOut<T> out) {
+    __shared__ __align__(16) T xs[256];
+    const int n = d.n, m = d.m, LD = d.LD;
+    const long item = blockIdx.x;
+    const int b = (int)(item / (N + 2)), i = (int)(item % (N + 2));
+    if (b >= B) return;
+    for (int t = threadIdx.x; t < LD; t += blockDim.x)
+        xs[t] = t < n ? ldg_cg(ws.dxw + ((size_t)b * (N + 2) + i) * LD + t) : T(0);
+    __syncthreads();
+    const T *Pi = ws.Pp + ((size_t)b * (N + 2) + i) * d.psize();
+    const size_t st = (size_t)b * (N + 1) + (i <= N ? i : 0);
+    const T *Kw = ws.Kk + st * d.ksize();
+    const int rows = n + (i <= N ? m : 0);
+    constexpr int V = 16 / (int)sizeof(T);
+    for (int r = threadIdx.x; r < rows; r += blockDim.x) {
+        const bool isP = r < n;
+        const T *row = isP ? Pi + (size_t)r * LD : Kw + (size_t)(r - n) * LD;
+        T acc0 = T(0), acc1 = T(0);
+        int k = 0;
+        for (; k + 2 * V <= LD; k += 2 * V) {
+            if constexpr (sizeof(T) == 4) {
+                const float4 a = __ldcg(reinterpret_cast<const float4 *>(row + k));
+                const float4 c = __ldcg(reinterpret_cast<const float4 *>(row + k + 4));
+                acc0 = fma(a.x, xs[k], acc0); acc1 = fma(a.y, xs[k + 1], acc1);
+                acc0 = fma(a.z, xs[k + 2], acc0); acc1 = fma(a.w, xs[k + 3], acc1);
+                acc0 = fma(c.x, xs[k + 4], acc0); acc1 = fma(c.y, xs[k + 5], acc1);
+                acc0 = fma(c.z, xs[k + 6], acc0); acc1 = fma(c.w, xs[k + 7], acc1);
             } else {
-                const size_t st = (size_t)b * (N + 1) + i;
-                const T *Kw = ws.Kk + st * d.ksize();
-                const int u0 = r0 - rows_l;
-                warp_gemv8<T>(m, n, Kw, LD, xs, u0, s);
-                if (lane < 8 && u0 + lane < m) {
-                    T v = s[0];
-#pragma unroll
-                    for (int q = 1; q < 8; ++q) v = lane == q ? s[q] : v;
-                    out.du[st * m + u0 + lane] = v + Kw[(size_t)m * LD + u0 + lane];
-                }
+                const double2 a = __ldcg(reinterpret_cast<const double2 *>(row + k));
+                const double2 c = __ldcg(reinterpret_cast<const double2 *>(row + k + 2));
+                acc0 = fma(a.x, xs[k], acc0); acc1 = fma(a.y, xs[k + 1], acc1);
+                acc0 = fma(c.x, xs[k + 2], acc0); acc1 = fma(c.y, xs[k + 3], acc1);
             }
         }
-        __syncthreads();
+        for (; k < LD; ++k) acc0 = fma(ldg_cg(row + k), xs[k], acc0);   // padding columns hold zeros in xs
+        const T v = acc0 + acc1;
+        if (isP) out.dlam[((size_t)b * (N + 2) + i) * n + r] = v + Pi[(size_t)n * LD + r];
+        else out.du[st * m + (r - n)] = v + Kw[(size_t)m * LD + (r - n)];
     }
 }
 

@@ -997,9 +997,8 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
             k_big_roll<T><<<B, 256, 0, st>>>(qp.dx0, B, N, d, ws, out.dx);
         }
         {
-            const int g = (int)std::min<long>((long)148 * 8, (long)B * (N + 2));
             Prof pf(h, "k_big_tail", st);
-            k_big_tail<T><<<g, 256, 0, st>>>(B, N, d, ws, out);
+            k_big_tail<T><<<(unsigned)((long)B * (N + 2)), 128, 0, st>>>(B, N, d, ws, out);
         }
         int launches = 4;
         if (info) {

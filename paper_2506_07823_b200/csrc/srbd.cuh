@@ -85,6 +85,11 @@ __device__ __forceinline__ void foot_con(int c, T mu, T fmin, T fmax, T &gx, T &
     h = (c == 4) ? -fmin : (c == 5) ? fmax : T(0);
 }
 
+// sin / cos of the Euler angles in the linearisation: fp32 uses the SFU approximation (absolute
+// error ~2^-21, below the fp32 rounding of the Jacobian entries it feeds); fp64 stays accurate.
+__device__ __forceinline__ void lin_sincos(float x, float *s, float *c) { __sincosf(x, s, c); }
+__device__ __forceinline__ void lin_sincos(double x, double *s, double *c) { sincos(x, s, c); }
+
 // Continuous dynamics f(x,u) for one component index r (all lanes may call with their own r).
 // Shared trig / rotation terms are recomputed per call (cheap, no smem traffic).
 template <typename T>
@@ -95,9 +100,9 @@ struct SrbdEval {
     T F[3];      // sum_j c_j f_j
 
     __device__ __forceinline__ void init(const SrbdConst &K, const T *x, const T *u, const T *feet, const uint8_t *con) {
-        sincos(x[3], &sr, &cr);
-        sincos(x[4], &sp, &cp);
-        sincos(x[5], &sy, &cy);
+        lin_sincos(x[3], &sr, &cr);
+        lin_sincos(x[4], &sp, &cp);
+        lin_sincos(x[5], &sy, &cy);
         icp = rcp_rn(cp);
         tp = sp * icp;
         R[0] = cy * cp; R[1] = cy * sp * sr - sy * cr; R[2] = cy * sp * cr + sy * sr;

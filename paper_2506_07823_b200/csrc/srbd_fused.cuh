@@ -354,16 +354,24 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
             const double ald = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
             const F al = (F)ald;
             double J = c0 + ald * (c1 + ald * c2);
+            // relaxed barriers: the logarithmic branches of a foot's six constraints
+            // share one logarithm, sum_c -mu log xi_c = -mu log prod_c xi_c (xi_c >= delta > 0;
+            // the product of six forces <= f_max stays far inside the fp32 range), the quadratic
+            // branches are added one by one; one MUFU.LG2 per stance foot instead of six
             F Jb = F(0.);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (!((cmask >> j) & 1)) continue;
+                F prod = F(1.), quad = F(0.);
 #pragma unroll
                 for (int cc = 0; cc < 6; ++cc) {
                     const F xv = fma(al, bdx[6 * j + cc], bx0[6 * j + cc]);
                     const F t = (xv - F(2.) * bdl) * ibdl;
-                    Jb += xv >= bdl ? -bmu * fast_log(xv) : F(0.5) * bmu * (t * t - F(1.)) - bmu * lbd;
+                    const bool lg = xv >= bdl;
+                    prod *= lg ? xv : F(1.);
+                    quad += lg ? F(0.) : F(0.5) * bmu * (t * t - F(1.)) - bmu * lbd;
                 }
+                Jb += quad - bmu * fast_log(prod);
             }
             J += (double)Jb;
             F xs[NX], us[NX];

@@ -12,6 +12,8 @@ All compute is in libpdilqr.so; this module only sequences calls and copies wind
 """
 from __future__ import annotations
 
+import contextlib
+
 import torch
 
 from .pdilqr import PDILQR_MODEL_SRBD, PdIlqr
@@ -56,14 +58,19 @@ class ClosedLoop:
         node -> tensor/None.  Returns the stats dict of the SQP iteration (device tensors)."""
         if self.horizon_left < self.k:
             raise RuntimeError("reference horizon exhausted")
-        self.it["x0"].copy_(self.x_plant)
-        self.h.step(self.it, self.stats, stream=stream)
-        for _ in range(self.k):
-            F = ext_force(self.node) if callable(ext_force) else ext_force
-            self.u_hold.copy_(self.it["u"][:, 0])
-            self.h.plant(self.it, self.x_plant, self.u_hold, F, dt=self.dt, substeps=self.sub, stream=stream)
-            self.h.shift(self.it, stream=stream)
-            self.node += 1
-            self._window()
+        # every copy and every library call of the tick on one stream (the caller's, else torch's
+        # current one), so the x0 / u_hold / window copies are ordered with step, plant and shift
+        ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+        with ctx:
+            s = torch.cuda.current_stream(self.x_plant.device)
+            self.it["x0"].copy_(self.x_plant)
+            self.h.step(self.it, self.stats, stream=s)
+            for _ in range(self.k):
+                F = ext_force(self.node) if callable(ext_force) else ext_force
+                self.u_hold.copy_(self.it["u"][:, 0])
+                self.h.plant(self.it, self.x_plant, self.u_hold, F, dt=self.dt, substeps=self.sub, stream=s)
+                self.h.shift(self.it, stream=s)
+                self.node += 1
+                self._window()
         self.t += 1
         return self.stats

@@ -510,14 +510,20 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     }
     cp_async_wait<0>();
     __syncwarp();
-    // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel
+    // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel; non-finite direction
+    // entries (dx, du, dlam) make info = -1 as on the other step paths (k_finalize_info rule)
+    bool nonfin = false;
     for (int t = lane; t < (N + 2) * NX; t += 32) {
         const int i = t / NX, a = t % NX;
         T prow[NX], xv[NX];
         ld_row<T, NX, true>(prow, Pp + (size_t)i * TP + a * NX);
         ld_row<T, NX, true>(xv, Dx + (size_t)i * NX);
-        Dl[t] = row_dot<T, NX>(prow, xv, Pp[(size_t)i * TP + NX * NX + a]);
+        const T v = row_dot<T, NX>(prow, xv, Pp[(size_t)i * TP + NX * NX + a]);
+        Dl[t] = v;
+        nonfin = nonfin || !isfinite(v) || !isfinite(Dx[t]);
     }
+    for (int t = lane; t < (N + 1) * NX; t += 32) nonfin = nonfin || !isfinite(Du[t]);
+    if (__any_sync(0xffffffffu, nonfin) && info == 0) info = -1;
     __syncwarp();
     // ---------------- line search: lane = stage; per alpha slot a (0 = current iterate,
     // a >= 1: alpha = 2^-(a-1)); per-lane partial sums in shared memory (no unrolled alpha loop).

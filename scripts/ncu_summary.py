@@ -21,6 +21,9 @@ def main(rep, prefix):
         for m in METRICS:
             if m in h:
                 d[m] = r[h.index(m)] + (" " + units[h.index(m)] if units[h.index(m)] else "")
+        for i, w in enumerate(h):   # tensor-pipe utilisation (tcgen05 kernels)
+            if ("tensor" in w or "pipe_tc" in w or "tcgen05" in w or "_tmem" in w or "utcmma" in w.lower()) and "pct" in w and r[i]:
+                d[w] = r[i] + (" " + units[i] if units[i] else "")
         stalls = []
         for i, w in enumerate(h):
             if w.startswith("smsp__average_warps_issue_stalled_") and w.endswith("_per_issue_active.ratio"):

@@ -489,6 +489,9 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         const T d0 = x0[r < NX ? r : 0] - x[r < NX ? r : 0];
         if (lane < NX) { sx[wl][r] = d0; Dx[r] = d0; }
     }
+    // non-finite direction entries (dx, du, dlam) make info = -1 as on the other step paths
+    // (k_finalize_info rule); checked in registers where they are produced
+    bool nonfin = false;
     // lanes 0..11: dx_{i+1} = Abar_i dx_i + bbar_i ; lanes 16..27: du_i = K_i dx_i + k_i
     const int roff = (lane < 16 ? 0 : 156) + (rowl ? r : 0) * NX;
     const int ooff = (lane < 16 ? 0 : 156) + NX * NX + (rowl ? r : 0);
@@ -501,6 +504,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         ld_row<T, NX, true>(rcur, blk + roff);
         ld_row<T, NX, true>(xv, sx[wl]);
         const T v = row_dot<T, NX>(rcur, xv, blk[ooff]);
+        nonfin = nonfin || !isfinite(v);
         __syncwarp();
         if (rowl) {
             if (lane < 16) { sx[wl][r] = v; Dx[(size_t)(i + 1) * NX + r] = v; }
@@ -510,9 +514,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     }
     cp_async_wait<0>();
     __syncwarp();
-    // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel; non-finite direction
-    // entries (dx, du, dlam) make info = -1 as on the other step paths (k_finalize_info rule)
-    bool nonfin = false;
+    // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel
     for (int t = lane; t < (N + 2) * NX; t += 32) {
         const int i = t / NX, a = t % NX;
         T prow[NX], xv[NX];
@@ -520,9 +522,8 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
         ld_row<T, NX, true>(xv, Dx + (size_t)i * NX);
         const T v = row_dot<T, NX>(prow, xv, Pp[(size_t)i * TP + NX * NX + a]);
         Dl[t] = v;
-        nonfin = nonfin || !isfinite(v) || !isfinite(Dx[t]);
+        nonfin = nonfin || !isfinite(v);
     }
-    for (int t = lane; t < (N + 1) * NX; t += 32) nonfin = nonfin || !isfinite(Du[t]);
     if (__any_sync(0xffffffffu, nonfin) && info == 0) info = -1;
     __syncwarp();
     // ---------------- line search: lane = stage; per alpha slot a (0 = current iterate,

@@ -14,6 +14,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "pdilqr.h"
 #include "lq.cuh"
 #include "srbd.cuh"
@@ -115,6 +117,7 @@ struct pdilqr_ctx {
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool fault_combine = false;    // PDILQR_FAULT_COMBINE=1: negative control of the parity tests
+    bool nvtx = false;             // PDILQR_NVTX=1: an NVTX range around every kernel launch (tracing)
     bool big_tc = false;           // large path, f32: tcgen05 3xTF32 products in k_big_ric (PDILQR_BIG_TC=1);
                                    // off by default: measured slower than the SIMT tiles (K7)
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
@@ -150,6 +153,7 @@ struct Prof {
     cudaEvent_t e1 = nullptr;
     const char *name;
     Prof(pdilqr_ctx *h_, const char *nm, cudaStream_t s) : h(h_), st(s), name(nm) {
+        if (h->nvtx) nvtxRangePushA(name);  // per-phase ranges for external timeline tools
         if (h->prof) {
             e1 = h->ev_get();
             cudaEventRecord(e1, st);
@@ -161,6 +165,7 @@ struct Prof {
             cudaEventRecord(e2, st);
             h->recs.push_back(ProfRec{name, e1, e2});
         }
+        if (h->nvtx) nvtxRangePop();
     }
 };
 }  // namespace
@@ -1256,6 +1261,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_FOLD_TPB")) h->fold_tpb = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FUSED")) h->fused = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FAULT_COMBINE")) h->fault_combine = std::atoi(e) != 0;
+    if (const char *e = std::getenv("PDILQR_NVTX")) h->nvtx = std::atoi(e) != 0;
     if (v == VBIG) {  // large path: cluster size of k_big_ric (CTAs per instance) so that B * CS fills the SMs
         if (const char *e = std::getenv("PDILQR_BIG_LEGACY")) h->big_legacy = std::atoi(e) != 0;
         DeviceGuard g(device);

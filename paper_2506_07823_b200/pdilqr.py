@@ -402,6 +402,23 @@ class PdIlqr:
                                       _ptr(stats_host["alpha"]), _ptr(stats_host["accepted"]),
                                       _ptr(stats_host["info"]), self._stream(stream)))
 
+    def capture_tick_host(self, it: dict, x0_host, u0_host, stats_host: dict, warmup: int = 1):
+        """pdilqr_tick_host captured once into a CUDA graph (the library call is graph-capturable:
+        no allocation, no host sync).  Returns the graph: per control tick the caller writes
+        x0_host, calls graph.replay(), synchronises, and reads u0_host / stats_host -- the same
+        copies and kernels as tick_host without the per-call host launch work."""
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                self.tick_host(it, x0_host, u0_host, stats_host, stream=s)
+            s.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                self.tick_host(it, x0_host, u0_host, stats_host, stream=s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return g
+
     def solve(self, it: dict, max_iters: int = 50, tol: float = 1e-6, stats: dict | None = None, stream=None):
         """pdilqr_solve: SQP iterations until every instance converged (theta <= tol and step <= tol)
         or max_iters.  Returns (stats, iters[B] device int32, iterations run)."""

@@ -218,3 +218,43 @@ def test_step_parity_scan_algorithms(P, O, monkeypatch, ks):
     """SRBD step in the latency regime with the Kogge-Stone (1) and Blelloch (0) reverse scans."""
     monkeypatch.setenv("PDILQR_SCAN_KS", ks)
     step_parity(P, O, 2, 50, torch.float32, seed=33, leaf_chunk=1, steps=2, dir_steps=(0,))
+
+
+def test_captured_tick_matches_tick_host(P):
+    """PdIlqr.capture_tick_host: a CUDA-graph replay of pdilqr_tick_host gives the same host outputs
+    and device iterate as the direct call (same copies and kernels)."""
+    B, N = 16, 50
+    prob = problem(B, N, 38, torch.float32)
+    outs = []
+    for captured in (False, True):
+        h = handle(P, prob, torch.float32, B, N)
+        d = to_device({k: prob[k] for k in ITER_KEYS}, torch.float32)
+        x0h = torch.from_numpy(prob["x0"].astype(np.float32)).pin_memory()
+        u0h = torch.empty(B, 12).pin_memory()
+        sh = {"cost": torch.empty(B).pin_memory(), "theta": torch.empty(B).pin_memory(),
+              "alpha": torch.empty(B).pin_memory(), "accepted": torch.empty(B, dtype=torch.int32).pin_memory(),
+              "info": torch.empty(B, dtype=torch.int32).pin_memory()}
+        if captured:
+            g = h.capture_tick_host(d, x0h, u0h, sh, warmup=0)   # capture does not execute
+            g.replay()
+        else:
+            h.tick_host(d, x0h, u0h, sh)
+        torch.cuda.synchronize()
+        outs.append((u0h.clone(), sh["alpha"].clone(), d["x"].clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a.cpu(), b.cpu())
+
+
+def test_nvtx_ranges_do_not_change_results(P, monkeypatch):
+    """PDILQR_NVTX=1 wraps every launch in an NVTX range (tracing); the step is unchanged."""
+    B, N = 8, 20
+    prob = problem(B, N, 39, torch.float32)
+    xs = []
+    for env in ("0", "1"):
+        monkeypatch.setenv("PDILQR_NVTX", env)
+        h = handle(P, prob, torch.float32, B, N)
+        d = to_device({k: prob[k] for k in ITER_KEYS}, torch.float32)
+        h.step(d)
+        torch.cuda.synchronize()
+        xs.append(d["x"].clone())
+    assert torch.equal(xs[0], xs[1])

@@ -22,7 +22,8 @@ def main(rep, prefix):
             if m in h:
                 d[m] = r[h.index(m)] + (" " + units[h.index(m)] if units[h.index(m)] else "")
         for i, w in enumerate(h):   # tensor-pipe utilisation (tcgen05 kernels)
-            if ("tensor" in w or "pipe_tc" in w or "tcgen05" in w or "_tmem" in w or "utcmma" in w.lower()) and "pct" in w and r[i]:
+            if (("tensor" in w or "pipe_tc" in w or "tcgen05" in w or "_tmem" in w or "utcmma" in w.lower()) and "pct" in w
+                    and r[i] and r[i].strip() not in ("0", "0.0")):
                 d[w] = r[i] + (" " + units[i] if units[i] else "")
         stalls = []
         for i, w in enumerate(h):

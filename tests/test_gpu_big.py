@@ -74,7 +74,7 @@ def test_odd_dimensions(P, O, dims):
     check(O, qp, out, 1e-4)
     for b in range(2):
         r = O.solve_lq_single(qp, b)
-        assert np.abs(out["K"][b] - r["K"]).max() <= 1e-3 * max(1.0, np.abs(r["K"]).max())
+        assert np.abs(out["K"][b] - r["K"]).max() <= 1e-4 * max(1.0, np.abs(r["K"]).max())
 
 
 def test_big_info(P):

@@ -29,6 +29,7 @@ def _dev(d, dtype):
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("case,B,N,n,m,chunk", [("dense", 5, 20, 12, 12, 0), ("dense", 3, 9, 5, 3, 1),
                                                 ("dense", 200, 30, 8, 4, 0), ("wb", 2, 12, 74, 32, 0),
+                                                ("dense", 2, 0, 4, 2, 0), ("dense", 2, 1, 3, 3, 1),
                                                 ("dense", 2, 7, 40, 24, 0)])
 def test_adjoint_parity(P, O, dtype, case, B, N, n, m, chunk):
     qp = rounded(synth.random_lq(B, N, n, m, seed=17 + n, kind=case), dtype)

@@ -86,7 +86,7 @@ def step_parity(P, O, B, R, N, dtype, seed, spacing=1.0, sample=None, tol=None):
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
-@pytest.mark.parametrize("R,N,B", [(1, 10, 2), (2, 12, 3), (4, 20, 2)])
+@pytest.mark.parametrize("R,N,B", [(1, 10, 2), (2, 12, 3), (4, 20, 2), (2, 0, 2), (3, 1, 1)])
 def test_multi_step_parity(P, O, dtype, R, N, B):
     step_parity(P, O, B, R, N, dtype, seed=20 + R, spacing=0.9)
 

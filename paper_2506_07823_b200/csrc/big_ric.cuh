@@ -368,6 +368,27 @@ __device__ __forceinline__ void warp_chol_solve2_any(int m, const T *L, int ld, 
     else warp_chol_solve2<T, 8>(m, L, ld, dinv, b0, b1);
 }
 
+// Copy an m x m row-major matrix (leading dimension lds, global memory) into the shared factor
+// buffer (leading dimension ldl): one warp per row, lanes over columns (coalesced, no index
+// division), all of a row's loads issued before its stores.
+template <typename T>
+__device__ __forceinline__ void copy_rows_to_factor(int m, const T *src, int lds, T *Ls, int ldl) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = wid; r < m; r += nw) {
+        T v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = lane + 32 * j;
+            v[j] = c < m ? ldg_cg(src + (size_t)r * lds + c) : T(0);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int c = lane + 32 * j;
+            if (c < m) Ls[(size_t)r * ldl + c] = v[j];
+        }
+    }
+}
+
 // Per-instance global scratch of k_big_ric (values of T): PB [n x ld(m)], W = [G | H | h]
 // [m x ld(m+n+1)], V [n x LD], g, w [LD each].
 __host__ __device__ inline size_t ric_slot(int n, int m) {
@@ -435,8 +456,7 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
         ric_gemv<T, true>(m, n, Bm, m, g, r, 1, W + m + n, ldw, gw, nwc);  // column m+n of W
         ric_sync(CS);
         // phase 3: Cholesky of G (every CTA, own shared memory), [K | k] = -G^-1 [H | h]
-        for (int t = threadIdx.x; t < m * m; t += RIC_THREADS)
-            Ls[(size_t)(t / m) * ldl + t % m] = ldg_cg(W + (size_t)(t / m) * ldw + t % m);
+        copy_rows_to_factor<T>(m, W, ldw, Ls, ldl);
         __syncthreads();
         if (!cta_chol<T>(m, Ls, ldl, dinv)) fail = min(fail, i + 1);
         for (int c0 = 2 * gw; c0 <= n; c0 += 2 * nwc) {
@@ -640,7 +660,7 @@ __global__ void __launch_bounds__(256) k_big_rchk(const T *R, int B, int N, int 
     for (long item = blockIdx.x; item < (long)B * (N + 1); item += gridDim.x) {
         const int b = (int)(item / (N + 1)), i = (int)(item % (N + 1));
         const T *Ri = R + (size_t)item * m * m;
-        for (int t = threadIdx.x; t < m * m; t += blockDim.x) Ls[(size_t)(t / m) * ldl + t % m] = Ri[t];
+        copy_rows_to_factor<T>(m, Ri, m, Ls, ldl);
         __syncthreads();
         const bool ok = cta_chol<T>(m, Ls, ldl, dinv);
         if (!ok && threadIdx.x == 0) atomicMin(fail + b, i + 1);

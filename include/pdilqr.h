@@ -207,7 +207,11 @@ pdilqr_status pdilqr_tick_host(pdilqr_handle h, pdilqr_iterate *it, const void *
  * iterations ran.  Instance b converges at iteration k when that iteration's accepted step has
  * theta <= tol and ||alpha (dx, du)||_inf <= tol, or when every alpha was rejected at a fixed
  * point: theta <= tol and |grad J . (dx, du)| <= tol max(1, |J|) (the linear model predicts no
- * decrease; R24).  A rejected step elsewhere is not convergence.  It is then frozen (later iterations neither
+ * decrease; R24).  A rejected step elsewhere is not convergence.  Levenberg-Marquardt
+ * ladder (R28): after a factorisation failure (info > 0) or an
+ * all-rejected line search away from a fixed point, the next iteration of that instance adds
+ * rho = 1e-6 (then x10 per retry, up to 1e-2) to every R_i; an accepted step resets rho to 0;
+ * info > 0 with rho exhausted stops the instance.  A converged instance is then frozen (later iterations neither
  * update it nor overwrite its stats with a step: they report its iterate with alpha = 0,
  * accepted = 0).  An instance whose info != 0 stops at that iteration.
  *   stats      as pdilqr_step, of each instance's last iteration (device, required)

@@ -111,6 +111,8 @@ def lib():
         L.oracle_srbd_line_search.restype = i
         L.oracle_srbd_step.argtypes = [PP, i, i, d, d] + [_dp] * 6 + [_up, _dp] + [_dp] * 4
         L.oracle_srbd_step.restype = i
+        L.oracle_srbd_step_rho.argtypes = [PP, i, i, d, d, d] + [_dp] * 6 + [_up, _dp] + [_dp] * 4
+        L.oracle_srbd_step_rho.restype = i
         L.oracle_srbd_step_batch.argtypes = [PP, i, i, i, d, d] + [_dp] * 6 + [_up, _dp, _dp, i]
         L.oracle_srbd_plant.argtypes = [PP, _dp, _dp, _dp, _up, C.c_void_p, d, i, _dp]
         MP = C.POINTER(MultiParams)
@@ -276,15 +278,16 @@ def srbd_line_search(prob, b, dx, du, n_alpha=10, c1=1e-4, theta_max=None):
     return j, Ja, tha, base
 
 
-def srbd_step_single(prob, b, n_alpha=10, c1=1e-4, theta_max=0.0):
-    """One SQP iteration of instance b; returns (x, u, lam, stats[5], dx, du, dlam) (copies)."""
+def srbd_step_single(prob, b, n_alpha=10, c1=1e-4, theta_max=0.0, rho=0.0):
+    """One SQP iteration of instance b (rho: LM shift added to every R_i, reading R28); returns
+    (x, u, lam, stats[5], dx, du, dlam) (copies)."""
     x = _c(prob["x"][b]).copy(); u = _c(prob["u"][b]).copy(); lam = _c(prob["lam"][b]).copy()
     N = x.shape[0] - 2
     st = np.zeros(5)
     dx = np.zeros((N + 2, 12)); du = np.zeros((N + 1, 12)); dl = np.zeros((N + 2, 12))
-    lib().oracle_srbd_step(C.byref(SrbdParams.from_dict(prob["params"])), N, n_alpha, c1, theta_max,
-                           x, u, lam, _c(prob["x0"][b]), _c(prob["x_ref"][b]), _uref(prob, b),
-                           _c(prob["contact"][b], np.uint8), _c(prob["feet"][b]), st, dx, du, dl)
+    lib().oracle_srbd_step_rho(C.byref(SrbdParams.from_dict(prob["params"])), N, n_alpha, c1, theta_max, float(rho),
+                               x, u, lam, _c(prob["x0"][b]), _c(prob["x_ref"][b]), _uref(prob, b),
+                               _c(prob["contact"][b], np.uint8), _c(prob["feet"][b]), st, dx, du, dl)
     return x, u, lam, st, dx, du, dl
 
 
@@ -360,38 +363,48 @@ def closed_loop(prob_long: dict, N: int, ticks: int, nodes_per_tick: int = 1, su
     return {"x_plant": np.stack(xs, 1), "stats": np.stack(sts, 1)}
 
 
-def srbd_solve(prob: dict, max_iters: int, tol: float, n_alpha=10, c1=1e-4, theta_max=0.0):
+def srbd_solve(prob: dict, max_iters: int, tol: float, n_alpha=10, c1=1e-4, theta_max=0.0, return_rho=False):
     """Multi-iteration solve, per instance: repeat the SQP iteration until the
     accepted step has theta <= tol and ||alpha (dx, du)||_inf <= tol, or every alpha is rejected at
     a fixed point (theta <= tol and |grad J . (dx, du)| <= tol max(1, |J|), R24)
-    (converged at k), or the
-    iteration fails (info != 0: stopped, -k), or max_iters.  In place on prob x/u/lam.
-    Returns (iters[B], stats[B][5] of each instance's last iteration)."""
+    (converged at k), or the iteration fails (info < 0, or info > 0 with the LM ladder exhausted:
+    stopped, -k), or max_iters.  Levenberg-Marquardt ladder (reading R28): after
+    a factorisation failure (info > 0) or an all-rejected search away from a fixed point, the next
+    iteration adds rho = 1e-6, then x10 per retry up to 1e-2, to every R_i; an accepted step resets
+    rho to 0.  In place on prob x/u/lam.  Returns (iters[B], stats[B][5] of each instance's last
+    iteration) (+ final rho[B] if return_rho)."""
     Bn = prob["x"].shape[0]
     iters = np.zeros(Bn, np.int32)
     st = np.zeros((Bn, 5))
+    rhos = np.zeros(Bn)
     for b in range(Bn):
+        rho = 0.0
         for k in range(1, max_iters + 1):
-            x, u, lam, s, dx, du, _ = srbd_step_single(prob, b, n_alpha, c1, theta_max)
+            x, u, lam, s, dx, du, _ = srbd_step_single(prob, b, n_alpha, c1, theta_max, rho)
+            fixed = False
+            if s[4] == 0 and not s[3]:
+                _, _, _, (J0, th0, g) = srbd_line_search(prob, b, dx, du, n_alpha, c1,
+                                                         None if theta_max <= 0 else theta_max)
+                fixed = th0 <= tol and abs(g) <= tol * max(1.0, abs(J0))
             prob["x"][b], prob["u"][b], prob["lam"][b] = x, u, lam
             st[b] = s
-            step = s[2] * max(np.abs(dx).max(), np.abs(du).max())
+            retry = False
+            if s[3]:
+                rho = 0.0
+            elif (s[4] > 0 or (s[4] == 0 and not fixed)) and rho < 1e-2:
+                rho = 1e-6 if rho == 0.0 else min(10.0 * rho, 1e-2)
+                retry = True
+            if retry:
+                continue
             if s[4] != 0:
                 iters[b] = -k
                 break
-            if s[3]:
-                conv = s[1] <= tol and step <= tol
-            else:   # every alpha rejected: a fixed point iff the linear model predicts no decrease
-                _, _, _, (J0, th0, g) = srbd_line_search(prob, b, dx, du, n_alpha, c1,
-                                                         None if theta_max <= 0 else theta_max)
-                conv = th0 <= tol and abs(g) <= tol * max(1.0, abs(J0))
-            if conv:
+            step = s[2] * max(np.abs(dx).max(), np.abs(du).max())
+            if (s[1] <= tol and step <= tol) if s[3] else fixed:
                 iters[b] = k
                 break
-    return iters, st
-
-
-# ----------------------------------------------------------------------------- multi-robot (NEXT-3)
+        rhos[b] = rho
+    return (iters, st, rhos) if return_rho else (iters, st)
 
 def _mp(prob):
     return C.byref(SrbdParams.from_dict(prob["params"])), C.byref(MultiParams.from_dict(prob["multi"]))

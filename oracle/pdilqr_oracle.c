@@ -740,11 +740,28 @@ int oracle_srbd_line_search(const oracle_srbd_params *P, int N, int n_alpha, dou
 /* One SQP/RTI iteration (one iteration per control tick): linearise -> LQ solve
  * (Riccati) -> dual update -> filter line search -> update x,u,lam in place (Eq. 16).
  * stats[5] = {cost, theta, alpha, accepted, info}.  dirs (dx,du,dlam) optional out. */
+/* The same iteration with a Levenberg-Marquardt shift rho added to every R_i after the
+ * linearisation (the ladder of pdilqr_solve, SPEC S:75 / S:362, reading R28). */
+int oracle_srbd_step_rho(const oracle_srbd_params *P, int N, int n_alpha, double c1, double theta_max, double rho,
+                         double *x, double *u, double *lam, const double *x0,
+                         const double *xref, const double *uref,
+                         const uint8_t *contact, const double *feet,
+                         double *stats, double *dx_out, double *du_out, double *dlam_out);
+
 int oracle_srbd_step(const oracle_srbd_params *P, int N, int n_alpha, double c1, double theta_max,
                      double *x, double *u, double *lam, const double *x0,
                      const double *xref, const double *uref,
                      const uint8_t *contact, const double *feet,
                      double *stats, double *dx_out, double *du_out, double *dlam_out) {
+    return oracle_srbd_step_rho(P, N, n_alpha, c1, theta_max, 0.0, x, u, lam, x0, xref, uref, contact, feet,
+                                stats, dx_out, du_out, dlam_out);
+}
+
+int oracle_srbd_step_rho(const oracle_srbd_params *P, int N, int n_alpha, double c1, double theta_max, double rho,
+                         double *x, double *u, double *lam, const double *x0,
+                         const double *xref, const double *uref,
+                         const uint8_t *contact, const double *feet,
+                         double *stats, double *dx_out, double *du_out, double *dlam_out) {
     const int n = NX, m = NU;
     const size_t S1 = (size_t)(N + 1);
     double *A = malloc(sizeof(double) * S1 * n * n), *Bm = malloc(sizeof(double) * S1 * n * m);
@@ -757,6 +774,9 @@ int oracle_srbd_step(const oracle_srbd_params *P, int N, int n_alpha, double c1,
     double theta_thr = theta_max > 0 ? theta_max : 1e-2 * (N + 1);
     int info = oracle_srbd_linearize(P, N, x, u, lam, x0, xref, uref, contact, feet,
                                      A, Bm, c, Q, R, S, q, r, Pt, pt, d0);
+    if (info == 0 && rho != 0.0)
+        for (size_t i = 0; i < S1; ++i)
+            for (int a = 0; a < m; ++a) R[i * m * m + IDX2(a, a, m)] += rho;
     if (info == 0) info = oracle_solve_lq(N, n, m, A, Bm, c, Q, R, S, q, r, Pt, pt, d0, dx, du, dl,
                                           NULL, NULL, NULL, NULL);
     if (info == 0) {

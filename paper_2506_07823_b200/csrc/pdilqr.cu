@@ -87,6 +87,7 @@ struct Layout {
     size_t elems, vslots, Pp, Kk, tel, tslots, dxw, fail, nonfin, pre, info_tmp, stats;
     size_t kinds_b, kinds_f, ls_part, ls_cnt;  // grid-scan slot kinds, multi-block line-search scratch
     size_t conv, active;                       // pdilqr_solve per-instance state, active counter
+    size_t rho;                                // pdilqr_solve Levenberg-Marquardt shift per instance (double)
     size_t qp[11];  // SRBD internal QP buffers (A, Bm, c, Q, R, S, q, r, Pt, pt, dx0)
     size_t dir[3];  // internal direction (dx, du, dlam)
     size_t adj[8];  // adjoint solve: linear terms (q, r, c, pt, dx0) and solution (wx, wu, wl)
@@ -128,6 +129,7 @@ struct pdilqr_ctx {
     int coop_ks2 = 0;
     // pdilqr_solve in progress: convergence bookkeeping handed to the update kernels
     int32_t *sc_conv = nullptr, *sc_active = nullptr;
+    double *sc_rho = nullptr;
     double sc_tol = 0.0;
     int sc_iter = 0;
     // per-kernel CUDA-event timing (host bookkeeping only; off unless pdilqr_profile(h, 1))
@@ -285,6 +287,7 @@ Layout make_layout(const pdilqr_config *c, int NX, int NU, int esz, int chunk, i
     L.ls_cnt = take(B * 4);
     L.conv = take(B * 4);
     L.active = take(8);
+    L.rho = take(B * 8);
     const size_t n = c->n, m = c->m;
     if (c->model != PDILQR_MODEL_LQ) {
         const size_t sz[11] = {(N + 1) * n * n, (N + 1) * n * m, (N + 1) * n, (N + 1) * n * n, (N + 1) * m * m,
@@ -367,6 +370,7 @@ SrbdIter<T> iter_of(const pdilqr_iterate *it, const pdilqr_ctx *h) {
     SrbdIter<T> r = iter_of<T>(it);
     r.conv = h->sc_conv;
     r.active = h->sc_active;
+    r.rho = h->sc_rho;
     r.tol = h->sc_tol;
     r.iter = h->sc_iter;
     return r;
@@ -623,7 +627,7 @@ pdilqr_status run_step_split(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         const size_t smem = 8 * sizeof(LinElemSmem<T>);
         set_smem(k_srbd_lin_elem<T>, smem);
         Prof pf(h, "k_srbd_lin_elem", st);
-        k_srbd_lin_elem<T><<<(unsigned)((nw + 7) / 8), 128, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, qp, pre);
+        k_srbd_lin_elem<T><<<(unsigned)((nw + 7) / 8), 128, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, qp, pre);
     }
     {
         const size_t smem = 8 * sizeof(FoldChainSmem<T, 12>);
@@ -670,9 +674,10 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
             const int ipb = tpb / 16;  // instances per block
             const size_t smem = (size_t)ipb * sizeof(FoldSmem<T>);
             set_smem(kern, smem);
-            kern<<<(B + ipb - 1) / ipb, tpb, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, info_tmp);
+            kern<<<(B + ipb - 1) / ipb, tpb, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, info_tmp);
         };
-        switch (h->occ_fold * 1000 + h->fold_tpb) {
+        if (h->sc_rho) go(k_srbd_bwd_fold<T, 4, 64, true>, 64);   // pdilqr_solve: Levenberg-Marquardt ladder
+        else switch (h->occ_fold * 1000 + h->fold_tpb) {
             case 4032: go(k_srbd_bwd_fold<T, 4, 32>, 32); break;
             case 4128: go(k_srbd_bwd_fold<T, 4, 128>, 128); break;
             case 3064: go(k_srbd_bwd_fold<T, 3, 64>, 64); break;
@@ -726,7 +731,7 @@ pdilqr_status run_step(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *stats, p
         set_smem(k_srbd_lin_elem<T>, smem);
         {
             Prof pf(h, "k_srbd_lin_elem", st);
-            k_srbd_lin_elem<T><<<(unsigned)((nw + 7) / 8), 128, smem, st>>>(h->K, iter_of<T>(it), B, N, ws, qp, pre);
+            k_srbd_lin_elem<T><<<(unsigned)((nw + 7) / 8), 128, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, qp, pre);
         }
         h->launches += 1;
         qp.S = nullptr;
@@ -1532,17 +1537,21 @@ pdilqr_status pdilqr_solve(pdilqr_handle h, pdilqr_iterate *it, int32_t max_iter
     const int B = h->cfg.batch;
     int32_t *conv = reinterpret_cast<int32_t *>(h->ws + h->lay.conv);
     int32_t *active = reinterpret_cast<int32_t *>(h->ws + h->lay.active);
+    double *rho = reinterpret_cast<double *>(h->ws + h->lay.rho);
     cudaMemsetAsync(conv, 0, (size_t)B * 4, st);
+    cudaMemsetAsync(rho, 0, (size_t)B * 8, st);
     int total = 0, run = 0;
     for (int k = 1; k <= max_iters; ++k) {
         cudaMemsetAsync(active, 0, 4, st);
         h->sc_conv = conv;
         h->sc_active = active;
+        h->sc_rho = rho;
         h->sc_tol = tol;
         h->sc_iter = k;
         h->launches = 0;
         s = (h->cfg.dtype == PDILQR_F32) ? run_step<float>(h, it, stats, nullptr, st) : run_step<double>(h, it, stats, nullptr, st);
         h->sc_conv = h->sc_active = nullptr;
+        h->sc_rho = nullptr;
         total += h->launches;
         if (s != PDILQR_OK) return s;
         run = k;

@@ -175,7 +175,8 @@ struct SrbdRow {
 
 template <typename T>
 __device__ __forceinline__ void srbd_stage_row(const SrbdConst &K, const T *x, const T *u, const T *feet,
-                                               const uint8_t *con, const T *ur, int r, SrbdRow<T> &o) {
+                                               const uint8_t *con, const T *ur, int r, SrbdRow<T> &o,
+                                               T rho = T(0)) {
     constexpr int NX = 12;
     T xv[NX], uv[NX];
     ld_row<T, NX, true>(xv, x);
@@ -283,7 +284,7 @@ __device__ __forceinline__ void srbd_stage_row(const SrbdConst &K, const T *x, c
     const T wu = stance ? T(K.wu_st) : T(K.wu_sw);
     T (&Rrow)[NX] = o.Rrow;
 #pragma unroll
-    for (int c = 0; c < NX; ++c) Rrow[c] = (c == r) ? wu : T(0);
+    for (int c = 0; c < NX; ++c) Rrow[c] = (c == r) ? wu + rho : T(0);   // rho: LM shift (pdilqr_solve)
     T rg = wu * (ur_r - (ur ? ur[r] : T(0)));
     {
         // barrier terms of this lane's foot j (stance only): gradient entry a, Hessian row a of the
@@ -319,7 +320,14 @@ struct SrbdIter {
     int32_t *conv = nullptr, *active = nullptr;
     double tol = 0.0;
     int iter = 0;
+    // Levenberg-Marquardt ladder of pdilqr_solve (reading R28): rho[b] is added to every R_i of
+    // instance b; the update kernel escalates it (0 -> 1e-6 -> ... -> 1e-2, x10) after a
+    // factorisation failure or an all-rejected line search and resets it after an accepted step.
+    double *rho = nullptr;
+    __device__ __forceinline__ double rho_of(int b) const { return rho ? rho[b] : 0.0; }
 };
+
+constexpr double kLmRho0 = 1e-6, kLmRhoMax = 1e-2;
 
 template <typename T>
 __global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T> it, int B, int N, LqArgs<T> outc,
@@ -357,7 +365,7 @@ __global__ void __launch_bounds__(128) k_srbd_linearize(SrbdConst K, SrbdIter<T>
     const T *ln = lam + NX;
     const T *ur = it.uref ? it.uref + st * NX : nullptr;
     SrbdRow<T> row;
-    srbd_stage_row<T>(K, x, u, feet, con, ur, r, row);
+    srbd_stage_row<T>(K, x, u, feet, con, ur, r, row, (T)it.rho_of(b));
     const T dt = T(K.dt);
     const T xr_r = x[r];
     const bool bad = row.bad || !isfinite(lam[r]);
@@ -485,8 +493,20 @@ __device__ __forceinline__ void commit_step(const SrbdIter<T> &it, const LsOut<T
             so.theta[b] = (T)thb;
             so.alpha[b] = alpha;
             so.accepted[b] = acc ? 1 : 0;
+            bool lm_retry = false;
+            if (it.rho) {   // LM ladder: escalate after a factorisation failure or an all-rejected search
+                const double r0 = it.rho[b];
+                const bool fixed = !acc && info == 0 && th0 <= it.tol && fabs(gslope) <= it.tol * fmax(1.0, fabs(J0));
+                if (acc) {
+                    it.rho[b] = 0.0;
+                } else if ((info > 0 || (info == 0 && !fixed)) && r0 < kLmRhoMax) {
+                    it.rho[b] = r0 == 0.0 ? kLmRho0 : fmin(10.0 * r0, kLmRhoMax);
+                    lm_retry = true;
+                }
+            }
             if (it.conv) {
-                if (info != 0) it.conv[b] = -it.iter;
+                if (lm_retry) atomicAdd(it.active, 1);
+                else if (info != 0) it.conv[b] = -it.iter;
                 // accepted: theta and ||alpha (dx, du)||_inf within tol; every alpha rejected: the
                 // iterate is kept, and it is a fixed point iff theta <= tol and the linear model
                 // predicts no decrease, |grad J . (dx, du)| <= tol max(1, |J|) (R24)

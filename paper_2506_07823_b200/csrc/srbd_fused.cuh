@@ -42,7 +42,7 @@ struct FoldSmem {
 // TPB threads per block (2 workers per warp); MINB * 128 / TPB blocks per SM keep the 128-register
 // cap.  Small blocks balance the one-wave grid across the 148 SMs (B = 4096: 512 blocks of 128
 // threads put 4 blocks on 68 SMs and 3 on 80; 1024 blocks of 64 threads put 7 or 6).
-template <typename T, int MINB, int TPB = 64>
+template <typename T, int MINB, int TPB = 64, bool LM = false>
 __global__ void __launch_bounds__(TPB, MINB * 128 / TPB) k_srbd_bwd_fold(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
                                                              int32_t *info_out) {
     constexpr int WS = 16, NX = 12;
@@ -109,6 +109,8 @@ __global__ void __launch_bounds__(TPB, MINB * 128 / TPB) k_srbd_bwd_fold(SrbdCon
     };
     prefetch(N + 1);
     prefetch(N);
+    // LM shift of pdilqr_solve's ladder (the LM instantiation); a plain step compiles it away
+    const T rho_b = LM ? (T)it.rho_of(b) : T(0);
     __syncwarp(mask);
     for (int i = N; i >= 0; --i) {
         prefetch(i - 1);
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(TPB, MINB * 128 / TPB) k_srbd_bwd_fold(SrbdCon
         const T *ur = has_ur ? cur + FS::IN_UR : nullptr;
         // ---------------- linearise stage i
         SrbdRow<T> row;
-        srbd_stage_row<T>(K, x, u, feet, con, ur, r, row);
+        srbd_stage_row<T>(K, x, u, feet, con, ur, r, row, rho_b);
         bad = bad || row.bad || !isfinite(lam[r]);
         T arow[NX];
 #pragma unroll
@@ -649,7 +651,7 @@ __global__ void __launch_bounds__(128) k_srbd_lin_elem(SrbdConst K, SrbdIter<T> 
     const T *ln = lam + NX;
     const T dt = T(K.dt);
     SrbdRow<T> row;
-    srbd_stage_row<T>(K, x, u, feet, con, ur, r, row);
+    srbd_stage_row<T>(K, x, u, feet, con, ur, r, row, (T)it.rho_of(b));
     const bool bad = row.bad || !isfinite(lam[r]);
     const T cr = (x[r] - x[NX + r]) + dt * row.fr;  // b_i = h(x_i, u_i) - x_{i+1}
     const unsigned mask = worker_mask<WS>();

@@ -471,3 +471,21 @@ def test_cost_slope_matches_central_difference(O):
                 fd = cd(prob, b, x, u, ddx, ddu)
                 _, _, _, (_, _, g) = O.srbd_line_search(prob, b, ddx, ddu)
                 assert g == pytest.approx(fd, rel=1e-7, abs=1e-7 * max(1.0, abs(fd)))
+
+
+def test_lm_ladder_recovers_singular_control_weight(O):
+    """Levenberg-Marquardt ladder (reading R28): with w_u_swing = 0 the swing-foot block
+    of R, hence of G = R + B^T P B (swing columns of B vanish), is singular and the plain iteration
+    fails its factorisation (info > 0).  The ladder adds rho = 1e-6 to every R_i, the swing controls
+    get a zero step (their gradient is zero) and the solve converges; an accepted step resets rho."""
+    prm = dict(synth.srbd_default_params(), w_u_swing=0.0)
+    pr = synth.srbd_problem(2, 20, seed=8, params=prm)
+    x, u, lam, st, dx, du, dl = O.srbd_step_single(pr, 0)
+    assert st[4] > 0 and st[3] == 0
+    x, u, lam, st, dx, du, dl = O.srbd_step_single(pr, 0, rho=1e-6)
+    assert st[4] == 0 and st[3] == 1
+    sw = ~pr["contact"][0].astype(bool)                      # swing feet: zero step
+    assert np.abs(du.reshape(21, 4, 3)[sw]).max() < 1e-9
+    it, st, rho = O.srbd_solve(pr, 60, 1e-8, return_rho=True)
+    assert (it > 0).all() and (st[:, 1] <= 1e-8).all()
+    assert (rho <= 1e-6).all()

@@ -115,6 +115,11 @@ struct pdilqr_ctx {
     int occ_fold = 4, occ_ls = 4;  // minimum resident CTAs per SM requested from ptxas (register cap: 128)
     int fold_tpb = 64;             // k_srbd_bwd_fold block size (32 / 64 / 128)
     int fused = 1;                 // 1: 2-kernel fused fold path (default), 0: 4-kernel split path
+    int linrec = 1;                // fused path: 1 stage-parallel linearisation records + record-fed fold (default),
+                                   // 0 linearisation inside the sequential fold (round-1/2 kernel)
+    int fold_mode = 2;             // record-fed fold: 2 = two rows per lane / five instances per warp (default),
+                                   // 1 = one instance per warp (column halves), 0 = two instances per warp (row per lane)
+    int fold_w = 14;               // fold_mode 1: MINB blocks/SM (12/14/16)
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool fault_combine = false;    // PDILQR_FAULT_COMBINE=1: negative control of the parity tests
@@ -668,7 +673,48 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         du = reinterpret_cast<T *>(h->ws + h->lay.dir[1]);
         dl = reinterpret_cast<T *>(h->ws + h->lay.dir[2]);
     }
-    {
+    if (h->linrec) {
+        // stage-parallel linearisation records (ws.elems is free on the single-chunk path)
+        T *rec = ws.elems;
+        {
+            constexpr int TPB = 32;
+            const size_t smem = (size_t)TPB * (LinRec::SIZE + 16 / sizeof(T)) * sizeof(T);
+            set_smem(k_srbd_lin_rec<T>, smem);
+            const long tot = (long)B * (N + 1);
+            Prof pf(h, "k_srbd_lin_rec", st);
+            k_srbd_lin_rec<T><<<(unsigned)((tot + TPB - 1) / TPB), TPB, smem, st>>>(h->K, iter_of<T>(it, h), B, N, rec);
+        }
+        Prof pf(h, "k_srbd_bwd_fold", st);
+        if (h->fold_mode == 2) {   // two rows per lane, five instances per warp (default)
+            const size_t smem = 5 * sizeof(FoldR2Smem<T>);
+            set_smem(k_srbd_bwd_fold_r2<T>, smem);
+            k_srbd_bwd_fold_r2<T><<<(B + 4) / 5, 32, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, rec, info_tmp);
+        } else if (h->fold_mode == 1) {   // one instance per warp (two lanes per row)
+            auto gw = [&](auto kern) {
+                const size_t smem = 2 * sizeof(FoldWSmem<T>);
+                set_smem(kern, smem);
+                kern<<<(B + 1) / 2, 64, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, rec, info_tmp);
+            };
+            switch (h->fold_w) {
+                case 12: gw(k_srbd_bwd_fold_w<T, 12>); break;
+                case 16: gw(k_srbd_bwd_fold_w<T, 16>); break;
+                default: gw(k_srbd_bwd_fold_w<T, 14>); break;
+            }
+        } else {
+        auto go = [&](auto kern, int tpb) {
+            const int ipb = tpb / 16;
+            const size_t smem = (size_t)ipb * sizeof(FoldRecSmem<T>);
+            set_smem(kern, smem);
+            kern<<<(B + ipb - 1) / ipb, tpb, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, rec, info_tmp);
+        };
+        switch (h->occ_fold * 1000 + h->fold_tpb) {
+            case 4064: go(k_srbd_bwd_fold_rec<T, 4, 64>, 64); break;
+            case 6064: go(k_srbd_bwd_fold_rec<T, 6, 64>, 64); break;
+            default: go(k_srbd_bwd_fold_rec<T, 5, 64>, 64); break;
+        }
+        }
+        h->launches += 1;
+    } else {
         Prof pf(h, "k_srbd_bwd_fold", st);
         auto go = [&](auto kern, int tpb) {
             const int ipb = tpb / 16;  // instances per block
@@ -1265,6 +1311,9 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_OCC_LS")) h->occ_ls = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_TPB")) h->fold_tpb = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FUSED")) h->fused = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_LINREC")) h->linrec = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_FOLD_W")) h->fold_w = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_FOLD_MODE")) h->fold_mode = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FAULT_COMBINE")) h->fault_combine = std::atoi(e) != 0;
     if (const char *e = std::getenv("PDILQR_NVTX")) h->nvtx = std::atoi(e) != 0;
     if (v == VBIG) {  // large path: cluster size of k_big_ric (CTAs per instance) so that B * CS fills the SMs

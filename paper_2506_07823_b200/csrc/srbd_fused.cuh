@@ -277,6 +277,1124 @@ __global__ void __launch_bounds__(TPB, MINB * 128 / TPB) k_srbd_bwd_fold(SrbdCon
     if (lane == 0 && live) info_out[b] = any_bad ? -1 : (fail != INT_MAX ? fail : 0);
 }
 
+// ------------------------------------------ stage-parallel linearisation record (fused path)
+// The linearisation and quadraticisation of stage i depends only on the
+// iterate, not on the Riccati recursion, so it runs stage-parallel BEFORE the fold: one thread per
+// (instance, stage) evaluates the model once (no per-row divergence, no redundant trig per lane)
+// and writes a compact record of the structurally nonzero parts; the fold reads it one stage ahead.
+// SRBD structure used (x = [p, Theta, v, w], u = 4 GRFs): dt Fx has nonzero rows 0-2 (dt at column
+// 6 + r), 3-5 and 9-11; dt Fu has rows 6-8 (dt/m on the stance feet's diagonal) and 9-11; R is
+// block diagonal with one 3x3 block per foot.
+struct LinRec {
+    static constexpr int FA = 0;     // dt Fx rows 3, 4, 5, 9, 10, 11 (6 x 12)
+    static constexpr int FB = 72;    // dt Fu rows 9, 10, 11 (3 x 12)
+    static constexpr int C = 108;    // b_i = h(x_i, u_i) - x_{i+1}
+    static constexpr int Q = 120;    // q_i = W_x (x - xref) + (lam_{i+1} - lam_i) + dt Fx^T lam_{i+1}
+    static constexpr int RV = 132;   // r_i = W_u (u - uref) + barrier gradient + dt Fu^T lam_{i+1}
+    static constexpr int BT = 144;   // b~_i = b_i - B R^-1 r_i  (Eq. 12)
+    static constexpr int RB = 156;   // R row r: the 3 entries of its foot block (columns 3(r/3)..+2)
+    static constexpr int BD = 192;   // dt / m on stance foot j, 0 on a swing foot (B rows 6-8)
+    static constexpr int FL = 196;   // flags (int in the first 4 bytes): 1 bad input / pitch guard, 2 R block not SPD
+    static constexpr int SIZE = 200;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(64) k_srbd_lin_rec(SrbdConst K, SrbdIter<T> it, int B, int N, T *rec) {
+    constexpr int NX = 12, RS = LinRec::SIZE, RP = RS + 16 / (int)sizeof(T);
+    using LR = LinRec;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T *sm = reinterpret_cast<T *>(smraw);
+    const long total = (long)B * (N + 1);
+    const long base = (long)blockIdx.x * blockDim.x;
+    const long g = base + threadIdx.x;
+    if (g < total) {
+        T *o = sm + (size_t)threadIdx.x * RP;
+        const int b = (int)(g / (N + 1)), i = (int)(g - (long)b * (N + 1));
+        const size_t sx = (size_t)b * (N + 2) + i, st = (size_t)g;
+        T xv[NX], xn[NX], uv[NX], fe[NX], lv[NX], ln[NX], xr[NX];
+        ld_row<T, NX, true>(xv, it.x + sx * NX);
+        ld_row<T, NX, true>(xn, it.x + (sx + 1) * NX);
+        ld_row<T, NX, true>(lv, it.lam + sx * NX);
+        ld_row<T, NX, true>(ln, it.lam + (sx + 1) * NX);
+        ld_row<T, NX, true>(xr, it.xref + sx * NX);
+        ld_row<T, NX, true>(uv, it.u + st * NX);
+        ld_row<T, NX, true>(fe, it.feet + st * NX);
+        const uint32_t cw = *reinterpret_cast<const uint32_t *>(it.con + st * 4);
+        const uint8_t con[4] = {(uint8_t)(cw & 0xff), (uint8_t)((cw >> 8) & 0xff), (uint8_t)((cw >> 16) & 0xff),
+                                (uint8_t)(cw >> 24)};
+        T urv[NX];
+        if (it.uref) ld_row<T, NX, true>(urv, it.uref + st * NX);
+        else zero(urv);
+        SrbdEval<T> ev;
+        ev.init(K, xv, uv, fe, con);
+        T fa[NX];
+        ev.f_all(K, xv, fa);
+        const T dt = T(K.dt);
+        bool bad = !(fabs((double)xv[4]) < kPitchGuard);
+#pragma unroll
+        for (int k = 0; k < NX; ++k)
+            bad = bad || !isfinite(fa[k]) || !isfinite(xv[k]) || !isfinite(uv[k]) || !isfinite(lv[k]);
+        // q accumulates dt Fx^T lam_{i+1}, rv accumulates dt Fu^T lam_{i+1}
+        T q[NX], rv[NX];
+        zero(q);
+        zero(rv);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) q[6 + a] = dt * ln[a];   // rows 0-2: dt at column 6 + r
+        const T w0 = xv[9], w1 = xv[10], w2 = xv[11];
+        auto put_fa = [&](int k, int row, const T (&v)[NX]) {   // dt * (row of Fx)
+            T d[NX];
+#pragma unroll
+            for (int c = 0; c < NX; ++c) { d[c] = dt * v[c]; q[c] = fma(d[c], ln[row], q[c]); }
+            st_row<T, NX, true>(o + LR::FA + k * NX, d);
+        };
+        {
+            T a3[NX], a4[NX], a5[NX];
+            zero(a3); zero(a4); zero(a5);
+            a3[3] = ev.tp * (ev.cr * w1 - ev.sr * w2);
+            a3[4] = (ev.sr * w1 + ev.cr * w2) * (ev.icp * ev.icp);
+            a3[9] = T(1); a3[10] = ev.sr * ev.tp; a3[11] = ev.cr * ev.tp;
+            a4[3] = -ev.sr * w1 - ev.cr * w2;
+            a4[10] = ev.cr; a4[11] = -ev.sr;
+            a5[3] = (ev.cr * w1 - ev.sr * w2) * ev.icp;
+            a5[4] = (ev.sr * w1 + ev.cr * w2) * ev.sp * (ev.icp * ev.icp);
+            a5[10] = ev.sr * ev.icp; a5[11] = ev.cr * ev.icp;
+            put_fa(0, 3, a3);
+            put_fa(1, 4, a4);
+            put_fa(2, 5, a5);
+        }
+        T bd[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            bd[j] = con[j] ? dt * T(K.imass) : T(0);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) rv[3 * j + a] = fma(bd[j], ln[6 + a], rv[3 * j + a]);
+        }
+        st_row<T, 4, true>(o + LR::BD, bd);
+        T Bw[3][NX];   // dt Fu rows 9-11 (kept for b~)
+        {
+            const T *R = ev.R;
+            const T t0 = ev.tau[0], t1 = ev.tau[1], t2 = ev.tau[2];
+            const T cy = ev.cy, sy = ev.sy, cp = ev.cp, sp = ev.sp, sr = ev.sr, cr = ev.cr;
+            const T v0[3] = {T(0), R[2] * t0 + R[5] * t1 + R[8] * t2, -(R[1] * t0 + R[4] * t1 + R[7] * t2)};
+            const T dP[9] = {-cy * sp, cy * cp * sr, cy * cp * cr, -sy * sp, sy * cp * sr, sy * cp * cr, -cp, -sp * sr, -sp * cr};
+            T v1[3], v2[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                v1[c] = dP[c] * t0 + dP[3 + c] * t1 + dP[6 + c] * t2;
+                v2[c] = -R[3 + c] * t0 + R[c] * t1;
+            }
+            T Iw[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) Iw[c] = T(K.I[3 * c]) * w0 + T(K.I[3 * c + 1]) * w1 + T(K.I[3 * c + 2]) * w2;
+            const T Wx[9] = {T(0), -w2, w1, w2, T(0), -w0, -w1, w0, T(0)};
+            const T IWx[9] = {T(0), -Iw[2], Iw[1], Iw[2], T(0), -Iw[0], -Iw[1], Iw[0], T(0)};
+            const T SF[9] = {T(0), -ev.F[2], ev.F[1], ev.F[2], T(0), -ev.F[0], -ev.F[1], ev.F[0], T(0)};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                T Ii[3], Ma[3], ar[NX], br[NX];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) Ii[c] = T(K.Iinv[3 * a + c]);
+#pragma unroll
+                for (int bb = 0; bb < 3; ++bb) Ma[bb] = Ii[0] * R[3 * bb] + Ii[1] * R[3 * bb + 1] + Ii[2] * R[3 * bb + 2];
+                zero(ar);
+                zero(br);
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) ar[cc] = Ma[0] * SF[cc] + Ma[1] * SF[3 + cc] + Ma[2] * SF[6 + cc];
+                ar[3] = Ii[0] * v0[0] + Ii[1] * v0[1] + Ii[2] * v0[2];
+                ar[4] = Ii[0] * v1[0] + Ii[1] * v1[1] + Ii[2] * v1[2];
+                ar[5] = Ii[0] * v2[0] + Ii[1] * v2[1] + Ii[2] * v2[2];
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    T s = T(0);
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const T WI = Wx[3 * c] * T(K.I[cc]) + Wx[3 * c + 1] * T(K.I[3 + cc]) + Wx[3 * c + 2] * T(K.I[6 + cc]);
+                        s += Ii[c] * (WI - IWx[3 * c + cc]);
+                    }
+                    ar[9 + cc] = -s;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (!con[j]) continue;
+                    const T rx = fe[3 * j] - xv[0], ry = fe[3 * j + 1] - xv[1], rz = fe[3 * j + 2] - xv[2];
+                    const T Sr[9] = {T(0), -rz, ry, rz, T(0), -rx, -ry, rx, T(0)};
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) br[3 * j + cc] = Ma[0] * Sr[cc] + Ma[1] * Sr[3 + cc] + Ma[2] * Sr[6 + cc];
+                }
+                put_fa(3 + a, 9 + a, ar);
+#pragma unroll
+                for (int c = 0; c < NX; ++c) { Bw[a][c] = dt * br[c]; rv[c] = fma(Bw[a][c], ln[9 + a], rv[c]); }
+                st_row<T, NX, true>(o + LR::FB + a * NX, Bw[a]);
+            }
+        }
+        // b_i, q_i
+        T c[NX];
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            c[k] = (xv[k] - xn[k]) + dt * fa[k];
+            q[k] = T(K.wx[k]) * (xv[k] - xr[k]) + ((ln[k] - lv[k]) + q[k]);
+        }
+        st_row<T, NX, true>(o + LR::C, c);
+        st_row<T, NX, true>(o + LR::Q, q);
+        // r_i, R blocks and z = R^-1 r per foot block (adjugate; SPD check)
+        const T rho = T(it.rho_of(b));
+        bool rfail = false;
+        T z[NX];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool stance = con[j] != 0;
+            const T wu = stance ? T(K.wu_st) : T(K.wu_sw);
+            const FootBarrier<T> fb = foot_barrier<T>(K, uv[3 * j], uv[3 * j + 1], uv[3 * j + 2]);
+            const T gb[3] = {fb.gx, fb.gy, fb.gz};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                T rg = wu * (uv[3 * j + a] - urv[3 * j + a]);
+                if (stance) rg += gb[a];
+                rv[3 * j + a] += rg;
+            }
+            const T hs = stance ? T(1) : T(0);
+            const T a00 = wu + rho + hs * fb.hxx, a11 = wu + rho + hs * fb.hyy, a22 = wu + rho + hs * fb.hzz;
+            const T a01 = T(0), a02 = hs * fb.hxz, a12 = hs * fb.hyz;
+            const T a10 = a01, a20 = a02, a21 = a12;
+            const T Rb[3][3] = {{a00, a01, a02}, {a10, a11, a12}, {a20, a21, a22}};
+#pragma unroll
+            for (int a = 0; a < 3; ++a) st_row<T, 3, false>(o + LR::RB + 3 * (3 * j + a), Rb[a]);
+            const T c00 = a11 * a22 - a12 * a21, c01 = a02 * a21 - a01 * a22, c02 = a01 * a12 - a02 * a11;
+            const T c10 = a12 * a20 - a10 * a22, c11 = a00 * a22 - a02 * a20, c12 = a02 * a10 - a00 * a12;
+            const T c20 = a10 * a21 - a11 * a20, c21 = a01 * a20 - a00 * a21, c22 = a00 * a11 - a01 * a10;
+            const T det = a00 * c00 + a01 * c10 + a02 * c20;
+            rfail = rfail || !(a00 > T(0)) || !(c22 > T(0)) || !(det > T(0)) || !isfinite(det);
+            const T r0 = rv[3 * j], r1 = rv[3 * j + 1], r2 = rv[3 * j + 2];
+            z[3 * j] = (c00 * r0 + c01 * r1 + c02 * r2) / det;
+            z[3 * j + 1] = (c10 * r0 + c11 * r1 + c12 * r2) / det;
+            z[3 * j + 2] = (c20 * r0 + c21 * r1 + c22 * r2) / det;
+        }
+        st_row<T, NX, true>(o + LR::RV, rv);
+        // b~ = b - B R^-1 r  (B rows 0-5 zero, rows 6-8 dt/m on the stance feet, rows 9-11 Bw)
+        T bt[NX];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) bt[k] = c[k];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            T s6 = T(0), s9 = T(0);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s6 = fma(bd[j], z[3 * j + a], s6);
+#pragma unroll
+            for (int t = 0; t < NX; ++t) s9 = fma(Bw[a][t], z[t], s9);
+            bt[6 + a] = c[6 + a] - s6;
+            bt[9 + a] = c[9 + a] - s9;
+        }
+        st_row<T, NX, true>(o + LR::BT, bt);
+#pragma unroll
+        for (int k = LR::FL; k < LR::SIZE; ++k) o[k] = T(0);
+        reinterpret_cast<int *>(o + LR::FL)[0] = (bad ? 1 : 0) | (rfail ? 2 : 0);
+    }
+    __syncthreads();
+    // coalesced copy of the block's records (contiguous in global memory) in 16-byte granules
+    const long nrec = total - base < (long)blockDim.x ? total - base : (long)blockDim.x;
+    if (nrec <= 0) return;
+    constexpr int EPC = 16 / (int)sizeof(T);
+    T *dst = rec + (size_t)base * RS;
+    for (long e = (long)threadIdx.x * EPC; e < nrec * RS; e += (long)blockDim.x * EPC) {
+        const int t = (int)(e / RS), k = (int)(e - (long)t * RS);
+        *reinterpret_cast<int4 *>(dst + e) = *reinterpret_cast<const int4 *>(sm + (size_t)t * RP + k);
+    }
+}
+
+// Per-worker shared memory of the record-fed fold: matrices of the recursion plus a two-slot ring
+// of linearisation records (stage i-1 lands while stage i is processed).
+template <typename T>
+struct FoldRecSmem {
+    T in[2][LinRec::SIZE];
+    T P[144], A[144], B[144], X[144], V[144], K[144];
+    T p[12], g[12], w[12], k[12];
+};
+
+// k_srbd_bwd_fold fed by k_srbd_lin_rec: the same recursion (policy, D7 combine, Eq. 5 rows,
+// Eq. 11-14) without the linearisation in the sequential loop.
+template <typename T, int MINB, int TPB = 64>
+__global__ void __launch_bounds__(TPB, MINB * 128 / TPB) k_srbd_bwd_fold_rec(SrbdConst K, SrbdIter<T> it, int B, int N,
+                                                                             LqWork<T> ws, const T *rec, int32_t *info_out) {
+    constexpr int WS = 16, NX = 12;
+    constexpr int TP = TE<NX>::SIZE;
+    using KL = KE<NX, NX>;
+    using LR = LinRec;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    FoldRecSmem<T> &s = reinterpret_cast<FoldRecSmem<T> *>(smraw)[threadIdx.x / WS];
+    const int lane = worker_lane<WS>();
+    const unsigned mask = 0xffffffffu;
+    const int b_raw = blockIdx.x * (blockDim.x / WS) + threadIdx.x / WS;
+    if (__all_sync(0xffffffffu, b_raw >= B)) return;
+    const bool live = b_raw < B;
+    const int b = live ? b_raw : B - 1;
+    const int r = lane < NX ? lane : 0;
+    const bool act = lane < NX;
+    const bool wr_g = act && live;
+    const T *xb = it.x + (size_t)b * (N + 2) * NX;
+    const T *lb = it.lam + (size_t)b * (N + 2) * NX;
+    const T *xrb = it.xref + (size_t)b * (N + 2) * NX;
+    const T *rb = rec + (size_t)b * (N + 1) * LR::SIZE;
+    T *Pp = ws.Pp + (size_t)b * (N + 2) * TP;
+    T *Kk = ws.Kk + (size_t)b * (N + 1) * KL::SIZE;
+    T *Te = ws.tel + (size_t)b * (N + 1) * TP;
+    const T dt = T(K.dt);
+    bool bad = false;
+    int fail = INT_MAX;
+    constexpr int EPC = 16 / (int)sizeof(T), NCH = LR::SIZE / EPC;
+    auto prefetch = [&](int sg) {
+        if (sg >= 0) {
+            T *d = s.in[sg & 1];
+            const T *src = rb + (size_t)sg * LR::SIZE;
+            for (int c = lane; c < NCH; c += WS) cp_async16(d + c * EPC, src + c * EPC);
+        }
+        cp_async_commit();
+    };
+    prefetch(N);
+    // terminal element e_{N+1} = suffix s_{N+1}: P = W_N, p = W_N (x_{N+1} - xref) - lam_{N+1}  (Eq. 13)
+    {
+        const T xr = xb[(N + 1) * NX + r], lr = lb[(N + 1) * NX + r];
+        T Prow[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) Prow[j] = (j == r) ? T(K.wxt[r]) : T(0);
+        const T pr = T(K.wxt[r]) * (xr - xrb[(N + 1) * NX + r]) - lr;
+        bad = bad || !isfinite(xr) || !isfinite(lr);
+        if (act) {
+            st_row<T, NX, true>(s.P + r * NX, Prow);
+            s.p[r] = pr;
+        }
+        if (wr_g) {
+            st_row<T, NX, true>(Pp + (size_t)(N + 1) * TP + r * NX, Prow);
+            Pp[(size_t)(N + 1) * TP + NX * NX + r] = pr;
+        }
+    }
+    // this lane's rows of the record: dt Fx row (3-5, 9-11), dt Fu row (9-11), R foot block row
+    const int fa_row = (r >= 3 && r <= 5) ? r - 3 : (r >= 9 ? r - 6 : 0);
+    const bool has_fa = (r >= 3 && r <= 5) || r >= 9;
+    const int fb_row = r >= 9 ? r - 9 : 0;
+    const bool has_fb = r >= 9;
+    const int jf = r / 3, a6 = r - 6;
+    for (int i = N; i >= 0; --i) {
+        prefetch(i - 1);
+        cp_async_wait<1>();
+        __syncwarp(mask);
+        const T *cur = s.in[i & 1];
+        {
+            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0];
+            bad = bad || (fl & 1);
+            if (fl & 2) fail = min(fail, i + 1);
+        }
+        T arow[NX], brow[NX], Rrow[NX];
+        {
+            T fr[NX], fb[NX], bd[4];
+            ld_row<T, NX, true>(fr, cur + LR::FA + fa_row * NX);
+            ld_row<T, NX, true>(fb, cur + LR::FB + fb_row * NX);
+            ld_row<T, 4, true>(bd, cur + LR::BD);
+            const T r0 = cur[LR::RB + 3 * r], r1 = cur[LR::RB + 3 * r + 1], r2 = cur[LR::RB + 3 * r + 2];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {
+                arow[j] = (j == r ? T(1) : T(0)) + (has_fa ? fr[j] : ((j >= 6 && j < 9 && j - 6 == r) ? dt : T(0)));
+                brow[j] = has_fb ? fb[j] : ((a6 >= 0 && a6 < 3 && j % 3 == a6) ? bd[j / 3] : T(0));
+                const T rj = (j % 3 == 0) ? r0 : (j % 3 == 1) ? r1 : r2;
+                Rrow[j] = (j / 3 == jf) ? rj : T(0);
+            }
+        }
+        const T qr = cur[LR::Q + r], rr = cur[LR::RV + r];
+        const T *sc = cur + LR::C, *sbt = cur + LR::BT;
+        if (act) {
+            st_row<T, NX, true>(s.A + r * NX, arow);
+            st_row<T, NX, true>(s.B + r * NX, brow);
+        }
+        __syncwarp(mask);
+        // ---------------- policy for stage i from s_{i+1} = (P_{i+1}, p_{i+1}) and the D7 combine
+        T prow[NX];
+        ld_row<T, NX, true>(prow, s.P + r * NX);
+        {
+            T pb[NX];
+            zero(pb);
+            row_mat<T, NX, NX, NX>(pb, prow, s.B);
+            const T gv = row_dot<T, NX>(prow, sc, s.p[r]);
+            if (act) { st_row<T, NX, true>(s.V + r * NX, pb); s.g[r] = gv; }
+        }
+        __syncwarp(mask);
+        {
+            // policy system  G [K | k] = -[H | h]  (G = R + B^T P B SPD, H = B^T P A, h = B^T (p + P b) + r)
+            T bcol[NX], pbcol[NX], G[NX], rhs[NX + 2];
+            ld_col<T, NX>(bcol, s.B + r, NX);
+            ld_col<T, NX>(pbcol, s.V + r, NX);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) G[j] = Rrow[j];
+            row_mat<T, NX, NX, NX>(G, bcol, s.V);
+            zero(*reinterpret_cast<T(*)[NX]>(rhs));
+            row_mat<T, NX, NX, NX>(*reinterpret_cast<T(*)[NX]>(rhs), pbcol, s.A);
+            rhs[NX] = row_dot<T, NX>(bcol, s.g, rr);
+            rhs[NX + 1] = T(0);
+            const T wr = row_dot<T, NX>(prow, sbt, s.p[r]);   // w = p_{i+1} + P_{i+1} b~_i
+            if (act) s.w[r] = wr;
+            int pr1;
+            const bool ok1 = gauss_jordan<T, WS, NX, NX + 2, false, true>(mask, G, rhs, lane, NX, pr1);
+            if (!ok1) fail = min(fail, i + 1);
+            if (act) {
+                T kr[NX];
+#pragma unroll
+                for (int j = 0; j < NX; ++j) kr[j] = -rhs[j];
+                st_row<T, NX, true>(s.K + r * NX, kr);
+                s.k[r] = -rhs[NX];
+                if (live) {
+                    st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + r * NX, kr);
+                    Kk[(size_t)i * KL::SIZE + KL::k + r] = -rhs[NX];
+                }
+            }
+        }
+        __syncwarp(mask);
+        {
+            // closed-loop transition (Abar_i, bbar_i) = (A + B K, B k + b)  (Eq. 14) = X of the combine (D7)
+            T abar[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) abar[j] = arow[j];
+            row_mat<T, NX, NX, NX>(abar, brow, s.K);
+            const T bb = row_dot<T, NX>(brow, s.k, sc[r]);
+            if (act) st_row<T, NX, true>(s.X + r * NX, abar);
+            if (wr_g) {
+                st_row<T, NX, true>(Te + (size_t)i * TP + r * NX, abar);
+                Te[(size_t)i * TP + NX * NX + r] = bb;
+            }
+        }
+        __syncwarp(mask);
+        {
+            T V[NX];
+            zero(V);
+            row_mat<T, NX, NX, NX>(V, prow, s.X);
+            if (act) st_row<T, NX, true>(s.V + r * NX, V);
+        }
+        T pn;
+        {
+            T xc[NX];
+            ld_col<T, NX>(xc, s.X + r, NX);
+            pn = row_dot<T, NX>(xc, s.w, qr);
+        }
+        __syncwarp(mask);
+        T Pn[NX];
+        {
+            T acol[NX];
+            ld_col<T, NX>(acol, s.A + r, NX);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) Pn[j] = (j == r) ? T(K.wx[r]) : T(0);
+            row_mat<T, NX, NX, NX>(Pn, acol, s.V);
+        }
+        __syncwarp(mask);
+        symmetrize_rows<T, NX>(Pn, s.V, mask, lane);
+        if (act) {
+            st_row<T, NX, true>(s.P + r * NX, Pn);
+            s.p[r] = pn;
+        }
+        if (wr_g) {
+            st_row<T, NX, true>(Pp + (size_t)i * TP + r * NX, Pn);
+            Pp[(size_t)i * TP + NX * NX + r] = pn;
+        }
+        __syncwarp(mask);
+    }
+    {
+        const T x0 = it.x0[(size_t)b * NX + r];
+        bad = bad || !isfinite(x0);
+    }
+    unsigned vb = bad ? 1u : 0u;
+#pragma unroll
+    for (int off = WS / 2; off >= 1; off >>= 1) vb |= __shfl_xor_sync(0xffffffffu, vb, off, WS);
+    const bool any_bad = vb != 0u;
+    if (lane == 0 && live) info_out[b] = any_bad ? -1 : (fail != INT_MAX ? fail : 0);
+}
+
+// ------------------------------------------ record-fed fold, one instance per warp (two lanes per row)
+// The recursion of k_srbd_bwd_fold_rec with every 12 x 12 matrix split by COLUMN halves over the
+// two half-warps: lane (h, r) = lane 16 h + r owns row r, columns [6h, 6h + 6).  Twice the
+// resident warps of the two-instances-per-warp fold for the same batch (the fold is latency-bound:
+// one dependent chain per instance), and the products skip the structurally zero rows of B
+// (rows 0-5: P B and B^T (P B) over k = 6..11 only).
+// Shared-memory matrices have a row stride of 16 (halves at columns 0..5 and 8..13: 16-byte
+// aligned half rows).  B and P B are stored with PERMUTED columns (natural column k at position
+// (k & 1) * 6 + (k >> 1)), so G = R + B^T P B comes out with the even columns in half 0 and the
+// odd ones in half 1: the elimination of column k then only shuffles the columns > k that are
+// still live in either half (36 instead of 72 shuffles over the 12 pivots).
+template <typename T>
+struct FoldWSmem {
+    static constexpr int LD = 16, MS = 12 * LD;
+    T in[2][LinRec::SIZE];
+    T P[MS], A[MS], Bp[MS], PB[MS], X[MS], K[MS];
+    T p[12], g[12], w[12], k[12];
+};
+
+__device__ __forceinline__ constexpr int fw_st(int j) { return j + (j >= 6 ? 2 : 0); }         // storage column
+__device__ __forceinline__ constexpr int fw_perm(int k) { return (k & 1) * 6 + (k >> 1); }     // permuted position
+
+template <typename T>
+__device__ __forceinline__ void ld6(T (&d)[6], const T *__restrict__ s) {   // 16-byte aligned source
+    if constexpr (sizeof(T) == 4) {
+        const float4 a = *reinterpret_cast<const float4 *>(s);
+        const float2 c = *reinterpret_cast<const float2 *>(s + 4);
+        d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w; d[4] = c.x; d[5] = c.y;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 6; j += 2) {
+            const double2 a = *reinterpret_cast<const double2 *>(s + j);
+            d[j] = a.x; d[j + 1] = a.y;
+        }
+    }
+}
+template <typename T>
+__device__ __forceinline__ void st6(T *__restrict__ d, const T (&v)[6]) {   // 16-byte aligned destination
+    if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4 *>(d) = make_float4(v[0], v[1], v[2], v[3]);
+        *reinterpret_cast<float2 *>(d + 4) = make_float2(v[4], v[5]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 6; j += 2) *reinterpret_cast<double2 *>(d + j) = make_double2(v[j], v[j + 1]);
+    }
+}
+template <typename T>
+__device__ __forceinline__ void ld6u(T (&d)[6], const T *__restrict__ s) {  // 8-byte aligned source (half of a 12-row)
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int j = 0; j < 6; j += 2) {
+            const float2 a = *reinterpret_cast<const float2 *>(s + j);
+            d[j] = a.x; d[j + 1] = a.y;
+        }
+    } else {
+        ld6<T>(d, s);
+    }
+}
+template <typename T>
+__device__ __forceinline__ void st6u(T *__restrict__ d, const T (&v)[6]) {
+    if constexpr (sizeof(T) == 4) {
+#pragma unroll
+        for (int j = 0; j < 6; j += 2) *reinterpret_cast<float2 *>(d + j) = make_float2(v[j], v[j + 1]);
+    } else {
+        st6<T>(d, v);
+    }
+}
+// out[j] += sum_{k in [K0, K1)} a[k] Y[k][half j]  (Y rows of stride 16, pointer at the half's first column)
+template <typename T, int K0, int K1>
+__device__ __forceinline__ void row_mat_h(T (&out)[6], const T (&a)[12], const T *__restrict__ Y) {
+#pragma unroll
+    for (int k = K0; k < K1; ++k) {
+        T y[6];
+        ld6<T>(y, Y + k * 16);
+#pragma unroll
+        for (int j = 0; j < 6; j += 2) ffma2(a[k], a[k], y[j], y[j + 1], out[j], out[j + 1]);
+    }
+}
+// full natural row r of a stride-16 matrix
+template <typename T>
+__device__ __forceinline__ void ld_row16(T (&d)[12], const T *__restrict__ row) {
+    T a[6], c[6];
+    ld6<T>(a, row);
+    ld6<T>(c, row + 8);
+#pragma unroll
+    for (int j = 0; j < 6; ++j) { d[j] = a[j]; d[6 + j] = c[j]; }
+}
+
+template <typename T, int MINB>
+__global__ void __launch_bounds__(64, MINB) k_srbd_bwd_fold_w(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+                                                              const T *rec, int32_t *info_out) {
+    constexpr int NX = 12, LD = 16;
+    constexpr int TP = TE<NX>::SIZE;
+    using KL = KE<NX, NX>;
+    using LR = LinRec;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    FoldWSmem<T> &s = reinterpret_cast<FoldWSmem<T> *>(smraw)[threadIdx.x / 32];
+    const int lane = threadIdx.x & 31, h = lane >> 4, r16 = lane & 15;
+    const int b = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (b >= B) return;   // warp-uniform
+    const int r = r16 < NX ? r16 : 0;
+    const bool act = r16 < NX;
+    const bool act0 = act && h == 0;   // writer of per-row scalars
+    const int c0 = 6 * h;              // natural columns [c0, c0 + 6) of this lane
+    const int so = 8 * h;              // their storage offset in a stride-16 row
+    const int rp = fw_st(fw_perm(r));  // storage column of natural column r in a permuted matrix
+    const T *xb = it.x + (size_t)b * (N + 2) * NX;
+    const T *lb = it.lam + (size_t)b * (N + 2) * NX;
+    const T *xrb = it.xref + (size_t)b * (N + 2) * NX;
+    const T *rb = rec + (size_t)b * (N + 1) * LR::SIZE;
+    T *Pp = ws.Pp + (size_t)b * (N + 2) * TP;
+    T *Kk = ws.Kk + (size_t)b * (N + 1) * KL::SIZE;
+    T *Te = ws.tel + (size_t)b * (N + 1) * TP;
+    const T dt = T(K.dt);
+    bool bad = false;
+    int fail = INT_MAX;
+    constexpr int EPC = 16 / (int)sizeof(T), NCH = LR::SIZE / EPC;
+    auto prefetch = [&](int sg) {
+        if (sg >= 0) {
+            T *d = s.in[sg & 1];
+            const T *src = rb + (size_t)sg * LR::SIZE;
+            for (int c = lane; c < NCH; c += 32) cp_async16(d + c * EPC, src + c * EPC);
+        }
+        cp_async_commit();
+    };
+    prefetch(N);
+    // terminal element e_{N+1}: P = W_N, p = W_N (x_{N+1} - xref) - lam_{N+1}  (Eq. 13)
+    {
+        const T xr = xb[(N + 1) * NX + r], lr = lb[(N + 1) * NX + r];
+        T Ph[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) Ph[j] = (c0 + j == r) ? T(K.wxt[r]) : T(0);
+        const T pr = T(K.wxt[r]) * (xr - xrb[(N + 1) * NX + r]) - lr;
+        bad = bad || !isfinite(xr) || !isfinite(lr);
+        if (act) {
+            st6<T>(s.P + r * LD + so, Ph);
+            st6u<T>(Pp + (size_t)(N + 1) * TP + r * NX + c0, Ph);
+        }
+        if (act0) {
+            s.p[r] = pr;
+            Pp[(size_t)(N + 1) * TP + NX * NX + r] = pr;
+        }
+    }
+    const int fa_row = (r >= 3 && r <= 5) ? r - 3 : (r >= 9 ? r - 6 : 0);
+    const bool has_fa = (r >= 3 && r <= 5) || r >= 9;
+    const int fb_row = r >= 9 ? r - 9 : 0;
+    const bool has_fb = r >= 9;
+    const int jf = r / 3, a6 = r - 6;
+    for (int i = N; i >= 0; --i) {
+        prefetch(i - 1);
+        cp_async_wait<1>();
+        __syncwarp();
+        const T *cur = s.in[i & 1];
+        {
+            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0];
+            bad = bad || (fl & 1);
+            if (fl & 2) fail = min(fail, i + 1);
+        }
+        // ---------------- this lane's parts of A_i (half row), B_i (full row), R_i (permuted half row)
+        T ah[6], brow[NX], Rp[6];
+        {
+            T fr[6], fb[NX], bd[4];
+            ld6u<T>(fr, cur + LR::FA + fa_row * NX + c0);
+            ld_row<T, NX, true>(fb, cur + LR::FB + fb_row * NX);
+            ld_row<T, 4, true>(bd, cur + LR::BD);
+            const T r0 = cur[LR::RB + 3 * r], r1 = cur[LR::RB + 3 * r + 1], r2 = cur[LR::RB + 3 * r + 2];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) {
+                const int jn = c0 + j;
+                ah[j] = (jn == r ? T(1) : T(0)) + (has_fa ? fr[j] : ((r < 3 && jn == 6 + r) ? dt : T(0)));
+            }
+#pragma unroll
+            for (int j = 0; j < NX; ++j)
+                brow[j] = has_fb ? fb[j] : ((a6 >= 0 && a6 < 3 && j % 3 == a6) ? bd[j / 3] : T(0));
+#pragma unroll
+            for (int jj = 0; jj < 6; ++jj) {
+                const int k = 2 * jj + h;   // natural column of permuted position 6 h + jj
+                const int kk = k - 3 * jf;
+                Rp[jj] = (kk == 0) ? r0 : (kk == 1) ? r1 : (kk == 2) ? r2 : T(0);
+            }
+        }
+        const T qr = cur[LR::Q + r], rr = cur[LR::RV + r];
+        const T *sc = cur + LR::C, *sbt = cur + LR::BT;
+        if (act) {
+            st6<T>(s.A + r * LD + so, ah);
+            T bp[6];
+#pragma unroll
+            for (int jj = 0; jj < 6; ++jj) bp[jj] = h ? brow[2 * jj + 1] : brow[2 * jj];
+            st6<T>(s.Bp + r * LD + so, bp);
+        }
+        __syncwarp();
+        // ---------------- policy for stage i from s_{i+1} = (P_{i+1}, p_{i+1})
+        T prow[NX];
+        ld_row16<T>(prow, s.P + r * LD);
+        {
+            T pb[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) pb[j] = T(0);
+            row_mat_h<T, 6, 12>(pb, prow, s.Bp + so);          // P B (B rows 0-5 are zero), permuted columns
+            const T gv = row_dot<T, NX>(prow, sc, s.p[r]);     // g = p_{i+1} + P_{i+1} b_i
+            const T wv = row_dot<T, NX>(prow, sbt, s.p[r]);    // w = p_{i+1} + P_{i+1} b~_i
+            if (act) st6<T>(s.PB + r * LD + so, pb);
+            if (act0) { s.g[r] = gv; s.w[r] = wv; }
+        }
+        __syncwarp();
+        T x[7];   // right-hand sides: H[r][c0..c0+6), and h[r] in half 0
+        T a[6];   // G[r][2 jj + h]
+        {
+            T bc[6], pbc[NX];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) bc[k] = s.Bp[(6 + k) * LD + rp];     // B[6 + k][r]
+#pragma unroll
+            for (int k = 0; k < NX; ++k) pbc[k] = s.PB[k * LD + rp];         // (P B)[k][r]
+#pragma unroll
+            for (int jj = 0; jj < 6; ++jj) a[jj] = Rp[jj];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) {                                     // G = R + B^T (P B)
+                T y[6];
+                ld6<T>(y, s.PB + (6 + k) * LD + so);
+#pragma unroll
+                for (int j = 0; j < 6; j += 2) ffma2(bc[k], bc[k], y[j], y[j + 1], a[j], a[j + 1]);
+            }
+            T hh[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) hh[j] = T(0);
+            row_mat_h<T, 0, 12>(hh, pbc, s.A + so);                           // H = (P B)^T A
+            T hv = rr;                                                          // h = B^T g + r
+#pragma unroll
+            for (int k = 0; k < 6; ++k) hv = fma(bc[k], s.g[6 + k], hv);
+#pragma unroll
+            for (int j = 0; j < 6; ++j) x[j] = hh[j];
+            x[6] = h == 0 ? hv : T(0);
+        }
+        {
+            // SPD Gauss-Jordan on G [K | k] = -[H | h] (unnormalised sweep, pivot rows scaled at the end)
+            bool ok = true;
+            T mypiv = T(1);
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                const int hk = k & 1, jk = k >> 1;
+                const T own = a[jk];
+                const T rk = rcp_rn(own);
+                const T ark = __shfl_sync(0xffffffffu, own, 16 * hk + r);
+                const T pv = __shfl_sync(0xffffffffu, own, 16 * hk + k);
+                const T rpv = __shfl_sync(0xffffffffu, rk, 16 * hk + k);
+                ok = ok && (pv > T(0)) && isfinite(pv);
+                const bool isp = r16 == k;
+                const T f = isp ? T(0) : ark * rpv;
+                if (isp) mypiv = pv;
+                const int src = 16 * h + k;
+#pragma unroll
+                for (int jj = 0; jj < 6; ++jj)
+                    if (2 * jj + 1 > k) a[jj] = fma(-f, __shfl_sync(0xffffffffu, a[jj], src), a[jj]);
+#pragma unroll
+                for (int j = 0; j < 6; j += 2) {
+                    const T p0 = __shfl_sync(0xffffffffu, x[j], src), p1 = __shfl_sync(0xffffffffu, x[j + 1], src);
+                    ffma2(-f, -f, p0, p1, x[j], x[j + 1]);
+                }
+                x[6] = fma(-f, __shfl_sync(0xffffffffu, x[6], src), x[6]);
+            }
+            const T inv = rcp_rn(mypiv);
+#pragma unroll
+            for (int j = 0; j < 7; ++j) x[j] *= -inv;   // [K | k] = -G^-1 [H | h]
+            if (!ok) fail = min(fail, i + 1);
+        }
+        {
+            T kh[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) kh[j] = x[j];
+            if (act) {
+                st6<T>(s.K + r * LD + so, kh);
+                st6u<T>(Kk + (size_t)i * KL::SIZE + KL::K + r * NX + c0, kh);
+            }
+            if (act0) {
+                s.k[r] = x[6];
+                Kk[(size_t)i * KL::SIZE + KL::k + r] = x[6];
+            }
+        }
+        __syncwarp();
+        {
+            // closed-loop transition (Abar_i, bbar_i) = (A + B K, B k + b)  (Eq. 14) = X of the D7 combine
+            T ab[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) ab[j] = ah[j];
+            row_mat_h<T, 0, 12>(ab, brow, s.K + so);
+            const T bb = row_dot<T, NX>(brow, s.k, sc[r]);
+            if (act) {
+                st6<T>(s.X + r * LD + so, ab);
+                st6u<T>(Te + (size_t)i * TP + r * NX + c0, ab);
+            }
+            if (act0) Te[(size_t)i * TP + NX * NX + r] = bb;
+        }
+        __syncwarp();
+        T pn;
+        {
+            T v[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) v[j] = T(0);
+            row_mat_h<T, 0, 12>(v, prow, s.X + so);            // V = P_{i+1} Abar_i
+            if (act) st6<T>(s.PB + r * LD + so, v);
+            T xc[NX];
+#pragma unroll
+            for (int k = 0; k < NX; ++k) xc[k] = s.X[k * LD + fw_st(r)];
+            pn = row_dot<T, NX>(xc, s.w, qr);                  // p_i = q_i + Abar_i^T w
+        }
+        __syncwarp();
+        T Pn[6];
+        {
+            T ac[NX];
+#pragma unroll
+            for (int k = 0; k < NX; ++k) ac[k] = s.A[k * LD + fw_st(r)];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) Pn[j] = (c0 + j == r) ? T(K.wx[r]) : T(0);
+            row_mat_h<T, 0, 12>(Pn, ac, s.PB + so);             // P_i = Q + A^T V
+        }
+        // re-symmetrise (R22) through the dead Abar buffer
+        if (act) st6<T>(s.X + r * LD + so, Pn);
+        __syncwarp();
+        {
+            T ct[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) ct[j] = s.X[(c0 + j) * LD + fw_st(r)];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) Pn[j] = T(0.5) * (Pn[j] + ct[j]);
+        }
+        __syncwarp();
+        if (act) {
+            st6<T>(s.P + r * LD + so, Pn);
+            st6u<T>(Pp + (size_t)i * TP + r * NX + c0, Pn);
+        }
+        if (act0) {
+            s.p[r] = pn;
+            Pp[(size_t)i * TP + NX * NX + r] = pn;
+        }
+        __syncwarp();
+    }
+    {
+        const T x0 = it.x0[(size_t)b * NX + r];
+        bad = bad || !isfinite(x0);
+    }
+    const bool any_bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) info_out[b] = any_bad ? -1 : (fail != INT_MAX ? fail : 0);
+}
+
+// ------------------------------------- record-fed fold, two rows per lane (five instances per warp)
+// The fold is bound by the shared-memory data pipe (LDS / STS / SHFL wavefronts; ncu r3_v1: 88 %
+// of peak), not by the FMA pipe: a row-per-lane 12 x 12 product makes every lane load all 144
+// entries of the other operand.  Here a worker is 6 lanes, lane l owns rows l and l + 6 of every
+// matrix (so every loaded operand row feeds two FFMA2 row updates), a warp carries 5 instances
+// (lanes 30, 31 shadow lane 29 and store nothing), and the products use the SRBD structure of the
+// linearisation record: B has zero rows 0-5 (P B and B^T P B over k = 6..11), A = I + dt Fx with
+// dt Fx nonzero only in rows 3-5, 9-11 plus dt at (r, 6 + r) for r < 3, so H = (P B)^T A and
+// P = Q + A^T V take the identity from registers and only 6 operand rows from shared memory.
+// Same recursion as k_srbd_bwd_fold_rec (policy Eq. 5 rows, D7 combine, Eq. 11-14, R22).
+template <typename T>
+struct FoldR2Smem {
+    T in[2][LinRec::SIZE];
+    T P[144], B6[72], PB[144], K[144], X[144];
+    T p[12], w[12], k[12];
+    T pad[sizeof(T) == 4 ? 8 : 6];   // slice stride = 4 (mod 32) words: the 5 workers' LDS.128 hit distinct banks
+};
+
+template <typename T>
+__global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
+                                                           const T *rec, int32_t *info_out) {
+    constexpr int NX = 12, NW = 5;
+    constexpr int TP = TE<NX>::SIZE;
+    using KL = KE<NX, NX>;
+    using LR = LinRec;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int L = threadIdx.x & 31;
+    const int w = L < 30 ? L / 6 : NW - 1;
+    const int l = L < 30 ? L - 6 * w : 5;
+    const bool lane_act = L < 30;
+    FoldR2Smem<T> &s = reinterpret_cast<FoldR2Smem<T> *>(smraw)[(threadIdx.x >> 5) * NW + w];
+    const int b_raw = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NW + w;
+    if (__all_sync(0xffffffffu, b_raw >= B)) return;
+    const bool live = b_raw < B;
+    const int b = live ? b_raw : B - 1;
+    const bool act = lane_act && live;        // smem + global writer
+    const int r0 = l, r1 = l + 6;             // this lane's rows
+    const int wb = 6 * w;                     // first lane of the worker
+    const T *xb = it.x + (size_t)b * (N + 2) * NX;
+    const T *lb = it.lam + (size_t)b * (N + 2) * NX;
+    const T *xrb = it.xref + (size_t)b * (N + 2) * NX;
+    const T *rb = rec + (size_t)b * (N + 1) * LR::SIZE;
+    T *Pp = ws.Pp + (size_t)b * (N + 2) * TP;
+    T *Kk = ws.Kk + (size_t)b * (N + 1) * KL::SIZE;
+    T *Te = ws.tel + (size_t)b * (N + 1) * TP;
+    const T dt = T(K.dt);
+    bool bad = false;
+    int fail = INT_MAX;
+    constexpr int EPC = 16 / (int)sizeof(T), NCH = LR::SIZE / EPC;
+    auto prefetch = [&](int sg) {
+        if (sg >= 0 && lane_act) {
+            T *d = s.in[sg & 1];
+            const T *src = rb + (size_t)sg * LR::SIZE;
+            for (int c = l; c < NCH; c += 6) cp_async16(d + c * EPC, src + c * EPC);
+        }
+        cp_async_commit();
+    };
+    prefetch(N);
+    // terminal element e_{N+1}: P = W_N, p = W_N (x_{N+1} - xref) - lam_{N+1}  (Eq. 13)
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+        const int r = l + 6 * sl;
+        const T xr = xb[(N + 1) * NX + r], lr = lb[(N + 1) * NX + r];
+        T Prow[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) Prow[j] = (j == r) ? T(K.wxt[r]) : T(0);
+        const T pr = T(K.wxt[r]) * (xr - xrb[(N + 1) * NX + r]) - lr;
+        bad = bad || !isfinite(xr) || !isfinite(lr);
+        if (act) {
+            st_row<T, NX, true>(s.P + r * NX, Prow);
+            s.p[r] = pr;
+            st_row<T, NX, true>(Pp + (size_t)(N + 1) * TP + r * NX, Prow);
+            Pp[(size_t)(N + 1) * TP + NX * NX + r] = pr;
+        }
+    }
+    const bool lhi = l >= 3;                  // rows l (3..5) and l + 6 (9..11) have dt Fx rows
+    const int fa0 = lhi ? l - 3 : 0, fa1 = lhi ? l : 0;
+    for (int i = N; i >= 0; --i) {
+        prefetch(i - 1);
+        cp_async_wait<1>();
+        __syncwarp();
+        const T *cur = s.in[i & 1];
+        {
+            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0];
+            bad = bad || (fl & 1);
+            if (fl & 2) fail = min(fail, i + 1);
+        }
+        // B row l + 6 (rows 6-8: dt/m on the stance feet' diagonal, 9-11 the record's dt Fu rows)
+        T b1[NX];
+        {
+            T fb[NX], bd[4];
+            ld_row<T, NX, true>(fb, cur + LR::FB + (lhi ? l - 3 : 0) * NX);
+            ld_row<T, 4, true>(bd, cur + LR::BD);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) b1[j] = lhi ? fb[j] : ((j % 3 == l) ? bd[j / 3] : T(0));
+            if (act) st_row<T, NX, true>(s.B6 + l * NX, b1);
+        }
+        __syncwarp();
+        // ---------------- P B (rows 0-5 of B are zero) and w = p + P b~
+        {
+            T pr0[NX], pr1[NX], pb0[NX], pb1[NX];
+            ld_row<T, NX, true>(pr0, s.P + r0 * NX);
+            ld_row<T, NX, true>(pr1, s.P + r1 * NX);
+            zero(pb0);
+            zero(pb1);
+#pragma unroll
+            for (int k = 6; k < 12; ++k) {
+                T y[NX];
+                ld_row<T, NX, true>(y, s.B6 + (k - 6) * NX);
+#pragma unroll
+                for (int j = 0; j < NX; ++j) ffma2(pr0[k], pr1[k], y[j], y[j], pb0[j], pb1[j]);
+            }
+            T bt[NX];
+            ld_row<T, NX, true>(bt, cur + LR::BT);
+            T w0 = s.p[r0], w1 = s.p[r1];
+#pragma unroll
+            for (int k = 0; k < NX; ++k) ffma2(pr0[k], pr1[k], bt[k], bt[k], w0, w1);
+            if (act) {
+                st_row<T, NX, true>(s.PB + r0 * NX, pb0);
+                st_row<T, NX, true>(s.PB + r1 * NX, pb1);
+                s.w[r0] = w0;
+                s.w[r1] = w1;
+            }
+        }
+        __syncwarp();
+        // ---------------- policy system  G [K | k] = -[H | h]:  G = R + (P B)^T B, H = (P B)^T A,
+        //                  h = r + B^T p + (P B)^T b  (P symmetric)
+        T a0[NX], a1[NX], x0[NX + 1], x1[NX + 1];
+        {
+            T pc0[NX], pc1[NX];
+#pragma unroll
+            for (int k = 0; k < NX; ++k) { pc0[k] = s.PB[k * NX + r0]; pc1[k] = s.PB[k * NX + r1]; }
+            {   // R rows (block diagonal, 3 x 3 per foot)
+                const int j0 = r0 / 3, j1 = r1 / 3;
+#pragma unroll
+                for (int j = 0; j < NX; ++j) {
+                    a0[j] = (j / 3 == j0) ? cur[LR::RB + 3 * r0 + (j % 3)] : T(0);
+                    a1[j] = (j / 3 == j1) ? cur[LR::RB + 3 * r1 + (j % 3)] : T(0);
+                }
+            }
+#pragma unroll
+            for (int k = 6; k < 12; ++k) {
+                T y[NX];
+                ld_row<T, NX, true>(y, s.B6 + (k - 6) * NX);
+#pragma unroll
+                for (int j = 0; j < NX; ++j) ffma2(pc0[k], pc1[k], y[j], y[j], a0[j], a1[j]);
+            }
+            // H: identity part and the dt at (k, 6 + k), k < 3, from registers; dt Fx rows 3-5, 9-11 from the record
+#pragma unroll
+            for (int j = 0; j < NX; ++j) { x0[j] = pc0[j]; x1[j] = pc1[j]; }
+#pragma unroll
+            for (int k = 0; k < 3; ++k) ffma2(dt, dt, pc0[k], pc1[k], x0[6 + k], x1[6 + k]);
+#pragma unroll
+            for (int t = 0; t < 6; ++t) {
+                const int k = t < 3 ? 3 + t : 6 + t;
+                T y[NX];
+                ld_row<T, NX, true>(y, cur + LR::FA + t * NX);
+#pragma unroll
+                for (int j = 0; j < NX; ++j) ffma2(pc0[k], pc1[k], y[j], y[j], x0[j], x1[j]);
+            }
+            // h = r + (P B)^T b + B^T p: B^T p over rows 6-8 (one stance term per row) and 9-11 (record)
+            T cv[NX], pv[NX];
+            ld_row<T, NX, true>(cv, cur + LR::C);
+            ld_row<T, NX, true>(pv, s.p);
+            T h0 = cur[LR::RV + r0], h1 = cur[LR::RV + r1];
+#pragma unroll
+            for (int k = 0; k < NX; ++k) ffma2(pc0[k], pc1[k], cv[k], cv[k], h0, h1);
+            {
+                const T bdj0 = cur[LR::BD + r0 / 3], bdj1 = cur[LR::BD + r1 / 3];
+                h0 = fma(bdj0, (r0 % 3 == 0) ? pv[6] : (r0 % 3 == 1) ? pv[7] : pv[8], h0);
+                h1 = fma(bdj1, (r1 % 3 == 0) ? pv[6] : (r1 % 3 == 1) ? pv[7] : pv[8], h1);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const T fb0 = cur[LR::FB + a * NX + r0], fb1 = cur[LR::FB + a * NX + r1];
+                    ffma2(fb0, fb1, pv[9 + a], pv[9 + a], h0, h1);
+                }
+            }
+            x0[NX] = h0;
+            x1[NX] = h1;
+        }
+        {
+            // SPD Gauss-Jordan, unnormalised sweep; pivot k lives in lane k % 6, slot k / 6
+            bool ok = true;
+            T piv0 = T(1), piv1 = T(1);
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                const int pl = k % 6, ps = k / 6;
+                const int src = wb + pl;
+                const T own = ps == 0 ? a0[k] : a1[k];
+                const T rk = rcp_rn(own);
+                const T pvv = __shfl_sync(0xffffffffu, own, src);
+                const T rpv = __shfl_sync(0xffffffffu, rk, src);
+                ok = ok && (pvv > T(0)) && isfinite(pvv);
+                const bool isp0 = ps == 0 && l == pl, isp1 = ps == 1 && l == pl;
+                const T f0 = isp0 ? T(0) : a0[k] * rpv;
+                const T f1 = isp1 ? T(0) : a1[k] * rpv;
+                if (isp0) piv0 = pvv;
+                if (isp1) piv1 = pvv;
+#pragma unroll
+                for (int j = k + 1; j < NX; ++j) {
+                    const T pj = __shfl_sync(0xffffffffu, ps == 0 ? a0[j] : a1[j], src);
+                    ffma2(-f0, -f1, pj, pj, a0[j], a1[j]);
+                }
+#pragma unroll
+                for (int j = 0; j <= NX; ++j) {
+                    const T pj = __shfl_sync(0xffffffffu, ps == 0 ? x0[j] : x1[j], src);
+                    ffma2(-f0, -f1, pj, pj, x0[j], x1[j]);
+                }
+            }
+            const T i0 = -rcp_rn(piv0), i1 = -rcp_rn(piv1);
+#pragma unroll
+            for (int j = 0; j <= NX; ++j) { x0[j] *= i0; x1[j] *= i1; }   // [K | k] = -G^-1 [H | h]
+            if (!ok) fail = min(fail, i + 1);
+        }
+        if (act) {
+            T kr0[NX], kr1[NX];
+#pragma unroll
+            for (int j = 0; j < NX; ++j) { kr0[j] = x0[j]; kr1[j] = x1[j]; }
+            st_row<T, NX, true>(s.K + r0 * NX, kr0);
+            st_row<T, NX, true>(s.K + r1 * NX, kr1);
+            s.k[r0] = x0[NX];
+            s.k[r1] = x1[NX];
+            st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + r0 * NX, kr0);
+            st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + r1 * NX, kr1);
+            Kk[(size_t)i * KL::SIZE + KL::k + r0] = x0[NX];
+            Kk[(size_t)i * KL::SIZE + KL::k + r1] = x1[NX];
+        }
+        __syncwarp();
+        {
+            // closed-loop transition (Abar_i, bbar_i) = (A + B K, B k + b)  (Eq. 14) = X of the D7 combine;
+            // rows 0-5 of B are zero: Abar row l = A row l
+            T ab0[NX], ab1[NX];
+            {
+                T f0[NX], f1[NX];
+                ld_row<T, NX, true>(f0, cur + LR::FA + fa0 * NX);
+                ld_row<T, NX, true>(f1, cur + LR::FA + fa1 * NX);
+#pragma unroll
+                for (int j = 0; j < NX; ++j) {
+                    ab0[j] = (j == r0 ? T(1) : T(0)) + (lhi ? f0[j] : ((j == 6 + l) ? dt : T(0)));
+                    ab1[j] = (j == r1 ? T(1) : T(0)) + (lhi ? f1[j] : T(0));
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                T y[NX];
+                ld_row<T, NX, true>(y, s.K + k * NX);
+#pragma unroll
+                for (int j = 0; j < NX; j += 2) ffma2(b1[k], b1[k], y[j], y[j + 1], ab1[j], ab1[j + 1]);
+            }
+            const T cb0 = cur[LR::C + r0];
+            const T bb1 = row_dot<T, NX>(b1, s.k, cur[LR::C + r1]);
+            if (act) {
+                st_row<T, NX, true>(s.X + r0 * NX, ab0);
+                st_row<T, NX, true>(s.X + r1 * NX, ab1);
+                st_row<T, NX, true>(Te + (size_t)i * TP + r0 * NX, ab0);
+                st_row<T, NX, true>(Te + (size_t)i * TP + r1 * NX, ab1);
+                Te[(size_t)i * TP + NX * NX + r0] = cb0;
+                Te[(size_t)i * TP + NX * NX + r1] = bb1;
+            }
+        }
+        __syncwarp();
+        T pn0, pn1;
+        {
+            // V = P_{i+1} Abar_i (into the dead P B buffer), p_i = q_i + Abar_i^T w
+            T pr0[NX], pr1[NX], v0[NX], v1[NX];
+            ld_row<T, NX, true>(pr0, s.P + r0 * NX);
+            ld_row<T, NX, true>(pr1, s.P + r1 * NX);
+            zero(v0);
+            zero(v1);
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                T y[NX];
+                ld_row<T, NX, true>(y, s.X + k * NX);
+#pragma unroll
+                for (int j = 0; j < NX; ++j) ffma2(pr0[k], pr1[k], y[j], y[j], v0[j], v1[j]);
+            }
+            if (act) {
+                st_row<T, NX, true>(s.PB + r0 * NX, v0);
+                st_row<T, NX, true>(s.PB + r1 * NX, v1);
+            }
+            T wv[NX];
+            ld_row<T, NX, true>(wv, s.w);
+            pn0 = cur[LR::Q + r0];
+            pn1 = cur[LR::Q + r1];
+#pragma unroll
+            for (int k = 0; k < NX; ++k) ffma2(s.X[k * NX + r0], s.X[k * NX + r1], wv[k], wv[k], pn0, pn1);
+        }
+        __syncwarp();
+        T P0[NX], P1[NX];
+        {
+            // P_i = Q + A^T V = Q + V + dt V[r - 6] (rows 6-8) + sum over the dt Fx rows t of dt Fx[t][r] V[t]
+            ld_row<T, NX, true>(P0, s.PB + r0 * NX);
+            ld_row<T, NX, true>(P1, s.PB + r1 * NX);
+            {
+                const T e1 = l < 3 ? dt : T(0);
+#pragma unroll
+                for (int j = 0; j < NX; ++j) P1[j] = fma(e1, P0[j], P1[j]);   // uses V row l (= r0) before Q is added
+            }
+#pragma unroll
+            for (int t = 0; t < 6; ++t) {
+                const int k = t < 3 ? 3 + t : 6 + t;
+                const T c0v = cur[LR::FA + t * NX + r0], c1v = cur[LR::FA + t * NX + r1];
+                T y[NX];
+                ld_row<T, NX, true>(y, s.PB + k * NX);
+#pragma unroll
+                for (int j = 0; j < NX; ++j) ffma2(c0v, c1v, y[j], y[j], P0[j], P1[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {
+                P0[j] += (j == r0) ? T(K.wx[r0]) : T(0);
+                P1[j] += (j == r1) ? T(K.wx[r1]) : T(0);
+            }
+        }
+        // re-symmetrise (R22) through the dead Abar buffer
+        if (act) {
+            st_row<T, NX, true>(s.X + r0 * NX, P0);
+            st_row<T, NX, true>(s.X + r1 * NX, P1);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+            P0[j] = T(0.5) * (P0[j] + s.X[j * NX + r0]);
+            P1[j] = T(0.5) * (P1[j] + s.X[j * NX + r1]);
+        }
+        __syncwarp();
+        if (act) {
+            st_row<T, NX, true>(s.P + r0 * NX, P0);
+            st_row<T, NX, true>(s.P + r1 * NX, P1);
+            s.p[r0] = pn0;
+            s.p[r1] = pn1;
+            st_row<T, NX, true>(Pp + (size_t)i * TP + r0 * NX, P0);
+            st_row<T, NX, true>(Pp + (size_t)i * TP + r1 * NX, P1);
+            Pp[(size_t)i * TP + NX * NX + r0] = pn0;
+            Pp[(size_t)i * TP + NX * NX + r1] = pn1;
+        }
+        __syncwarp();
+    }
+    {
+        const T xa = it.x0[(size_t)b * NX + r0], xc = it.x0[(size_t)b * NX + r1];
+        bad = bad || !isfinite(xa) || !isfinite(xc);
+    }
+    // per worker: OR of bad over its 6 lanes, then lane 0 of the worker writes info
+    const unsigned bm = __ballot_sync(0xffffffffu, bad && lane_act);
+    const bool any_bad = ((bm >> wb) & 0x3fu) != 0u;
+    if (l == 0 && act) info_out[b] = any_bad ? -1 : (fail != INT_MAX ? fail : 0);
+}
+
 // ------------------------------------------------------------------ forward + line search
 // Line-search contribution of stage i (0..N+1) for every alpha slot a = 0..na (a = 0: current
 // iterate, a >= 1: alpha = 2^-(a-1)): adds J_i(a) to aJ[a][lane] and ||defect_i(a)||_2 to

@@ -120,6 +120,7 @@ struct pdilqr_ctx {
     int fold_mode = 2;             // record-fed fold: 2 = two rows per lane / five instances per warp (default),
                                    // 1 = one instance per warp (column halves), 0 = two instances per warp (row per lane)
     int fold_w = 14;               // fold_mode 1: MINB blocks/SM (12/14/16)
+    int fold_nw = 4;               // fold_mode 2: instances per warp (2..5)
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool fault_combine = false;    // PDILQR_FAULT_COMBINE=1: negative control of the parity tests
@@ -686,9 +687,17 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         }
         Prof pf(h, "k_srbd_bwd_fold", st);
         if (h->fold_mode == 2) {   // two rows per lane, five instances per warp (default)
-            const size_t smem = 5 * sizeof(FoldR2Smem<T>);
-            set_smem(k_srbd_bwd_fold_r2<T>, smem);
-            k_srbd_bwd_fold_r2<T><<<(B + 4) / 5, 32, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, rec, info_tmp);
+            auto g2 = [&](auto kern, int nw, size_t slice) {
+                const size_t smem = (size_t)nw * slice;
+                set_smem(kern, smem);
+                kern<<<(B + nw - 1) / nw, 32, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, rec, info_tmp);
+            };
+            switch (h->fold_nw) {
+                case 2: g2(k_srbd_bwd_fold_r2<T, 2>, 2, sizeof(FoldR2Smem<T, 2>)); break;
+                case 3: g2(k_srbd_bwd_fold_r2<T, 3>, 3, sizeof(FoldR2Smem<T, 3>)); break;
+                case 5: g2(k_srbd_bwd_fold_r2<T, 5>, 5, sizeof(FoldR2Smem<T, 5>)); break;
+                default: g2(k_srbd_bwd_fold_r2<T, 4>, 4, sizeof(FoldR2Smem<T, 4>)); break;
+            }
         } else if (h->fold_mode == 1) {   // one instance per warp (two lanes per row)
             auto gw = [&](auto kern) {
                 const size_t smem = 2 * sizeof(FoldWSmem<T>);
@@ -1314,6 +1323,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_LINREC")) h->linrec = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_W")) h->fold_w = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_MODE")) h->fold_mode = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_FOLD_NW")) h->fold_nw = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FAULT_COMBINE")) h->fault_combine = std::atoi(e) != 0;
     if (const char *e = std::getenv("PDILQR_NVTX")) h->nvtx = std::atoi(e) != 0;
     if (v == VBIG) {  // large path: cluster size of k_big_ric (CTAs per instance) so that B * CS fills the SMs

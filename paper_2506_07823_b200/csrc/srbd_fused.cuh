@@ -1053,32 +1053,34 @@ __global__ void __launch_bounds__(64, MINB) k_srbd_bwd_fold_w(SrbdConst K, SrbdI
 // of peak), not by the FMA pipe: a row-per-lane 12 x 12 product makes every lane load all 144
 // entries of the other operand.  Here a worker is 6 lanes, lane l owns rows l and l + 6 of every
 // matrix (so every loaded operand row feeds two FFMA2 row updates), a warp carries 5 instances
-// (lanes 30, 31 shadow lane 29 and store nothing), and the products use the SRBD structure of the
+// (lanes 6 NW .. 31 shadow the last lane and store nothing; NW = 4 or 5), and the products use the SRBD structure of the
 // linearisation record: B has zero rows 0-5 (P B and B^T P B over k = 6..11), A = I + dt Fx with
 // dt Fx nonzero only in rows 3-5, 9-11 plus dt at (r, 6 + r) for r < 3, so H = (P B)^T A and
 // P = Q + A^T V take the identity from registers and only 6 operand rows from shared memory.
 // Same recursion as k_srbd_bwd_fold_rec (policy Eq. 5 rows, D7 combine, Eq. 11-14, R22).
-template <typename T>
+// Slice stride (fp32 words) = 8 (mod 32) for 2-4 workers per warp (row loads and the 6-lane column
+// loads of the workers hit disjoint banks), 4 (mod 32) for 5 workers (row loads disjoint).
+template <typename T, int NW>
 struct FoldR2Smem {
     T in[2][LinRec::SIZE];
     T P[144], B6[72], PB[144], K[144], X[144];
     T p[12], w[12], k[12];
-    T pad[sizeof(T) == 4 ? 8 : 6];   // slice stride = 4 (mod 32) words: the 5 workers' LDS.128 hit distinct banks
+    T pad[NW <= 4 ? 12 : 8];
 };
 
-template <typename T>
+template <typename T, int NW>
 __global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
                                                            const T *rec, int32_t *info_out) {
-    constexpr int NX = 12, NW = 5;
+    constexpr int NX = 12, NL = 6 * NW;
     constexpr int TP = TE<NX>::SIZE;
     using KL = KE<NX, NX>;
     using LR = LinRec;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int L = threadIdx.x & 31;
-    const int w = L < 30 ? L / 6 : NW - 1;
-    const int l = L < 30 ? L - 6 * w : 5;
-    const bool lane_act = L < 30;
-    FoldR2Smem<T> &s = reinterpret_cast<FoldR2Smem<T> *>(smraw)[(threadIdx.x >> 5) * NW + w];
+    const int w = L < NL ? L / 6 : NW - 1;
+    const int l = L < NL ? L - 6 * w : 5;
+    const bool lane_act = L < NL;
+    FoldR2Smem<T, NW> &s = reinterpret_cast<FoldR2Smem<T, NW> *>(smraw)[(threadIdx.x >> 5) * NW + w];
     const int b_raw = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NW + w;
     if (__all_sync(0xffffffffu, b_raw >= B)) return;
     const bool live = b_raw < B;
@@ -1408,141 +1410,179 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
                                          double (*aJ)[32], double (*aT)[32], T (*sDel)[32], int lane, double &g,
                                          unsigned &guard, int a_lo = 0, int a_hi = -1, bool add_g = true) {
     // alpha slots a_lo..a_hi (default: all 0..na); add_g: this call also accumulates the slope g
+    (void)sDel;
     if (a_hi < 0) a_hi = na;
     constexpr int NX = 12;
     using F = T;
-        const T *xi = x + (size_t)i * NX, *dxi = Dx + (size_t)i * NX;
-        const T *xri = xr + (size_t)i * NX;
-        if (i == N + 1) {  // terminal cost: quadratic in alpha
-            double c0 = 0, c1 = 0, c2 = 0;
-#pragma unroll
-            for (int k = 0; k < NX; ++k) {
-                const double e = (double)xi[k] - (double)xri[k], d = (double)dxi[k];
-                c0 += 0.5 * K.wxt[k] * e * e; c1 += K.wxt[k] * e * d; c2 += 0.5 * K.wxt[k] * d * d;
-            }
-            for (int a = a_lo; a <= a_hi; ++a) {
-                const double al = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
-                aJ[a][lane] += c0 + al * (c1 + al * c2);
-            }
-            if (add_g) g += c1;
-            return;
-        }
-        const T *ui = u + (size_t)i * NX, *dui = Du + (size_t)i * NX;
-        const T *feet = it.feet + ((size_t)b * (N + 1) + i) * 12;
-        const uint8_t *con = it.con + ((size_t)b * (N + 1) + i) * 4;
-        const T *uri = urf ? urf + (size_t)i * NX : nullptr;
-        F xs0[NX], dxs[NX], us0[NX], dus[NX], fe[12];
-#pragma unroll
-        for (int k = 0; k < NX; ++k) {
-            xs0[k] = (F)xi[k]; dxs[k] = (F)dxi[k]; us0[k] = (F)ui[k]; dus[k] = (F)dui[k];
-            fe[k] = (F)feet[k];
-            sDel[k][lane] = (F)(xi[NX + k] - xi[k]);
-            sDel[NX + k][lane] = (F)(dxi[NX + k] - dxi[k]);
-        }
-        const uint8_t cmask = (uint8_t)((con[0] ? 1 : 0) | (con[1] ? 2 : 0) | (con[2] ? 4 : 0) | (con[3] ? 8 : 0));
-        // quadratic tracking costs: c0 + c1 a + c2 a^2
+    const T *xi = x + (size_t)i * NX, *dxi = Dx + (size_t)i * NX;
+    const T *xri = xr + (size_t)i * NX;
+    if (i == N + 1) {  // terminal cost: quadratic in alpha
         double c0 = 0, c1 = 0, c2 = 0;
 #pragma unroll
         for (int k = 0; k < NX; ++k) {
             const double e = (double)xi[k] - (double)xri[k], d = (double)dxi[k];
-            c0 += 0.5 * K.wx[k] * e * e; c1 += K.wx[k] * e * d; c2 += 0.5 * K.wx[k] * d * d;
-            const double wu = ((cmask >> (k / 3)) & 1) ? K.wu_st : K.wu_sw;
-            const double eu = (double)ui[k] - (uri ? (double)uri[k] : 0.0), du_ = (double)dui[k];
-            c0 += 0.5 * wu * eu * eu; c1 += wu * eu * du_; c2 += 0.5 * wu * du_ * du_;
+            c0 += 0.5 * K.wxt[k] * e * e; c1 += K.wxt[k] * e * d; c2 += 0.5 * K.wxt[k] * d * d;
+        }
+        for (int a = a_lo; a <= a_hi; ++a) {
+            const double al = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
+            aJ[a][lane] += c0 + al * (c1 + al * c2);
         }
         if (add_g) g += c1;
-        // barrier arguments xi0 + a dxi of the stance-foot constraints and their slopes at a = 0
-        F bx0[24], bdx[24];
+        return;
+    }
+    const T *ui = u + (size_t)i * NX, *dui = Du + (size_t)i * NX;
+    const T *feet = it.feet + ((size_t)b * (N + 1) + i) * 12;
+    const uint8_t *con = it.con + ((size_t)b * (N + 1) + i) * 4;
+    const T *uri = urf ? urf + (size_t)i * NX : nullptr;
+    const uint8_t cmask = (uint8_t)((con[0] ? 1 : 0) | (con[1] ? 2 : 0) | (con[2] ? 4 : 0) | (con[3] ? 8 : 0));
+    // quadratic tracking costs: c0 + c1 a + c2 a^2
+    double c0 = 0, c1 = 0, c2 = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+    for (int k = 0; k < NX; ++k) {
+        const double e = (double)xi[k] - (double)xri[k], d = (double)dxi[k];
+        c0 += 0.5 * K.wx[k] * e * e; c1 += K.wx[k] * e * d; c2 += 0.5 * K.wx[k] * d * d;
+        const double wu = ((cmask >> (k / 3)) & 1) ? K.wu_st : K.wu_sw;
+        const double eu = (double)ui[k] - (uri ? (double)uri[k] : 0.0), du_ = (double)dui[k];
+        c0 += 0.5 * wu * eu * eu; c1 += wu * eu * du_; c2 += 0.5 * wu * du_ * du_;
+    }
+    if (add_g) g += c1;
+    // stance feet compacted into slots q < ns (foot (perm >> 2q) & 3); per slot the force f0 + a df.
+    // Everything affine in alpha is hoisted out of the alpha loop:
+    //   torque  sum_q (r_q - a dp) x (f_q + a df_q) = tau0 + a tau1 + a^2 tau2  (r_q = foothold - p),
+    //   defect rows 0-2 (v) and 6-8 (F/m + g) are affine: d = A + a B.
+    int ns = 0, perm = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if ((cmask >> j) & 1) { perm |= j << (2 * ns); ++ns; }
+    const F dp[3] = {(F)dxi[0], (F)dxi[1], (F)dxi[2]};
+    F f0[4][3], df[4][3];
+    F tau0[3] = {F(0), F(0), F(0)}, tau1[3] = {F(0), F(0), F(0)}, tau2[3] = {F(0), F(0), F(0)};
+    F Fs0[3] = {F(0), F(0), F(0)}, Fs1[3] = {F(0), F(0), F(0)};
+    const F mu = (F)K.mu, fmn = (F)K.fmin, fmx = (F)K.fmax;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const bool on = q < ns;
+        const int j = (perm >> (2 * q)) & 3;
+        F fq[3], dq[3], rq[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            fq[c] = on ? (F)ui[3 * j + c] : F(0);
+            dq[c] = on ? (F)dui[3 * j + c] : F(0);
+            rq[c] = (F)feet[3 * j + c] - (F)xi[c];
+            f0[q][c] = fq[c];
+            df[q][c] = dq[c];
+            Fs0[c] += fq[c];
+            Fs1[c] += dq[c];
+        }
+        tau0[0] += rq[1] * fq[2] - rq[2] * fq[1];
+        tau0[1] += rq[2] * fq[0] - rq[0] * fq[2];
+        tau0[2] += rq[0] * fq[1] - rq[1] * fq[0];
+        tau1[0] += (rq[1] * dq[2] - rq[2] * dq[1]) - (dp[1] * fq[2] - dp[2] * fq[1]);
+        tau1[1] += (rq[2] * dq[0] - rq[0] * dq[2]) - (dp[2] * fq[0] - dp[0] * fq[2]);
+        tau1[2] += (rq[0] * dq[1] - rq[1] * dq[0]) - (dp[0] * fq[1] - dp[1] * fq[0]);
+        tau2[0] -= dp[1] * dq[2] - dp[2] * dq[1];
+        tau2[1] -= dp[2] * dq[0] - dp[0] * dq[2];
+        tau2[2] -= dp[0] * dq[1] - dp[1] * dq[0];
+        if (add_g && on) {   // barrier part of the slope at a = 0
 #pragma unroll
             for (int cc = 0; cc < 6; ++cc) {
                 F gx, gy, gz, h;
-                foot_con<F>(cc, (F)K.mu, (F)K.fmin, (F)K.fmax, gx, gy, gz, h);
-                bx0[6 * j + cc] = gx * us0[3 * j] + gy * us0[3 * j + 1] + gz * us0[3 * j + 2] + h;
-                bdx[6 * j + cc] = gx * dus[3 * j] + gy * dus[3 * j + 1] + gz * dus[3 * j + 2];
-                if (add_g && ((cmask >> j) & 1)) {
-                    F d1, d2;
-                    barrier_d12<F>(bx0[6 * j + cc], (F)K.bmu, (F)K.bdelta, (F)K.ibd2, d1, d2);
-                    g += (double)d1 * (double)bdx[6 * j + cc];
-                }
+                foot_con<F>(cc, mu, fmn, fmx, gx, gy, gz, h);
+                F d1, d2;
+                barrier_d12<F>(gx * fq[0] + gy * fq[1] + gz * fq[2] + h, (F)K.bmu, (F)K.bdelta, (F)K.ibd2, d1, d2);
+                g += (double)d1 * (double)(gx * dq[0] + gy * dq[1] + gz * dq[2]);
             }
-        }
-        const F bmu = (F)K.bmu, bdl = (F)K.bdelta, ibdl = (F)K.ibd, lbd = fast_log((F)K.bdelta);
-        const F im = (F)K.imass;
-        for (int a = a_lo; a <= a_hi; ++a) {
-            const double ald = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
-            const F al = (F)ald;
-            double J = c0 + ald * (c1 + ald * c2);
-            // relaxed barriers: the logarithmic branches of a foot's six constraints
-            // share one logarithm, sum_c -mu log xi_c = -mu log prod_c xi_c (xi_c >= delta > 0;
-            // the product of six forces <= f_max stays far inside the fp32 range), the quadratic
-            // branches are added one by one; one MUFU.LG2 per stance foot instead of six
-            F Jb = F(0.);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (!((cmask >> j) & 1)) continue;
-                F prod = F(1.), quad = F(0.);
-#pragma unroll
-                for (int cc = 0; cc < 6; ++cc) {
-                    const F xv = fma(al, bdx[6 * j + cc], bx0[6 * j + cc]);
-                    const F t = (xv - F(2.) * bdl) * ibdl;
-                    const bool lg = xv >= bdl;
-                    prod *= lg ? xv : F(1.);
-                    quad += lg ? F(0.) : F(0.5) * bmu * (t * t - F(1.)) - bmu * lbd;
-                }
-                Jb += quad - bmu * fast_log(prod);
-            }
-            J += (double)Jb;
-            F xs[NX], us[NX];
-#pragma unroll
-            for (int k = 0; k < NX; ++k) { xs[k] = fma(al, dxs[k], xs0[k]); us[k] = fma(al, dus[k], us0[k]); }
-            if (!(fabs(xs[4]) < (F)kPitchGuard)) guard |= 1u << a;
-            // SRBD f(xs, us) (fast SFU trig): same equations as SrbdEval
-            F sr, cr, sp, cp, sy, cy;
-            fast_sincos(xs[3], &sr, &cr);
-            fast_sincos(xs[4], &sp, &cp);
-            fast_sincos(xs[5], &sy, &cy);
-            const F icp = rcp_rn(cp), tp = sp * icp;
-            const F R0 = cy * cp, R1 = cy * sp * sr - sy * cr, R2 = cy * sp * cr + sy * sr;
-            const F R3 = sy * cp, R4 = sy * sp * sr + cy * cr, R5 = sy * sp * cr - cy * sr;
-            const F R6 = -sp, R7 = cp * sr, R8 = cp * cr;
-            F t0 = F(0.), t1 = F(0.), t2 = F(0.), F0 = F(0.), F1 = F(0.), F2 = F(0.);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if (!((cmask >> j) & 1)) continue;
-                const F fx = us[3 * j], fy = us[3 * j + 1], fz = us[3 * j + 2];
-                const F rx = fe[3 * j] - xs[0], ry = fe[3 * j + 1] - xs[1], rz = fe[3 * j + 2] - xs[2];
-                t0 += ry * fz - rz * fy; t1 += rz * fx - rx * fz; t2 += rx * fy - ry * fx;
-                F0 += fx; F1 += fy; F2 += fz;
-            }
-            const F w0 = xs[9], w1 = xs[10], w2 = xs[11];
-            F Iw[3], rh[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) Iw[c] = (F)K.I[3 * c] * w0 + (F)K.I[3 * c + 1] * w1 + (F)K.I[3 * c + 2] * w2;
-            rh[0] = R0 * t0 + R3 * t1 + R6 * t2 - (w1 * Iw[2] - w2 * Iw[1]);
-            rh[1] = R1 * t0 + R4 * t1 + R7 * t2 - (w2 * Iw[0] - w0 * Iw[2]);
-            rh[2] = R2 * t0 + R5 * t1 + R8 * t2 - (w0 * Iw[1] - w1 * Iw[0]);
-            F fv[NX];
-            fv[0] = xs[6]; fv[1] = xs[7]; fv[2] = xs[8];
-            fv[3] = w0 + sr * tp * w1 + cr * tp * w2;
-            fv[4] = cr * w1 - sr * w2;
-            fv[5] = (sr * w1 + cr * w2) * icp;
-            fv[6] = F0 * im + (F)K.g[0]; fv[7] = F1 * im + (F)K.g[1]; fv[8] = F2 * im + (F)K.g[2];
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                fv[9 + c] = (F)K.Iinv[3 * c] * rh[0] + (F)K.Iinv[3 * c + 1] * rh[1] + (F)K.Iinv[3 * c + 2] * rh[2];
-            const F dtf = (F)K.dt;
-            F d2 = F(0.);
-#pragma unroll
-            for (int k = 0; k < NX; ++k) {
-                const F d = fma(al, sDel[NX + k][lane], sDel[k][lane]) - dtf * fv[k];
-                d2 = fma(d, d, d2);
-            }
-            aJ[a][lane] += J;
-            aT[a][lane] += (double)sqrt(d2);
         }
     }
+    const F dtf = (F)K.dt, im = (F)K.imass;
+    // affine defect rows: 0-2 (f = v), 6-8 (f = F / m + g)
+    F LA[6], LB[6];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        LA[c] = (F)(xi[NX + c] - xi[c]) - dtf * (F)xi[6 + c];
+        LB[c] = (F)(dxi[NX + c] - dxi[c]) - dtf * (F)dxi[6 + c];
+        LA[3 + c] = (F)(xi[NX + 6 + c] - xi[6 + c]) - dtf * (Fs0[c] * im + (F)K.g[c]);
+        LB[3 + c] = (F)(dxi[NX + 6 + c] - dxi[6 + c]) - dtf * (Fs1[c] * im);
+    }
+    // nonlinear rows 3-5 (Euler rates) and 9-11 (angular acceleration): differences of the iterate / direction
+    F N0[6], N1[6], th0[3], dth[3], om0[3], dom[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        N0[c] = (F)(xi[NX + 3 + c] - xi[3 + c]);
+        N1[c] = (F)(dxi[NX + 3 + c] - dxi[3 + c]);
+        N0[3 + c] = (F)(xi[NX + 9 + c] - xi[9 + c]);
+        N1[3 + c] = (F)(dxi[NX + 9 + c] - dxi[9 + c]);
+        th0[c] = (F)xi[3 + c]; dth[c] = (F)dxi[3 + c];
+        om0[c] = (F)xi[9 + c]; dom[c] = (F)dxi[9 + c];
+    }
+    const F bmu = (F)K.bmu, bdl = (F)K.bdelta, ibdl = (F)K.ibd, lbd = fast_log((F)K.bdelta);
+    for (int a = a_lo; a <= a_hi; ++a) {
+        const double ald = a == 0 ? 0.0 : ldexp(1.0, -(a - 1));
+        const F al = (F)ald;
+        double J = c0 + ald * (c1 + ald * c2);
+        // relaxed barriers: the logarithmic branches of a foot's six constraints
+        // share one logarithm, sum_c -mu log xi_c = -mu log prod_c xi_c (xi_c >= delta > 0;
+        // the product of six forces <= f_max stays far inside the fp32 range), the quadratic
+        // branches are added one by one; one MUFU.LG2 per stance foot
+        F Jb = F(0.);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (q >= ns) break;
+            const F fx = fma(al, df[q][0], f0[q][0]), fy = fma(al, df[q][1], f0[q][1]), fz = fma(al, df[q][2], f0[q][2]);
+            const F mfz = mu * fz;
+            const F xv[6] = {mfz - fx, mfz + fx, mfz - fy, mfz + fy, fz - fmn, fmx - fz};
+            F prod = F(1.), quad = F(0.);
+#pragma unroll
+            for (int cc = 0; cc < 6; ++cc) {
+                const F t = (xv[cc] - F(2.) * bdl) * ibdl;
+                const bool lg = xv[cc] >= bdl;
+                prod *= lg ? xv[cc] : F(1.);
+                quad += lg ? F(0.) : F(0.5) * bmu * (t * t - F(1.)) - bmu * lbd;
+            }
+            Jb += quad - bmu * fast_log(prod);
+        }
+        J += (double)Jb;
+        F th[3], w[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) { th[c] = fma(al, dth[c], th0[c]); w[c] = fma(al, dom[c], om0[c]); }
+        if (!(fabs(th[1]) < (F)kPitchGuard)) guard |= 1u << a;
+        // SRBD f(x + a dx, u + a du) rows 3-5 and 9-11 (fast SFU trig): same equations as SrbdEval
+        F sr, cr, sp, cp, sy, cy;
+        fast_sincos(th[0], &sr, &cr);
+        fast_sincos(th[1], &sp, &cp);
+        fast_sincos(th[2], &sy, &cy);
+        const F icp = rcp_rn(cp), tp = sp * icp;
+        const F R0 = cy * cp, R1 = cy * sp * sr - sy * cr, R2 = cy * sp * cr + sy * sr;
+        const F R3 = sy * cp, R4 = sy * sp * sr + cy * cr, R5 = sy * sp * cr - cy * sr;
+        const F R6 = -sp, R7 = cp * sr, R8 = cp * cr;
+        const F t0 = fma(al, fma(al, tau2[0], tau1[0]), tau0[0]);
+        const F t1 = fma(al, fma(al, tau2[1], tau1[1]), tau0[1]);
+        const F t2 = fma(al, fma(al, tau2[2], tau1[2]), tau0[2]);
+        F Iw[3], rh[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Iw[c] = (F)K.I[3 * c] * w[0] + (F)K.I[3 * c + 1] * w[1] + (F)K.I[3 * c + 2] * w[2];
+        rh[0] = R0 * t0 + R3 * t1 + R6 * t2 - (w[1] * Iw[2] - w[2] * Iw[1]);
+        rh[1] = R1 * t0 + R4 * t1 + R7 * t2 - (w[2] * Iw[0] - w[0] * Iw[2]);
+        rh[2] = R2 * t0 + R5 * t1 + R8 * t2 - (w[0] * Iw[1] - w[1] * Iw[0]);
+        F fv[6];
+        fv[0] = w[0] + sr * tp * w[1] + cr * tp * w[2];
+        fv[1] = cr * w[1] - sr * w[2];
+        fv[2] = (sr * w[1] + cr * w[2]) * icp;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            fv[3 + c] = (F)K.Iinv[3 * c] * rh[0] + (F)K.Iinv[3 * c + 1] * rh[1] + (F)K.Iinv[3 * c + 2] * rh[2];
+        F d2 = F(0.);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const F dl = fma(al, LB[k], LA[k]);
+            d2 = fma(dl, dl, d2);
+            const F dn = fma(al, N1[k], N0[k]) - dtf * fv[k];
+            d2 = fma(dn, dn, d2);
+        }
+        aJ[a][lane] += J;
+        aT[a][lane] += (double)sqrt(d2);
+    }
+}
 
 // Per-warp shared memory of k_srbd_fwd_ls: during the rollout a ring of D stage blocks
 // [(Abar_i, bbar_i) | (K_i, k_i)] filled by cp.async D-1 stages ahead; during the line search the

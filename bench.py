@@ -76,8 +76,18 @@ def flops_per_instance(N: int, n: int = 12, m: int = 12, chunk: int | None = Non
     # combine with X = Abar: V = P Abar, P' = Q + A^T V (4 n^3), w = p + P b~, p' = Abar^T w + q
     # (4 n^2), b~ = b - B R^-1 r (2 n m + blockwise R^-1 r, 6 m)
     fold_s0 = (N + 1) * (4 * n ** 3 + 4 * n ** 2 + 2 * n * m + 6 * m)
+    # the record-fed fold (k_srbd_bwd_fold_r2) skips the structural zeros of the SRBD linearisation:
+    # B has nb = 6 nonzero rows (6-11), dt Fx has na = 6 general rows (3-5, 9-11) plus dt at (r, 6 + r),
+    # r < 3, so A = I + dt Fx enters H = (P B)^T A and P' = Q + A^T V through na rows; per stage:
+    # P B 2 n nb m, G = R + (P B)^T B 2 m nb m, H 2 m na n + 6 m, h = r + (P B)^T b + B^T p 2 n m + 2 nb m,
+    # SPD solve m^3/3 + 2 m^2 (n+1), Abar = A + B K 2 nb m n, bbar 2 nb m, V = P Abar 2 n^3,
+    # p' = q + Abar^T w 2 n^2, P' 2 na n^2 + 6 n, w = p + P b~ 2 n^2  (the flops it has to do)
+    nb = na = 6
+    fold_struct = (N + 1) * (2 * n * nb * m + 2 * m * nb * m + 2 * m * na * n + 6 * m + 2 * n * m + 2 * nb * m
+                             + m ** 3 / 3 + 2 * m ** 2 * (n + 1) + 2 * nb * m * n + 2 * nb * m + 2 * n ** 3
+                             + 2 * n ** 2 + 2 * na * n ** 2 + 6 * n + 2 * n ** 2)
     return {"k_elem_init": init, "k_scan_bwd": bwd, "k_policy": policy, "k_scan_fwd": fwd, "k_tail": tail,
-            "k_srbd_bwd_fold": policy + fold_s0,
+            "k_srbd_bwd_fold": fold_struct, "k_srbd_bwd_fold_dense": policy + fold_s0,
             "k_srbd_fwd_ls": Lf * 2 * n ** 2 + tail}
 
 
@@ -408,7 +418,7 @@ def main():
 
     # --------------------------------------------------------------- roofline of the dominant kernel
     fl = flops_per_instance(N, chunk=h_chunk(args, B, N))
-    kern = {k: v for k, v in prof.items() if k in fl}
+    kern = {k: v for k, v in prof.items() if k in fl and not k.endswith("_dense")}
     dom = max(kern, key=lambda k: kern[k][1]) if kern else None
     sm_mhz = clocks.get("sm_max_mhz") or 1965.0
     peak = fp32_peak_tflops(sm_mhz)
@@ -426,6 +436,12 @@ def main():
                 "share_of_step": (tot / launches) / step_ms,
                 "peak_basis": f"FP32 FMA pipe: 148 SMs x 128 lanes x 2 flop x {sm_mhz:.0f} MHz (max SM clock)",
                 "per_kernel_ms": {k: v[1] / v[0] for k, v in prof.items()}}
+        if dom == "k_srbd_bwd_fold":   # the same time against the dense D7 flop count (structural zeros included)
+            dn = fl["k_srbd_bwd_fold_dense"] * B / avg_s / 1e12
+            roof["dense_equivalent"] = {"achieved": dn, "frac": dn / peak,
+                                        "flops_per_launch": fl["k_srbd_bwd_fold_dense"] * B,
+                                        "basis": "dense 12x12 D7 Riccati-form count (DESIGN.md Roofline); "
+                                                 "`achieved` above counts only the structurally nonzero products"}
         mp = measured_peaks()
         if mp.get("bf16_tflops"):
             scale = float(mp["bf16_tflops"]) / 2250.0
@@ -548,7 +564,8 @@ def ncu_traffic(kernel: str):
         except (OSError, ValueError):
             continue
         for r in rows:
-            if r.get("kernel", "").split("<")[0].split()[-1] == kernel and (best is None or key > best[0]):
+            name = r.get("kernel", "").split("<")[0].split()[-1]
+            if (name == kernel or name.startswith(kernel + "_r")) and (best is None or key > best[0]):
                 tot = 0.0
                 for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     v, u = r[k].split()

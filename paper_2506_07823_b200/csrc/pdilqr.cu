@@ -121,6 +121,7 @@ struct pdilqr_ctx {
                                    // 1 = one instance per warp (column halves), 0 = two instances per warp (row per lane)
     int fold_w = 14;               // fold_mode 1: MINB blocks/SM (12/14/16)
     int fold_nw = 4;               // fold_mode 2: instances per warp (2..5)
+    int lin_staged = 0;            // k_srbd_lin_rec: 1 = records staged in shared memory, 0 = direct 16-byte stores
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool fault_combine = false;    // PDILQR_FAULT_COMBINE=1: negative control of the parity tests
@@ -678,12 +679,17 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         // stage-parallel linearisation records (ws.elems is free on the single-chunk path)
         T *rec = ws.elems;
         {
-            constexpr int TPB = 32;
-            const size_t smem = (size_t)TPB * (LinRec::SIZE + 16 / sizeof(T)) * sizeof(T);
-            set_smem(k_srbd_lin_rec<T>, smem);
             const long tot = (long)B * (N + 1);
             Prof pf(h, "k_srbd_lin_rec", st);
-            k_srbd_lin_rec<T><<<(unsigned)((tot + TPB - 1) / TPB), TPB, smem, st>>>(h->K, iter_of<T>(it, h), B, N, rec);
+            if (h->lin_staged) {
+                constexpr int TPB = 32;
+                const size_t smem = (size_t)TPB * (LinRec::SIZE + 16 / sizeof(T)) * sizeof(T);
+                set_smem(k_srbd_lin_rec<T, true>, smem);
+                k_srbd_lin_rec<T, true><<<(unsigned)((tot + TPB - 1) / TPB), TPB, smem, st>>>(h->K, iter_of<T>(it, h), B, N, rec);
+            } else {
+                constexpr int TPB = 128;
+                k_srbd_lin_rec<T, false><<<(unsigned)((tot + TPB - 1) / TPB), TPB, 0, st>>>(h->K, iter_of<T>(it, h), B, N, rec);
+            }
         }
         Prof pf(h, "k_srbd_bwd_fold", st);
         if (h->fold_mode == 2) {   // two rows per lane, five instances per warp (default)
@@ -1324,6 +1330,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_FOLD_W")) h->fold_w = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_MODE")) h->fold_mode = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_NW")) h->fold_nw = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_LIN_STAGED")) h->lin_staged = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FAULT_COMBINE")) h->fault_combine = std::atoi(e) != 0;
     if (const char *e = std::getenv("PDILQR_NVTX")) h->nvtx = std::atoi(e) != 0;
     if (v == VBIG) {  // large path: cluster size of k_big_ric (CTAs per instance) so that B * CS fills the SMs

@@ -298,8 +298,10 @@ struct LinRec {
     static constexpr int SIZE = 200;
 };
 
-template <typename T>
-__global__ void __launch_bounds__(64) k_srbd_lin_rec(SrbdConst K, SrbdIter<T> it, int B, int N, T *rec) {
+// STAGED = true: records assembled in shared memory and copied out coalesced; false: each thread
+// writes its record with 16-byte stores (no shared memory, occupancy set by registers only).
+template <typename T, bool STAGED>
+__global__ void __launch_bounds__(STAGED ? 64 : 128, STAGED ? 1 : 4) k_srbd_lin_rec(SrbdConst K, SrbdIter<T> it, int B, int N, T *rec) {
     constexpr int NX = 12, RS = LinRec::SIZE, RP = RS + 16 / (int)sizeof(T);
     using LR = LinRec;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(64) k_srbd_lin_rec(SrbdConst K, SrbdIter<T> it
     const long base = (long)blockIdx.x * blockDim.x;
     const long g = base + threadIdx.x;
     if (g < total) {
-        T *o = sm + (size_t)threadIdx.x * RP;
+        T *o = STAGED ? sm + (size_t)threadIdx.x * RP : rec + (size_t)g * RS;
         const int b = (int)(g / (N + 1)), i = (int)(g - (long)b * (N + 1));
         const size_t sx = (size_t)b * (N + 2) + i, st = (size_t)g;
         T xv[NX], xn[NX], uv[NX], fe[NX], lv[NX], ln[NX], xr[NX];
@@ -489,6 +491,7 @@ __global__ void __launch_bounds__(64) k_srbd_lin_rec(SrbdConst K, SrbdIter<T> it
         for (int k = LR::FL; k < LR::SIZE; ++k) o[k] = T(0);
         reinterpret_cast<int *>(o + LR::FL)[0] = (bad ? 1 : 0) | (rfail ? 2 : 0);
     }
+    if constexpr (!STAGED) return;
     __syncthreads();
     // coalesced copy of the block's records (contiguous in global memory) in 16-byte granules
     const long nrec = total - base < (long)blockDim.x ? total - base : (long)blockDim.x;
@@ -1430,20 +1433,33 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
         if (add_g) g += c1;
         return;
     }
-    const T *ui = u + (size_t)i * NX, *dui = Du + (size_t)i * NX;
-    const T *feet = it.feet + ((size_t)b * (N + 1) + i) * 12;
-    const uint8_t *con = it.con + ((size_t)b * (N + 1) + i) * 4;
-    const T *uri = urf ? urf + (size_t)i * NX : nullptr;
-    const uint8_t cmask = (uint8_t)((con[0] ? 1 : 0) | (con[1] ? 2 : 0) | (con[2] ? 4 : 0) | (con[3] ? 8 : 0));
+    // every row of the stage in registers with 16-byte loads (rows are 16-byte aligned)
+    T xa[NX], xb1[NX], da[NX], db[NX], ua[NX], dua[NX], fe[NX];
+    ld_row<T, NX, true>(xa, xi);
+    ld_row<T, NX, true>(xb1, xi + NX);
+    ld_row<T, NX, true>(da, dxi);
+    ld_row<T, NX, true>(db, dxi + NX);
+    ld_row<T, NX, true>(ua, u + (size_t)i * NX);
+    ld_row<T, NX, true>(dua, Du + (size_t)i * NX);
+    ld_row<T, NX, true>(fe, it.feet + ((size_t)b * (N + 1) + i) * 12);
+    const uint32_t cw = *reinterpret_cast<const uint32_t *>(it.con + ((size_t)b * (N + 1) + i) * 4);
+    const uint8_t cmask = (uint8_t)(((cw & 0xffu) ? 1 : 0) | ((cw & 0xff00u) ? 2 : 0) | ((cw & 0xff0000u) ? 4 : 0) |
+                                    ((cw & 0xff000000u) ? 8 : 0));
     // quadratic tracking costs: c0 + c1 a + c2 a^2
     double c0 = 0, c1 = 0, c2 = 0;
+    {
+        T xrv[NX], urv[NX];
+        ld_row<T, NX, true>(xrv, xri);
+        if (urf) ld_row<T, NX, true>(urv, urf + (size_t)i * NX);
+        else zero(urv);
 #pragma unroll
-    for (int k = 0; k < NX; ++k) {
-        const double e = (double)xi[k] - (double)xri[k], d = (double)dxi[k];
-        c0 += 0.5 * K.wx[k] * e * e; c1 += K.wx[k] * e * d; c2 += 0.5 * K.wx[k] * d * d;
-        const double wu = ((cmask >> (k / 3)) & 1) ? K.wu_st : K.wu_sw;
-        const double eu = (double)ui[k] - (uri ? (double)uri[k] : 0.0), du_ = (double)dui[k];
-        c0 += 0.5 * wu * eu * eu; c1 += wu * eu * du_; c2 += 0.5 * wu * du_ * du_;
+        for (int k = 0; k < NX; ++k) {
+            const double e = (double)xa[k] - (double)xrv[k], d = (double)da[k];
+            c0 += 0.5 * K.wx[k] * e * e; c1 += K.wx[k] * e * d; c2 += 0.5 * K.wx[k] * d * d;
+            const double wu = ((cmask >> (k / 3)) & 1) ? K.wu_st : K.wu_sw;
+            const double eu = (double)ua[k] - (double)urv[k], du_ = (double)dua[k];
+            c0 += 0.5 * wu * eu * eu; c1 += wu * eu * du_; c2 += 0.5 * wu * du_ * du_;
+        }
     }
     if (add_g) g += c1;
     // stance feet compacted into slots q < ns (foot (perm >> 2q) & 3); per slot the force f0 + a df.
@@ -1454,7 +1470,7 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
 #pragma unroll
     for (int j = 0; j < 4; ++j)
         if ((cmask >> j) & 1) { perm |= j << (2 * ns); ++ns; }
-    const F dp[3] = {(F)dxi[0], (F)dxi[1], (F)dxi[2]};
+    const F dp[3] = {(F)da[0], (F)da[1], (F)da[2]};
     F f0[4][3], df[4][3];
     F tau0[3] = {F(0), F(0), F(0)}, tau1[3] = {F(0), F(0), F(0)}, tau2[3] = {F(0), F(0), F(0)};
     F Fs0[3] = {F(0), F(0), F(0)}, Fs1[3] = {F(0), F(0), F(0)};
@@ -1466,9 +1482,13 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
         F fq[3], dq[3], rq[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            fq[c] = on ? (F)ui[3 * j + c] : F(0);
-            dq[c] = on ? (F)dui[3 * j + c] : F(0);
-            rq[c] = (F)feet[3 * j + c] - (F)xi[c];
+            // foot j's entries by compile-time selects (no runtime register indexing)
+            const F uf = j == 0 ? (F)ua[c] : j == 1 ? (F)ua[3 + c] : j == 2 ? (F)ua[6 + c] : (F)ua[9 + c];
+            const F df_ = j == 0 ? (F)dua[c] : j == 1 ? (F)dua[3 + c] : j == 2 ? (F)dua[6 + c] : (F)dua[9 + c];
+            const F ff = j == 0 ? (F)fe[c] : j == 1 ? (F)fe[3 + c] : j == 2 ? (F)fe[6 + c] : (F)fe[9 + c];
+            fq[c] = on ? uf : F(0);
+            dq[c] = on ? df_ : F(0);
+            rq[c] = ff - (F)xa[c];
             f0[q][c] = fq[c];
             df[q][c] = dq[c];
             Fs0[c] += fq[c];
@@ -1499,21 +1519,21 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
     F LA[6], LB[6];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        LA[c] = (F)(xi[NX + c] - xi[c]) - dtf * (F)xi[6 + c];
-        LB[c] = (F)(dxi[NX + c] - dxi[c]) - dtf * (F)dxi[6 + c];
-        LA[3 + c] = (F)(xi[NX + 6 + c] - xi[6 + c]) - dtf * (Fs0[c] * im + (F)K.g[c]);
-        LB[3 + c] = (F)(dxi[NX + 6 + c] - dxi[6 + c]) - dtf * (Fs1[c] * im);
+        LA[c] = (F)(xb1[c] - xa[c]) - dtf * (F)xa[6 + c];
+        LB[c] = (F)(db[c] - da[c]) - dtf * (F)da[6 + c];
+        LA[3 + c] = (F)(xb1[6 + c] - xa[6 + c]) - dtf * (Fs0[c] * im + (F)K.g[c]);
+        LB[3 + c] = (F)(db[6 + c] - da[6 + c]) - dtf * (Fs1[c] * im);
     }
     // nonlinear rows 3-5 (Euler rates) and 9-11 (angular acceleration): differences of the iterate / direction
     F N0[6], N1[6], th0[3], dth[3], om0[3], dom[3];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        N0[c] = (F)(xi[NX + 3 + c] - xi[3 + c]);
-        N1[c] = (F)(dxi[NX + 3 + c] - dxi[3 + c]);
-        N0[3 + c] = (F)(xi[NX + 9 + c] - xi[9 + c]);
-        N1[3 + c] = (F)(dxi[NX + 9 + c] - dxi[9 + c]);
-        th0[c] = (F)xi[3 + c]; dth[c] = (F)dxi[3 + c];
-        om0[c] = (F)xi[9 + c]; dom[c] = (F)dxi[9 + c];
+        N0[c] = (F)(xb1[3 + c] - xa[3 + c]);
+        N1[c] = (F)(db[3 + c] - da[3 + c]);
+        N0[3 + c] = (F)(xb1[9 + c] - xa[9 + c]);
+        N1[3 + c] = (F)(db[9 + c] - da[9 + c]);
+        th0[c] = (F)xa[3 + c]; dth[c] = (F)da[3 + c];
+        om0[c] = (F)xa[9 + c]; dom[c] = (F)da[9 + c];
     }
     const F bmu = (F)K.bmu, bdl = (F)K.bdelta, ibdl = (F)K.ibd, lbd = fast_log((F)K.bdelta);
     for (int a = a_lo; a <= a_hi; ++a) {
@@ -1585,12 +1605,12 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
 }
 
 // Per-warp shared memory of k_srbd_fwd_ls: during the rollout a ring of D stage blocks
-// [(Abar_i, bbar_i) | (K_i, k_i)] filled by cp.async D-1 stages ahead; during the line search the
-// per-lane alpha partial sums and the defect deltas (the two phases never overlap).
+// [(Abar_i, bbar_i) | (K_i, k_i) | (P_i, p_i)] filled by cp.async D-1 stages ahead; during the line
+// search the per-lane alpha partial sums (the two phases never overlap).
 template <typename T>
 struct FwdLsSmem {
-    static constexpr int NA = 16, BLK = 2 * 156, D = sizeof(T) == 8 ? 4 : 8;
-    static constexpr size_t LS = 2 * NA * 32 * sizeof(double) + 24 * 32 * sizeof(T);
+    static constexpr int NA = 16, BLK = 3 * 156, D = sizeof(T) == 8 ? 3 : 6;
+    static constexpr size_t LS = 2 * NA * 32 * sizeof(double);
     static constexpr size_t RING = (size_t)D * BLK * sizeof(T);
     static constexpr size_t PER_WARP = LS > RING ? LS : RING;
 };
@@ -1635,9 +1655,9 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     auto issue = [&](int s) {  // stage s -> ring slot s % D (always commits a group)
         if (s <= N) {
             T *dst = ring + (size_t)(s % D) * SM::BLK;
-            const T *sa = Te + (size_t)s * TP, *sk = Kk + (size_t)s * KL::SIZE;
-            for (int c = lane; c < 2 * CH; c += 32)
-                cp_async16(dst + c * EPC, c < CH ? sa + c * EPC : sk + (c - CH) * EPC);
+            const T *sa = Te + (size_t)s * TP, *sk = Kk + (size_t)s * KL::SIZE, *sp = Pp + (size_t)s * TP;
+            for (int c = lane; c < 3 * CH; c += 32)
+                cp_async16(dst + c * EPC, c < CH ? sa + c * EPC : c < 2 * CH ? sk + (c - CH) * EPC : sp + (c - 2 * CH) * EPC);
         }
         cp_async_commit();
     };
@@ -1652,37 +1672,42 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     // non-finite direction entries (dx, du, dlam) make info = -1 as on the other step paths
     // (k_finalize_info rule); checked in registers where they are produced
     bool nonfin = false;
-    // lanes 0..11: dx_{i+1} = Abar_i dx_i + bbar_i ; lanes 16..27: du_i = K_i dx_i + k_i
+    // lanes 0..11: dx_{i+1} = Abar_i dx_i + bbar_i (the dependent chain);
+    // lanes 16..27: du_i = K_i dx_i + k_i (Eq. 6) and dlam_i = P_i dx_i + p_i (Eq. 7) off the chain
     const int roff = (lane < 16 ? 0 : 156) + (rowl ? r : 0) * NX;
     const int ooff = (lane < 16 ? 0 : 156) + NX * NX + (rowl ? r : 0);
+    const int poff = 312 + (rowl ? r : 0) * NX, pbo = 312 + NX * NX + (rowl ? r : 0);
     for (int i = 0; i <= N; ++i) {
         issue(i + D - 1);
         cp_async_wait<D - 1>();
         __syncwarp();
         const T *blk = ring + (size_t)(i % D) * SM::BLK;
-        T rcur[NX], xv[NX];
+        T rcur[NX], xv[NX], prw[NX];
         ld_row<T, NX, true>(rcur, blk + roff);
         ld_row<T, NX, true>(xv, sx[wl]);
         const T v = row_dot<T, NX>(rcur, xv, blk[ooff]);
-        nonfin = nonfin || !isfinite(v);
+        T vl = T(0);
+        if (lane >= 16) {
+            ld_row<T, NX, true>(prw, blk + poff);
+            vl = row_dot<T, NX>(prw, xv, blk[pbo]);
+        }
+        nonfin = nonfin || !isfinite(v) || !isfinite(vl);
         __syncwarp();
         if (rowl) {
             if (lane < 16) { sx[wl][r] = v; Dx[(size_t)(i + 1) * NX + r] = v; }
-            else Du[(size_t)i * NX + r] = v;
+            else { Du[(size_t)i * NX + r] = v; Dl[(size_t)i * NX + r] = vl; }
         }
         __syncwarp();
     }
     cp_async_wait<0>();
     __syncwarp();
-    // dlam_i = P_i dx_i + p_i  (Eq. 7), all (stage, row) pairs in parallel
-    for (int t = lane; t < (N + 2) * NX; t += 32) {
-        const int i = t / NX, a = t % NX;
-        T prow[NX], xv[NX];
-        ld_row<T, NX, true>(prow, Pp + (size_t)i * TP + a * NX);
-        ld_row<T, NX, true>(xv, Dx + (size_t)i * NX);
-        const T v = row_dot<T, NX>(prow, xv, Pp[(size_t)i * TP + NX * NX + a]);
-        Dl[t] = v;
-        nonfin = nonfin || !isfinite(v);
+    if (lane >= 16 && rowl) {   // dlam_{N+1} = P_{N+1} dx_{N+1} + p_{N+1}
+        T prw[NX], xv[NX];
+        ld_row<T, NX, true>(prw, Pp + (size_t)(N + 1) * TP + r * NX);
+        ld_row<T, NX, true>(xv, sx[wl]);
+        const T vl = row_dot<T, NX>(prw, xv, Pp[(size_t)(N + 1) * TP + NX * NX + r]);
+        Dl[(size_t)(N + 1) * NX + r] = vl;
+        nonfin = nonfin || !isfinite(vl);
     }
     if (__any_sync(0xffffffffu, nonfin) && info == 0) info = -1;
     __syncwarp();
@@ -1694,7 +1719,7 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     // the model are evaluated in fp32 (fast sincos / log: SFU), sums in fp64.
     double(*aJ)[32] = reinterpret_cast<double(*)[32]>(mine);
     double(*aT)[32] = reinterpret_cast<double(*)[32]>(mine + NA * 32 * sizeof(double));
-    T(*sDel)[32] = reinterpret_cast<T(*)[32]>(mine + 2 * NA * 32 * sizeof(double));
+    T(*sDel)[32] = nullptr;
     for (int a = 0; a <= na; ++a) { aJ[a][lane] = 0.0; aT[a][lane] = 0.0; }
     unsigned guard = 0u;  // bit a: some trial state of slot a leaves the pitch guard
     double g = 0.0;
@@ -1888,7 +1913,7 @@ __global__ void __launch_bounds__(32) k_srbd_ls_multi(SrbdConst K, SrbdIter<T> i
     // info_in == nullptr: the info word (k_finalize_info's rule) is derived here from fail / nonfin / pre
     constexpr int NX = 12, NA = 16, PW = 2 * NA + 2;
     __shared__ double aJ[NA][32], aT[NA][32];
-    __shared__ T sDel[24][32];
+    T(*sDel)[32] = nullptr;
     // grid (S * AG, B): block x = ag * S + sblk evaluates stages 32 sblk.. for alpha slots
     // [ag * ca, ag * ca + ca) (ca = ceil((na + 1) / AG)); slots it does not own stay zero in its partial
     const int lane = threadIdx.x, S = gridDim.x / AG, sblk = blockIdx.x % S, ag = blockIdx.x / S, b = blockIdx.y;

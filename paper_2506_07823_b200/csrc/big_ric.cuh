@@ -137,13 +137,129 @@ __device__ void ric_gemm(int Mr, int Nc, int K, T alpha, const T *A, int lda, co
     }
 }
 
-// The products of k_big_ric: SIMT FP32 tiles (ric_gemm) or, with UT (float only), tcgen05 tensor
-// cores in 3xTF32 (tc_gemm, tc.cuh).  Same contract.
-template <typename T, int TR, int TC_, bool TA, bool TB, int TM, bool UT>
+// ---------------------------------------------------------------- warp-level tensor-core products
+// mma.sync.m16n8k8 TF32 with FP32 accumulation in the 3xTF32 split (x = hi + lo, hi = rn_tf32(x),
+// lo = rn_tf32(x - hi); A B ~ hi hi + hi lo + lo hi, the dropped lo lo and the rounding of lo are
+// O(2^-22) relative: FP32-level accuracy).  One warp per (16 MF) x (8 NF) output tile,
+// tiles spread over all warps of the cluster; fragments are loaded straight from global memory
+// (L2-resident per instance) one k-step ahead, so there is no shared-memory staging and no block
+// barrier inside a product.  Same contract as ric_gemm (Cin may alias C).
+__device__ __forceinline__ uint32_t f2tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <bool TA, bool TB, int MF, int NF>
+__device__ void mma_gemm(int Mr, int Nc, int K, float alpha, const float *A, int lda, const float *Bm, int ldb,
+                         const float *Cin, int ldci, float *C, int ldc, int part, int nparts) {
+    constexpr int WM = 16 * MF, WN = 8 * NF;
+    const int lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+    const int nw = blockDim.x >> 5;
+    const int gw = part * nw + (threadIdx.x >> 5), ngw = nparts * nw;
+    const int tmn = (Mr + WM - 1) / WM, tnn = (Nc + WN - 1) / WN;
+    auto ldA = [&](int r, int k) -> float {
+        return (r < Mr && k < K) ? __ldcg(TA ? A + (size_t)k * lda + r : A + (size_t)r * lda + k) : 0.f;
+    };
+    auto ldB = [&](int k, int c) -> float {
+        return (k < K && c < Nc) ? __ldcg(TB ? Bm + (size_t)c * ldb + k : Bm + (size_t)k * ldb + c) : 0.f;
+    };
+    for (int t = gw; t < tmn * tnn; t += ngw) {
+        const int m0 = (t / tnn) * WM, n0 = (t % tnn) * WN;
+        float acc[MF][NF][4];
+#pragma unroll
+        for (int a = 0; a < MF; ++a)
+#pragma unroll
+            for (int c = 0; c < NF; ++c)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) acc[a][c][e] = 0.f;
+        float fa[MF][4], fb[NF][2];
+        auto fetch = [&](int k0, float (&xa)[MF][4], float (&xb)[NF][2]) {
+#pragma unroll
+            for (int a = 0; a < MF; ++a) {
+                const int r = m0 + 16 * a + g;
+                xa[a][0] = ldA(r, k0 + tg);
+                xa[a][1] = ldA(r + 8, k0 + tg);
+                xa[a][2] = ldA(r, k0 + tg + 4);
+                xa[a][3] = ldA(r + 8, k0 + tg + 4);
+            }
+#pragma unroll
+            for (int c = 0; c < NF; ++c) {
+                const int cc = n0 + 8 * c + g;
+                xb[c][0] = ldB(k0 + tg, cc);
+                xb[c][1] = ldB(k0 + tg + 4, cc);
+            }
+        };
+        fetch(0, fa, fb);
+        for (int k0 = 0; k0 < K; k0 += 8) {
+            float na[MF][4], nb[NF][2];
+            const bool more = k0 + 8 < K;
+            if (more) fetch(k0 + 8, na, nb);
+            uint32_t ah[MF][4], al[MF][4], bh[NF][2], bl[NF][2];
+#pragma unroll
+            for (int a = 0; a < MF; ++a)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    ah[a][e] = f2tf32(fa[a][e]);
+                    al[a][e] = f2tf32(fa[a][e] - __uint_as_float(ah[a][e]));
+                }
+#pragma unroll
+            for (int c = 0; c < NF; ++c)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    bh[c][e] = f2tf32(fb[c][e]);
+                    bl[c][e] = f2tf32(fb[c][e] - __uint_as_float(bh[c][e]));
+                }
+#pragma unroll
+            for (int a = 0; a < MF; ++a)
+#pragma unroll
+                for (int c = 0; c < NF; ++c) {
+                    mma_tf32(acc[a][c], al[a], bh[c]);
+                    mma_tf32(acc[a][c], ah[a], bl[c]);
+                    mma_tf32(acc[a][c], ah[a], bh[c]);
+                }
+            if (more) {
+#pragma unroll
+                for (int a = 0; a < MF; ++a)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) fa[a][e] = na[a][e];
+#pragma unroll
+                for (int c = 0; c < NF; ++c) { fb[c][0] = nb[c][0]; fb[c][1] = nb[c][1]; }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < MF; ++a)
+#pragma unroll
+            for (int c = 0; c < NF; ++c)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int r = m0 + 16 * a + g + (e >= 2 ? 8 : 0);
+                    const int cc = n0 + 8 * c + 2 * tg + (e & 1);
+                    if (r < Mr && cc < Nc) {
+                        const float cin = Cin ? __ldcg(Cin + (size_t)r * ldci + cc) : 0.f;
+                        C[(size_t)r * ldc + cc] = fmaf(alpha, acc[a][c][e], cin);
+                    }
+                }
+    }
+}
+
+// The products of k_big_ric: SIMT FP32 tiles (ric_gemm), with UT (float only) tcgen05 tensor cores
+// in 3xTF32 (tc_gemm, tc.cuh), with MM (float only) warp-level mma.sync in 3xTF32 (mma_gemm).
+// Same contract.
+template <typename T, int TR, int TC_, bool TA, bool TB, int TM, bool UT, bool MM = false>
 __device__ __forceinline__ void big_gemm(int Mr, int Nc, int K, const T *A, int lda, const T *Bm, int ldb, const T *Cin,
                                          int ldci, T *C, int ldc, int part, int nparts, RicTiles<T, TM> &tiles,
                                          TcSmem *tcs, TcPhase &ph) {
-    if constexpr (UT) {
+    if constexpr (MM && sizeof(T) == 4) {
+        mma_gemm<TA, TB, 1, 4>(Mr, Nc, K, 1.0f, reinterpret_cast<const float *>(A), lda,
+                               reinterpret_cast<const float *>(Bm), ldb, reinterpret_cast<const float *>(Cin), ldci,
+                               reinterpret_cast<float *>(C), ldc, part, nparts);
+    } else if constexpr (UT) {
         tc_gemm<TA, TB>(Mr, Nc, K, 1.0f, A, lda, Bm, ldb, Cin, ldci, C, ldc, part, nparts, *tcs, ph);
     } else {
         ric_gemm<T, TR, TC_, TA, TB, TM>(Mr, Nc, K, T(1), A, lda, Bm, ldb, Cin, ldci, C, ldc, part, nparts, tiles);
@@ -406,11 +522,12 @@ constexpr uint32_t RIC_TMEM_COLS = 128;
 
 // Fused reverse scan + policy (phases 1-7 above), one cluster of CS CTAs per instance.
 // Writes P_i, p_i (ws.Pp), K_i, k_i (ws.Kk, out.K, out.k), Abar_i, bbar_i (ws.tel).
-template <typename T, int TN, int TU, bool UT = false>
+template <typename T, int TN, int TU, bool UT = false, bool MM = false>
 __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B, int N, BigDims<T> d, BigWork<T> ws,
                                                          LqOut<T> out, int CS) {
     static_assert(!UT || sizeof(T) == 4, "tensor-core products are FP32 (3xTF32) only");
-    constexpr int TM = UT ? 1 : (TN > TU ? TN : TU);
+    static_assert(!MM || sizeof(T) == 4, "mma.sync products are FP32 (3xTF32) only");
+    constexpr int TM = (UT || MM) ? 1 : (TN > TU ? TN : TU);
     __shared__ RicTiles<T, TM> tiles;
     extern __shared__ __align__(16) unsigned char dyn[];
     const int n = d.n, m = d.m, LD = d.LD, LDU = d.LDU;
@@ -447,12 +564,12 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
         T *Kw = ws.Kk + st * d.ksize(), *kw = Kw + (size_t)m * LD;
         T *Ab = ws.tel + st * d.psize(), *bb = Ab + (size_t)n * LD;
         // phase 1: PB = P' B ; g = p' + P' c
-        big_gemm<T, TN, TU, false, false, TM, UT>(n, m, n, Pn, LD, Bm, m, nullptr, 0, PB, ldpb, rank, CS, tiles, tcs, ph);
+        big_gemm<T, TN, TU, false, false, TM, UT, MM>(n, m, n, Pn, LD, Bm, m, nullptr, 0, PB, ldpb, rank, CS, tiles, tcs, ph);
         ric_gemv<T, false>(n, n, Pn, LD, c, pn, 1, g, 1, gw, nwc);
         ric_sync(CS);
         // phase 2: W = [R + B^T PB | S + PB^T A | r + B^T g]
-        big_gemm<T, TU, TU, true, false, TM, UT>(m, m, n, Bm, m, PB, ldpb, R, m, W, ldw, rank, CS, tiles, tcs, ph);
-        big_gemm<T, TU, TN, true, false, TM, UT>(m, n, n, PB, ldpb, A, n, S, n, W + m, ldw, rank, CS, tiles, tcs, ph);
+        big_gemm<T, TU, TU, true, false, TM, UT, MM>(m, m, n, Bm, m, PB, ldpb, R, m, W, ldw, rank, CS, tiles, tcs, ph);
+        big_gemm<T, TU, TN, true, false, TM, UT, MM>(m, n, n, PB, ldpb, A, n, S, n, W + m, ldw, rank, CS, tiles, tcs, ph);
         ric_gemv<T, true>(m, n, Bm, m, g, r, 1, W + m + n, ldw, gw, nwc);  // column m+n of W
         ric_sync(CS);
         // phase 3: Cholesky of G (every CTA, own shared memory), [K | k] = -G^-1 [H | h]
@@ -489,16 +606,16 @@ __global__ void __launch_bounds__(RIC_THREADS, 2) k_big_ric(LqArgs<T> qp, int B,
         }
         ric_sync(CS);
         // phase 4: Abar = A + B K ; bbar = c + B k
-        big_gemm<T, TN, TN, false, false, TM, UT>(n, n, m, Bm, m, Kw, LD, A, n, Ab, LD, rank, CS, tiles, tcs, ph);
+        big_gemm<T, TN, TN, false, false, TM, UT, MM>(n, n, m, Bm, m, Kw, LD, A, n, Ab, LD, rank, CS, tiles, tcs, ph);
         ric_gemv<T, false>(n, m, Bm, m, kw, c, 1, bb, 1, gw, nwc);
         ric_sync(CS);
         // phase 5: V = P' Abar ; w = p' + P' bbar
-        big_gemm<T, TN, TN, false, false, TM, UT>(n, n, n, Pn, LD, Ab, LD, nullptr, 0, V, LD, rank, CS, tiles, tcs, ph);
+        big_gemm<T, TN, TN, false, false, TM, UT, MM>(n, n, n, Pn, LD, Ab, LD, nullptr, 0, V, LD, rank, CS, tiles, tcs, ph);
         ric_gemv<T, false>(n, n, Pn, LD, bb, pn, 1, w, 1, gw, nwc);
         ric_sync(CS);
         // phase 6: P_i = Q + A^T V (+ S^T K) ; p_i = q + A^T w (+ S^T k)   (same tiles / rows: no barrier)
-        big_gemm<T, TN, TN, true, false, TM, UT>(n, n, n, A, n, V, LD, qp.Q + st * n * n, n, Pc, LD, rank, CS, tiles, tcs, ph);
-        if (S) big_gemm<T, TN, TN, true, false, TM, UT>(n, n, m, S, n, Kw, LD, Pc, LD, Pc, LD, rank, CS, tiles, tcs, ph);
+        big_gemm<T, TN, TN, true, false, TM, UT, MM>(n, n, n, A, n, V, LD, qp.Q + st * n * n, n, Pc, LD, rank, CS, tiles, tcs, ph);
+        if (S) big_gemm<T, TN, TN, true, false, TM, UT, MM>(n, n, m, S, n, Kw, LD, Pc, LD, Pc, LD, rank, CS, tiles, tcs, ph);
         ric_gemv<T, true>(n, n, A, n, w, q, 1, pc, 1, gw, nwc);
         if (S) ric_gemv<T, true>(n, m, S, n, kw, pc, 1, pc, 1, gw, nwc);
         ric_sync(CS);

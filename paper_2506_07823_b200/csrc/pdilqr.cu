@@ -126,6 +126,7 @@ struct pdilqr_ctx {
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool fault_combine = false;    // PDILQR_FAULT_COMBINE=1: negative control of the parity tests
     bool nvtx = false;             // PDILQR_NVTX=1: an NVTX range around every kernel launch (tracing)
+    bool big_mma = false;          // large path, f32: warp-level mma.sync 3xTF32 products in k_big_ric (PDILQR_BIG_MMA)
     bool big_tc = false;           // large path, f32: tcgen05 3xTF32 products in k_big_ric (PDILQR_BIG_TC=1);
                                    // off by default: measured slower than the SIMT tiles (K7)
     bool grid_scan = false;        // latency regime: cooperative grid-wide scans + multi-block line search
@@ -1005,11 +1006,13 @@ namespace pdq {
 template <typename T>
 using RicKernT = void (*)(LqArgs<T>, int, int, BigDims<T>, BigWork<T>, LqOut<T>, int);
 template <typename T>
-RicKernT<T> ric_kernel(bool t52, bool ut) {
+RicKernT<T> ric_kernel(bool t52, bool ut, bool mm) {
     if constexpr (std::is_same<T, float>::value) {
+        if (mm) return k_big_ric<float, 1, 1, false, true>;
         if (ut) return k_big_ric<float, 1, 1, true>;
     }
     (void)ut;
+    (void)mm;
     return t52 ? k_big_ric<T, 5, 2> : k_big_ric<T, 3, 3>;
 }
 template <typename T>
@@ -1043,7 +1046,8 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
             k_big_rchk<T><<<g, tpb, ric_smem, st>>>(qp.R, B, N, m, ws.fail);
         }
         {
-            auto kern = ric_kernel<T>(t52, ut);
+            const bool mm = std::is_same<T, float>::value && h->big_mma && !ut;
+            auto kern = ric_kernel<T>(t52, ut, mm);
             const size_t smem = ut ? ric_smem_bytes_tc(m) : ric_smem;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (h->ric_cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -1059,7 +1063,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
             at[0].val.clusterDim.z = 1;
             lc.attrs = at;
             lc.numAttrs = 1;
-            Prof pf(h, ut ? "k_big_ric_tc" : "k_big_ric", st);
+            Prof pf(h, ut ? "k_big_ric_tc" : mm ? "k_big_ric_mma" : "k_big_ric", st);
             cudaError_t e = cudaLaunchKernelEx(&lc, kern, qp, B, N, d, ws, out, h->ric_cs);
             if (e != cudaSuccess) return fail(PDILQR_ERR_CUDA, "k_big_ric launch (cluster %d): %s", h->ric_cs, cudaGetErrorString(e));
         }
@@ -1125,7 +1129,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
 
 template <typename T>
 bool ric_cluster_fits(int cs, size_t smem, bool ut) {
-    const void *kern = (const void *)ric_kernel<T>(false, ut);
+    const void *kern = (const void *)ric_kernel<T>(false, ut, false);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t lc{};
@@ -1342,6 +1346,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
         while (cs < 16 && (long)cfg->batch * cs * 2 <= sms) cs *= 2;
         if (const char *e = std::getenv("PDILQR_BIG_CS")) cs = std::max(1, std::min(16, std::atoi(e)));
         if (const char *e = std::getenv("PDILQR_BIG_TC")) h->big_tc = std::atoi(e) != 0;
+        if (const char *e = std::getenv("PDILQR_BIG_MMA")) h->big_mma = std::atoi(e) != 0;
         const bool ut = esz == 4 && h->big_tc && ric_smem_bytes_tc(cfg->m) <= 227 * 1024;
         const size_t smem = ut ? ric_smem_bytes_tc(cfg->m) : ric_smem_bytes(cfg->m, esz);
         while (cs > 1 && ric_smem_bytes(cfg->m, esz) <= kRicSmemMax) {  // the device must co-schedule a whole cluster

@@ -20,11 +20,13 @@ def P():
     return P
 
 
-@pytest.fixture(autouse=True, params=["simt", "tc"])
+@pytest.fixture(autouse=True, params=["simt", "tc", "mma"])
 def products(request, monkeypatch):
-    """Every large-path test runs with the SIMT FP32 products and with the tcgen05 3xTF32 products
-    of k_big_ric (PDILQR_BIG_TC=1; tc.cuh) -- the same parity bar for both."""
+    """Every large-path test runs with the SIMT FP32 products, the tcgen05 3xTF32 products
+    (PDILQR_BIG_TC=1; tc.cuh) and the warp-level mma.sync 3xTF32 products (PDILQR_BIG_MMA=1;
+    big_ric.cuh mma_gemm) of k_big_ric -- the same parity bar for all three."""
     monkeypatch.setenv("PDILQR_BIG_TC", "1" if request.param == "tc" else "0")
+    monkeypatch.setenv("PDILQR_BIG_MMA", "1" if request.param == "mma" else "0")
     return request.param
 
 

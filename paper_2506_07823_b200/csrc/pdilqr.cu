@@ -121,7 +121,8 @@ struct pdilqr_ctx {
                                    // 1 = one instance per warp (column halves), 0 = two instances per warp (row per lane)
     int fold_w = 14;               // fold_mode 1: MINB blocks/SM (12/14/16)
     int fold_nw = 4;               // fold_mode 2: instances per warp (2..5)
-    int lin_staged = 0;            // k_srbd_lin_rec: 1 = records staged in shared memory, 0 = direct 16-byte stores
+    int lin_staged = 2;            // k_srbd_lin_rec: 2 = two warps (state / control halves) per 32 stages (default),
+                                   // 1 = one thread per stage, records staged in shared memory, 0 = direct 16-byte stores
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
     bool big_legacy = false;       // large path: PDILQR_BIG_LEGACY=1 forces the element/fold/policy kernels
     bool fault_combine = false;    // PDILQR_FAULT_COMBINE=1: negative control of the parity tests
@@ -682,7 +683,11 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         {
             const long tot = (long)B * (N + 1);
             Prof pf(h, "k_srbd_lin_rec", st);
-            if (h->lin_staged) {
+            if (h->lin_staged == 2) {   // two warps per 32 stages (state / control halves)
+                const size_t smem = (size_t)32 * (LinRec::SIZE + 16 / sizeof(T)) * sizeof(T);
+                set_smem(k_srbd_lin_rec2<T>, smem);
+                k_srbd_lin_rec2<T><<<(unsigned)((tot + 31) / 32), 64, smem, st>>>(h->K, iter_of<T>(it, h), B, N, rec);
+            } else if (h->lin_staged) {
                 constexpr int TPB = 32;
                 const size_t smem = (size_t)TPB * (LinRec::SIZE + 16 / sizeof(T)) * sizeof(T);
                 set_smem(k_srbd_lin_rec<T, true>, smem);

@@ -504,6 +504,233 @@ __global__ void __launch_bounds__(STAGED ? 64 : 128, STAGED ? 1 : 4) k_srbd_lin_
     }
 }
 
+// The same record by two warps per 32 stages (block of 64 threads, no divergence): warp 0 the
+// state half (dt Fx rows, q, b, input checks), warp 1 the control half (dt Fu rows, R blocks, r,
+// b~ = b - B R^-1 r, SPD check); both evaluate the model's shared terms.  Half the registers of
+// k_srbd_lin_rec per thread, twice the resident warps.  Flag words: FL[0] (state), FL[1] (control).
+template <typename T>
+__global__ void __launch_bounds__(64, 8) k_srbd_lin_rec2(SrbdConst K, SrbdIter<T> it, int B, int N, T *rec) {
+    constexpr int NX = 12, RS = LinRec::SIZE, RP = RS + 16 / (int)sizeof(T);
+    using LR = LinRec;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T *sm = reinterpret_cast<T *>(smraw);
+    const long total = (long)B * (N + 1);
+    const long base = (long)blockIdx.x * 32;
+    const int t = threadIdx.x & 31, half = threadIdx.x >> 5;
+    const long g = base + t;
+    if (g < total) {
+        T *o = sm + (size_t)t * RP;
+        const int b = (int)(g / (N + 1)), i = (int)(g - (long)b * (N + 1));
+        const size_t sx = (size_t)b * (N + 2) + i, st = (size_t)g;
+        const T dt = T(K.dt);
+        T xv[NX], uv[NX], fe[NX], ln[NX];
+        ld_row<T, NX, true>(xv, it.x + sx * NX);
+        ld_row<T, NX, true>(uv, it.u + st * NX);
+        ld_row<T, NX, true>(fe, it.feet + st * NX);
+        ld_row<T, NX, true>(ln, it.lam + (sx + 1) * NX);
+        const uint32_t cw = *reinterpret_cast<const uint32_t *>(it.con + st * 4);
+        const uint8_t con[4] = {(uint8_t)(cw & 0xff), (uint8_t)((cw >> 8) & 0xff), (uint8_t)((cw >> 16) & 0xff),
+                                (uint8_t)(cw >> 24)};
+        SrbdEval<T> ev;
+        ev.init(K, xv, uv, fe, con);
+        T c[NX];
+        {
+            T xn[NX], fa[NX];
+            ld_row<T, NX, true>(xn, it.x + (sx + 1) * NX);
+            ev.f_all(K, xv, fa);
+#pragma unroll
+            for (int k = 0; k < NX; ++k) c[k] = (xv[k] - xn[k]) + dt * fa[k];   // b_i = h(x_i, u_i) - x_{i+1}
+            if (half == 0) {
+                bool bad = !(fabs((double)xv[4]) < kPitchGuard);
+                T lv[NX];
+                ld_row<T, NX, true>(lv, it.lam + sx * NX);
+#pragma unroll
+                for (int k = 0; k < NX; ++k)
+                    bad = bad || !isfinite(fa[k]) || !isfinite(xv[k]) || !isfinite(uv[k]) || !isfinite(lv[k]);
+                reinterpret_cast<int *>(o + LR::FL)[0] = bad ? 1 : 0;
+                st_row<T, NX, true>(o + LR::C, c);
+#pragma unroll
+                for (int k = 0; k < NX; ++k) c[k] = ln[k] - lv[k];   // state half: c now holds lam_{i+1} - lam_i
+            }
+        }
+        const T w0 = xv[9], w1 = xv[10], w2 = xv[11];
+        if (half == 0) {
+            // ---- state half: dt Fx rows 3-5, 9-11 and q = W_x (x - xref) + (lam_{i+1} - lam_i) + dt Fx^T lam_{i+1}
+            T q[NX];
+            zero(q);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) q[6 + a] = dt * ln[a];
+            auto put_fa = [&](int k, int row, const T (&v)[NX]) {
+                T d[NX];
+#pragma unroll
+                for (int cc = 0; cc < NX; ++cc) { d[cc] = dt * v[cc]; q[cc] = fma(d[cc], ln[row], q[cc]); }
+                st_row<T, NX, true>(o + LR::FA + k * NX, d);
+            };
+            {
+                T a3[NX], a4[NX], a5[NX];
+                zero(a3); zero(a4); zero(a5);
+                a3[3] = ev.tp * (ev.cr * w1 - ev.sr * w2);
+                a3[4] = (ev.sr * w1 + ev.cr * w2) * (ev.icp * ev.icp);
+                a3[9] = T(1); a3[10] = ev.sr * ev.tp; a3[11] = ev.cr * ev.tp;
+                a4[3] = -ev.sr * w1 - ev.cr * w2;
+                a4[10] = ev.cr; a4[11] = -ev.sr;
+                a5[3] = (ev.cr * w1 - ev.sr * w2) * ev.icp;
+                a5[4] = (ev.sr * w1 + ev.cr * w2) * ev.sp * (ev.icp * ev.icp);
+                a5[10] = ev.sr * ev.icp; a5[11] = ev.cr * ev.icp;
+                put_fa(0, 3, a3);
+                put_fa(1, 4, a4);
+                put_fa(2, 5, a5);
+            }
+            {
+                const T *R = ev.R;
+                const T t0 = ev.tau[0], t1 = ev.tau[1], t2 = ev.tau[2];
+                const T cy = ev.cy, sy = ev.sy, cp = ev.cp, sp = ev.sp, sr = ev.sr, cr = ev.cr;
+                const T v0[3] = {T(0), R[2] * t0 + R[5] * t1 + R[8] * t2, -(R[1] * t0 + R[4] * t1 + R[7] * t2)};
+                const T dP[9] = {-cy * sp, cy * cp * sr, cy * cp * cr, -sy * sp, sy * cp * sr, sy * cp * cr, -cp, -sp * sr, -sp * cr};
+                T v1[3], v2[3];
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    v1[cc] = dP[cc] * t0 + dP[3 + cc] * t1 + dP[6 + cc] * t2;
+                    v2[cc] = -R[3 + cc] * t0 + R[cc] * t1;
+                }
+                T Iw[3];
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) Iw[cc] = T(K.I[3 * cc]) * w0 + T(K.I[3 * cc + 1]) * w1 + T(K.I[3 * cc + 2]) * w2;
+                const T Wx[9] = {T(0), -w2, w1, w2, T(0), -w0, -w1, w0, T(0)};
+                const T IWx[9] = {T(0), -Iw[2], Iw[1], Iw[2], T(0), -Iw[0], -Iw[1], Iw[0], T(0)};
+                const T SF[9] = {T(0), -ev.F[2], ev.F[1], ev.F[2], T(0), -ev.F[0], -ev.F[1], ev.F[0], T(0)};
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    T Ii[3], Ma[3], ar[NX];
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) Ii[cc] = T(K.Iinv[3 * a + cc]);
+#pragma unroll
+                    for (int bb = 0; bb < 3; ++bb) Ma[bb] = Ii[0] * R[3 * bb] + Ii[1] * R[3 * bb + 1] + Ii[2] * R[3 * bb + 2];
+                    zero(ar);
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) ar[cc] = Ma[0] * SF[cc] + Ma[1] * SF[3 + cc] + Ma[2] * SF[6 + cc];
+                    ar[3] = Ii[0] * v0[0] + Ii[1] * v0[1] + Ii[2] * v0[2];
+                    ar[4] = Ii[0] * v1[0] + Ii[1] * v1[1] + Ii[2] * v1[2];
+                    ar[5] = Ii[0] * v2[0] + Ii[1] * v2[1] + Ii[2] * v2[2];
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) {
+                        T sacc = T(0);
+#pragma unroll
+                        for (int e = 0; e < 3; ++e) {
+                            const T WI = Wx[3 * e] * T(K.I[cc]) + Wx[3 * e + 1] * T(K.I[3 + cc]) + Wx[3 * e + 2] * T(K.I[6 + cc]);
+                            sacc += Ii[e] * (WI - IWx[3 * e + cc]);
+                        }
+                        ar[9 + cc] = -sacc;
+                    }
+                    put_fa(3 + a, 9 + a, ar);
+                }
+            }
+            T xr[NX];
+            ld_row<T, NX, true>(xr, it.xref + sx * NX);
+#pragma unroll
+            for (int k = 0; k < NX; ++k) q[k] = T(K.wx[k]) * (xv[k] - xr[k]) + (c[k] + q[k]);   // c holds lam_{i+1} - lam_i
+            st_row<T, NX, true>(o + LR::Q, q);
+        } else {
+            // ---- control half: dt Fu rows 9-11, R blocks, r, b~
+            T rv[NX], bd[4];
+            zero(rv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                bd[j] = con[j] ? dt * T(K.imass) : T(0);
+#pragma unroll
+                for (int a = 0; a < 3; ++a) rv[3 * j + a] = fma(bd[j], ln[6 + a], rv[3 * j + a]);
+            }
+            st_row<T, 4, true>(o + LR::BD, bd);
+            T Bw[3][NX];
+            {
+                const T *R = ev.R;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    T Ii[3], Ma[3], br[NX];
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc) Ii[cc] = T(K.Iinv[3 * a + cc]);
+#pragma unroll
+                    for (int bb = 0; bb < 3; ++bb) Ma[bb] = Ii[0] * R[3 * bb] + Ii[1] * R[3 * bb + 1] + Ii[2] * R[3 * bb + 2];
+                    zero(br);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (!con[j]) continue;
+                        const T rx = fe[3 * j] - xv[0], ry = fe[3 * j + 1] - xv[1], rz = fe[3 * j + 2] - xv[2];
+                        const T Sr[9] = {T(0), -rz, ry, rz, T(0), -rx, -ry, rx, T(0)};
+#pragma unroll
+                        for (int cc = 0; cc < 3; ++cc) br[3 * j + cc] = Ma[0] * Sr[cc] + Ma[1] * Sr[3 + cc] + Ma[2] * Sr[6 + cc];
+                    }
+#pragma unroll
+                    for (int cc = 0; cc < NX; ++cc) { Bw[a][cc] = dt * br[cc]; rv[cc] = fma(Bw[a][cc], ln[9 + a], rv[cc]); }
+                    st_row<T, NX, true>(o + LR::FB + a * NX, Bw[a]);
+                }
+            }
+            T urv[NX];
+            if (it.uref) ld_row<T, NX, true>(urv, it.uref + st * NX);
+            else zero(urv);
+            const T rho = T(it.rho_of(b));
+            bool rfail = false;
+            T z[NX];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const bool stance = con[j] != 0;
+                const T wu = stance ? T(K.wu_st) : T(K.wu_sw);
+                const FootBarrier<T> fb = foot_barrier<T>(K, uv[3 * j], uv[3 * j + 1], uv[3 * j + 2]);
+                const T gb[3] = {fb.gx, fb.gy, fb.gz};
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    T rg = wu * (uv[3 * j + a] - urv[3 * j + a]);
+                    if (stance) rg += gb[a];
+                    rv[3 * j + a] += rg;
+                }
+                const T hs = stance ? T(1) : T(0);
+                const T a00 = wu + rho + hs * fb.hxx, a11 = wu + rho + hs * fb.hyy, a22 = wu + rho + hs * fb.hzz;
+                const T a01 = T(0), a02 = hs * fb.hxz, a12 = hs * fb.hyz;
+                const T a10 = a01, a20 = a02, a21 = a12;
+                const T Rb[3][3] = {{a00, a01, a02}, {a10, a11, a12}, {a20, a21, a22}};
+#pragma unroll
+                for (int a = 0; a < 3; ++a) st_row<T, 3, false>(o + LR::RB + 3 * (3 * j + a), Rb[a]);
+                const T c00 = a11 * a22 - a12 * a21, c01 = a02 * a21 - a01 * a22, c02 = a01 * a12 - a02 * a11;
+                const T c10 = a12 * a20 - a10 * a22, c11 = a00 * a22 - a02 * a20, c12 = a02 * a10 - a00 * a12;
+                const T c20 = a10 * a21 - a11 * a20, c21 = a01 * a20 - a00 * a21, c22 = a00 * a11 - a01 * a10;
+                const T det = a00 * c00 + a01 * c10 + a02 * c20;
+                rfail = rfail || !(a00 > T(0)) || !(c22 > T(0)) || !(det > T(0)) || !isfinite(det);
+                const T r0 = rv[3 * j], r1 = rv[3 * j + 1], r2 = rv[3 * j + 2];
+                z[3 * j] = (c00 * r0 + c01 * r1 + c02 * r2) / det;
+                z[3 * j + 1] = (c10 * r0 + c11 * r1 + c12 * r2) / det;
+                z[3 * j + 2] = (c20 * r0 + c21 * r1 + c22 * r2) / det;
+            }
+            st_row<T, NX, true>(o + LR::RV, rv);
+            T bt[NX];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) bt[k] = c[k];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                T s6 = T(0), s9 = T(0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) s6 = fma(bd[j], z[3 * j + a], s6);
+#pragma unroll
+                for (int tt = 0; tt < NX; ++tt) s9 = fma(Bw[a][tt], z[tt], s9);
+                bt[6 + a] = c[6 + a] - s6;
+                bt[9 + a] = c[9 + a] - s9;
+            }
+            st_row<T, NX, true>(o + LR::BT, bt);
+            reinterpret_cast<int *>(o + LR::FL)[1] = rfail ? 2 : 0;
+            if constexpr (sizeof(T) == 4) { o[LR::FL + 2] = T(0); o[LR::FL + 3] = T(0); }
+            else { o[LR::FL + 1] = T(0); o[LR::FL + 2] = T(0); o[LR::FL + 3] = T(0); }
+        }
+    }
+    __syncthreads();
+    const long nrec = total - base < 32 ? total - base : 32;
+    if (nrec <= 0) return;
+    constexpr int EPC = 16 / (int)sizeof(T);
+    T *dst = rec + (size_t)base * RS;
+    for (long e = (long)threadIdx.x * EPC; e < nrec * RS; e += (long)blockDim.x * EPC) {
+        const int tt = (int)(e / RS), k = (int)(e - (long)tt * RS);
+        *reinterpret_cast<int4 *>(dst + e) = *reinterpret_cast<const int4 *>(sm + (size_t)tt * RP + k);
+    }
+}
+
 // Per-worker shared memory of the record-fed fold: matrices of the recursion plus a two-slot ring
 // of linearisation records (stage i-1 lands while stage i is processed).
 template <typename T>
@@ -582,7 +809,7 @@ __global__ void __launch_bounds__(TPB, MINB * 128 / TPB) k_srbd_bwd_fold_rec(Srb
         __syncwarp(mask);
         const T *cur = s.in[i & 1];
         {
-            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0];
+            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0] | reinterpret_cast<const int *>(cur + LR::FL)[1];
             bad = bad || (fl & 1);
             if (fl & 2) fail = min(fail, i + 1);
         }
@@ -861,7 +1088,7 @@ __global__ void __launch_bounds__(64, MINB) k_srbd_bwd_fold_w(SrbdConst K, SrbdI
         __syncwarp();
         const T *cur = s.in[i & 1];
         {
-            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0];
+            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0] | reinterpret_cast<const int *>(cur + LR::FL)[1];
             bad = bad || (fl & 1);
             if (fl & 2) fail = min(fail, i + 1);
         }
@@ -1136,7 +1363,7 @@ __global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIte
         __syncwarp();
         const T *cur = s.in[i & 1];
         {
-            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0];
+            const int fl = reinterpret_cast<const int *>(cur + LR::FL)[0] | reinterpret_cast<const int *>(cur + LR::FL)[1];
             bad = bad || (fl & 1);
             if (fl & 2) fail = min(fail, i + 1);
         }

@@ -759,7 +759,7 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
             constexpr int WPB = LsWarps<T>::value;
             kern<<<(B + WPB - 1) / WPB, 32 * WPB, 0, st>>>(h->K, iter_of<T>(it, h), B, N, ws, dx, du, dl, info_tmp, so, nullptr);
         };
-        switch (h->occ_ls) {
+        switch (sizeof(T) == 8 ? 2 : h->occ_ls) {   // fp64: 2 blocks/SM (the 128-register cap spills)
             case 3: go(k_srbd_fwd_ls<T, 3>); break;
             case 4: go(k_srbd_fwd_ls<T, 4>); break;
             default: go(k_srbd_fwd_ls<T, 2>); break;

@@ -509,7 +509,7 @@ __global__ void __launch_bounds__(STAGED ? 64 : 128, STAGED ? 1 : 4) k_srbd_lin_
 // b~ = b - B R^-1 r, SPD check); both evaluate the model's shared terms.  Half the registers of
 // k_srbd_lin_rec per thread, twice the resident warps.  Flag words: FL[0] (state), FL[1] (control).
 template <typename T>
-__global__ void __launch_bounds__(64, 8) k_srbd_lin_rec2(SrbdConst K, SrbdIter<T> it, int B, int N, T *rec) {
+__global__ void __launch_bounds__(64, sizeof(T) == 4 ? 8 : 4) k_srbd_lin_rec2(SrbdConst K, SrbdIter<T> it, int B, int N, T *rec) {
     constexpr int NX = 12, RS = LinRec::SIZE, RP = RS + 16 / (int)sizeof(T);
     using LR = LinRec;
     extern __shared__ __align__(16) unsigned char smraw[];

@@ -258,3 +258,28 @@ def test_nvtx_ranges_do_not_change_results(P, monkeypatch):
         torch.cuda.synchronize()
         xs.append(d["x"].clone())
     assert torch.equal(xs[0], xs[1])
+
+
+FUSED_VARIANTS = {
+    "default": {},                              # k_srbd_lin_rec2 + k_srbd_bwd_fold_r2 (4 per warp)
+    "nw5": {"PDILQR_FOLD_NW": "5"},             # two rows per lane, 5 instances per warp
+    "mode1": {"PDILQR_FOLD_MODE": "1"},         # one instance per warp, column halves
+    "mode0": {"PDILQR_FOLD_MODE": "0"},         # row per lane, two instances per warp
+    "lin1": {"PDILQR_LIN_STAGED": "1"},         # records by one thread per stage
+    "linrec0": {"PDILQR_LINREC": "0"},          # linearisation inside the sequential fold
+}
+
+
+@pytest.mark.parametrize("variant", list(FUSED_VARIANTS))
+@pytest.mark.parametrize("N", [0, 1, 7, 50])
+def test_step_parity_fused_variants(P, O, monkeypatch, variant, N):
+    """The single-chunk fused path (leaf_chunk = N + 2 forces it at any batch) in every kernel
+    variant behind a switch, B = 9 (partial warps: shadow workers must store nothing), two steps."""
+    for k, v in FUSED_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    step_parity(P, O, 9, N, torch.float32, seed=70 + N, leaf_chunk=N + 2, steps=2)
+
+
+@pytest.mark.parametrize("N", [7, 50])
+def test_step_parity_fused_f64(P, O, N):
+    step_parity(P, O, 9, N, torch.float64, seed=80 + N, leaf_chunk=N + 2, steps=2, dir_steps=(0, 1))

@@ -121,6 +121,7 @@ struct pdilqr_ctx {
                                    // 1 = one instance per warp (column halves), 0 = two instances per warp (row per lane)
     int fold_w = 14;               // fold_mode 1: MINB blocks/SM (12/14/16)
     int fold_nw = 4;               // fold_mode 2: instances per warp (2..5)
+    int fold_cp = 1;               // fold_mode 2: stance-compacted policy solve (PDILQR_FOLD_CP=0: all 12 pivots)
     int lin_staged = 2;            // k_srbd_lin_rec: 2 = two warps (state / control halves) per 32 stages (default),
                                    // 1 = one thread per stage, records staged in shared memory, 0 = direct 16-byte stores
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
@@ -704,7 +705,8 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
                 set_smem(kern, smem);
                 kern<<<(B + nw - 1) / nw, 32, smem, st>>>(h->K, iter_of<T>(it, h), B, N, ws, rec, info_tmp);
             };
-            switch (h->fold_nw) {
+            if (!h->fold_cp) g2(k_srbd_bwd_fold_r2<T, 4, false>, 4, sizeof(FoldR2Smem<T, 4>));
+            else switch (h->fold_nw) {
                 case 2: g2(k_srbd_bwd_fold_r2<T, 2>, 2, sizeof(FoldR2Smem<T, 2>)); break;
                 case 3: g2(k_srbd_bwd_fold_r2<T, 3>, 3, sizeof(FoldR2Smem<T, 3>)); break;
                 case 5: g2(k_srbd_bwd_fold_r2<T, 5>, 5, sizeof(FoldR2Smem<T, 5>)); break;
@@ -1339,6 +1341,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_FOLD_W")) h->fold_w = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_MODE")) h->fold_mode = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_NW")) h->fold_nw = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_FOLD_CP")) h->fold_cp = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_LIN_STAGED")) h->lin_staged = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FAULT_COMBINE")) h->fault_combine = std::atoi(e) != 0;
     if (const char *e = std::getenv("PDILQR_NVTX")) h->nvtx = std::atoi(e) != 0;

@@ -1298,7 +1298,13 @@ struct FoldR2Smem {
     T pad[NW <= 4 ? 12 : 8];
 };
 
-template <typename T, int NW>
+// CP (stance compaction): the controls of a swing foot have zero columns in B, so they decouple
+// from the policy system (G block diagonal: the stance block and the swing feet's R blocks, H = 0 and
+// K = 0 on the swing rows, k = -R^-1 r there).  Per stage and instance the feet are permuted stance
+// first (B's columns permuted when stored, so P B, G, H, h come out permuted), the elimination runs
+// over the first 3 ns pivots only (ns = stance feet; the warp's maximum), and K, k are written back in
+// the natural control order.  Same arithmetic on every element that is not structurally zero.
+template <typename T, int NW, bool CP = true>
 __global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIter<T> it, int B, int N, LqWork<T> ws,
                                                            const T *rec, int32_t *info_out) {
     constexpr int NX = 12, NL = 6 * NW;
@@ -1368,15 +1374,40 @@ __global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIte
             if (fl & 2) fail = min(fail, i + 1);
         }
         // B row l + 6 (rows 6-8: dt/m on the stance feet' diagonal, 9-11 the record's dt Fu rows)
-        T b1[NX];
+        T b1[NX], bd[4];
+        int perm = 0xE4, ncm = NX;   // foot of permuted position q = (perm >> 2q) & 3 (identity without CP)
         {
-            T fb[NX], bd[4];
+            T fb[NX];
             ld_row<T, NX, true>(fb, cur + LR::FB + (lhi ? l - 3 : 0) * NX);
             ld_row<T, 4, true>(bd, cur + LR::BD);
 #pragma unroll
             for (int j = 0; j < NX; ++j) b1[j] = lhi ? fb[j] : ((j % 3 == l) ? bd[j / 3] : T(0));
-            if (act) st_row<T, NX, true>(s.B6 + l * NX, b1);
+            if constexpr (CP) {
+                int ns = 0, q = 0;
+                perm = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (bd[j] != T(0)) { perm |= j << (2 * q); ++q; ++ns; }
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (bd[j] == T(0)) { perm |= j << (2 * q); ++q; }
+                ncm = __reduce_max_sync(0xffffffffu, 3 * ns);
+                T bp[NX];
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    const int fq = (perm >> (2 * qq)) & 3;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        bp[3 * qq + a] = fq == 0 ? b1[a] : fq == 1 ? b1[3 + a] : fq == 2 ? b1[6 + a] : b1[9 + a];
+                }
+                if (act) st_row<T, NX, true>(s.B6 + l * NX, bp);
+            } else {
+                if (act) st_row<T, NX, true>(s.B6 + l * NX, b1);
+            }
         }
+        // this lane's compacted rows c0 = l, c1 = l + 6 are the controls o0, o1 (identity without CP)
+        const int o0 = 3 * ((perm >> (2 * (l / 3))) & 3) + l % 3;
+        const int o1 = 3 * ((perm >> (2 * (2 + l / 3))) & 3) + l % 3;
         __syncwarp();
         // ---------------- P B (rows 0-5 of B are zero) and w = p + P b~
         {
@@ -1412,12 +1443,12 @@ __global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIte
             T pc0[NX], pc1[NX];
 #pragma unroll
             for (int k = 0; k < NX; ++k) { pc0[k] = s.PB[k * NX + r0]; pc1[k] = s.PB[k * NX + r1]; }
-            {   // R rows (block diagonal, 3 x 3 per foot)
+            {   // R rows (block diagonal, 3 x 3 per foot; the permutation keeps foot blocks together)
                 const int j0 = r0 / 3, j1 = r1 / 3;
 #pragma unroll
                 for (int j = 0; j < NX; ++j) {
-                    a0[j] = (j / 3 == j0) ? cur[LR::RB + 3 * r0 + (j % 3)] : T(0);
-                    a1[j] = (j / 3 == j1) ? cur[LR::RB + 3 * r1 + (j % 3)] : T(0);
+                    a0[j] = (j / 3 == j0) ? cur[LR::RB + 3 * o0 + (j % 3)] : T(0);
+                    a1[j] = (j / 3 == j1) ? cur[LR::RB + 3 * o1 + (j % 3)] : T(0);
                 }
             }
 #pragma unroll
@@ -1444,16 +1475,16 @@ __global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIte
             T cv[NX], pv[NX];
             ld_row<T, NX, true>(cv, cur + LR::C);
             ld_row<T, NX, true>(pv, s.p);
-            T h0 = cur[LR::RV + r0], h1 = cur[LR::RV + r1];
+            T h0 = cur[LR::RV + o0], h1 = cur[LR::RV + o1];
 #pragma unroll
             for (int k = 0; k < NX; ++k) ffma2(pc0[k], pc1[k], cv[k], cv[k], h0, h1);
             {
-                const T bdj0 = cur[LR::BD + r0 / 3], bdj1 = cur[LR::BD + r1 / 3];
-                h0 = fma(bdj0, (r0 % 3 == 0) ? pv[6] : (r0 % 3 == 1) ? pv[7] : pv[8], h0);
-                h1 = fma(bdj1, (r1 % 3 == 0) ? pv[6] : (r1 % 3 == 1) ? pv[7] : pv[8], h1);
+                const T bdj0 = cur[LR::BD + o0 / 3], bdj1 = cur[LR::BD + o1 / 3];
+                h0 = fma(bdj0, (o0 % 3 == 0) ? pv[6] : (o0 % 3 == 1) ? pv[7] : pv[8], h0);
+                h1 = fma(bdj1, (o1 % 3 == 0) ? pv[6] : (o1 % 3 == 1) ? pv[7] : pv[8], h1);
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const T fb0 = cur[LR::FB + a * NX + r0], fb1 = cur[LR::FB + a * NX + r1];
+                    const T fb0 = cur[LR::FB + a * NX + o0], fb1 = cur[LR::FB + a * NX + o1];
                     ffma2(fb0, fb1, pv[9 + a], pv[9 + a], h0, h1);
                 }
             }
@@ -1461,34 +1492,46 @@ __global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIte
             x1[NX] = h1;
         }
         {
-            // SPD Gauss-Jordan, unnormalised sweep; pivot k lives in lane k % 6, slot k / 6
+            // SPD Gauss-Jordan, unnormalised sweep; pivot k lives in lane k % 6, slot k / 6.  The pivot
+            // count NP is a compile-time bound per branch (6: every instance of the warp has at most two
+            // stance feet; 12 otherwise), so neither loop carries a branch.
             bool ok = true;
-            T piv0 = T(1), piv1 = T(1);
+            // rows that never pivot (swing rows beyond the warp's last pivot) keep their diagonal
+            T piv0 = CP ? a0[0] : T(1), piv1 = CP ? a1[0] : T(1);
+            if constexpr (CP) {
 #pragma unroll
-            for (int k = 0; k < NX; ++k) {
-                const int pl = k % 6, ps = k / 6;
-                const int src = wb + pl;
-                const T own = ps == 0 ? a0[k] : a1[k];
-                const T rk = rcp_rn(own);
-                const T pvv = __shfl_sync(0xffffffffu, own, src);
-                const T rpv = __shfl_sync(0xffffffffu, rk, src);
-                ok = ok && (pvv > T(0)) && isfinite(pvv);
-                const bool isp0 = ps == 0 && l == pl, isp1 = ps == 1 && l == pl;
-                const T f0 = isp0 ? T(0) : a0[k] * rpv;
-                const T f1 = isp1 ? T(0) : a1[k] * rpv;
-                if (isp0) piv0 = pvv;
-                if (isp1) piv1 = pvv;
-#pragma unroll
-                for (int j = k + 1; j < NX; ++j) {
-                    const T pj = __shfl_sync(0xffffffffu, ps == 0 ? a0[j] : a1[j], src);
-                    ffma2(-f0, -f1, pj, pj, a0[j], a1[j]);
-                }
-#pragma unroll
-                for (int j = 0; j <= NX; ++j) {
-                    const T pj = __shfl_sync(0xffffffffu, ps == 0 ? x0[j] : x1[j], src);
-                    ffma2(-f0, -f1, pj, pj, x0[j], x1[j]);
-                }
+                for (int j = 1; j < NX; ++j) { piv0 = (j == r0) ? a0[j] : piv0; piv1 = (j == r1) ? a1[j] : piv1; }
             }
+            auto gj = [&](auto np_tag) {
+                constexpr int NP = decltype(np_tag)::value;
+#pragma unroll
+                for (int k = 0; k < NP; ++k) {
+                    const int pl = k % 6, ps = k / 6;
+                    const int src = wb + pl;
+                    const T own = ps == 0 ? a0[k] : a1[k];
+                    const T rk = rcp_rn(own);
+                    const T pvv = __shfl_sync(0xffffffffu, own, src);
+                    const T rpv = __shfl_sync(0xffffffffu, rk, src);
+                    ok = ok && (pvv > T(0)) && isfinite(pvv);
+                    const bool isp0 = ps == 0 && l == pl, isp1 = ps == 1 && l == pl;
+                    const T f0 = isp0 ? T(0) : a0[k] * rpv;
+                    const T f1 = isp1 ? T(0) : a1[k] * rpv;
+                    if (isp0) piv0 = pvv;
+                    if (isp1) piv1 = pvv;
+#pragma unroll
+                    for (int j = k + 1; j < NP; ++j) {   // columns >= NP are zero in the rows that pivot
+                        const T pj = __shfl_sync(0xffffffffu, ps == 0 ? a0[j] : a1[j], src);
+                        ffma2(-f0, -f1, pj, pj, a0[j], a1[j]);
+                    }
+#pragma unroll
+                    for (int j = 0; j <= NX; ++j) {
+                        const T pj = __shfl_sync(0xffffffffu, ps == 0 ? x0[j] : x1[j], src);
+                        ffma2(-f0, -f1, pj, pj, x0[j], x1[j]);
+                    }
+                }
+            };
+            if (CP && ncm <= 6) gj(std::integral_constant<int, 6>{});
+            else gj(std::integral_constant<int, NX>{});
             const T i0 = -rcp_rn(piv0), i1 = -rcp_rn(piv1);
 #pragma unroll
             for (int j = 0; j <= NX; ++j) { x0[j] *= i0; x1[j] *= i1; }   // [K | k] = -G^-1 [H | h]
@@ -1498,14 +1541,14 @@ __global__ void __launch_bounds__(32, 6) k_srbd_bwd_fold_r2(SrbdConst K, SrbdIte
             T kr0[NX], kr1[NX];
 #pragma unroll
             for (int j = 0; j < NX; ++j) { kr0[j] = x0[j]; kr1[j] = x1[j]; }
-            st_row<T, NX, true>(s.K + r0 * NX, kr0);
-            st_row<T, NX, true>(s.K + r1 * NX, kr1);
-            s.k[r0] = x0[NX];
-            s.k[r1] = x1[NX];
-            st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + r0 * NX, kr0);
-            st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + r1 * NX, kr1);
-            Kk[(size_t)i * KL::SIZE + KL::k + r0] = x0[NX];
-            Kk[(size_t)i * KL::SIZE + KL::k + r1] = x1[NX];
+            st_row<T, NX, true>(s.K + o0 * NX, kr0);
+            st_row<T, NX, true>(s.K + o1 * NX, kr1);
+            s.k[o0] = x0[NX];
+            s.k[o1] = x1[NX];
+            st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + o0 * NX, kr0);
+            st_row<T, NX, true>(Kk + (size_t)i * KL::SIZE + KL::K + o1 * NX, kr1);
+            Kk[(size_t)i * KL::SIZE + KL::k + o0] = x0[NX];
+            Kk[(size_t)i * KL::SIZE + KL::k + o1] = x1[NX];
         }
         __syncwarp();
         {

@@ -82,12 +82,19 @@ def flops_per_instance(N: int, n: int = 12, m: int = 12, chunk: int | None = Non
     # P B 2 n nb m, G = R + (P B)^T B 2 m nb m, H 2 m na n + 6 m, h = r + (P B)^T b + B^T p 2 n m + 2 nb m,
     # SPD solve m^3/3 + 2 m^2 (n+1), Abar = A + B K 2 nb m n, bbar 2 nb m, V = P Abar 2 n^3,
     # p' = q + Abar^T w 2 n^2, P' 2 na n^2 + 6 n, w = p + P b~ 2 n^2  (the flops it has to do)
+    # With the stance compaction the controls of swing feet (zero columns of B) drop out as well:
+    # ms = stance controls (6 under the trot of configs 2/3), the count below replaces m by ms in
+    # every term that multiplies a column of B or a row of the policy.
     nb = na = 6
-    fold_struct = (N + 1) * (2 * n * nb * m + 2 * m * nb * m + 2 * m * na * n + 6 * m + 2 * n * m + 2 * nb * m
-                             + m ** 3 / 3 + 2 * m ** 2 * (n + 1) + 2 * nb * m * n + 2 * nb * m + 2 * n ** 3
-                             + 2 * n ** 2 + 2 * na * n ** 2 + 6 * n + 2 * n ** 2)
+    ms = 6
+
+    def fold_count(mm):
+        return (N + 1) * (2 * n * nb * mm + 2 * mm * nb * mm + 2 * mm * na * n + 6 * mm + 2 * n * mm + 2 * nb * mm
+                          + mm ** 3 / 3 + 2 * mm ** 2 * (n + 1) + 2 * nb * mm * n + 2 * nb * mm + 2 * n ** 3
+                          + 2 * n ** 2 + 2 * na * n ** 2 + 6 * n + 2 * n ** 2)
     return {"k_elem_init": init, "k_scan_bwd": bwd, "k_policy": policy, "k_scan_fwd": fwd, "k_tail": tail,
-            "k_srbd_bwd_fold": fold_struct, "k_srbd_bwd_fold_dense": policy + fold_s0,
+            "k_srbd_bwd_fold": policy + fold_s0, "k_srbd_bwd_fold_struct": fold_count(m),
+            "k_srbd_bwd_fold_stance": fold_count(ms),
             "k_srbd_fwd_ls": Lf * 2 * n ** 2 + tail}
 
 
@@ -418,7 +425,7 @@ def main():
 
     # --------------------------------------------------------------- roofline of the dominant kernel
     fl = flops_per_instance(N, chunk=h_chunk(args, B, N))
-    kern = {k: v for k, v in prof.items() if k in fl and not k.endswith("_dense")}
+    kern = {k: v for k, v in prof.items() if k in fl}
     dom = max(kern, key=lambda k: kern[k][1]) if kern else None
     sm_mhz = clocks.get("sm_max_mhz") or 1965.0
     peak = fp32_peak_tflops(sm_mhz)
@@ -436,12 +443,16 @@ def main():
                 "share_of_step": (tot / launches) / step_ms,
                 "peak_basis": f"FP32 FMA pipe: 148 SMs x 128 lanes x 2 flop x {sm_mhz:.0f} MHz (max SM clock)",
                 "per_kernel_ms": {k: v[1] / v[0] for k, v in prof.items()}}
-        if dom == "k_srbd_bwd_fold":   # the same time against the dense D7 flop count (structural zeros included)
-            dn = fl["k_srbd_bwd_fold_dense"] * B / avg_s / 1e12
-            roof["dense_equivalent"] = {"achieved": dn, "frac": dn / peak,
-                                        "flops_per_launch": fl["k_srbd_bwd_fold_dense"] * B,
-                                        "basis": "dense 12x12 D7 Riccati-form count (DESIGN.md Roofline); "
-                                                 "`achieved` above counts only the structurally nonzero products"}
+        if dom == "k_srbd_bwd_fold":   # the same time against the flops left after the structural zeros
+            roof["flops_basis"] = ("algorithmic: the dense 12x12 D7 Riccati-form count per stage (policy + "
+                                   "4n^3 + 4n^2 + 2nm + 6m, DESIGN.md Roofline), the basis of the earlier rounds")
+            for key, what in (("k_srbd_bwd_fold_struct", "the products without the structurally zero rows of B "
+                               "and the identity part of A"),
+                              ("k_srbd_bwd_fold_stance", "as struct, and without the swing-foot controls (zero "
+                               "columns of B; 6 stance controls under the trot) -- the flops the kernel has to do")):
+                v = fl[key] * B / avg_s / 1e12
+                roof[key.replace("k_srbd_bwd_fold_", "count_")] = {"achieved": v, "frac": v / peak,
+                                                                   "flops_per_launch": fl[key] * B, "basis": what}
         mp = measured_peaks()
         if mp.get("bf16_tflops"):
             scale = float(mp["bf16_tflops"]) / 2250.0

@@ -261,7 +261,8 @@ def test_nvtx_ranges_do_not_change_results(P, monkeypatch):
 
 
 FUSED_VARIANTS = {
-    "default": {},                              # k_srbd_lin_rec2 + k_srbd_bwd_fold_r2 (4 per warp)
+    "default": {},                              # k_srbd_lin_rec2 + k_srbd_bwd_fold_r2 (4 per warp, stance-compacted)
+    "cp0": {"PDILQR_FOLD_CP": "0"},             # two rows per lane, all 12 pivots
     "nw5": {"PDILQR_FOLD_NW": "5"},             # two rows per lane, 5 instances per warp
     "mode1": {"PDILQR_FOLD_MODE": "1"},         # one instance per warp, column halves
     "mode0": {"PDILQR_FOLD_MODE": "0"},         # row per lane, two instances per warp

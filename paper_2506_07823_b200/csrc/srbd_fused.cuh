@@ -1922,12 +1922,26 @@ __global__ void __launch_bounds__(128, MINB) k_srbd_fwd_ls(SrbdConst K, SrbdIter
     T *ring = reinterpret_cast<T *>(mine);
     constexpr int CH = 156 * (int)sizeof(T) / 16;  // 16-byte chunks per 156-entry block
     constexpr int EPC = 16 / (int)sizeof(T);
+    // per-lane chunk slots of a stage block, fixed for the whole rollout: chunk c = lane + 32 q of the
+    // [(Abar, bbar) | (K, k) | (P, p)] block comes from array c / CH at offset (c mod CH) chunks; the
+    // three arrays share the per-stage stride TP, so a stage only adds s * TP to the slot pointers
+    constexpr int NQ = (3 * CH + 31) / 32;
+    const T *srcq[NQ];
+    int dstq[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int c = lane + 32 * q;
+        const int blk = c < CH ? 0 : c < 2 * CH ? 1 : 2;
+        srcq[q] = (c < 3 * CH) ? (blk == 0 ? Te : blk == 1 ? Kk : Pp) + (c - blk * CH) * EPC : nullptr;
+        dstq[q] = c * EPC;
+    }
     auto issue = [&](int s) {  // stage s -> ring slot s % D (always commits a group)
         if (s <= N) {
             T *dst = ring + (size_t)(s % D) * SM::BLK;
-            const T *sa = Te + (size_t)s * TP, *sk = Kk + (size_t)s * KL::SIZE, *sp = Pp + (size_t)s * TP;
-            for (int c = lane; c < 3 * CH; c += 32)
-                cp_async16(dst + c * EPC, c < CH ? sa + c * EPC : c < 2 * CH ? sk + (c - CH) * EPC : sp + (c - 2 * CH) * EPC);
+            const size_t so = (size_t)s * TP;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                if (srcq[q]) cp_async16(dst + dstq[q], srcq[q] + so);
         }
         cp_async_commit();
     };

@@ -230,10 +230,19 @@ __device__ __forceinline__ bool combine_cheap(CombineSmem<T, NX> &s, unsigned ma
 // Terminal element i = N+1 (Eq. 13, reading R4): A~ = C~ = b~ = 0, P~ = P_{N+1}, p~ = p_{N+1}.
 // Padded instantiations (n < NX or m < NU): state rows/cols >= n are zero, R is padded with
 // the identity; the padded entries of every element are then exactly zero.
+// Per-worker shared memory words of k_elem_init: ZS, ZB, zr; the exact instantiation also stages the
+// stage's R, S, B, A, Q, r, c, q there with one cp.async burst (all global loads in flight at once
+// instead of two dependent load phases around the elimination; ncu r2_elem: the kernel was bound by
+// global-load latency, long-scoreboard 2.7 per issue at 8 warps per SM).
+template <int NX, int NU, bool EX>
+__host__ __device__ constexpr int elem_init_smw() {
+    return 2 * NU * NX + round_up4(NU) + (EX ? 5 * NX * NX + 3 * NX : 0);
+}
+
 template <typename T, int NX, int NU, bool EX>
-__global__ void __launch_bounds__(128) k_elem_init(LqArgs<T> qp, int B, int N, int n, int m, LqWork<T> ws) {
+__global__ void __launch_bounds__(128, (sizeof(T) == 4 && NX <= 12) ? 3 : 1) k_elem_init(LqArgs<T> qp, int B, int N, int n, int m, LqWork<T> ws) {
     constexpr int WS = worker_width(NX > NU ? NX : NU);
-    constexpr int SMW = 2 * NU * NX + round_up4(NU);  // per-worker smem: ZS, ZB, zr
+    constexpr int SMW = elem_init_smw<NX, NU, EX>();
     using L = VE<NX>;
     extern __shared__ __align__(16) unsigned char smraw[];
     const int lane = worker_lane<WS>();
@@ -262,19 +271,45 @@ __global__ void __launch_bounds__(128) k_elem_init(LqArgs<T> qp, int B, int N, i
         return;
     }
     const size_t st = (size_t)b * (N + 1) + i;
+    // exact instantiation: the stage's R, S, B, A, Q (NX x NX each) and r, c, q into shared memory,
+    // 16-byte cp.async chunks spread over the worker's lanes, one wait
+    T *stg = sm + 2 * NU * NX + round_up4(NU);
+    const T *gR = qp.R + st * m * m, *gS = qp.S + st * m * n, *gB = qp.Bm + st * n * m;
+    const T *gA = qp.A + st * n * n, *gQ = qp.Q + st * n * n;
+    if constexpr (EX) {
+        constexpr int EPC = 16 / (int)sizeof(T), MC = NX * NX / EPC, VC = NX / EPC;
+        for (int ch = lane; ch < 5 * MC + 3 * VC; ch += WS) {
+            if (ch < 5 * MC) {
+                const int am = ch / MC, k = (ch - am * MC) * EPC;
+                const T *src = am == 0 ? gR : am == 1 ? gS : am == 2 ? gB : am == 3 ? gA : gQ;
+                cp_async16(stg + am * NX * NX + k, src + k);
+            } else {
+                const int av = (ch - 5 * MC) / VC, k = (ch - 5 * MC - av * VC) * EPC;
+                const T *src = av == 0 ? qp.r + st * m : av == 1 ? qp.c + st * n : qp.q + st * n;
+                cp_async16(stg + 5 * NX * NX + av * NX + k, src + k);
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncwarp(mask);
+        gR = stg; gS = stg + NX * NX; gB = stg + 2 * NX * NX; gA = stg + 3 * NX * NX; gQ = stg + 4 * NX * NX;
+    }
+    const T *vr_ = EX ? stg + 5 * NX * NX : qp.r + st * m;
+    const T *vc_ = EX ? stg + 5 * NX * NX + NX : qp.c + st * n;
+    const T *vq_ = EX ? stg + 5 * NX * NX + 2 * NX : qp.q + st * n;
     // --- GJ rows: lane r < NU owns row r of R and of [S | r | B^T]
     {
         const int ru = lane < NU ? lane : 0;
         T a[NU], rhs[2 * NX + 1];
         const bool valid = EX || ru < m;
         if (valid) {
-            ld_row<T, NU, EX>(a, qp.R + st * m * m + ru * m, m);
+            ld_row<T, NU, EX>(a, gR + ru * m, m);
             T srow[NX], bcol[NX];
-            ld_row<T, NX, EX>(srow, qp.S + st * m * n + ru * n, n);
-            ld_col<T, NX>(bcol, qp.Bm + st * n * m + ru, m, n);
+            ld_row<T, NX, EX>(srow, gS + ru * n, n);
+            ld_col<T, NX>(bcol, gB + ru, m, n);
 #pragma unroll
             for (int j = 0; j < NX; ++j) { rhs[j] = srow[j]; rhs[NX + 1 + j] = bcol[j]; }
-            rhs[NX] = qp.r[st * m + ru];
+            rhs[NX] = vr_[ru];
         } else {
 #pragma unroll
             for (int j = 0; j < NU; ++j) a[j] = (j == ru) ? T(1) : T(0);
@@ -298,14 +333,14 @@ __global__ void __launch_bounds__(128) k_elem_init(LqArgs<T> qp, int B, int N, i
     T brow[NU], scol[NU], row[NX], out[NX];
     const bool vr = EX || r < n;
     if (vr) {
-        ld_row<T, NU, EX>(brow, qp.Bm + st * n * m + r * m, m);
-        ld_col<T, NU>(scol, qp.S + st * m * n + r, n, m);
+        ld_row<T, NU, EX>(brow, gB + r * m, m);
+        ld_col<T, NU>(scol, gS + r, n, m);
     } else {
         zero(brow);
         zero(scol);
     }
     // A~
-    if (vr) ld_row<T, NX, EX>(row, qp.A + st * n * n + r * n, n);
+    if (vr) ld_row<T, NX, EX>(row, gA + r * n, n);
     else zero(row);
 #pragma unroll
     for (int k = 0; k < NU; ++k) {
@@ -320,7 +355,7 @@ __global__ void __launch_bounds__(128) k_elem_init(LqArgs<T> qp, int B, int N, i
     row_mat<T, NU, NX, NX>(out, brow, ZB);
     if (lane < NX) st_row<T, NX, true>(e + L::C + r * NX, out);
     // P~ = Q - S^T (R^-1 S)
-    if (vr) ld_row<T, NX, EX>(row, qp.Q + st * n * n + r * n, n);
+    if (vr) ld_row<T, NX, EX>(row, gQ + r * n, n);
     else zero(row);
 #pragma unroll
     for (int k = 0; k < NU; ++k) {
@@ -330,8 +365,8 @@ __global__ void __launch_bounds__(128) k_elem_init(LqArgs<T> qp, int B, int N, i
         for (int j = 0; j < NX; ++j) row[j] = fma(-scol[k], y[j], row[j]);
     }
     if (lane < NX) st_row<T, NX, true>(e + L::P + r * NX, row);
-    const T cb = vr ? qp.c[st * n + r] : T(0);
-    const T qq = vr ? qp.q[st * n + r] : T(0);
+    const T cb = vr ? vc_[r] : T(0);
+    const T qq = vr ? vq_[r] : T(0);
     T bt = cb, pt = qq;
 #pragma unroll
     for (int k = 0; k < NU; ++k) { bt = fma(-brow[k], zr[k], bt); pt = fma(-scol[k], zr[k], pt); }

@@ -445,7 +445,7 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
     if (!skip_init) {  // element init
         const int wpb = 128 / WS;
         const long nw = (long)B * (N + 2);
-        const size_t smem = (size_t)wpb * (2 * NU * NX + round_up4(NU)) * sizeof(T);
+        const size_t smem = (size_t)wpb * elem_init_smw<NX, NU, EX>() * sizeof(T);
         set_smem(k_elem_init<T, NX, NU, EX>, smem);
         Prof pf(h, "k_elem_init", st);
         k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
@@ -893,7 +893,7 @@ pdilqr_status run_seg_reduce(pdilqr_ctx *h, const LqArgs<T> &qp, T *S_out, int32
         const bool ex = h->var == V12;
         const int wpb = 128 / WS;
         const long nw = (long)B * (N + 2);
-        const size_t smem = (size_t)wpb * (2 * NU * NX + round_up4(NU)) * sizeof(T);
+        const size_t smem = (size_t)wpb * elem_init_smw<NX, NU, true>() * sizeof(T);
         {
             Prof pf(h, "k_elem_init", st);
             if (ex) {

@@ -1,0 +1,17 @@
+"""pdilqr_solve_lq on the config-3 SRBD linearisation (generic LQ handle, B = 4096, N = 50), for ncu."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from workloads import synth
+import paper_2506_07823_b200 as P
+B, N = 4096, 50
+prob = synth.srbd_problem(B, N=N, seed=synth.BASE_SEED)
+keys = ("x", "u", "lam", "x0", "x_ref", "u_ref", "contact", "feet")
+it = {k: torch.from_numpy(np.ascontiguousarray(prob[k] if prob[k].dtype == np.uint8 else prob[k].astype(np.float32))).cuda() for k in keys}
+hs = P.PdIlqr(N=N, n=12, m=12, batch=B, dtype=torch.float32, model="srbd", srbd=prob["params"])
+qp = hs.linearize(it); qp.pop("info", None)
+h = P.PdIlqr(N=N, n=12, m=12, batch=B, dtype=torch.float32)
+out = h.solve_lq(qp)
+for _ in range(3): h.solve_lq(qp, out=out)
+torch.cuda.synchronize()
+print("ok", bool((out["info"] == 0).all()))

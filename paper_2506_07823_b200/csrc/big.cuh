@@ -353,6 +353,92 @@ __global__ void __launch_bounds__(BIG_THREADS) k_big_fold(int B, int N, BigDims<
     if (fail != INT_MAX && threadIdx.x == 0) atomicMin(ws.fail + b, (1 << 24) | fail);
 }
 
+// ------------------------------------------------- reverse associative scan for large n (tree)
+// One Kogge-Stone level of the reverse scan over the N+2 value elements (Eq. 11 full rule
+// with readings R1-R3; the small-n path's D9 order): for every instance b and j < L - dl,
+// dst_j = src_j (x) src_{j+dl}; the elements with j + dl >= L are already complete suffixes and are
+// copied.  One CTA per combine (persistent over (instance, j)), CTA-level dense algebra with the
+// pivoted Gauss-Jordan on W = [I + C1 P2 | A1 | C1 | b1 - C1 p2]:
+//   X = M^-1 A1, Y = M^-1 C1, z = M^-1 (b1 - C1 p2);  A = A2 X,  b = A2 z + b2,
+//   C = A2 Y A2^T + C2,  P = A1^T (P2 X) + P1,  p = X^T (p2 + P2 b1) + p1   (C, P re-symmetrised, R22).
+// Scratch slot: W (n x ld(3n+1), global unless it fits shared memory), T1 (n x LD), two vectors.
+template <typename T>
+__global__ void __launch_bounds__(BIG_THREADS) k_bigks_level(int B, int N, int dl, BigDims<T> d, BigWork<T> ws,
+                                                             const T *src, T *dst, int w_in_smem) {
+    __shared__ GemmSmem<T> gsm;
+    __shared__ GjShared gjs;
+    extern __shared__ __align__(16) unsigned char dyn[];
+    const int n = d.n, LD = d.LD, ldw = ld_of(3 * n + 1), L = N + 2;
+    const size_t es = d.esize();
+    T *slot = ws.scratch + (size_t)blockIdx.x * ws.slot;
+    T *W = w_in_smem ? reinterpret_cast<T *>(dyn) : slot;
+    T *T1 = slot + (size_t)n * ldw, *v1 = T1 + (size_t)n * LD, *v2 = v1 + LD;
+    for (long item = blockIdx.x; item < (long)B * L; item += gridDim.x) {
+        const int b = (int)(item / L), j = (int)(item % L);
+        const T *e1 = src + ((size_t)b * L + j) * es;
+        T *o = dst + ((size_t)b * L + j) * es;
+        if (j + dl >= L) {   // complete suffix: unchanged
+            for (size_t t = threadIdx.x; t < es; t += BIG_THREADS) o[t] = e1[t];
+            __syncthreads();
+            continue;
+        }
+        const T *e2 = src + ((size_t)b * L + j + dl) * es;
+        const T *A1 = e1, *C1 = e1 + (size_t)n * LD, *P1 = e1 + (size_t)2 * n * LD, *b1 = e1 + (size_t)3 * n * LD, *p1 = b1 + LD;
+        const T *A2 = e2, *C2 = e2 + (size_t)n * LD, *P2 = e2 + (size_t)2 * n * LD, *b2 = e2 + (size_t)3 * n * LD, *p2 = b2 + LD;
+        T *oA = o, *oC = o + (size_t)n * LD, *oP = o + (size_t)2 * n * LD, *ob = o + (size_t)3 * n * LD, *op = ob + LD;
+        cta_gemv<T, false>(n, n, T(1), C1, LD, p2, T(0), v1);            // C1 p2
+        for (int t = threadIdx.x; t < n * (3 * n + 1); t += BIG_THREADS) {
+            const int r = t / (3 * n + 1), c = t - r * (3 * n + 1);
+            T v;
+            if (c < n) v = (r == c) ? T(1) : T(0);
+            else if (c < 2 * n) v = A1[(size_t)r * LD + (c - n)];
+            else if (c < 3 * n) v = C1[(size_t)r * LD + (c - 2 * n)];
+            else v = b1[r] - v1[r];
+            W[(size_t)r * ldw + c] = v;
+        }
+        __syncthreads();
+        cta_gemm<T, false, false>(n, n, n, T(1), C1, LD, P2, LD, T(1), W, ldw, gsm);   // M = I + C1 P2
+        if (!cta_gj<T, true>(n, 2 * n + 1, W, ldw, gjs) && threadIdx.x == 0) atomicMin(ws.fail + b, (1 << 24) | (j + 1));
+        const T *X = W + n, *Y = W + 2 * n;
+        for (int r = threadIdx.x; r < n; r += BIG_THREADS) v2[r] = W[(size_t)r * ldw + 3 * n];   // z
+        __syncthreads();
+        cta_gemm<T, false, false>(n, n, n, T(1), A2, LD, X, ldw, T(0), oA, LD, gsm);           // A = A2 X
+        cta_gemv<T, false>(n, n, T(1), A2, LD, v2, T(0), ob);                                  // A2 z
+        for (int r = threadIdx.x; r < n; r += BIG_THREADS) ob[r] += b2[r];
+        __syncthreads();
+        cta_gemm<T, false, true>(n, n, n, T(1), Y, ldw, A2, LD, T(0), T1, LD, gsm);            // Y A2^T
+        for (int t = threadIdx.x; t < n * LD; t += BIG_THREADS) oC[t] = C2[t];
+        __syncthreads();
+        cta_gemm<T, false, false>(n, n, n, T(1), A2, LD, T1, LD, T(1), oC, LD, gsm);          // C = A2 Y A2^T + C2
+        cta_gemm<T, false, false>(n, n, n, T(1), P2, LD, X, ldw, T(0), T1, LD, gsm);           // P2 X
+        for (int t = threadIdx.x; t < n * LD; t += BIG_THREADS) oP[t] = P1[t];
+        __syncthreads();
+        cta_gemm<T, true, false>(n, n, n, T(1), A1, LD, T1, LD, T(1), oP, LD, gsm);           // P = A1^T P2 X + P1
+        cta_gemv<T, false>(n, n, T(1), P2, LD, b1, T(0), v1);                                  // P2 b1
+        for (int r = threadIdx.x; r < n; r += BIG_THREADS) v1[r] += p2[r];                    // w
+        __syncthreads();
+        cta_gemv<T, true>(n, n, T(1), X, ldw, v1, T(0), op);                                   // X^T w
+        for (int r = threadIdx.x; r < n; r += BIG_THREADS) op[r] += p1[r];
+        __syncthreads();
+        cta_symmetrize<T>(n, oC, LD);
+        cta_symmetrize<T>(n, oP, LD);
+    }
+}
+
+// Read-out after the last level: (P_i, p_i) = (P~, p~) of the complete suffix s_i (reading R5).
+template <typename T>
+__global__ void k_bigks_readout(int B, int N, BigDims<T> d, const T *s, T *Pp) {
+    const int L = N + 2, n = d.n, LD = d.LD;
+    const size_t es = d.esize(), ps = d.psize();
+    const long tot = (long)B * L * (long)ps;
+    for (long t = (long)blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += (long)gridDim.x * blockDim.x) {
+        const long el = t / (long)ps;
+        const size_t k = (size_t)(t - el * (long)ps);
+        const T *e = s + (size_t)el * es;
+        Pp[(size_t)el * ps + k] = k < (size_t)n * LD ? e[(size_t)2 * n * LD + k] : e[(size_t)3 * n * LD + LD + (k - (size_t)n * LD)];
+    }
+}
+
 // ------------------------------------------------------------------------------- policy
 // Per stage: PB = P_{i+1} B, g = p_{i+1} + P_{i+1} b; W = [G | H | h] with G = R + B^T PB,
 // H = S + PB^T A, h = B^T g + r; GJ (SPD) -> K = -G^-1 H, k = -G^-1 h; Abar = A + B K,

@@ -85,6 +85,7 @@ bool pick_variant(int n, int m, Variant &v, int &NX, int &NU) {
 
 struct Layout {
     size_t elems, vslots, Pp, Kk, tel, tslots, dxw, fail, nonfin, pre, info_tmp, stats;
+    size_t elems2 = 0;  // large path with leaf_chunk = 1: second element buffer of the tree scan
     size_t kinds_b, kinds_f, ls_part, ls_cnt;  // grid-scan slot kinds, multi-block line-search scratch
     size_t conv, active;                       // pdilqr_solve per-instance state, active counter
     size_t rho;                                // pdilqr_solve Levenberg-Marquardt shift per instance (double)
@@ -226,7 +227,8 @@ size_t big_slot(int n, int m) {
     const size_t init = (size_t)m * ld_of(m + 2 * n + 1);
     const size_t fold = (size_t)n * ld_of(n) * 2 + (size_t)n * ld_of(2 * n) + 2 * ld_of(n);
     const size_t pol = (size_t)n * ld_of(m) + (size_t)m * ld_of(m + n + 1) + ld_of(n);
-    return (std::max({init, fold, pol, ric_slot(n, m)}) + 63) / 64 * 64;
+    const size_t ks = (size_t)n * ld_of(3 * n + 1) + (size_t)n * ld_of(n) + 2 * ld_of(n);  // k_bigks_level
+    return (std::max({init, fold, pol, ks, ric_slot(n, m)}) + 63) / 64 * 64;
 }
 constexpr int kBigPersistent = 148 * 4;  // CTAs of the persistent (stage-parallel) big kernels
 constexpr size_t kRicSmemMax = 200 * 1024;  // k_big_ric keeps the m x m Cholesky factor in shared memory
@@ -237,6 +239,7 @@ Layout make_big_layout(const pdilqr_config *c, int esz) {
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off = align_up(off + bytes); return o; };
     L.elems = take(B * (N + 2) * (3 * n * LD + 2 * LD) * esz);
+    if (c->leaf_chunk == 1) L.elems2 = take(B * (N + 2) * (3 * n * LD + 2 * LD) * esz);   // tree scan
     L.Pp = take(B * (N + 2) * (n * LD + LD) * esz);
     L.Kk = take(B * (N + 1) * (m * LD + LDU) * esz);
     L.tel = take(B * (N + 1) * (n * LD + LD) * esz);
@@ -1042,7 +1045,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
     ws.fail = reinterpret_cast<int32_t *>(h->ws + h->lay.fail);
     cudaMemsetAsync(ws.fail, 0x7f, (size_t)B * 4, st);
     const size_t ric_smem = ric_smem_bytes(m, (int)sizeof(T));
-    if (ric_smem <= kRicSmemMax && !h->big_legacy) {  // fused Riccati-form fold (big_ric.cuh)
+    if (ric_smem <= kRicSmemMax && !h->big_legacy && !h->lay.elems2) {  // fused Riccati-form fold (big_ric.cuh)
         const bool t52 = n <= 80 && m <= 32 && h->ric_cs == 1;  // config-5-like: 80-row n tiles, 32-wide m tiles
         const bool ut = ric_use_tc<T>(h, m);                      // tcgen05 3xTF32 products (tc.cuh)
         {
@@ -1104,12 +1107,34 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
         Prof pf(h, "k_big_init", st);
         k_big_init<T><<<gpers, BIG_THREADS, in ? wb : 0, st>>>(qp, B, N, d, ws, in);
     }
-    {
+    int scan_launches = 0;
+    if (h->lay.elems2) {
+        // leaf_chunk = 1: the paper's reverse associative scan over the N+2 elements,
+        // Kogge-Stone levels dl = 1, 2, 4, ... with CTA-level full combines, then the read-out
+        const size_t wb = wbytes(n, 3 * n + 1);
+        const int in = wb <= kSmemW;
+        if (in) cudaFuncSetAttribute(k_bigks_level<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);
+        T *bufs[2] = {ws.elems, reinterpret_cast<T *>(h->ws + h->lay.elems2)};
+        int cur = 0;
+        const int Lr = N + 2;
+        const int gk = (int)std::min<long>((long)kBigPersistent, (long)B * Lr);
+        for (int dl = 1; dl < Lr; dl *= 2) {
+            Prof pf(h, "k_bigks_level", st);
+            k_bigks_level<T><<<gk, BIG_THREADS, in ? wb : 0, st>>>(B, N, dl, d, ws, bufs[cur], bufs[1 - cur], in);
+            cur = 1 - cur;
+            ++scan_launches;
+        }
+        Prof pf(h, "k_bigks_readout", st);
+        const long tot = (long)B * Lr * (long)(n * d.LD + d.LD);
+        k_bigks_readout<T><<<(unsigned)std::min<long>((tot + 255) / 256, 148 * 16), 256, 0, st>>>(B, N, d, bufs[cur], ws.Pp);
+        ++scan_launches;
+    } else {
         const size_t wb = wbytes(n, 2 * n);
         const int in = wb <= kSmemW;
         if (in) cudaFuncSetAttribute(k_big_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wb);  // + static tiles
         Prof pf(h, "k_big_fold", st);
         k_big_fold<T><<<B, BIG_THREADS, in ? wb : 0, st>>>(B, N, d, ws, in);
+        ++scan_launches;
     }
     {
         const size_t wb = wbytes(m, m + n + 1);
@@ -1122,7 +1147,7 @@ pdilqr_status run_big(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t 
         Prof pf(h, "k_big_fwd", st);
         k_big_fwd<T><<<B, BIG_THREADS, 0, st>>>(qp.dx0, B, N, d, ws, out);
     }
-    int launches = 4;
+    int launches = 3 + scan_launches;
     if (info) {
         int32_t *nonfin = reinterpret_cast<int32_t *>(h->ws + h->lay.nonfin);
         cudaMemsetAsync(nonfin, 0, (size_t)B * 4, st);

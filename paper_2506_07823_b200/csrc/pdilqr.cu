@@ -767,6 +767,7 @@ pdilqr_status run_step_fused(pdilqr_ctx *h, pdilqr_iterate *it, pdilqr_stats *st
         switch (sizeof(T) == 8 ? 2 : h->occ_ls) {   // fp64: 2 blocks/SM (the 128-register cap spills)
             case 3: go(k_srbd_fwd_ls<T, 3>); break;
             case 4: go(k_srbd_fwd_ls<T, 4>); break;
+            case 5: go(k_srbd_fwd_ls<T, 5>); break;
             default: go(k_srbd_fwd_ls<T, 2>); break;
         }
     }

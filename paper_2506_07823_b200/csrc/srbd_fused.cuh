@@ -1821,13 +1821,21 @@ __device__ __forceinline__ void ls_stage(const SrbdConst &K, const SrbdIter<T> &
             const F fx = fma(al, df[q][0], f0[q][0]), fy = fma(al, df[q][1], f0[q][1]), fz = fma(al, df[q][2], f0[q][2]);
             const F mfz = mu * fz;
             const F xv[6] = {mfz - fx, mfz + fx, mfz - fy, mfz + fy, fz - fmn, fmx - fz};
-            F prod = F(1.), quad = F(0.);
+            bool alllog = true;
 #pragma unroll
-            for (int cc = 0; cc < 6; ++cc) {
-                const F t = (xv[cc] - F(2.) * bdl) * ibdl;
-                const bool lg = xv[cc] >= bdl;
-                prod *= lg ? xv[cc] : F(1.);
-                quad += lg ? F(0.) : F(0.5) * bmu * (t * t - F(1.)) - bmu * lbd;
+            for (int cc = 0; cc < 6; ++cc) alllog = alllog && xv[cc] >= bdl;
+            F prod = F(1.), quad = F(0.);
+            if (alllog) {   // the common case: every constraint in the logarithmic branch (same product order)
+#pragma unroll
+                for (int cc = 0; cc < 6; ++cc) prod *= xv[cc];
+            } else {
+#pragma unroll
+                for (int cc = 0; cc < 6; ++cc) {
+                    const F t = (xv[cc] - F(2.) * bdl) * ibdl;
+                    const bool lg = xv[cc] >= bdl;
+                    prod *= lg ? xv[cc] : F(1.);
+                    quad += lg ? F(0.) : F(0.5) * bmu * (t * t - F(1.)) - bmu * lbd;
+                }
             }
             Jb += quad - bmu * fast_log(prod);
         }

@@ -373,6 +373,198 @@ __global__ void __launch_bounds__(128, (sizeof(T) == 4 && NX <= 12) ? 3 : 1) k_e
     if (lane < NX) { e[L::b + r] = bt; e[L::p + r] = pt; }
 }
 
+// Element initialisation for exact 12 x 12 problems with TWO ROWS PER LANE (design D11 of the
+// fused fold applied to Eq. 12): a worker is 6 lanes, lane l owns rows l and l + 6, 4 items (instance,
+// stage) per warp (lanes 24-31 shadow lane 23 and store nothing).  The stage's R, S, B, A, Q, r, c, q
+// arrive in one cp.async burst; the SPD Gauss-Jordan on R with the 25 right-hand sides [S | r | B^T]
+// keeps both rows of a lane in one FFMA2; then A~ = A - B Z_S, C~ = B Z_B, P~ = Q - S^T Z_S,
+// b~ = c - B z_r, p~ = q - S^T z_r with every loaded operand row feeding two row updates.  A terminal
+// item (i = N+1) runs the same code on R = I and then writes Eq. 13 instead (the warp's shuffles stay
+// converged).  Same arithmetic as k_elem_init.
+template <typename T>
+struct ElemR2Smem {
+    T R[144], S[144], Bm[144], A[144], Q[144], r[12], c[12], q[12];
+    T ZS[144], ZB[144], zr[12];
+    T pad[8];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(64) k_elem_init_r2(LqArgs<T> qp, int B, int N, LqWork<T> ws) {
+    constexpr int NX = 12, NW = 4, NL = 6 * NW, NRHS = 2 * NX + 1;
+    using L = VE<NX>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    const int Ln = threadIdx.x & 31;
+    const int w = Ln < NL ? Ln / 6 : NW - 1;
+    const int l = Ln < NL ? Ln - 6 * w : 5;
+    const bool lane_act = Ln < NL;
+    ElemR2Smem<T> &s = reinterpret_cast<ElemR2Smem<T> *>(smraw)[(threadIdx.x >> 5) * NW + w];
+    const int L2 = N + 2;
+    const long total = (long)B * L2;
+    const long item_raw = ((long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * NW + w;
+    if (__all_sync(0xffffffffu, item_raw >= total)) return;
+    const bool live = item_raw < total;
+    const long item = live ? item_raw : total - 1;
+    const int b = (int)(item / L2), i = (int)(item - (long)b * L2);
+    const bool term = i == N + 1;
+    const bool act = lane_act && live;
+    const int r0 = l, r1 = l + 6, wb = 6 * w;
+    const size_t st = (size_t)b * (N + 1) + (term ? 0 : i);
+    // ---- stage inputs (a terminal item uses R = I and zeros: same elimination, result discarded)
+    if (!term) {
+        constexpr int EPC = 16 / (int)sizeof(T), MC = NX * NX / EPC, VC = NX / EPC;
+        if (lane_act) {
+            for (int ch = l; ch < 5 * MC + 3 * VC; ch += 6) {
+                if (ch < 5 * MC) {
+                    const int am = ch / MC, k = (ch - am * MC) * EPC;
+                    const T *src = am == 0 ? qp.R + st * 144 : am == 1 ? qp.S + st * 144 : am == 2 ? qp.Bm + st * 144
+                                 : am == 3 ? qp.A + st * 144 : qp.Q + st * 144;
+                    cp_async16(s.R + am * 144 + k, src + k);
+                } else {
+                    const int av = (ch - 5 * MC) / VC, k = (ch - 5 * MC - av * VC) * EPC;
+                    const T *src = av == 0 ? qp.r + st * 12 : av == 1 ? qp.c + st * 12 : qp.q + st * 12;
+                    cp_async16(s.r + av * 12 + k, src + k);
+                }
+            }
+        }
+        cp_async_commit();
+        cp_async_wait<0>();
+    } else if (lane_act) {
+        for (int t = l; t < 5 * 144 + 36; t += 6) s.R[t] = (t < 144 && t % 13 == 0) ? T(1) : T(0);
+    }
+    __syncwarp();
+    // ---- SPD Gauss-Jordan: lane l holds rows l, l + 6 of R and of [S | r | B^T]
+    T a0[NX], a1[NX], x0[NRHS], x1[NRHS];
+    ld_row<T, NX, true>(a0, s.R + r0 * NX);
+    ld_row<T, NX, true>(a1, s.R + r1 * NX);
+    {
+        T t0[NX], t1[NX];
+        ld_row<T, NX, true>(t0, s.S + r0 * NX);
+        ld_row<T, NX, true>(t1, s.S + r1 * NX);
+#pragma unroll
+        for (int j = 0; j < NX; ++j) { x0[j] = t0[j]; x1[j] = t1[j]; }
+        x0[NX] = s.r[r0];
+        x1[NX] = s.r[r1];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) { x0[NX + 1 + j] = s.Bm[j * NX + r0]; x1[NX + 1 + j] = s.Bm[j * NX + r1]; }
+    }
+    bool ok = true;
+    T piv0 = T(1), piv1 = T(1);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) {
+        const int pl = k % 6, ps = k / 6;
+        const int src = wb + pl;
+        const T own = ps == 0 ? a0[k] : a1[k];
+        const T rk = rcp_rn(own);
+        const T pvv = __shfl_sync(0xffffffffu, own, src);
+        const T rpv = __shfl_sync(0xffffffffu, rk, src);
+        ok = ok && (pvv > T(0)) && isfinite(pvv);
+        const bool isp0 = ps == 0 && l == pl, isp1 = ps == 1 && l == pl;
+        const T f0 = isp0 ? T(0) : a0[k] * rpv;
+        const T f1 = isp1 ? T(0) : a1[k] * rpv;
+        if (isp0) piv0 = pvv;
+        if (isp1) piv1 = pvv;
+#pragma unroll
+        for (int j = k + 1; j < NX; ++j) {
+            const T pj = __shfl_sync(0xffffffffu, ps == 0 ? a0[j] : a1[j], src);
+            ffma2(-f0, -f1, pj, pj, a0[j], a1[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < NRHS; ++j) {
+            const T pj = __shfl_sync(0xffffffffu, ps == 0 ? x0[j] : x1[j], src);
+            ffma2(-f0, -f1, pj, pj, x0[j], x1[j]);
+        }
+    }
+    {
+        const T i0 = rcp_rn(piv0), i1 = rcp_rn(piv1);
+#pragma unroll
+        for (int j = 0; j < NRHS; ++j) { x0[j] *= i0; x1[j] *= i1; }
+    }
+    if (!term && !ok && l == 0 && act) atomicMin(ws.fail + b, i + 1);
+    if (lane_act) {   // Z_S, z_r, Z_B rows (all lanes of live and shadow workers write their own slice)
+        T zs0[NX], zs1[NX], zb0[NX], zb1[NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) { zs0[j] = x0[j]; zs1[j] = x1[j]; zb0[j] = x0[NX + 1 + j]; zb1[j] = x1[NX + 1 + j]; }
+        st_row<T, NX, true>(s.ZS + r0 * NX, zs0);
+        st_row<T, NX, true>(s.ZS + r1 * NX, zs1);
+        st_row<T, NX, true>(s.ZB + r0 * NX, zb0);
+        st_row<T, NX, true>(s.ZB + r1 * NX, zb1);
+        s.zr[r0] = x0[NX];
+        s.zr[r1] = x1[NX];
+    }
+    __syncwarp();
+    T *e = ws.elems + ((size_t)b * L2 + i) * L::SIZE;
+    if (term) {   // Eq. 13: A~ = C~ = 0, P~ = P_{N+1}, b~ = 0, p~ = p_{N+1}
+        if (act) {
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+                const int r = l + 6 * sl;
+                T z[NX], pr[NX];
+                zero(z);
+                ld_row<T, NX, true>(pr, qp.Pt + (size_t)b * 144 + r * NX);
+                st_row<T, NX, true>(e + L::A + r * NX, z);
+                st_row<T, NX, true>(e + L::C + r * NX, z);
+                st_row<T, NX, true>(e + L::P + r * NX, pr);
+                e[L::b + r] = T(0);
+                e[L::p + r] = qp.pt[(size_t)b * NX + r];
+            }
+        }
+        return;
+    }
+    // ---- element rows r0, r1
+    T br0[NX], br1[NX], sc0[NX], sc1[NX];
+    ld_row<T, NX, true>(br0, s.Bm + r0 * NX);
+    ld_row<T, NX, true>(br1, s.Bm + r1 * NX);
+#pragma unroll
+    for (int k = 0; k < NX; ++k) { sc0[k] = s.S[k * NX + r0]; sc1[k] = s.S[k * NX + r1]; }
+    {   // A~ = A - B Z_S
+        T o0[NX], o1[NX];
+        ld_row<T, NX, true>(o0, s.A + r0 * NX);
+        ld_row<T, NX, true>(o1, s.A + r1 * NX);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            T y[NX];
+            ld_row<T, NX, true>(y, s.ZS + k * NX);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) ffma2(-br0[k], -br1[k], y[j], y[j], o0[j], o1[j]);
+        }
+        if (act) { st_row<T, NX, true>(e + L::A + r0 * NX, o0); st_row<T, NX, true>(e + L::A + r1 * NX, o1); }
+    }
+    {   // C~ = B Z_B
+        T o0[NX], o1[NX];
+        zero(o0);
+        zero(o1);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            T y[NX];
+            ld_row<T, NX, true>(y, s.ZB + k * NX);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) ffma2(br0[k], br1[k], y[j], y[j], o0[j], o1[j]);
+        }
+        if (act) { st_row<T, NX, true>(e + L::C + r0 * NX, o0); st_row<T, NX, true>(e + L::C + r1 * NX, o1); }
+    }
+    {   // P~ = Q - S^T Z_S
+        T o0[NX], o1[NX];
+        ld_row<T, NX, true>(o0, s.Q + r0 * NX);
+        ld_row<T, NX, true>(o1, s.Q + r1 * NX);
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            T y[NX];
+            ld_row<T, NX, true>(y, s.ZS + k * NX);
+#pragma unroll
+            for (int j = 0; j < NX; ++j) ffma2(-sc0[k], -sc1[k], y[j], y[j], o0[j], o1[j]);
+        }
+        if (act) { st_row<T, NX, true>(e + L::P + r0 * NX, o0); st_row<T, NX, true>(e + L::P + r1 * NX, o1); }
+    }
+    T bt0 = s.c[r0], bt1 = s.c[r1], pt0 = s.q[r0], pt1 = s.q[r1];
+#pragma unroll
+    for (int k = 0; k < NX; ++k) {
+        const T z = s.zr[k];
+        ffma2(-br0[k], -br1[k], z, z, bt0, bt1);
+        ffma2(-sc0[k], -sc1[k], z, z, pt0, pt1);
+    }
+    if (act) { e[L::b + r0] = bt0; e[L::b + r1] = bt1; e[L::p + r0] = pt0; e[L::p + r1] = pt1; }
+}
+
 // Negative control of the parity tests (PDILQR_FAULT_COMBINE=1, never set in
 // production): perturb P~[0][0] of the element of stage floor(N/2) of instance 0 by 1e-3 (1 + |P~00|),
 // so every combine that consumes it is wrong; the parity tests must then fail for instance 0.

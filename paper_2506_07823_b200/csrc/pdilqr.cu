@@ -123,6 +123,7 @@ struct pdilqr_ctx {
     int fold_w = 14;               // fold_mode 1: MINB blocks/SM (12/14/16)
     int fold_nw = 4;               // fold_mode 2: instances per warp (2..5)
     int fold_cp = 1;               // fold_mode 2: stance-compacted policy solve (PDILQR_FOLD_CP=0: all 12 pivots)
+    int elem_r2 = 0;               // generic LQ, exact 12x12: PDILQR_ELEM_R2=1 -> k_elem_init_r2 (two rows per lane; measured slower)
     int lin_staged = 2;            // k_srbd_lin_rec: 2 = two warps (state / control halves) per 32 stages (default),
                                    // 1 = one thread per stage, records staged in shared memory, 0 = direct 16-byte stores
     int ric_cs = 1;                // large path: CTAs per instance (thread-block cluster size) of k_big_ric
@@ -448,10 +449,21 @@ pdilqr_status run_lq(pdilqr_ctx *h, const LqArgs<T> &qp, LqOut<T> out, int32_t *
     if (!skip_init) {  // element init
         const int wpb = 128 / WS;
         const long nw = (long)B * (N + 2);
-        const size_t smem = (size_t)wpb * elem_init_smw<NX, NU, EX>() * sizeof(T);
-        set_smem(k_elem_init<T, NX, NU, EX>, smem);
         Prof pf(h, "k_elem_init", st);
-        k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
+        bool done = false;
+        if constexpr (EX && NX == 12 && NU == 12) {
+            if (h->elem_r2 && qp.S) {   // two rows per lane, 8 items per 64-thread block
+                const size_t smem2 = 8 * sizeof(ElemR2Smem<T>);
+                set_smem(k_elem_init_r2<T>, smem2);
+                k_elem_init_r2<T><<<(unsigned)((nw + 7) / 8), 64, smem2, st>>>(qp, B, N, ws);
+                done = true;
+            }
+        }
+        if (!done) {
+            const size_t smem = (size_t)wpb * elem_init_smw<NX, NU, EX>() * sizeof(T);
+            set_smem(k_elem_init<T, NX, NU, EX>, smem);
+            k_elem_init<T, NX, NU, EX><<<(unsigned)((nw + wpb - 1) / wpb), wpb * WS, smem, st>>>(qp, B, N, n, m, ws);
+        }
         ++launches;
         if (h->fault_combine) {  // negative control (tests only): corrupt one element of instance 0
             k_fault_inject<T, NX><<<1, 1, 0, st>>>(ws, N);
@@ -1369,6 +1381,7 @@ pdilqr_status pdilqr_create(const pdilqr_config *cfg, int device, void *workspac
     if (const char *e = std::getenv("PDILQR_FOLD_NW")) h->fold_nw = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FOLD_CP")) h->fold_cp = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_LIN_STAGED")) h->lin_staged = std::atoi(e);
+    if (const char *e = std::getenv("PDILQR_ELEM_R2")) h->elem_r2 = std::atoi(e);
     if (const char *e = std::getenv("PDILQR_FAULT_COMBINE")) h->fault_combine = std::atoi(e) != 0;
     if (const char *e = std::getenv("PDILQR_NVTX")) h->nvtx = std::atoi(e) != 0;
     if (v == VBIG) {  // large path: cluster size of k_big_ric (CTAs per instance) so that B * CS fills the SMs

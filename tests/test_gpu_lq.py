@@ -86,6 +86,17 @@ def test_random_dense_12x12(P, O, dtype, chunk):
     assert ref is not None
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("N", [0, 1, 50])
+def test_elem_init_two_rows_per_lane(P, O, monkeypatch, dtype, N):
+    """The opt-in two-rows-per-lane element initialisation (PDILQR_ELEM_R2=1, k_elem_init_r2):
+    B = 37 (partial warps: shadow workers store nothing), terminal items in every warp mix."""
+    monkeypatch.setenv("PDILQR_ELEM_R2", "1")
+    qp = rounded(synth.random_lq(37, N, 12, 12, seed=111 + N), dtype)
+    out, _ = run_gpu(P, qp, dtype, N + 2)
+    check(O, qp, dtype, out)
+
+
 @pytest.mark.parametrize("dims", [(3, 2, 9), (5, 1, 17), (8, 4, 30), (8, 8, 11), (16, 16, 20), (13, 7, 25), (1, 1, 5)])
 @pytest.mark.parametrize("chunk", [1, 5, 0])
 def test_padded_dimensions(P, O, dims, chunk):

@@ -221,7 +221,14 @@ int default_chunk(const pdilqr_config *c) {
     if (c->leaf_chunk > 0) return c->leaf_chunk;
     // Batch-parallelism already fills 148 SMs for large B: fold each instance in one chunk.
     // For small B use the full tree (span 2 ceil(log2 L)).  See DESIGN.md "Scan schedule".
-    return c->batch >= 148 ? c->N + 2 : 1;
+    if (c->batch >= 148) return c->N + 2;
+    if (c->model != PDILQR_MODEL_SRBD) return 1;
+    // SRBD step, measured crossover (profiles/r2_crossover_b.txt): the fused fold's latency is
+    // ~4 us per stage whatever the batch, the tree's time grows with B * L; mid batches take the
+    // fold for short horizons and 8-stage chunks for long ones
+    const long L = (long)c->N + 2;
+    if ((long)c->batch * L <= 2500) return 1;
+    return L <= 64 ? c->N + 2 : 8;
 }
 
 size_t big_slot(int n, int m) {

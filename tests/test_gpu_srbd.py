@@ -142,7 +142,7 @@ def test_step_parity_perturbed_batch(P, O, dtype):
     tree scans with the M-solve combine).  The first-step direction and iterate change are held to
     the north-star 1e-4 (f32; measured worst 4e-5 with cond(KKT) ~ 6e8) and 1e-9 (f64), eta to 1e-5
     at every step."""
-    step_parity(P, O, 64, 50, dtype, seed=32, perturb=1.0, steps=2,
+    step_parity(P, O, 64, 50, dtype, seed=32, perturb=1.0, steps=2, leaf_chunk=1,
                 dir_steps=(0, 1) if dtype == torch.float64 else (0,))
 
 

@@ -284,3 +284,10 @@ def test_step_parity_fused_variants(P, O, monkeypatch, variant, N):
 @pytest.mark.parametrize("N", [7, 50])
 def test_step_parity_fused_f64(P, O, N):
     step_parity(P, O, 9, N, torch.float64, seed=80 + N, leaf_chunk=N + 2, steps=2, dir_steps=(0, 1))
+
+
+@pytest.mark.parametrize("N", [400, 1000])
+def test_step_parity_fused_long_horizon(P, O, N):
+    """The fused single-chunk path (records + two-rows-per-lane fold, fp32) over long horizons: the
+    D7 recursion never factorises M = I + C~P~, so the first-step direction holds 1e-4."""
+    step_parity(P, O, 9, N, torch.float32, seed=90 + N, leaf_chunk=N + 2, steps=1, dir_steps=(0,))

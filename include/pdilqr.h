@@ -91,8 +91,13 @@ typedef struct {
     double theta_max;       /* filter threshold on theta (reading R10); <= 0 -> 1e-2 (N+1)    */
     int32_t leaf_chunk;     /* scan leaf chunk c >= 1: elements folded sequentially per chunk,
                                chunk summaries combined by a Blelloch tree (Eq. 8).
-                               1 = pure tree over all N+2 elements; >= N+2 = single chunk
-                               (sequential fold).  0 -> library default.                     */
+                               1 = pure tree over all N+2 elements (n, m <= 16: Kogge-Stone /
+                               Blelloch scans; 16 < n, m <= 256: Kogge-Stone levels of CTA-level
+                               full combines); >= N+2 = single chunk (sequential fold).
+                               0 -> library default: N+2 for batch >= 148; below that 1, except
+                               for the SRBD step with batch (N+2) > 2500 (N+2 when N+2 <= 64,
+                               else 8) -- the measured crossover (D1).  Large-n
+                               handles take the fold unless leaf_chunk == 1.                  */
     int32_t export_policy;  /* reserved (K,k are written whenever pdilqr_dir.K/k are non-NULL) */
     pdilqr_srbd_params srbd;/* used iff model == PDILQR_MODEL_SRBD or MULTI_SRBD (per robot)  */
     pdilqr_multi_params multi; /* used iff model == PDILQR_MODEL_MULTI_SRBD                   */
